@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark: uncompressed-equivalent gradient GB/s per sync (encode + exchange +
+decode) of the B200 TAGC exchange, BASELINE.json's metric.
+
+Workload (BASELINE config 2, "GPT-2 small (124M) shaped per-layer gradient
+buckets, layer-selective compression"): every rank holds a full GPT-2-small
+(tied head, 124,439,808 fp32) gradient laid out by the reference's own layer
+list (model.cpp:39-64); make_shards(specs, N, N) gives one shard per rank;
+non_attention_linear policy (+ out-proj), theta = 99 per rank, ratio 10,
+4-bit index, seed 77. A step is one full exchange: every rank sparsifies and
+encodes all shards, the index/sketch/raw blocks are reduce-scattered over
+NCCL, and every owner peels its shard back to dense fp32. Accumulators carry
+error feedback across steps. Gradients are synthetic log-normal magnitudes with
+fair signs (the distribution of the reference's SyntheticStream,
+train.cpp:445-459), generated on device; 498 MB per rank, > L2 (126 MB).
+
+value = N * 124,439,808 * 4 B / (device time per step, max over ranks).
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libtagc_ref.so: tagc_reduce_shard with World(N, parallel), all
+host threads) on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+THETA, RATIO, WIDTH, SEED = 99.0, 10, 4, 77
+WORKLOAD = "gpt2-small-124M-tied/non_attention_linear/theta99/r10/w4"
+METRIC = "uncompressed-equivalent gradient GB/s per sync (encode+RS+decode)"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for i, nm in enumerate(names):
+                    if "Active" in r[2 + i] and "Not" not in r[2 + i]:
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_specs():
+    import paper_2504_05638_b200 as tagc
+
+    return tagc.gpt2_specs()
+
+
+def cfg_obj():
+    import paper_2504_05638_b200 as tagc
+
+    return tagc.CompressionConfig(theta=THETA, ratio=RATIO, index_width=WIDTH,
+                                  policy="non_attention_linear", include_out_proj=True, seed=SEED)
+
+
+def algorithmic_bytes(shards, rank, world):
+    """SURVEY.md §8(d) bytes for this rank: encode reads g, acc and writes acc,
+    index (w/8) and sketch zero-fill (4/r) per compressed element plus a
+    24*d scatter RMW (d = kept density, 1 - theta/100); select reads g, acc."""
+    import paper_2504_05638_b200 as tagc
+
+    comp = 0
+    for sh in shards:
+        for s in sh.segments:
+            if tagc.kind_compressible(s.kind, "non_attention_linear", True) and s.size() >= 1024:
+                comp += s.size()
+    dens = 1.0 - THETA / 100.0
+    enc = comp * (12.0 + WIDTH / 8.0 + 4.0 / RATIO + 24.0 * dens)
+    sel = comp * 8.0
+    return comp, enc, sel
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_05638_b200 as tagc
+
+    world = args.gpus
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = f"cuda:{local}"
+    specs = workload_specs()
+    shards = tagc.make_shards(specs, world, world)
+    total = shards[-1].end
+    n_params = sum(s.param_count for s in specs)
+    cfg = cfg_obj()
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    ctx = tagc.Context(cfg, world_size=world, rank=rank, device=local, stream=stream.cuda_stream)
+    if world > 1:
+        obj = [tagc.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_nccl(obj[0])
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    grad = torch.empty(total, device=dev)
+    mag = torch.randn(total, device=dev, generator=gen).exp_()
+    sign = torch.randint(0, 2, (total,), device=dev, generator=gen, dtype=torch.int8)
+    grad.copy_(torch.where(sign.bool(), -mag, mag))
+    del mag, sign
+    if total > n_params:
+        grad[n_params:] = 0.0  # make_shards pad tail
+    acc = torch.zeros(total, device=dev)
+    owned = sum(s.size() for s in shards if s.owner == rank)
+    out = torch.empty(max(owned, 1), device=dev)
+    torch.cuda.synchronize()
+
+    def step(stats=False):
+        return ctx.tagc_reduce_shards(shards, grad, acc, out, stats=stats)
+
+    for _ in range(args.warmup):
+        step()
+    _, st = step(stats=True)  # untimed: peel statistics of this config
+    rounds = ctx.last_peel_rounds()
+    ctx.set_timing(True)
+    step()
+    stage_ms = ctx.last_timing()
+    launches_per_step = ctx.last_launches()
+    ctx.set_timing(False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    clk = clocks.stop()
+
+    # per-stage device time of one step with stage events (select, encode, exchange, decode)
+    ctx.set_timing(True)
+    stage_acc = [0.0] * 4
+    for _ in range(args.steps):
+        step()
+        t = ctx.last_timing()
+        stage_acc = [a + b for a, b in zip(stage_acc, t)]
+    ctx.set_timing(False)
+    stage_ms = [a / args.steps for a in stage_acc]
+
+    # uncompressed comparator: ncclReduceScatter fp32 of the same shards
+    base_out = torch.empty(shards[0].size(), device=dev)
+    for _ in range(args.warmup):
+        ctx.baseline_reduce_shards(shards, grad, base_out)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctx.baseline_reduce_shards(shards, grad, base_out)
+    e1.record(stream)
+    barrier()
+    base_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+
+    # e2e through the C-ABI with host buffers: H2D of the step's gradient from
+    # pinned memory, the exchange, D2H of the owner's decoded shard.
+    host_grad = torch.empty(total, dtype=torch.float32, pin_memory=True)
+    host_grad.copy_(grad.cpu())
+    host_out = torch.empty(max(owned, 1), dtype=torch.float32, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        grad.copy_(host_grad, non_blocking=True)
+        ctx.tagc_reduce_shards(shards, grad, acc, out, stats=False)
+        host_out.copy_(out, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+
+    comp, enc_bytes, sel_bytes = algorithmic_bytes(shards, rank, world)
+    hbm, peak_kind = peaks()
+    enc_ms = stage_ms[1]
+    achieved = enc_bytes / (enc_ms * 1e-3) / 1e9 if enc_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "encode_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    uncompressed = n_params * 4.0
+    value = world * uncompressed / (ms * 1e-3) / 1e9
+    result = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic log-normal gradients (SyntheticStream distribution), generated on device",
+        "config": {
+            "workload": WORKLOAD,
+            "params_per_rank": n_params,
+            "shards": f"make_shards(gpt2_small, {world}, {world})",
+            "compressed_params_per_rank": comp,
+            "peel": {"presence": st.presence, "peeled": st.peeled, "unresolved": st.unresolved,
+                     "rounds": rounds[0], "tail_rounds": rounds[1]},
+            "l2": "inputs larger than L2 (498 MB per rank)",
+            "parallelism": f"dp{world} (one process per GPU, NCCL reduce-scatter)",
+        },
+        "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4)},
+        "roofline": {"kernel": "k_encode (split + index + sketch scatter)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": int(enc_bytes)},
+        "stages_ms": {"select": round(stage_ms[0], 4), "encode": round(stage_ms[1], 4),
+                      "exchange": round(stage_ms[2], 4), "decode": round(stage_ms[3], 4)},
+        "select_roofline": {"achieved": round(sel_bytes / (stage_ms[0] * 1e-3) / 1e9, 1)
+                            if stage_ms[0] > 0 else 0.0, "unit": "GB/s",
+                            "frac": round(sel_bytes / (stage_ms[0] * 1e-3) / 1e9 / hbm, 4)
+                            if stage_ms[0] > 0 else 0.0},
+        "uncompressed_rs": {"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
+                            "unit": "GB/s", "ms_per_step": round(base_ms, 4)},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args, specs, world, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def sample_shards(specs, world, budget_elems):
+    """A bounded sample of the workload: the shard plan of make_shards(specs,
+    W, W) restricted to its first segments up to ~budget_elems per rank."""
+    import oracle as O
+    import paper_2504_05638_b200 as tagc
+
+    shards = tagc.make_shards(specs, world, world)
+    out, used = [], 0
+    for sh in shards:
+        segs = []
+        for s in sh.segments:
+            if used >= budget_elems:
+                break
+            segs.append(O.Segment(s.kind, s.begin, s.end, s.name))
+            used += s.size()
+        if segs:
+            out.append(O.Shard(sh.id, sh.owner, segs[0].begin, segs[-1].end, segs))
+    return out, used
+
+
+def cpu_baseline(args, specs, world, budget_s=20.0):
+    """The reference's own CPU path (oracle/_ref) on the host cores, bounded."""
+    import numpy as np
+
+    import oracle as O
+
+    if not O.Ref.available():
+        return {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    ref = O.Ref()
+    budget = args.cpu_elems
+    shards, used = sample_shards(specs, world, budget)
+    end = max(s.end for s in shards)
+    grads = list(O.Oracle().stream(end, 2024, count=world))
+    cfg = O.Config(THETA, RATIO, WIDTH, "non_attention_linear", True, SEED, 3, False, 1024)
+    # each shard's grads are sliced by the reference wrapper from the flat buffers
+    secs = ref.time_reduce_shards(shards, grads, cfg, reps=1)
+    t = float(secs.min())
+    return {"value": round(world * used * 4 / t / 1e9, 5), "unit": "GB/s",
+            "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"first {used} params per rank of the workload ({len(shards)} shard(s)), "
+                      f"tagc_reduce_shard World({world}, parallel), OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}",
+            "seconds": round(t, 3)}
+
+
+def run_reference(args):
+    world = args.gpus
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as O
+
+    if not O.Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtagc_ref.so not built"}))
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    specs = workload_specs()
+    shards, used = sample_shards(specs, world, args.cpu_elems)
+    end = max(s.end for s in shards)
+    grads = list(O.Oracle().stream(end, 2024, count=world))
+    cfg = O.Config(THETA, RATIO, WIDTH, "non_attention_linear", True, SEED, 3, False, 1024)
+    ref = O.Ref()
+    ref.time_reduce_shards(shards, grads, cfg, reps=max(0, min(args.warmup, 1)) or 1)
+    secs = ref.time_reduce_shards(shards, grads, cfg, reps=args.steps)
+    t = float(secs.mean())
+    value = world * used * 4 / t / 1e9
+    sample = (f"first {used} params per rank of {WORKLOAD} ({len(shards)} shard(s)), "
+              f"tagc_reduce_shard World({world}, parallel)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic SyntheticStream gradients (reference generator)",
+        "config": {"workload": WORKLOAD, "sample_params_per_rank": used},
+        "cpu_baseline": {"value": round(value, 5), "unit": "GB/s", "cores": os.cpu_count(),
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-elems", type=int, default=24_000_000,
+                    help="params per rank in the bounded CPU-reference sample")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,263 @@
+/*
+ * tagc_b200.h — C-ABI of the B200-native TAGC compressed gradient-exchange
+ * path (libtagc_b200.so). Plain pointers and sizes only; no torch types.
+ *
+ * This boundary replaces the reference's per-shard exchange
+ *   tagc::tagc_reduce_shard       (reference proj/include/tagc/hook.hpp:76-80,
+ *                                  proj/src/hook.cpp:98-200)
+ *   tagc::baseline_reduce_shard   (hook.hpp:84-86, hook.cpp:90-96)
+ * and the per-layer codec calls it is built from:
+ *   tagc::sparsify / apply_accumulator        (sparsify.hpp:23-38)
+ *   tagc::Index::create / merge_indices / presence (index.hpp:26,36,50)
+ *   tagc::CountSketch::compress / sketch_add  (sketch.hpp:44-46,65)
+ *   tagc::peeling_decompress / estimation_decompress (decode.hpp:25-32)
+ * plus the host-side policy/config/model calls (config.hpp:16-35,
+ * layers.hpp:35-50, hook.hpp:42-43,98-104, sketch.hpp:21-28).
+ *
+ * Conventions (mirroring the reference):
+ *  - Status: TAGC_OK (0); TAGC_INVALID (2) wherever the reference throws
+ *    std::invalid_argument; TAGC_RUNTIME (1) for any other failure (CUDA,
+ *    NCCL, allocation). tagc_last_error() returns a thread-local message.
+ *    The CLI mapping 0/1/2 follows reference cli.cpp:375-382.
+ *  - Buffers marked "dev" are caller-owned device pointers; the accumulator
+ *    is in/out and persists across steps (reference train.cpp:249-252).
+ *  - Work is enqueued on the context's stream. Calls that return statistics
+ *    (a non-NULL stats/tau/count out-pointer) synchronise that stream once at
+ *    the end; with NULL stats pointers nothing blocks the host.
+ *  - There is no CPU fallback: every compute entry point runs sm_100a CUDA
+ *    kernels and fails with TAGC_RUNTIME when no device is usable.
+ */
+#ifndef TAGC_B200_H
+#define TAGC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define TAGC_B200_ABI_VERSION 1
+
+enum tagc_status { TAGC_OK = 0, TAGC_RUNTIME = 1, TAGC_INVALID = 2 };
+
+/* reference config.hpp:10 */
+enum tagc_policy {
+  TAGC_POLICY_ALL_LAYERS = 0,
+  TAGC_POLICY_NON_ATTENTION_LINEAR = 1,
+  TAGC_POLICY_NONE = 2
+};
+
+/* reference layers.hpp:12-22 */
+enum tagc_layer_kind {
+  TAGC_KIND_EMBEDDING = 0,
+  TAGC_KIND_POSITIONAL_EMBEDDING = 1,
+  TAGC_KIND_ATTENTION_QKV = 2,
+  TAGC_KIND_ATTENTION_OUT_PROJ = 3,
+  TAGC_KIND_FEED_FORWARD = 4,
+  TAGC_KIND_LM_HEAD = 5,
+  TAGC_KIND_NORM = 6,
+  TAGC_KIND_BIAS = 7,
+  TAGC_KIND_OTHER = 8
+};
+
+/* reference CompressionConfig, config.hpp:16-35 (same fields, same defaults
+ * via tagc_config_default). */
+typedef struct tagc_config {
+  double theta;                  /* sparsification threshold, percent */
+  uint32_t ratio;                /* 1 = codec bypass, else one of {2,4,10} */
+  uint32_t index_width;          /* 1 or 4 */
+  int32_t policy;                /* enum tagc_policy */
+  int32_t include_out_proj;      /* bool */
+  uint64_t seed;                 /* hash seed, one per exchange */
+  uint32_t sketch_rows;          /* k, default 3 */
+  int32_t allow_low_theta;       /* bool */
+  uint64_t min_compress_segment; /* default 1024 */
+} tagc_config;
+
+/* reference LayerSegment, hook.hpp:21-28 (global flat coordinates) */
+typedef struct tagc_segment {
+  int32_t kind; /* enum tagc_layer_kind */
+  uint64_t begin, end;
+  const char* name; /* ledger tag component; may be NULL ("seg<i>") */
+} tagc_segment;
+
+/* reference ShardSpec, hook.hpp:30-38 */
+typedef struct tagc_shard {
+  uint32_t id, owner;
+  uint64_t begin, end;
+  const tagc_segment* segments;
+  uint32_t num_segments;
+} tagc_shard;
+
+/* reference PeelStats, hook.hpp:45-59 */
+typedef struct tagc_peel_stats {
+  uint64_t presence, peeled, unresolved, index_lost, index_spurious, compressed_segments,
+      baseline_segments;
+} tagc_peel_stats;
+
+/* reference SketchGeometry, sketch.hpp:21-28 */
+typedef struct tagc_sketch_geom {
+  uint32_t n, ratio, rows, buckets_per_row;
+} tagc_sketch_geom;
+
+/* reference CommVolume, hook.hpp:88-93 */
+typedef struct tagc_comm_volume {
+  double index_bits, sketch_bits, total_bits, factor;
+} tagc_comm_volume;
+
+/* reference LayerSpec, layers.hpp:27-31 */
+typedef struct tagc_layer_spec {
+  const char* name;
+  int32_t kind;
+  uint64_t param_count;
+} tagc_layer_spec;
+
+/* ------------------------------------------------------------ errors / misc */
+const char* tagc_last_error(void);
+int tagc_abi_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int tagc_device_count(void);
+
+/* -------------------------------------------------- host policy and models */
+void tagc_config_default(tagc_config* out);
+/* CompressionConfig::validate_for_world (config.cpp:53-59) */
+int tagc_config_validate(const tagc_config* cfg, uint32_t world_size);
+/* CompressionConfig::theta_floor (config.cpp:27-35) */
+int tagc_theta_floor(uint32_t ratio, double* out);
+/* kind_compressible (layers.cpp:42-65): returns 0/1, or -1 for a bad enum */
+int tagc_kind_compressible(int32_t kind, int32_t policy, int32_t include_out_proj);
+/* sketch_geometry (sketch.cpp:11-27) */
+int tagc_sketch_geometry(uint32_t n, uint32_t ratio, uint32_t rows, tagc_sketch_geom* out);
+/* words_needed (index.cpp:17-20) */
+uint32_t tagc_index_words(uint32_t n, uint32_t width);
+/* comm_volume_model / lhc_comm_volume_model (hook.cpp:202-236); n == 0 means
+ * "no explicit length" (the asymptotic 32/ratio payload). */
+int tagc_comm_volume_model(const tagc_config* cfg, uint32_t world_size, uint64_t n,
+                           tagc_comm_volume* out);
+int tagc_lhc_comm_volume_model(const tagc_config* cfg, uint32_t world_size, uint64_t n,
+                               tagc_comm_volume* out);
+
+/* make_shards (hook.cpp:30-61). The returned set owns its segments; segment
+ * names point into the set ("pad" for the alignment tail). */
+typedef struct tagc_shard_set tagc_shard_set;
+int tagc_make_shards(const tagc_layer_spec* layers, uint32_t n_layers, uint32_t shard_count,
+                     uint32_t world_size, tagc_shard_set** out);
+uint32_t tagc_shard_set_count(const tagc_shard_set* set);
+/* Fills *out with shard i; pointers stay valid until tagc_shard_set_destroy. */
+int tagc_shard_set_get(const tagc_shard_set* set, uint32_t i, tagc_shard* out);
+void tagc_shard_set_destroy(tagc_shard_set* set);
+
+/* ---------------------------------------------------------------- context */
+typedef struct tagc_ctx tagc_ctx;
+/* world_size/rank describe the caller's process in a real multi-GPU world
+ * (nccl_comm = an ncclComm_t, or NULL and call tagc_ctx_init_nccl). For the
+ * simulated-world entry points (suffix _sim) the context may be created with
+ * world_size = 1, rank = 0; the simulated W comes from the call.
+ * stream: a cudaStream_t (cudaStreamLegacy = (void*)1 for the legacy default
+ * stream) or NULL for a context-owned non-blocking stream. */
+int tagc_ctx_create(const tagc_config* cfg, uint32_t world_size, uint32_t rank, int device,
+                    void* nccl_comm, void* cuda_stream, tagc_ctx** out);
+void tagc_ctx_destroy(tagc_ctx* ctx);
+/* Replace the compression config (validated against the ctx world). */
+int tagc_ctx_set_config(tagc_ctx* ctx, const tagc_config* cfg);
+void* tagc_ctx_stream(tagc_ctx* ctx);
+/* NCCL bootstrap helpers (the 128-byte ncclUniqueId is exchanged by the
+ * caller, e.g. torch.distributed.broadcast_object_list). */
+int tagc_nccl_unique_id(uint8_t out[128]);
+int tagc_ctx_init_nccl(tagc_ctx* ctx, const uint8_t unique_id[128]);
+/* Traffic ledger as CSV in the reference's format (collectives.cpp:70-78). */
+int tagc_ctx_ledger_csv(tagc_ctx* ctx, char* buf, size_t len, size_t* needed);
+int tagc_ctx_ledger_reset(tagc_ctx* ctx);
+/* Device bytes the context currently holds in workspaces. */
+uint64_t tagc_ctx_workspace_bytes(const tagc_ctx* ctx);
+/* Optional per-stage device timing of the last fused call (ms): select,
+ * encode, exchange, decode. Enabled by tagc_ctx_set_timing(ctx, 1). */
+int tagc_ctx_set_timing(tagc_ctx* ctx, int enabled);
+int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[4]);
+/* Kernel launches enqueued by the last fused call. */
+uint64_t tagc_ctx_last_launches(const tagc_ctx* ctx);
+/* Synchronise the context stream and surface deferred device errors (a NaN
+ * input found by an asynchronous call without stats returns TAGC_INVALID). */
+int tagc_ctx_sync(tagc_ctx* ctx);
+/* Peel rounds of the last fused call that returned stats:
+ * out[0] = grid-wide rounds, out[1] = single-CTA tail rounds. */
+int tagc_ctx_last_peel_rounds(tagc_ctx* ctx, uint32_t out[2]);
+
+/* -------------------------------------------- fused exchange: simulated world
+ * tagc_reduce_shard (hook.cpp:98-200) with W logical ranks on this GPU.
+ * grads[r], accs[r]: dev, shard.size() floats each (accs mutated for
+ * compressed segments only); out: dev, shard.size() floats (the owner's
+ * decoded shard). stats may be NULL. */
+int tagc_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
+                          const float* const* grads, float* const* accs, float* out,
+                          tagc_peel_stats* stats);
+/* baseline_reduce_shard (hook.cpp:90-96): ascending-rank fp32 sum. */
+int tagc_baseline_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
+                                   const float* const* grads, float* out);
+
+/* ---------------------------------------------- fused exchange: NCCL world
+ * One process per GPU. grad/acc: dev, this rank's flat buffers covering every
+ * shard (shards[i].begin .. end index into them). out: dev, the concatenation
+ * (in shard order) of the shards this rank owns. The index and sketch (and
+ * raw segments) of all shards are exchanged in one grouped NCCL
+ * reduce-scatter. stats (may be NULL) covers this rank's owned shards. */
+int tagc_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                       const float* grad, float* acc, float* out, tagc_peel_stats* stats);
+/* Single-shard form of the above (reference tagc_reduce_shard call shape);
+ * out is written on the owner rank only. */
+int tagc_reduce_shard(tagc_ctx* ctx, const tagc_shard* shard, const float* grad, float* acc,
+                      float* out, tagc_peel_stats* stats);
+/* Uncompressed comparator: ncclReduceScatter fp32 of the shards (requires
+ * n_shards == world_size with shard i owned by rank i, as make_shards(W, W)
+ * gives). out: dev, shard size floats. */
+int tagc_baseline_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                                const float* grad, float* out);
+
+/* ------------------------------------------------- per-layer codec (device)
+ * Each mirrors one reference function on one vector of n elements. */
+/* apply_accumulator (sparsify.cpp:9-16): out = g + acc */
+int tagc_apply_accumulator(tagc_ctx* ctx, const float* g, const float* acc, float* out,
+                           uint64_t n);
+/* sparsify (sparsify.cpp:18-49). sparse/residual dev (n each); tau and
+ * zero_count host out-pointers (may be NULL). */
+int tagc_sparsify(tagc_ctx* ctx, const float* g, uint32_t n, double theta, float* sparse,
+                  float* residual, float* tau, uint64_t* zero_count);
+/* Index::create (index.cpp:32-41): words dev, tagc_index_words(n,width) u32 */
+int tagc_index_create(tagc_ctx* ctx, const float* values, uint32_t n, uint32_t width,
+                      uint32_t* words);
+/* merge_indices (index.cpp:80-93): wrapping u32 word sum of `world` inputs */
+int tagc_merge_indices(tagc_ctx* ctx, const uint32_t* const* words, uint32_t world,
+                       uint32_t n_words, uint32_t* out);
+/* Index::presence (index.cpp:51-57): positions (dev, capacity n) ascending */
+int tagc_index_presence(tagc_ctx* ctx, const uint32_t* words, uint32_t n, uint32_t width,
+                        uint32_t* positions, uint32_t* count);
+/* CountSketch::compress (sketch.cpp:37-67): sketch dev, rows*m floats */
+int tagc_sketch_compress(tagc_ctx* ctx, const float* values, uint32_t n, uint32_t ratio,
+                         uint32_t rows, uint64_t seed, float* sketch);
+/* sketch_add (sketch.cpp:69-75): out = a + b */
+int tagc_sketch_add(tagc_ctx* ctx, const float* a, const float* b, float* out, uint64_t len);
+/* peeling_decompress (decode.cpp:53-140). presence dev (count entries),
+ * sketch dev (rows*m, not modified), values dev (n). unresolved dev
+ * (capacity count, ascending) may be NULL; n_unresolved / peeled_fraction
+ * host out-pointers may be NULL. */
+int tagc_peeling_decompress(tagc_ctx* ctx, const uint32_t* presence, uint32_t count, uint32_t n,
+                            uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
+                            float* values, uint32_t* unresolved, uint32_t* n_unresolved,
+                            double* peeled_fraction);
+/* estimation_decompress (decode.cpp:24-51): out dev, one value per target */
+int tagc_estimation_decompress(tagc_ctx* ctx, const uint32_t* presence, uint32_t count,
+                               uint32_t n, uint32_t ratio, uint32_t rows, uint64_t seed,
+                               const float* sketch, const uint32_t* targets, uint32_t n_targets,
+                               float* out);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAGC_B200_H */

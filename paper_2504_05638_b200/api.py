@@ -1,0 +1,410 @@
+"""Python mirror of the reference compressor API for the exchange path, over the
+C-ABI (libtagc_b200.so). Names, argument meaning and error behaviour follow
+the reference (tagc::CompressionConfig, make_shards, tagc_reduce_shard, ...);
+device buffers are torch CUDA tensors used as plain memory (torch is plumbing,
+every computation runs in the library's sm_100a kernels).
+
+u32 buffers (index words, positions) are carried in torch.int32 tensors and
+reinterpreted bit-for-bit.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _lib
+from ._lib import TagcError, TagcInvalidArgument, check, lib
+
+POLICY = {"all_layers": 0, "non_attention_linear": 1, "none": 2}
+KIND = {
+    "embedding": 0,
+    "positional_embedding": 1,
+    "attention_qkv": 2,
+    "attention_out_proj": 3,
+    "feed_forward": 4,
+    "lm_head": 5,
+    "norm": 6,
+    "bias": 7,
+    "other": 8,
+}
+KIND_NAME = {v: k for k, v in KIND.items()}
+
+__all__ = [
+    "CompressionConfig", "LayerSpec", "LayerSegment", "ShardSpec", "PeelStats", "Context",
+    "make_shards", "kind_compressible", "sketch_geometry", "words_needed", "theta_floor",
+    "comm_volume_model", "lhc_comm_volume_model", "TagcError", "TagcInvalidArgument",
+    "device_count",
+]
+
+
+@dataclass
+class CompressionConfig:
+    """reference config.hpp:16-35"""
+
+    theta: float = 0.0
+    ratio: int = 1
+    index_width: int = 4
+    policy: str = "non_attention_linear"
+    include_out_proj: bool = True
+    seed: int = 0
+    sketch_rows: int = 3
+    allow_low_theta: bool = False
+    min_compress_segment: int = 1024
+
+    def c(self) -> _lib.Config:
+        if self.policy not in POLICY:
+            raise TagcInvalidArgument(2, f"unknown policy: {self.policy}")
+        return _lib.Config(float(self.theta), int(self.ratio), int(self.index_width),
+                           POLICY[self.policy], int(bool(self.include_out_proj)),
+                           int(self.seed) & (2**64 - 1), int(self.sketch_rows),
+                           int(bool(self.allow_low_theta)), int(self.min_compress_segment))
+
+    def validate_for_world(self, world_size: int) -> None:
+        check(lib.tagc_config_validate(C.byref(self.c()), world_size), "validate_for_world")
+
+    def validate(self) -> None:
+        self.validate_for_world(1)
+
+
+@dataclass
+class LayerSpec:
+    """reference layers.hpp:27-31"""
+
+    name: str
+    kind: str
+    param_count: int
+
+
+@dataclass
+class LayerSegment:
+    """reference hook.hpp:21-28"""
+
+    name: str
+    kind: str
+    begin: int
+    end: int
+
+    def size(self) -> int:
+        return self.end - self.begin
+
+
+@dataclass
+class ShardSpec:
+    """reference hook.hpp:30-38"""
+
+    id: int
+    owner: int
+    begin: int
+    end: int
+    segments: List[LayerSegment] = field(default_factory=list)
+
+    def size(self) -> int:
+        return self.end - self.begin
+
+
+@dataclass
+class PeelStats:
+    """reference hook.hpp:45-59"""
+
+    presence: int = 0
+    peeled: int = 0
+    unresolved: int = 0
+    index_lost: int = 0
+    index_spurious: int = 0
+    compressed_segments: int = 0
+    baseline_segments: int = 0
+
+    def peel_success(self) -> float:
+        return 1.0 if self.presence == 0 else self.peeled / self.presence
+
+    def index_collision_rate(self) -> float:
+        truth = self.presence + self.index_lost - self.index_spurious
+        return 0.0 if truth == 0 else (self.index_lost + self.index_spurious) / truth
+
+
+class _ShardC:
+    def __init__(self, shard: ShardSpec):
+        self.names = [s.name.encode() for s in shard.segments]
+        n = max(1, len(shard.segments))
+        self.segs = (_lib.Segment * n)(*[
+            _lib.Segment(KIND[s.kind], s.begin, s.end, nm)
+            for s, nm in zip(shard.segments, self.names)])
+        self.c = _lib.Shard(shard.id, shard.owner, shard.begin, shard.end, self.segs,
+                            len(shard.segments))
+
+
+def device_count() -> int:
+    return int(lib.tagc_device_count())
+
+
+def theta_floor(ratio: int) -> float:
+    out = C.c_double()
+    check(lib.tagc_theta_floor(ratio, C.byref(out)), "theta_floor")
+    return out.value
+
+
+def kind_compressible(kind: str, policy: str, include_out_proj: bool = True) -> bool:
+    """reference layers.cpp:42-65"""
+    r = lib.tagc_kind_compressible(KIND[kind], POLICY[policy], int(include_out_proj))
+    if r < 0:
+        raise TagcInvalidArgument(2, "bad kind/policy")
+    return bool(r)
+
+
+def sketch_geometry(n: int, ratio: int, rows: int = 3) -> dict:
+    g = _lib.SketchGeom()
+    check(lib.tagc_sketch_geometry(n, ratio, rows, C.byref(g)), "sketch_geometry")
+    return {"n": g.n, "ratio": g.ratio, "rows": g.rows, "buckets_per_row": g.buckets_per_row}
+
+
+def words_needed(n: int, width: int) -> int:
+    return int(lib.tagc_index_words(n, width))
+
+
+def _volume(fn, cfg, world, n):
+    v = _lib.CommVolume()
+    check(fn(C.byref(cfg.c()), world, int(n or 0), C.byref(v)), "comm_volume_model")
+    return {"index_bits": v.index_bits, "sketch_bits": v.sketch_bits,
+            "total_bits": v.total_bits, "factor": v.factor}
+
+
+def comm_volume_model(cfg: CompressionConfig, world_size: int, n: Optional[int] = None) -> dict:
+    """reference hook.cpp:202-226"""
+    return _volume(lib.tagc_comm_volume_model, cfg, world_size, n)
+
+
+def lhc_comm_volume_model(cfg: CompressionConfig, world_size: int, n: Optional[int] = None) -> dict:
+    """reference hook.cpp:228-236"""
+    return _volume(lib.tagc_lhc_comm_volume_model, cfg, world_size, n)
+
+
+def make_shards(layers: Sequence[LayerSpec], shard_count: int, world_size: int) -> List[ShardSpec]:
+    """reference hook.cpp:30-61"""
+    names = [l.name.encode() for l in layers]
+    arr = (_lib.LayerSpecC * max(1, len(layers)))(*[
+        _lib.LayerSpecC(nm, KIND[l.kind], int(l.param_count)) for l, nm in zip(layers, names)])
+    h = C.c_void_p()
+    check(lib.tagc_make_shards(arr, len(layers), shard_count, world_size, C.byref(h)), "make_shards")
+    try:
+        out = []
+        for i in range(lib.tagc_shard_set_count(h)):
+            s = _lib.Shard()
+            check(lib.tagc_shard_set_get(h, i, C.byref(s)))
+            segs = [LayerSegment(s.segments[j].name.decode(), KIND_NAME[s.segments[j].kind],
+                                 int(s.segments[j].begin), int(s.segments[j].end))
+                    for j in range(s.num_segments)]
+            out.append(ShardSpec(int(s.id), int(s.owner), int(s.begin), int(s.end), segs))
+        return out
+    finally:
+        lib.tagc_shard_set_destroy(h)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _ptr_array(ts):
+    return (C.c_void_p * len(ts))(*[_ptr(t) for t in ts])
+
+
+class Context:
+    """Owns a tagc_ctx (one CUDA stream, workspaces, ledger, optional NCCL comm).
+
+    By default the context enqueues on torch's current CUDA stream so torch
+    allocations and library kernels are ordered without extra syncs.
+    """
+
+    def __init__(self, cfg: CompressionConfig, world_size: int = 1, rank: int = 0, device: int = 0,
+                 nccl_comm: int = 0, stream: Optional[int] = None):
+        import torch
+
+        self.torch = torch
+        self.cfg = cfg
+        self.device = device
+        self.world_size = world_size
+        self.rank = rank
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+            if stream == 0:
+                stream = 1  # cudaStreamLegacy: torch's default stream
+        h = C.c_void_p()
+        check(lib.tagc_ctx_create(C.byref(cfg.c()), world_size, rank, device, nccl_comm or None,
+                                  stream or None, C.byref(h)), "ctx_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.tagc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ misc
+    def set_config(self, cfg: CompressionConfig):
+        check(lib.tagc_ctx_set_config(self.h, C.byref(cfg.c())), "set_config")
+        self.cfg = cfg
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib.tagc_nccl_unique_id(buf), "nccl_unique_id")
+        return bytes(buf)
+
+    def init_nccl(self, uid: bytes):
+        buf = (C.c_uint8 * 128)(*uid)
+        check(lib.tagc_ctx_init_nccl(self.h, buf), "init_nccl")
+
+    def ledger_csv(self) -> str:
+        need = C.c_size_t()
+        check(lib.tagc_ctx_ledger_csv(self.h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib.tagc_ctx_ledger_csv(self.h, buf, len(buf), None))
+        return buf.value.decode()
+
+    def ledger_reset(self):
+        check(lib.tagc_ctx_ledger_reset(self.h))
+
+    def workspace_bytes(self) -> int:
+        return int(lib.tagc_ctx_workspace_bytes(self.h))
+
+    def set_timing(self, on: bool):
+        check(lib.tagc_ctx_set_timing(self.h, int(on)))
+
+    def last_timing(self):
+        out = (C.c_float * 4)()
+        check(lib.tagc_ctx_last_timing(self.h, out))
+        return list(out)
+
+    def last_launches(self) -> int:
+        return int(lib.tagc_ctx_last_launches(self.h))
+
+    def last_peel_rounds(self):
+        out = (C.c_uint32 * 2)()
+        check(lib.tagc_ctx_last_peel_rounds(self.h, out))
+        return list(out)
+
+    def sync(self):
+        check(lib.tagc_ctx_sync(self.h), "sync")
+
+    def _empty(self, n, dtype=None):
+        t = self.torch
+        return t.empty(int(n), dtype=dtype or t.float32, device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------------ fused exchange
+    def tagc_reduce_shard_sim(self, shard: ShardSpec, grads, accs, out=None, stats=True):
+        """reference tagc_reduce_shard (hook.cpp:98-200) with len(grads) simulated ranks."""
+        w = len(grads)
+        if len(accs) != w:
+            raise TagcInvalidArgument(2, "need one accumulator per rank")
+        for g, a in zip(grads, accs):
+            if g.numel() != shard.size() or a.numel() != shard.size():
+                raise TagcInvalidArgument(2, "gradient slice length does not match the shard")
+        out = self._empty(shard.size()) if out is None else out
+        sc = _ShardC(shard)
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shard_sim(self.h, C.byref(sc.c), w, _ptr_array(grads), _ptr_array(accs),
+                                        _ptr(out), C.byref(st) if stats else None), "tagc_reduce_shard")
+        return out, (PeelStats(**st.as_dict()) if stats else None)
+
+    def baseline_reduce_shard_sim(self, shard: ShardSpec, grads, out=None):
+        for g in grads:
+            if g.numel() != shard.size():
+                raise TagcInvalidArgument(2, "gradient slice length does not match the shard")
+        out = self._empty(shard.size()) if out is None else out
+        sc = _ShardC(shard)
+        check(lib.tagc_baseline_reduce_shard_sim(self.h, C.byref(sc.c), len(grads), _ptr_array(grads),
+                                                 _ptr(out)), "baseline_reduce_shard")
+        return out
+
+    def tagc_reduce_shards(self, shards: Sequence[ShardSpec], grad, acc, out=None, stats=True):
+        """One process per GPU: exchange every shard, decode the owned ones."""
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        out = self._empty(max(owned, 1)) if out is None else out
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shards(self.h, arr, len(scs), _ptr(grad), _ptr(acc), _ptr(out),
+                                     C.byref(st) if stats else None), "tagc_reduce_shards")
+        return out, (PeelStats(**st.as_dict()) if stats else None)
+
+    def baseline_reduce_shards(self, shards: Sequence[ShardSpec], grad, out=None):
+        L = shards[0].size()
+        out = self._empty(L) if out is None else out
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        check(lib.tagc_baseline_reduce_shards(self.h, arr, len(scs), _ptr(grad), _ptr(out)),
+              "baseline_reduce_shards")
+        return out
+
+    # ------------------------------------------------------------ per-layer codec
+    def apply_accumulator(self, g, acc):
+        out = self._empty(g.numel())
+        check(lib.tagc_apply_accumulator(self.h, _ptr(g), _ptr(acc), _ptr(out), g.numel()))
+        return out
+
+    def sparsify(self, g, theta: float):
+        """reference sparsify (sparsify.cpp:18-49): (sparse, residual, tau, zero_count)"""
+        n = g.numel()
+        sparse, residual = self._empty(n), self._empty(n)
+        tau = C.c_float()
+        zc = C.c_uint64()
+        check(lib.tagc_sparsify(self.h, _ptr(g), n, float(theta), _ptr(sparse), _ptr(residual),
+                                C.byref(tau), C.byref(zc)), "sparsify")
+        return sparse, residual, tau.value, int(zc.value)
+
+    def index_create(self, values, width: int):
+        words = self._empty(max(1, words_needed(values.numel(), width)), self.torch.int32)
+        check(lib.tagc_index_create(self.h, _ptr(values), values.numel(), width, _ptr(words)),
+              "index_create")
+        return words
+
+    def merge_indices(self, words_list):
+        out = self._empty(words_list[0].numel(), self.torch.int32)
+        check(lib.tagc_merge_indices(self.h, _ptr_array(words_list), len(words_list),
+                                     words_list[0].numel(), _ptr(out)), "merge_indices")
+        return out
+
+    def index_presence(self, words, n: int, width: int):
+        pos = self._empty(max(1, n), self.torch.int32)
+        cnt = C.c_uint32()
+        check(lib.tagc_index_presence(self.h, _ptr(words), n, width, _ptr(pos), C.byref(cnt)),
+              "presence")
+        return pos[: cnt.value]
+
+    def sketch_compress(self, values, ratio: int, seed: int, rows: int = 3):
+        g = sketch_geometry(values.numel(), ratio, rows)
+        out = self._empty(rows * g["buckets_per_row"])
+        check(lib.tagc_sketch_compress(self.h, _ptr(values), values.numel(), ratio, rows,
+                                       int(seed) & (2**64 - 1), _ptr(out)), "compress")
+        return out
+
+    def sketch_add(self, a, b):
+        out = self._empty(a.numel())
+        check(lib.tagc_sketch_add(self.h, _ptr(a), _ptr(b), _ptr(out), a.numel()), "sketch_add")
+        return out
+
+    def peeling_decompress(self, presence, sketch, n: int, ratio: int, seed: int, rows: int = 3):
+        """reference peeling_decompress (decode.cpp:53-140): (values, unresolved, peeled_fraction)"""
+        cnt = presence.numel()
+        vals = self._empty(n)
+        unres = self._empty(max(1, cnt), self.torch.int32)
+        nu = C.c_uint32()
+        pf = C.c_double()
+        check(lib.tagc_peeling_decompress(self.h, _ptr(presence) if cnt else None, cnt, n, ratio, rows,
+                                          int(seed) & (2**64 - 1), _ptr(sketch), _ptr(vals),
+                                          _ptr(unres), C.byref(nu), C.byref(pf)), "peeling_decompress")
+        return vals, unres[: nu.value], pf.value
+
+    def estimation_decompress(self, presence, sketch, targets, n: int, ratio: int, seed: int,
+                              rows: int = 3):
+        out = self._empty(max(1, targets.numel()))
+        check(lib.tagc_estimation_decompress(self.h, _ptr(presence), presence.numel(), n, ratio, rows,
+                                             int(seed) & (2**64 - 1), _ptr(sketch), _ptr(targets),
+                                             targets.numel(), _ptr(out)), "estimation_decompress")
+        self.sync()
+        return out[: targets.numel()]

@@ -1,0 +1,131 @@
+// device.cuh — descriptors shared by the host engine and the sm_100a kernels,
+// plus the device forms of the wire-format hash (reference hash.hpp:25-47).
+#pragma once
+
+#include <cstdint>
+
+namespace tagc_b200 {
+
+constexpr int kMaxRows = 8;
+// Elements per tile: 256 threads x 16 elements. Tiles are word-aligned for
+// both index widths (multiple of 32 positions).
+constexpr uint32_t kTile = 4096;
+constexpr uint32_t kTileThreads = 256;
+// Segments at or below this length skip the sampling pre-pass: every nonzero
+// key is a threshold candidate.
+constexpr uint32_t kSmallSegment = 65536;
+// Sample geometry: first kSampleChunk elements of every `sample_stride`-th tile.
+constexpr uint32_t kSampleChunk = 1024;
+constexpr uint32_t kSampleBins = 4096;  // top 12 bits of the 31-bit magnitude key
+constexpr uint32_t kSampleShift = 19;
+constexpr uint32_t kRadixBins = 2048;   // 11/10/10-bit digits of the key
+constexpr uint32_t kDecWordTile = 1024; // merged-index words per decode build tile
+
+// Per-row hash coefficients (reference hash.hpp:27-33), derived on the host.
+struct RowCoef {
+  uint64_t pos_a, pos_b, sgn_a, sgn_b;
+};
+struct HashParams {
+  RowCoef row[kMaxRows];
+  uint32_t rows;
+};
+
+// Item flags
+enum : uint32_t {
+  kWidth4 = 1u << 0,     // index width 4 (else 1)
+  kAligned16 = 1u << 1,  // g and acc (when present) are 16-byte aligned
+  kHasAcc = 1u << 2,     // combined = g + acc, residual written back to acc
+  kWriteIndex = 1u << 3,
+  kWriteSketch = 1u << 4,
+  kSelect = 1u << 5,      // tau from the select pipeline; else tau = 0
+  kWriteSparse = 1u << 6, // per-stage sparsify outputs
+  kWriteResidual = 1u << 7,
+};
+
+// One (rank, segment) unit of sparsify + encode work.
+struct EncItem {
+  const float* g;
+  float* acc;
+  float* sparse;    // optional (kWriteSparse)
+  float* residual;  // optional (kWriteResidual)
+  uint32_t* index;  // segment index words
+  float* sketch;    // rows*m floats
+  uint64_t tile_begin;
+  uint64_t sample_begin;  // first sample-work id (sample kernel)
+  uint64_t cand_off;      // offset into the candidate key pool
+  uint32_t n, m, c, flags;
+  uint32_t cand_cap, sample_stride, sample_tiles, pad;
+};
+
+// Select state per item (device; reset by the window kernel every call).
+struct SelState {
+  uint32_t klo, khi;            // candidate window on the 31-bit key
+  uint32_t cnt_zero, cnt_lo;    // keys == 0, 0 < key < klo
+  uint32_t cnt_in, status;      // candidates appended; 0 ok / 1 fallback / 2 NaN
+  uint32_t tau_key, prefix;     // threshold key; fallback radix prefix
+  uint32_t rank, kept;          // fallback residual rank; kept elements (zero_count)
+  uint32_t fshift, pad1;        // fine-bin shift of the window: bin = (key - klo) >> fshift
+};
+
+// One owner-side decode unit (one compressed segment).
+struct DecItem {
+  const uint32_t* words;  // merged index (or presence bitmap, width 1)
+  float* sketch;          // summed sketch rows*m (mutated into the residual)
+  float* out;             // dense output for the segment (n floats)
+  uint64_t slot_base;     // first global slot id (rows*m per item)
+  uint64_t bitmap_off;    // recovered-bitmap word offset
+  uint64_t word_tile_begin;
+  uint64_t list_off;      // presence list offset
+  uint32_t n, m, flags, n_words;
+};
+
+struct DecStats {  // per decode item, device
+  uint32_t presence, unresolved, overflow, pad;
+};
+
+// -------------------------------------------------------------- device hash
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t dev_bucket(const RowCoef& c, uint32_t p, uint32_t m) {
+  const uint64_t h = c.pos_a * (uint64_t(p) + 0x9E3779B9ull) + c.pos_b;  // hash.hpp:36
+  return uint32_t(h >> 32) % m;                                            // hash.hpp:37
+}
+__device__ __forceinline__ float dev_sign(const RowCoef& c, uint32_t p) {
+  const uint64_t h = c.sgn_a * (uint64_t(p) + 0x85EBCA77ull) + c.sgn_b;  // hash.hpp:41
+  return (h >> 63) ? 1.0f : -1.0f;                                         // hash.hpp:42
+}
+__device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+// Row coefficients with a runtime row index, without dynamic indexing into
+// the kernel-parameter struct (which would spill it to local memory).
+__device__ __forceinline__ RowCoef row_coef(const HashParams& hp, uint32_t row) {
+  RowCoef c = hp.row[0];
+#pragma unroll
+  for (uint32_t r = 1; r < uint32_t(kMaxRows); ++r)
+    if (row == r) c = hp.row[r];
+  return c;
+}
+#endif
+
+// Host: coefficient derivation (hash.hpp:15-33).
+inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+inline RowCoef make_row_coef(uint64_t seed, uint32_t row) {
+  RowCoef c;
+  const uint64_t s = splitmix64(seed ^ (0xA24BAED4963EE407ULL * (uint64_t)(row + 1u)));
+  c.pos_a = splitmix64(s) | 1ULL;
+  c.pos_b = splitmix64(c.pos_a);
+  c.sgn_a = splitmix64(c.pos_b) | 1ULL;
+  c.sgn_b = splitmix64(c.sgn_a);
+  return c;
+}
+inline HashParams make_hash_params(uint64_t seed, uint32_t rows) {
+  HashParams h{};
+  h.rows = rows;
+  for (uint32_t r = 0; r < rows && r < (uint32_t)kMaxRows; ++r) h.row[r] = make_row_coef(seed, r);
+  return h;
+}
+
+}  // namespace tagc_b200

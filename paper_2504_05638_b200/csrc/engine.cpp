@@ -1,0 +1,761 @@
+// engine.cpp — orchestration of the B200 exchange (see engine.hpp).
+//
+// Per call, for every compressed segment (reference hook.cpp:137-189):
+//   select  : tau = c-th smallest |g+acc| per (rank, segment)      [encode.cu]
+//   encode  : residual -> acc, packed index, count sketch           [encode.cu]
+//   exchange: simulated world -> rank folds on this GPU;
+//             NCCL world     -> one grouped reduce-scatter of the owner-major
+//                               (sketch+raw) f32 and index u32 blocks
+//   decode  : peel + estimate into the owner's dense shard          [decode.cu]
+// Raw segments (unflagged or below min_compress_segment) are exchanged as
+// plain fp32 sums (hook.cpp:125-135) and leave the accumulator untouched.
+#include "engine.hpp"
+
+#include "nccl_dl.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace tagc_b200 {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+namespace {
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// sparsify.cpp:30-31 — same double expression as the reference.
+uint32_t threshold_rank(double theta, uint64_t n) {
+  uint64_t c = static_cast<uint64_t>(std::ceil(theta * static_cast<double>(n) / 100.0));
+  if (c > n) c = n;
+  return static_cast<uint32_t>(c);
+}
+
+std::string seg_name(const LayerSegment& s, uint32_t i) {
+  return s.name.empty() ? "seg" + std::to_string(i) : s.name;
+}
+
+void check_shard(const ShardSpec& sh, uint32_t world) {
+  if (sh.owner >= world) throw InvalidArgument("shard owner rank out of range");
+  for (const LayerSegment& s : sh.segments) {
+    if (s.begin < sh.begin || s.end > sh.end || s.end <= s.begin)
+      throw InvalidArgument("segment outside its shard");
+    if (s.end - s.begin > 0xFFFFFFFFull) throw InvalidArgument("segment longer than 2^32 - 1");
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Workspace
+Workspace::~Workspace() {
+  for (auto& [k, b] : bufs_) cudaFree(b.ptr);
+}
+
+void* Workspace::get(const std::string& name, size_t bytes, bool zero_on_alloc, cudaStream_t s) {
+  bytes = std::max<size_t>(bytes, 16);
+  Buf& b = bufs_[name];
+  if (b.bytes >= bytes) return b.ptr;
+  if (b.ptr) {
+    cuda_check(cudaStreamSynchronize(s), "workspace sync");
+    cudaFree(b.ptr);
+    total_ -= b.bytes;
+    b.ptr = nullptr;
+    b.bytes = 0;
+  }
+  const size_t want = align_up(bytes + bytes / 8, 256);  // headroom against regrowth
+  cuda_check(cudaMalloc(&b.ptr, want), ("workspace alloc " + name).c_str());
+  b.bytes = want;
+  total_ += want;
+  if (zero_on_alloc) cuda_check(cudaMemsetAsync(b.ptr, 0, want, s), "workspace zero");
+  return b.ptr;
+}
+
+// ------------------------------------------------------------------ Engine
+Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int device,
+               void* nccl_comm, void* stream)
+    : cfg_(cfg), world_(world), rank_(rank), device_(device) {
+  if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
+  cfg_.validate_for_world(world);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw CudaError("no CUDA device available (the B200 path has no CPU fallback)");
+  if (device < 0) device_ = 0;
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  if (prop.major < 10)
+    throw CudaError("device " + std::string(prop.name) + " is not sm_100-class");
+  di_.sms = prop.multiProcessorCount;
+  di_.dev = device_;
+  if (stream) {
+    stream_ = static_cast<cudaStream_t>(stream);
+  } else {
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream create");
+    own_stream_ = true;
+  }
+  comm_ = static_cast<ncclComm_t>(nccl_comm);
+  for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event create");
+}
+
+Engine::~Engine() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (own_comm_ && comm_) nccl().CommDestroy(comm_);
+  if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::set_config(const CompressionConfig& cfg) {
+  cfg.validate_for_world(world_);
+  cfg_ = cfg;
+}
+
+void Engine::init_nccl(const uint8_t id[128]) {
+  if (comm_) throw InvalidArgument("context already has an NCCL communicator");
+  ncclUniqueId uid;
+  static_assert(sizeof(uid) == 128, "ncclUniqueId size");
+  std::memcpy(&uid, id, 128);
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  nccl_check(nccl().CommInitRank(&comm_, int(world_), uid, int(rank_)), "ncclCommInitRank");
+  own_comm_ = true;
+}
+
+void Engine::last_timing(float out[4]) const {
+  for (int i = 0; i < 4; ++i) {
+    out[i] = 0.f;
+    if (timing_) cudaEventElapsedTime(&out[i], ev_[i], ev_[i + 1]);
+  }
+}
+
+void Engine::ev_record(int i) {
+  if (timing_) cuda_check(cudaEventRecord(ev_[i], stream_), "event record");
+}
+
+void Engine::upload(const void* host, size_t bytes, void* dev) {
+  if (bytes) cuda_check(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+}
+
+uint32_t* Engine::err_flag() {
+  return static_cast<uint32_t*>(ws_.get("err", 64, true, stream_));
+}
+
+void Engine::fetch_rounds() {
+  uint32_t q[4] = {0, 0, 0, 0};
+  cuda_check(cudaMemcpyAsync(q, ws_.get("qcount", 16), 16, cudaMemcpyDeviceToHost, stream_), "D2H q");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  rounds_[0] = q[2];
+  rounds_[1] = q[3];
+}
+
+void Engine::sync_check() {
+  cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+  uint32_t err = 0;
+  cuda_check(cudaMemcpy(&err, err_flag(), 4, cudaMemcpyDeviceToHost), "D2H err");
+  if (err & 1u) throw InvalidArgument("sparsify: NaN gradient value");
+}
+
+// ------------------------------------------------------------ select/encode
+void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashParams& hp,
+                               bool want_kept, const char*) {
+  const uint32_t n = uint32_t(items.size());
+  if (n == 0) return;
+  bool select = (items[0].flags & kSelect) != 0;
+  uint64_t tiles = 0, samples = 0, cand = 0;
+  for (EncItem& e : items) {
+    if (((e.flags & kSelect) != 0) != select) throw CudaError("mixed select batch");
+    const uint64_t t = (uint64_t(e.n) + kTile - 1) / kTile;
+    e.tile_begin = tiles;
+    tiles += t;
+    e.sample_begin = samples;
+    e.sample_stride = 0;
+    e.sample_tiles = 0;
+    if (select && e.n > kSmallSegment) {
+      const uint64_t stride = std::max<uint64_t>(1, std::min<uint64_t>(8, t / 16));
+      e.sample_stride = uint32_t(stride);
+      e.sample_tiles = uint32_t((t + stride - 1) / stride);
+      samples += e.sample_tiles;
+    }
+    e.cand_off = cand;
+    e.cand_cap = select ? (e.n <= kSmallSegment ? e.n : std::max<uint32_t>(kSmallSegment, e.n / 16)) : 0;
+    cand += e.cand_cap;
+  }
+  auto* d_items = static_cast<EncItem*>(ws_.get("enc_items", n * sizeof(EncItem), false, stream_));
+  upload(items.data(), n * sizeof(EncItem), d_items);
+  auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
+  uint32_t* err = err_flag();
+  cuda_check(cudaMemsetAsync(err, 0, 16, stream_), "err reset");
+  if (select) {
+    auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleBins * 4, true, stream_));
+    auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
+    auto* fine = static_cast<uint32_t*>(ws_.get("fine_hist", size_t(n) * kRadixBins * 4, true, stream_));
+    auto* cd = static_cast<uint32_t*>(ws_.get("cand", cand * 4, false, stream_));
+    auto* sl = static_cast<uint32_t*>(ws_.get("sel_list", size_t(n) * 8192 * 4, false, stream_));
+    launches_ += launch_select(di_, d_items, state, n, tiles, samples, sh, fh, fine, cd, sl, err, stream_);
+  } else if (want_kept) {
+    cuda_check(cudaMemsetAsync(state, 0, n * sizeof(SelState), stream_), "state reset");
+  }
+  ev_record(1);
+  launches_ += launch_encode(di_, d_items, state, n, tiles, hp, err, want_kept ? state : nullptr, w4,
+                             stream_);
+  ev_record(2);
+  cuda_check(cudaGetLastError(), "select/encode launch");
+}
+
+// ------------------------------------------------------------------ decode
+void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved) {
+  const uint32_t n = uint32_t(items.size());
+  dec_stats_.assign(n, DecStats{});
+  if (n == 0) return;
+  uint64_t slots = 0, bm = 0, wt = 0, list = 0;
+  for (DecItem& d : items) {
+    d.slot_base = slots;
+    slots += uint64_t(hp.rows) * d.m;
+    d.bitmap_off = bm;
+    bm += (uint64_t(d.n) + 31) / 32;
+    d.word_tile_begin = wt;
+    wt += (uint64_t(d.n_words) + kDecWordTile - 1) / kDecWordTile;
+    d.list_off = list;
+    list += d.n;
+  }
+  if (slots >= (1ull << 31)) throw CudaError("decode batch exceeds 2^31 sketch buckets");
+  auto* d_items = static_cast<DecItem*>(ws_.get("dec_items", n * sizeof(DecItem), false, stream_));
+  upload(items.data(), n * sizeof(DecItem), d_items);
+  DecodeWork w{};
+  w.items = d_items;
+  w.n_items = n;
+  w.total_word_tiles = wt;
+  w.total_slots = slots;
+  w.slot_state = static_cast<unsigned long long*>(ws_.get("slot_state", slots * 8, false, stream_));
+  w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
+  w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
+  w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
+  w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
+  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 16, false, stream_));
+  w.stats = static_cast<DecStats*>(ws_.get("dec_stats", n * sizeof(DecStats), false, stream_));
+  w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
+                                 : nullptr;
+  cuda_check(cudaMemsetAsync(w.slot_state, 0, slots * 8, stream_), "slot reset");
+  cuda_check(cudaMemsetAsync(w.bitmap, 0, bm * 4, stream_), "bitmap reset");
+  cuda_check(cudaMemsetAsync(w.qcount, 0, 16, stream_), "qcount reset");
+  cuda_check(cudaMemsetAsync(w.stats, 0, n * sizeof(DecStats), stream_), "stats reset");
+  static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
+  if (dbg) {
+    w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));
+    cuda_check(cudaMemsetAsync(w.dbg, 0, 64 * 8, stream_), "dbg reset");
+  }
+  launches_ += launch_decode(di_, w, hp, stream_);
+  cuda_check(cudaGetLastError(), "decode launch");
+  if (dbg) {
+    unsigned long long t[64];
+    cuda_check(cudaMemcpyAsync(t, w.dbg, sizeof(t), cudaMemcpyDeviceToHost, stream_), "dbg");
+    cuda_check(cudaStreamSynchronize(stream_), "dbg sync");
+    std::fprintf(stderr, "[peel]");
+    for (int i = 1; i < 64 && t[i]; ++i) std::fprintf(stderr, " %.1f", (t[i] - t[i - 1]) / 1e3);
+    std::fprintf(stderr, " us\n");
+  }
+}
+
+// ------------------------------------------------------------ simulated world
+void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
+                              float* const* accs, float* out, PeelStats* stats) {
+  if (world == 0) throw InvalidArgument("world size must be at least 1");
+  cfg_.validate_for_world(world);  // hook.cpp:105
+  check_shard(shard, world);
+  launches_ = 0;
+  ev_record(0);
+  const uint32_t w = cfg_.index_width, rows = cfg_.sketch_rows;
+  std::vector<SegPlan> plan;
+  uint64_t NW = 0, SK = 0;
+  for (uint32_t i = 0; i < shard.segments.size(); ++i) {
+    const LayerSegment& s = shard.segments[i];
+    SegPlan p;
+    p.seg = i;
+    p.lo = s.begin - shard.begin;
+    p.len = s.size();
+    p.tag = "shard" + std::to_string(shard.id) + "/" + seg_name(s, i);
+    p.compressed = kind_compressible(s.kind, cfg_.policy, cfg_.include_out_proj) &&
+                   cfg_.ratio > 1 && p.len >= cfg_.min_compress_segment;  // hook.cpp:120-122
+    if (p.compressed) {
+      p.m = sketch_geometry(uint32_t(p.len), cfg_.ratio, rows).buckets_per_row;  // hook.cpp:138
+      p.n_words = words_needed(uint32_t(p.len), w);
+      p.word_off = NW;
+      NW += align_up(p.n_words, 4);
+      p.sk_off = SK;
+      SK += align_up(uint64_t(rows) * p.m, 4);
+    }
+    plan.push_back(p);
+  }
+  const HashParams hp = make_hash_params(cfg_.seed, rows);
+  auto* idx_all = static_cast<uint32_t*>(ws_.get("sim_idx", world * NW * 4, false, stream_));
+  auto* sk_all = static_cast<float*>(ws_.get("sim_sk", world * SK * 4, false, stream_));
+  auto* merged = static_cast<uint32_t*>(ws_.get("sim_merged", NW * 4, false, stream_));
+  auto* summed = static_cast<float*>(ws_.get("sim_summed", SK * 4, false, stream_));
+  // device pointer tables: [grads x world][idx x world][sk x world]
+  std::vector<const void*> ptrs;
+  for (uint32_t r = 0; r < world; ++r) ptrs.push_back(grads[r]);
+  for (uint32_t r = 0; r < world; ++r) ptrs.push_back(idx_all + r * NW);
+  for (uint32_t r = 0; r < world; ++r) ptrs.push_back(sk_all + r * SK);
+  auto* d_ptrs = static_cast<const void**>(ws_.get("sim_ptrs", ptrs.size() * 8, false, stream_));
+  upload(ptrs.data(), ptrs.size() * 8, d_ptrs);
+  if (SK) cuda_check(cudaMemsetAsync(sk_all, 0, world * SK * 4, stream_), "sketch zero");
+
+  std::vector<EncItem> enc;
+  for (uint32_t r = 0; r < world; ++r) {
+    for (const SegPlan& p : plan) {
+      if (!p.compressed) continue;
+      EncItem e{};
+      e.g = grads[r] + p.lo;
+      e.acc = accs[r] + p.lo;
+      e.index = idx_all + r * NW + p.word_off;
+      e.sketch = sk_all + r * SK + p.sk_off;
+      e.n = uint32_t(p.len);
+      e.m = p.m;
+      e.c = threshold_rank(cfg_.theta, p.len);
+      e.flags = (w == 4 ? kWidth4 : 0u) | kHasAcc | kWriteIndex | kWriteSketch | kSelect |
+                ((aligned16(e.g) && aligned16(e.acc)) ? kAligned16 : 0u);
+      enc.push_back(e);
+    }
+  }
+  run_select_encode(enc, w == 4, hp, false, "sim");
+  // exchange: ascending-rank folds (collectives.cpp:127-166)
+  launches_ += launch_rank_sum_u32(reinterpret_cast<const uint32_t* const*>(d_ptrs + world), world,
+                                   merged, NW, stream_);
+  launches_ += launch_rank_sum_f32(reinterpret_cast<const float* const*>(d_ptrs + 2 * world), world,
+                                   summed, SK, stream_);
+  std::vector<RawItem> raw;
+  uint64_t max_raw = 0;
+  for (const SegPlan& p : plan)
+    if (!p.compressed) {
+      raw.push_back(RawItem{out + p.lo, p.len, p.lo});
+      max_raw = std::max(max_raw, p.len);
+    }
+  if (!raw.empty()) {
+    auto* d_raw = static_cast<RawItem*>(ws_.get("sim_raw", raw.size() * sizeof(RawItem), false, stream_));
+    upload(raw.data(), raw.size() * sizeof(RawItem), d_raw);
+    launches_ += launch_raw_sum(d_raw, uint32_t(raw.size()), max_raw,
+                                reinterpret_cast<const float* const*>(d_ptrs), world, stream_);
+  }
+  ev_record(3);
+  std::vector<DecItem> dec;
+  std::vector<DiagItem> diag;
+  uint32_t max_words = 0;
+  for (const SegPlan& p : plan) {
+    if (!p.compressed) continue;
+    DecItem d{};
+    d.words = merged + p.word_off;
+    d.sketch = summed + p.sk_off;
+    d.out = out + p.lo;
+    d.n = uint32_t(p.len);
+    d.m = p.m;
+    d.flags = w == 4 ? kWidth4 : 0u;
+    d.n_words = p.n_words;
+    dec.push_back(d);
+    diag.push_back(DiagItem{merged + p.word_off, p.word_off, uint32_t(p.len), p.n_words, w, 0});
+    max_words = std::max(max_words, p.n_words);
+  }
+  run_decode(dec, hp, false);
+  ev_record(4);
+  unsigned long long* ls = nullptr;
+  if (!diag.empty()) {
+    auto* d_diag = static_cast<DiagItem*>(ws_.get("sim_diag", diag.size() * sizeof(DiagItem), false, stream_));
+    upload(diag.data(), diag.size() * sizeof(DiagItem), d_diag);
+    ls = static_cast<unsigned long long*>(ws_.get("sim_ls", diag.size() * 16, false, stream_));
+    cuda_check(cudaMemsetAsync(ls, 0, diag.size() * 16, stream_), "ls reset");
+    launches_ += launch_index_diag(d_diag, uint32_t(diag.size()), max_words,
+                                   reinterpret_cast<const uint32_t* const*>(d_ptrs + world), world, ls,
+                                   stream_);
+  }
+  cuda_check(cudaGetLastError(), "sim launch");
+  // ledger (hook.cpp:125-166)
+  for (const SegPlan& p : plan) {
+    if (p.compressed) {
+      ledger_.record(CollectiveOp::all_reduce, "index/" + p.tag, p.len * w, p.len);
+      ledger_.record(CollectiveOp::reduce, "sketch/" + p.tag, uint64_t(rows) * p.m * 32, p.len);
+    } else {
+      ledger_.record(CollectiveOp::reduce_scatter, "grad/" + p.tag, p.len * 32, p.len);
+    }
+  }
+  if (stats) {
+    std::vector<unsigned long long> lsh(diag.size() * 2, 0);
+    dec_stats_.resize(dec.size());
+    if (!dec.empty()) {
+      cuda_check(cudaMemcpyAsync(dec_stats_.data(), ws_.get("dec_stats", 16), dec.size() * sizeof(DecStats),
+                                 cudaMemcpyDeviceToHost, stream_), "D2H stats");
+      cuda_check(cudaMemcpyAsync(lsh.data(), ls, lsh.size() * 8, cudaMemcpyDeviceToHost, stream_), "D2H ls");
+    }
+    sync_check();
+    if (!dec.empty()) fetch_rounds();
+    PeelStats st;
+    for (size_t i = 0; i < dec.size(); ++i) {
+      if (dec_stats_[i].overflow) throw CudaError("decode bucket state overflow");
+      st.presence += dec_stats_[i].presence;
+      st.unresolved += dec_stats_[i].unresolved;
+      st.index_lost += lsh[2 * i];
+      st.index_spurious += lsh[2 * i + 1];
+    }
+    st.peeled = st.presence - st.unresolved;
+    st.compressed_segments = dec.size();
+    st.baseline_segments = plan.size() - dec.size();
+    *stats = st;
+  }
+}
+
+void Engine::baseline_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
+                          float* out) {
+  if (world == 0) throw InvalidArgument("world size must be at least 1");
+  check_shard(shard, world);
+  launches_ = 0;
+  auto* d_ptrs = static_cast<const float**>(ws_.get("base_ptrs", world * 8, false, stream_));
+  upload(grads, world * 8, d_ptrs);
+  launches_ += launch_rank_sum_f32(d_ptrs, world, out, shard.size(), stream_);
+  cuda_check(cudaGetLastError(), "baseline launch");
+  ledger_.record(CollectiveOp::reduce_scatter, "grad/shard" + std::to_string(shard.id),
+                 shard.size() * 32, shard.size());
+}
+
+// ------------------------------------------------------------------ NCCL world
+void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
+                           float* out, PeelStats* stats) {
+  cfg_.validate_for_world(world_);
+  for (const ShardSpec& s : shards) check_shard(s, world_);
+  if (world_ > 1 && !comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
+  launches_ = 0;
+  ev_record(0);
+  const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
+  // owner-major block layout
+  std::vector<uint64_t> skc(W, 0), rawc(W, 0), wc(W, 0);
+  std::vector<SegPlan> plan;
+  for (uint32_t si = 0; si < shards.size(); ++si) {
+    const ShardSpec& sh = shards[si];
+    for (uint32_t i = 0; i < sh.segments.size(); ++i) {
+      const LayerSegment& s = sh.segments[i];
+      SegPlan p;
+      p.shard = si;
+      p.seg = i;
+      p.lo = s.begin - sh.begin;
+      p.len = s.size();
+      p.tag = "shard" + std::to_string(sh.id) + "/" + seg_name(s, i);
+      p.compressed = kind_compressible(s.kind, cfg_.policy, cfg_.include_out_proj) &&
+                     cfg_.ratio > 1 && p.len >= cfg_.min_compress_segment;
+      const uint32_t o = sh.owner;
+      if (p.compressed) {
+        p.m = sketch_geometry(uint32_t(p.len), cfg_.ratio, rows).buckets_per_row;
+        p.n_words = words_needed(uint32_t(p.len), w);
+        p.word_off = wc[o];
+        wc[o] += align_up(p.n_words, 4);
+        p.sk_off = skc[o];
+        skc[o] += align_up(uint64_t(rows) * p.m, 4);
+      }
+      plan.push_back(p);
+    }
+  }
+  for (SegPlan& p : plan)
+    if (!p.compressed) {
+      const uint32_t o = shards[p.shard].owner;
+      p.raw_off = skc[o] + rawc[o];
+      rawc[o] += align_up(p.len, 4);
+    }
+  uint64_t Bf = 0, Bu = 0;
+  for (uint32_t o = 0; o < W; ++o) {
+    Bf = std::max(Bf, skc[o] + rawc[o]);
+    Bu = std::max(Bu, wc[o]);
+  }
+  Bf = align_up(std::max<uint64_t>(Bf, 32), 32);
+  Bu = align_up(std::max<uint64_t>(Bu, 32), 32);
+  // owned-shard output offsets
+  std::vector<uint64_t> out_off(shards.size(), ~0ull);
+  uint64_t oc = 0;
+  for (uint32_t si = 0; si < shards.size(); ++si)
+    if (shards[si].owner == rank_) {
+      out_off[si] = oc;
+      oc += shards[si].size();
+    }
+  auto* send_f = static_cast<float*>(ws_.get("nc_send_f", W * Bf * 4, false, stream_));
+  auto* send_u = static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
+  float* recv_f = send_f;
+  uint32_t* recv_u = send_u;
+  if (W > 1) {
+    recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
+    recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
+  }
+  for (uint32_t o = 0; o < W; ++o)
+    if (skc[o]) cuda_check(cudaMemsetAsync(send_f + o * Bf, 0, skc[o] * 4, stream_), "sketch zero");
+  const HashParams hp = make_hash_params(cfg_.seed, rows);
+  std::vector<EncItem> enc;
+  std::vector<CopyItem> pack, unpack;
+  for (const SegPlan& p : plan) {
+    const ShardSpec& sh = shards[p.shard];
+    const uint32_t o = sh.owner;
+    if (p.compressed) {
+      EncItem e{};
+      e.g = grad + sh.begin + p.lo;
+      e.acc = acc + sh.begin + p.lo;
+      e.index = send_u + o * Bu + p.word_off;
+      e.sketch = send_f + o * Bf + p.sk_off;
+      e.n = uint32_t(p.len);
+      e.m = p.m;
+      e.c = threshold_rank(cfg_.theta, p.len);
+      e.flags = (w == 4 ? kWidth4 : 0u) | kHasAcc | kWriteIndex | kWriteSketch | kSelect |
+                ((aligned16(e.g) && aligned16(e.acc)) ? kAligned16 : 0u);
+      enc.push_back(e);
+    } else if (W == 1) {  // no exchange: raw segments go straight to the output
+      unpack.push_back(CopyItem{grad + sh.begin + p.lo, out + out_off[p.shard] + p.lo, p.len, 0});
+    } else {
+      pack.push_back(CopyItem{grad + sh.begin + p.lo, send_f + o * Bf + p.raw_off, p.len, 0});
+      if (o == rank_)
+        unpack.push_back(CopyItem{recv_f + p.raw_off, out + out_off[p.shard] + p.lo, p.len, 0});
+    }
+  }
+  run_select_encode(enc, w == 4, hp, false, "nccl");
+  if (!pack.empty()) {
+    const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
+    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", pack.size() * sizeof(CopyItem), false, stream_));
+    upload(pack.data(), pack.size() * sizeof(CopyItem), d_pack);
+    launches_ += launch_copy_items(di_, d_pack, uint32_t(pack.size()), tt, stream_);
+  }
+  if (W > 1) {
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
+               "ncclReduceScatter f32");
+    nccl_check(nccl().ReduceScatter(send_u, recv_u, Bu, ncclUint32, ncclSum, comm_, stream_),
+               "ncclReduceScatter u32");
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    ledger_.wire_bytes += W * (Bf + Bu) * 4;
+  }
+  ev_record(3);
+  std::vector<DecItem> dec;
+  for (const SegPlan& p : plan) {
+    if (!p.compressed || shards[p.shard].owner != rank_) continue;
+    DecItem d{};
+    d.words = recv_u + p.word_off;
+    d.sketch = recv_f + p.sk_off;
+    d.out = out + out_off[p.shard] + p.lo;
+    d.n = uint32_t(p.len);
+    d.m = p.m;
+    d.flags = w == 4 ? kWidth4 : 0u;
+    d.n_words = p.n_words;
+    dec.push_back(d);
+  }
+  run_decode(dec, hp, false);
+  if (!unpack.empty()) {
+    const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
+    auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
+    upload(unpack.data(), unpack.size() * sizeof(CopyItem), d_un);
+    launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_);
+  }
+  ev_record(4);
+  cuda_check(cudaGetLastError(), "nccl-world launch");
+  uint64_t n_raw_owned = 0;
+  for (const SegPlan& p : plan) {
+    if (p.compressed) {
+      ledger_.record(CollectiveOp::all_reduce, "index/" + p.tag, p.len * w, p.len);
+      ledger_.record(CollectiveOp::reduce, "sketch/" + p.tag, uint64_t(rows) * p.m * 32, p.len);
+    } else {
+      ledger_.record(CollectiveOp::reduce_scatter, "grad/" + p.tag, p.len * 32, p.len);
+      if (shards[p.shard].owner == rank_) ++n_raw_owned;
+    }
+  }
+  if (stats) {
+    dec_stats_.resize(dec.size());
+    if (!dec.empty())
+      cuda_check(cudaMemcpyAsync(dec_stats_.data(), ws_.get("dec_stats", 16), dec.size() * sizeof(DecStats),
+                                 cudaMemcpyDeviceToHost, stream_), "D2H stats");
+    sync_check();
+    if (!dec.empty()) fetch_rounds();
+    PeelStats st;
+    for (const DecStats& d : dec_stats_) {
+      if (d.overflow) throw CudaError("decode bucket state overflow");
+      st.presence += d.presence;
+      st.unresolved += d.unresolved;
+    }
+    st.peeled = st.presence - st.unresolved;
+    // A 4-bit index is exact for W <= 15 (config.cpp:55-58), so no position is
+    // lost or fabricated; the 1-bit diagnostic needs the per-rank supports and
+    // is only computed in the simulated world.
+    st.compressed_segments = dec.size();
+    st.baseline_segments = n_raw_owned;
+    *stats = st;
+  }
+}
+
+void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out) {
+  if (shards.size() != world_) throw InvalidArgument("baseline needs one shard per rank");
+  const uint64_t L = shards[0].size();
+  for (uint32_t i = 0; i < shards.size(); ++i) {
+    if (shards[i].owner != i || shards[i].size() != L || shards[i].begin != shards[0].begin + i * L)
+      throw InvalidArgument("baseline needs equal contiguous shards with shard i owned by rank i");
+  }
+  launches_ = 0;
+  const float* base = grad + shards[0].begin;
+  if (world_ == 1) {
+    cuda_check(cudaMemcpyAsync(out, base, L * 4, cudaMemcpyDeviceToDevice, stream_), "D2D");
+  } else {
+    if (!comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
+    nccl_check(nccl().ReduceScatter(base, out, L, ncclFloat32, ncclSum, comm_, stream_),
+               "ncclReduceScatter baseline");
+    ledger_.wire_bytes += uint64_t(world_) * L * 4;
+  }
+  for (const ShardSpec& s : shards)
+    ledger_.record(CollectiveOp::reduce_scatter, "grad/shard" + std::to_string(s.id), s.size() * 32,
+                   s.size());
+}
+
+// ------------------------------------------------------------------ codec API
+void Engine::sparsify(const float* g, uint32_t n, double theta, float* sparse, float* residual,
+                      float* tau, uint64_t* zero_count) {
+  if (!(theta >= 0.0 && theta <= 100.0))
+    throw InvalidArgument("sparsification threshold must lie in [0, 100]");  // sparsify.cpp:19-20
+  if (n == 0) throw InvalidArgument("sparsify: empty gradient");             // :21
+  launches_ = 0;
+  std::vector<EncItem> it(1);
+  EncItem& e = it[0];
+  e.g = g;
+  e.sparse = sparse;
+  e.residual = residual;
+  e.n = n;
+  e.c = threshold_rank(theta, n);
+  e.flags = kSelect | kWriteSparse | kWriteResidual | (aligned16(g) ? kAligned16 : 0u);
+  const HashParams hp = make_hash_params(0, 1);
+  run_select_encode(it, true, hp, true, "sparsify");
+  SelState st{};
+  cuda_check(cudaMemcpyAsync(&st, ws_.get("sel_state", 16), sizeof(SelState), cudaMemcpyDeviceToHost,
+                             stream_), "D2H state");
+  sync_check();
+  if (tau) std::memcpy(tau, &st.tau_key, 4);
+  if (zero_count) *zero_count = uint64_t(n) - st.kept;
+}
+
+void Engine::index_create(const float* v, uint32_t n, uint32_t width, uint32_t* words) {
+  if (width != 1 && width != 4) throw InvalidArgument("index width must be 1 or 4");
+  if (n == 0) throw InvalidArgument("index needs at least one position");
+  launches_ = 0;
+  std::vector<EncItem> it(1);
+  it[0].g = v;
+  it[0].index = words;
+  it[0].n = n;
+  it[0].flags = kWriteIndex | (width == 4 ? kWidth4 : 0u) | (aligned16(v) ? kAligned16 : 0u);
+  run_select_encode(it, width == 4, make_hash_params(0, 1), false, "index");
+}
+
+void Engine::merge_indices(const uint32_t* const* words, uint32_t world, uint32_t n_words,
+                           uint32_t* out) {
+  if (world == 0) throw InvalidArgument("merge_indices: no inputs");
+  launches_ = 0;
+  auto* d = static_cast<const uint32_t**>(ws_.get("merge_ptrs", world * 8, false, stream_));
+  upload(words, world * 8, d);
+  launches_ += launch_rank_sum_u32(d, world, out, n_words, stream_);
+}
+
+void Engine::index_presence(const uint32_t* words, uint32_t n, uint32_t width, uint32_t* positions,
+                            uint32_t* count) {
+  if (width != 1 && width != 4) throw InvalidArgument("index width must be 1 or 4");
+  if (n == 0) throw InvalidArgument("index needs at least one position");
+  launches_ = 0;
+  const size_t sb = index_presence_scratch_bytes(n, width);
+  void* scratch = ws_.get("presence_scratch", sb, false, stream_);
+  auto* cnt = static_cast<uint32_t*>(ws_.get("presence_count", 4, false, stream_));
+  launches_ += launch_index_presence(words, n, width, positions, cnt, scratch, sb, stream_);
+  if (count) {
+    cuda_check(cudaMemcpyAsync(count, cnt, 4, cudaMemcpyDeviceToHost, stream_), "D2H count");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+  }
+}
+
+void Engine::sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t rows,
+                             uint64_t seed, float* sketch) {
+  if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
+  const SketchGeometry g = sketch_geometry(n, ratio, rows);
+  launches_ = 0;
+  cuda_check(cudaMemsetAsync(sketch, 0, uint64_t(rows) * g.buckets_per_row * 4, stream_), "zero");
+  std::vector<EncItem> it(1);
+  it[0].g = v;
+  it[0].sketch = sketch;
+  it[0].n = n;
+  it[0].m = g.buckets_per_row;
+  it[0].flags = kWriteSketch | (aligned16(v) ? kAligned16 : 0u);
+  run_select_encode(it, true, make_hash_params(seed, rows), false, "compress");
+}
+
+void Engine::add(const float* a, const float* b, float* out, uint64_t n) {
+  launches_ = launch_add(a, b, out, n, stream_);
+}
+
+void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32_t n,
+                                uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
+                                float* values, uint32_t* unresolved, uint32_t* n_unresolved,
+                                double* pf) {
+  if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
+  const SketchGeometry g = sketch_geometry(n, ratio, rows);
+  launches_ = 0;
+  const uint64_t nb = (uint64_t(n) + 31) / 32;
+  auto* bitmap = static_cast<uint32_t*>(ws_.get("peel_presence", nb * 4, false, stream_));
+  auto* sk = static_cast<float*>(ws_.get("peel_sketch", uint64_t(rows) * g.buckets_per_row * 4, false, stream_));
+  uint32_t* err = err_flag();
+  cuda_check(cudaMemsetAsync(err, 0, 4, stream_), "err reset");
+  cuda_check(cudaMemsetAsync(bitmap, 0, nb * 4, stream_), "bitmap zero");
+  cuda_check(cudaMemcpyAsync(sk, sketch, uint64_t(rows) * g.buckets_per_row * 4, cudaMemcpyDeviceToDevice,
+                             stream_), "sketch copy");
+  launches_ += launch_presence_to_bitmap(presence, count, n, bitmap, err, stream_);
+  std::vector<DecItem> d(1);
+  d[0].words = bitmap;
+  d[0].sketch = sk;
+  d[0].out = values;
+  d[0].n = n;
+  d[0].m = g.buckets_per_row;
+  d[0].flags = 0;  // presence bitmap == width-1 index
+  d[0].n_words = uint32_t(nb);
+  const HashParams hp = make_hash_params(seed, rows);
+  run_decode(d, hp, true);
+  DecStats ds{};
+  uint32_t e = 0;
+  cuda_check(cudaMemcpyAsync(&ds, ws_.get("dec_stats", 16), sizeof(ds), cudaMemcpyDeviceToHost, stream_), "D2H");
+  cuda_check(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, stream_), "D2H err");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (e & 1u) throw InvalidArgument("presence position out of range for sketch geometry");
+  if (e & 2u) throw InvalidArgument("presence set contains a duplicate position");
+  if (ds.overflow) throw CudaError("decode bucket state overflow");
+  if (unresolved && ds.unresolved) {
+    auto* un = static_cast<uint32_t*>(ws_.get("unresolved", 16));
+    auto* alt = static_cast<uint32_t*>(ws_.get("unresolved_alt", ds.unresolved * 4, false, stream_));
+    const size_t sb = sort_scratch_bytes(ds.unresolved);
+    void* scratch = ws_.get("sort_scratch", sb, false, stream_);
+    launches_ += launch_sort_u32(un, alt, ds.unresolved, scratch, sb, stream_);
+    cuda_check(cudaMemcpyAsync(unresolved, un, ds.unresolved * 4, cudaMemcpyDeviceToDevice, stream_), "D2D");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+  }
+  if (n_unresolved) *n_unresolved = ds.unresolved;
+  if (pf) *pf = count == 0 ? 1.0 : double(ds.presence - ds.unresolved) / double(ds.presence);
+}
+
+void Engine::estimation_decompress(const uint32_t* presence, uint32_t count, uint32_t n,
+                                   uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
+                                   const uint32_t* targets, uint32_t n_targets, float* out) {
+  if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
+  const SketchGeometry g = sketch_geometry(n, ratio, rows);
+  launches_ = 0;
+  const uint64_t nb = (uint64_t(n) + 31) / 32;
+  auto* bitmap = static_cast<uint32_t*>(ws_.get("peel_presence", nb * 4, false, stream_));
+  uint32_t* err = err_flag();
+  cuda_check(cudaMemsetAsync(err, 0, 4, stream_), "err reset");
+  cuda_check(cudaMemsetAsync(bitmap, 0, nb * 4, stream_), "bitmap zero");
+  launches_ += launch_presence_to_bitmap(presence, count, n, bitmap, err, stream_);
+  launches_ += launch_estimate_targets(targets, n_targets, bitmap, n, g.buckets_per_row, sketch,
+                                       make_hash_params(seed, rows), out, err, stream_);
+  uint32_t e = 0;
+  cuda_check(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, stream_), "D2H err");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (e & 1u) throw InvalidArgument("presence position out of range for sketch geometry");
+  if (e & 4u) throw InvalidArgument("estimation target outside the presence set");
+}
+
+}  // namespace tagc_b200

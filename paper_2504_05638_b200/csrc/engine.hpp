@@ -1,0 +1,134 @@
+// engine.hpp — the B200 exchange engine behind the C-ABI: plans device
+// layouts for a shard list, owns workspaces, enqueues the sm_100a kernels and
+// the NCCL exchange on one stream. C++ mirror of reference hook.cpp:98-200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace tagc_b200 {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void cuda_check(cudaError_t e, const char* what);
+void nccl_check(ncclResult_t r, const char* what);
+
+// Device arena of named, grow-only buffers (memory laid out once per plan and
+// reused across steps).
+class Workspace {
+ public:
+  ~Workspace();
+  void* get(const std::string& name, size_t bytes, bool zero_on_alloc = false,
+            cudaStream_t s = nullptr);
+  uint64_t bytes() const { return total_; }
+
+ private:
+  struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs_;
+  uint64_t total_ = 0;
+};
+
+struct SegPlan {
+  uint32_t shard = 0;        // index into the shard list
+  uint32_t seg = 0;          // index into shard.segments
+  uint64_t lo = 0, len = 0;  // shard-relative offset, length
+  bool compressed = false;
+  uint32_t m = 0, n_words = 0;
+  uint64_t word_off = 0, sk_off = 0, raw_off = 0;  // offsets inside an owner block
+  std::string tag;
+};
+
+struct PlanTotals {
+  uint64_t enc_tiles = 0, enc_samples = 0, cand = 0;
+  uint64_t dec_word_tiles = 0, dec_slots = 0, dec_bitmap_words = 0, dec_list = 0;
+};
+
+class Engine {
+ public:
+  Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int device, void* nccl_comm,
+         void* stream);
+  ~Engine();
+
+  void set_config(const CompressionConfig& cfg);
+  const CompressionConfig& config() const { return cfg_; }
+  cudaStream_t stream() const { return stream_; }
+  TrafficLedger& ledger() { return ledger_; }
+  uint64_t workspace_bytes() const { return ws_.bytes(); }
+  void init_nccl(const uint8_t id[128]);
+  void set_timing(bool on) { timing_ = on; }
+  void last_timing(float out[4]) const;
+  uint64_t last_launches() const { return launches_; }
+  // peel rounds of the last decode that returned stats: {grid rounds, single-CTA tail rounds}
+  void last_peel_rounds(uint32_t out[2]) const { out[0] = rounds_[0]; out[1] = rounds_[1]; }
+
+  // hook.cpp:98-200 with `world` logical ranks on this GPU.
+  void reduce_shard_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
+                        float* const* accs, float* out, PeelStats* stats);
+  // hook.cpp:90-96
+  void baseline_sim(const ShardSpec& shard, uint32_t world, const float* const* grads, float* out);
+  // One process per GPU, NCCL exchange.
+  void reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
+                     float* out, PeelStats* stats);
+  void baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out);
+
+  // Per-stage codec entry points (single vector).
+  void sparsify(const float* g, uint32_t n, double theta, float* sparse, float* residual,
+                float* tau, uint64_t* zero_count);
+  void index_create(const float* v, uint32_t n, uint32_t width, uint32_t* words);
+  void merge_indices(const uint32_t* const* words, uint32_t world, uint32_t n_words, uint32_t* out);
+  void index_presence(const uint32_t* words, uint32_t n, uint32_t width, uint32_t* positions,
+                      uint32_t* count);
+  void sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t rows, uint64_t seed,
+                       float* sketch);
+  void add(const float* a, const float* b, float* out, uint64_t n);
+  void peeling_decompress(const uint32_t* presence, uint32_t count, uint32_t n, uint32_t ratio,
+                          uint32_t rows, uint64_t seed, const float* sketch, float* values,
+                          uint32_t* unresolved, uint32_t* n_unresolved, double* pf);
+  void estimation_decompress(const uint32_t* presence, uint32_t count, uint32_t n, uint32_t ratio,
+                             uint32_t rows, uint64_t seed, const float* sketch,
+                             const uint32_t* targets, uint32_t n_targets, float* out);
+  // Synchronise and surface deferred device errors (NaN input -> invalid).
+  void sync_check();
+
+ private:
+  struct EncBatch;
+  void run_select_encode(std::vector<EncItem>& items, bool w4, const HashParams& hp,
+                         bool want_kept, const char* tag);
+  void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved);
+  void upload(const void* host, size_t bytes, void* dev);
+  void ev_record(int i);
+  uint32_t* err_flag();
+
+  CompressionConfig cfg_;
+  uint32_t world_, rank_;
+  int device_;
+  DevInfo di_;
+  cudaStream_t stream_ = nullptr;
+  bool own_stream_ = false;
+  ncclComm_t comm_ = nullptr;
+  bool own_comm_ = false;
+  Workspace ws_;
+  TrafficLedger ledger_;
+  bool timing_ = false;
+  cudaEvent_t ev_[5] = {};
+  uint64_t launches_ = 0;
+  // host mirrors of the last decode's per-item stats (device -> host)
+  std::vector<DecStats> dec_stats_;
+  uint32_t rounds_[2] = {0, 0};
+  void fetch_rounds();
+};
+
+}  // namespace tagc_b200

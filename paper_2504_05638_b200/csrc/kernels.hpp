@@ -1,0 +1,121 @@
+// kernels.hpp — host launchers for the sm_100a kernels (encode.cu, decode.cu).
+// All launchers enqueue on `stream` and return the number of kernel launches
+// they issued (the engine reports the total as gpu_launches).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace tagc_b200 {
+
+struct DevInfo {
+  int sms = 148;
+  int dev = 0;
+};
+
+// ---------------------------------------------------------------- select
+// Threshold selection for `n_items` items (all with kSelect). Device arrays:
+// items[n_items], state[n_items], sample_hist[n_items * kSampleBins] (zero on
+// entry, left zero), fb_hist[n_items * kRadixBins] (same), cand pool, err flag.
+// total_tiles / total_samples are the host-known sums.
+int launch_select(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                  uint64_t total_tiles, uint64_t total_samples, uint32_t* sample_hist,
+                  uint32_t* fb_hist, uint32_t* fine_hist, uint32_t* cand, uint32_t* sel_list,
+                  uint32_t* err, cudaStream_t stream);
+
+// ---------------------------------------------------------------- encode
+// Split + index + sketch scatter (+ acc / sparse / residual writes).
+int launch_encode(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
+                  uint64_t total_tiles, const HashParams& hp, const uint32_t* err,
+                  SelState* kept_state, bool width4, cudaStream_t stream);
+
+// ------------------------------------------------------- elementwise / sums
+// out[i] = sum_{r<world} in[r][i], ascending rank order (reference rank_sum,
+// kernels.cpp:43-63). in_ptrs: device array of `world` pointers.
+int launch_rank_sum_f32(const float* const* in_ptrs, uint32_t world, float* out, uint64_t n,
+                        cudaStream_t stream);
+// Wrapping u32 word sum (kernels.cpp:65-84).
+int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t* out, uint64_t n,
+                        cudaStream_t stream);
+// out = a + b (sketch_add / apply_accumulator).
+int launch_add(const float* a, const float* b, float* out, uint64_t n, cudaStream_t stream);
+
+// Strided segment copies: dst[i] = src[i] for each item (pack/unpack raw
+// segments around the reduce-scatter).
+struct CopyItem {
+  const float* src;
+  float* dst;
+  uint64_t n;
+  uint64_t tile_begin;  // filled by launch_copy_items' caller via copy_tiles()
+};
+constexpr uint32_t kCopyTile = 4096;
+// Assigns tile_begin; returns the total tile count.
+uint64_t copy_tiles(CopyItem* items, uint32_t n_items);
+int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
+                      cudaStream_t stream);
+
+// Raw (uncompressed) segments in a simulated world: dst[i] = sum_r src_r[i]
+// in ascending rank order. srcs: device array [n_items * world].
+struct RawItem {
+  float* dst;
+  uint64_t n;
+  uint64_t src_off;  // offset added to every rank's base pointer
+};
+int launch_raw_sum(const RawItem* items, uint32_t n_items, uint64_t max_n,
+                   const float* const* rank_bases, uint32_t world, cudaStream_t stream);
+
+// Index diagnostics (hook.cpp:282-294): per decode item, lost/spurious counts
+// from per-rank words (rank_words[r] + word_off) and the merged words.
+struct DiagItem {
+  const uint32_t* merged;
+  uint64_t word_off;  // into each rank's index buffer
+  uint32_t n, n_words, width, pad;
+};
+int launch_index_diag(const DiagItem* items, uint32_t n_items, uint32_t max_words,
+                      const uint32_t* const* rank_words, uint32_t world,
+                      unsigned long long* lost_spurious /* 2 per item */, cudaStream_t stream);
+
+// ---------------------------------------------------------------- decode
+struct DecodeWork {
+  const DecItem* items;
+  uint32_t n_items;
+  uint64_t total_word_tiles;
+  uint64_t total_slots;
+  unsigned long long* slot_state;  // (count << 40) | key_sum, total_slots
+  uint32_t* bitmap;                // recovered bits
+  uint32_t* plist;                 // presence lists
+  uint32_t* queue[2];              // capacity total_slots each
+  uint32_t* qcount;                // [2] + rounds counter
+  DecStats* stats;                 // n_items
+  uint32_t* unresolved;            // optional: per item region at list_off
+  unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
+};
+// Peel + estimate. Zero-fills each item's `out`, rebuilds bucket state from
+// the merged index, peels in synchronous rounds inside one cooperative
+// persistent kernel, and estimates the rest (decode.cpp:53-140 semantics).
+int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
+                  cudaStream_t stream);
+
+// Presence list -> bitmap (width-1 index) with bounds/duplicate checks for the
+// standalone peeling API (decode.cpp:15-20, :89-94). err bit 1 = OOB, 2 = dup.
+int launch_presence_to_bitmap(const uint32_t* presence, uint32_t count, uint32_t n,
+                              uint32_t* bitmap, uint32_t* err, cudaStream_t stream);
+// Median-of-rows estimate for explicit targets (decode.cpp:24-51); err bit 4
+// when a target is outside the presence bitmap.
+int launch_estimate_targets(const uint32_t* targets, uint32_t n_targets, const uint32_t* bitmap,
+                            uint32_t n, uint32_t m, const float* sketch, const HashParams& hp,
+                            float* out, uint32_t* err, cudaStream_t stream);
+// Index::presence: ascending positions with field != 0 (index.cpp:51-57).
+int launch_index_presence(const uint32_t* words, uint32_t n, uint32_t width, uint32_t* positions,
+                          uint32_t* count_dev, void* scratch, size_t scratch_bytes,
+                          cudaStream_t stream);
+size_t index_presence_scratch_bytes(uint32_t n, uint32_t width);
+// Sort a u32 list in place (ascending); scratch from sort_scratch_bytes.
+int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* scratch,
+                    size_t scratch_bytes, cudaStream_t stream);
+size_t sort_scratch_bytes(uint32_t count);
+
+}  // namespace tagc_b200
