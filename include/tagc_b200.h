@@ -211,6 +211,19 @@ int tagc_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shard
  * out is written on the owner rank only. */
 int tagc_reduce_shard(tagc_ctx* ctx, const tagc_shard* shard, const float* grad, float* acc,
                       float* out, tagc_peel_stats* stats);
+/* The owner-major exchange layout tagc_reduce_shards uses on `rank` (pure
+ * host computation; exposed so a foreign transport can reproduce the
+ * exchange). Owner o's f32 block is [o*block_f32, (o+1)*block_f32) of the
+ * send buffer: compressed-segment sketches at sk_off, raw segments at raw_off;
+ * its u32 block [o*block_u32, ...) holds index words at word_off. `out` may be
+ * NULL to query *n_out (one entry per segment, shard order). */
+typedef struct tagc_seg_plan {
+  uint32_t shard, seg, compressed, buckets_per_row, n_words, owner;
+  uint64_t lo, len, word_off, sk_off, raw_off, out_off;
+} tagc_seg_plan;
+int tagc_plan_exchange(const tagc_config* cfg, const tagc_shard* shards, uint32_t n_shards,
+                       uint32_t world_size, uint32_t rank, tagc_seg_plan* out, uint32_t* n_out,
+                       uint64_t* block_f32, uint64_t* block_u32);
 /* Uncompressed comparator: ncclReduceScatter fp32 of the shards (requires
  * n_shards == world_size with shard i owned by rank i, as make_shards(W, W)
  * gives). out: dev, shard size floats. */

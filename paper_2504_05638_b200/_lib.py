@@ -75,6 +75,12 @@ class CommVolume(C.Structure):
                 ("total_bits", C.c_double), ("factor", C.c_double)]
 
 
+class SegPlan(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("shard", "seg", "compressed", "buckets_per_row", "n_words",
+                                          "owner")] + \
+               [(k, C.c_uint64) for k in ("lo", "len", "word_off", "sk_off", "raw_off", "out_off")]
+
+
 class LayerSpecC(C.Structure):
     _fields_ = [("name", C.c_char_p), ("kind", C.c_int32), ("param_count", C.c_uint64)]
 
@@ -119,6 +125,9 @@ SIGNATURES = {
     "tagc_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_reduce_shard": (C.c_int, [VP, C.POINTER(Shard), VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_baseline_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP]),
+    "tagc_plan_exchange": (C.c_int, [C.POINTER(Config), C.POINTER(Shard), U32, U32, U32,
+                                     C.POINTER(SegPlan), C.POINTER(U32), C.POINTER(U64),
+                                     C.POINTER(U64)]),
     "tagc_apply_accumulator": (C.c_int, [VP, VP, VP, VP, U64]),
     "tagc_sparsify": (C.c_int, [VP, VP, U32, C.c_double, VP, VP, C.POINTER(C.c_float),
                                 C.POINTER(U64)]),

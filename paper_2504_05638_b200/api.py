@@ -34,7 +34,7 @@ __all__ = [
     "CompressionConfig", "LayerSpec", "LayerSegment", "ShardSpec", "PeelStats", "Context",
     "make_shards", "kind_compressible", "sketch_geometry", "words_needed", "theta_floor",
     "comm_volume_model", "lhc_comm_volume_model", "TagcError", "TagcInvalidArgument",
-    "device_count",
+    "device_count", "plan_exchange",
 ]
 
 
@@ -198,6 +198,22 @@ def make_shards(layers: Sequence[LayerSpec], shard_count: int, world_size: int) 
         return out
     finally:
         lib.tagc_shard_set_destroy(h)
+
+
+def plan_exchange(cfg: CompressionConfig, shards: Sequence[ShardSpec], world_size: int, rank: int):
+    """Owner-major exchange layout of tagc_reduce_shards on `rank`:
+    (list of per-segment dicts, f32 block size, u32 block size)."""
+    scs = [_ShardC(s) for s in shards]
+    arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+    n = C.c_uint32()
+    bf, bu = C.c_uint64(), C.c_uint64()
+    check(lib.tagc_plan_exchange(C.byref(cfg.c()), arr, len(scs), world_size, rank, None, C.byref(n),
+                                 C.byref(bf), C.byref(bu)), "plan_exchange")
+    segs = (_lib.SegPlan * max(1, n.value))()
+    check(lib.tagc_plan_exchange(C.byref(cfg.c()), arr, len(scs), world_size, rank, segs, C.byref(n),
+                                 C.byref(bf), C.byref(bu)), "plan_exchange")
+    out = [{k: int(getattr(segs[i], k)) for k, _ in _lib.SegPlan._fields_} for i in range(n.value)]
+    return out, int(bf.value), int(bu.value)
 
 
 def _ptr(t) -> int:

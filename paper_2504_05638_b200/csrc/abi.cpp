@@ -301,6 +301,30 @@ int tagc_reduce_shard(tagc_ctx* ctx, const tagc_shard* shard, const float* grad,
   return tagc_reduce_shards(ctx, shard, 1, grad, acc, out, stats);
 }
 
+int tagc_plan_exchange(const tagc_config* cfg, const tagc_shard* shards, uint32_t n_shards,
+                       uint32_t world_size, uint32_t rank, tagc_seg_plan* out, uint32_t* n_out,
+                       uint64_t* block_f32, uint64_t* block_u32) {
+  return guarded([&] {
+    const CompressionConfig c = to_cfg(cfg);
+    c.validate_for_world(world_size);
+    if (rank >= world_size) throw InvalidArgument("rank must be below the world size");
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    const ExchangePlan P = plan_exchange(v, c, world_size, rank);
+    if (n_out) *n_out = uint32_t(P.segs.size());
+    if (block_f32) *block_f32 = P.Bf;
+    if (block_u32) *block_u32 = P.Bu;
+    if (out)
+      for (size_t i = 0; i < P.segs.size(); ++i) {
+        const SegPlan& p = P.segs[i];
+        const uint64_t oo = P.out_off[p.shard];
+        out[i] = tagc_seg_plan{p.shard, p.seg, p.compressed ? 1u : 0u, p.m, p.n_words,
+                               v[p.shard].owner, p.lo, p.len, p.word_off, p.sk_off, p.raw_off,
+                               oo == ~0ull ? ~0ull : oo + p.lo};
+      }
+  });
+}
+
 int tagc_baseline_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
                                 const float* grad, float* out) {
   return guarded([&] {

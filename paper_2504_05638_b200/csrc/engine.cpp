@@ -56,6 +56,61 @@ void check_shard(const ShardSpec& sh, uint32_t world) {
 
 }  // namespace
 
+// ------------------------------------------------------------------ planning
+ExchangePlan plan_exchange(const std::vector<ShardSpec>& shards, const CompressionConfig& cfg,
+                           uint32_t W, uint32_t rank) {
+  const uint32_t w = cfg.index_width, rows = cfg.sketch_rows;
+  ExchangePlan P;
+  P.skc.assign(W, 0);
+  P.rawc.assign(W, 0);
+  P.wc.assign(W, 0);
+  for (uint32_t si = 0; si < shards.size(); ++si) {
+    const ShardSpec& sh = shards[si];
+    if (sh.owner >= W) throw InvalidArgument("shard owner rank out of range");
+    for (uint32_t i = 0; i < sh.segments.size(); ++i) {
+      const LayerSegment& s = sh.segments[i];
+      SegPlan p;
+      p.shard = si;
+      p.seg = i;
+      p.lo = s.begin - sh.begin;
+      p.len = s.size();
+      p.tag = "shard" + std::to_string(sh.id) + "/" + seg_name(s, i);
+      p.compressed = kind_compressible(s.kind, cfg.policy, cfg.include_out_proj) && cfg.ratio > 1 &&
+                     p.len >= cfg.min_compress_segment;  // hook.cpp:120-122
+      const uint32_t o = sh.owner;
+      if (p.compressed) {
+        p.m = sketch_geometry(uint32_t(p.len), cfg.ratio, rows).buckets_per_row;  // hook.cpp:138
+        p.n_words = words_needed(uint32_t(p.len), w);
+        p.word_off = P.wc[o];
+        P.wc[o] += align_up(p.n_words, 4);
+        p.sk_off = P.skc[o];
+        P.skc[o] += align_up(uint64_t(rows) * p.m, 4);
+      }
+      P.segs.push_back(p);
+    }
+  }
+  for (SegPlan& p : P.segs)
+    if (!p.compressed) {
+      const uint32_t o = shards[p.shard].owner;
+      p.raw_off = P.skc[o] + P.rawc[o];
+      P.rawc[o] += align_up(p.len, 4);
+    }
+  for (uint32_t o = 0; o < W; ++o) {
+    P.Bf = std::max(P.Bf, P.skc[o] + P.rawc[o]);
+    P.Bu = std::max(P.Bu, P.wc[o]);
+  }
+  P.Bf = align_up(std::max<uint64_t>(P.Bf, 32), 32);
+  P.Bu = align_up(std::max<uint64_t>(P.Bu, 32), 32);
+  P.out_off.assign(shards.size(), ~0ull);
+  uint64_t oc = 0;
+  for (uint32_t si = 0; si < shards.size(); ++si)
+    if (shards[si].owner == rank) {
+      P.out_off[si] = oc;
+      oc += shards[si].size();
+    }
+  return P;
+}
+
 // ------------------------------------------------------------------ Workspace
 Workspace::~Workspace() {
   for (auto& [k, b] : bufs_) cudaFree(b.ptr);
@@ -432,54 +487,11 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   launches_ = 0;
   ev_record(0);
   const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
-  // owner-major block layout
-  std::vector<uint64_t> skc(W, 0), rawc(W, 0), wc(W, 0);
-  std::vector<SegPlan> plan;
-  for (uint32_t si = 0; si < shards.size(); ++si) {
-    const ShardSpec& sh = shards[si];
-    for (uint32_t i = 0; i < sh.segments.size(); ++i) {
-      const LayerSegment& s = sh.segments[i];
-      SegPlan p;
-      p.shard = si;
-      p.seg = i;
-      p.lo = s.begin - sh.begin;
-      p.len = s.size();
-      p.tag = "shard" + std::to_string(sh.id) + "/" + seg_name(s, i);
-      p.compressed = kind_compressible(s.kind, cfg_.policy, cfg_.include_out_proj) &&
-                     cfg_.ratio > 1 && p.len >= cfg_.min_compress_segment;
-      const uint32_t o = sh.owner;
-      if (p.compressed) {
-        p.m = sketch_geometry(uint32_t(p.len), cfg_.ratio, rows).buckets_per_row;
-        p.n_words = words_needed(uint32_t(p.len), w);
-        p.word_off = wc[o];
-        wc[o] += align_up(p.n_words, 4);
-        p.sk_off = skc[o];
-        skc[o] += align_up(uint64_t(rows) * p.m, 4);
-      }
-      plan.push_back(p);
-    }
-  }
-  for (SegPlan& p : plan)
-    if (!p.compressed) {
-      const uint32_t o = shards[p.shard].owner;
-      p.raw_off = skc[o] + rawc[o];
-      rawc[o] += align_up(p.len, 4);
-    }
-  uint64_t Bf = 0, Bu = 0;
-  for (uint32_t o = 0; o < W; ++o) {
-    Bf = std::max(Bf, skc[o] + rawc[o]);
-    Bu = std::max(Bu, wc[o]);
-  }
-  Bf = align_up(std::max<uint64_t>(Bf, 32), 32);
-  Bu = align_up(std::max<uint64_t>(Bu, 32), 32);
-  // owned-shard output offsets
-  std::vector<uint64_t> out_off(shards.size(), ~0ull);
-  uint64_t oc = 0;
-  for (uint32_t si = 0; si < shards.size(); ++si)
-    if (shards[si].owner == rank_) {
-      out_off[si] = oc;
-      oc += shards[si].size();
-    }
+  const ExchangePlan P = plan_exchange(shards, cfg_, W, rank_);
+  const std::vector<SegPlan>& plan = P.segs;
+  const std::vector<uint64_t>& skc = P.skc;
+  const std::vector<uint64_t>& out_off = P.out_off;
+  const uint64_t Bf = P.Bf, Bu = P.Bu;
   auto* send_f = static_cast<float*>(ws_.get("nc_send_f", W * Bf * 4, false, stream_));
   auto* send_u = static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
   float* recv_f = send_f;

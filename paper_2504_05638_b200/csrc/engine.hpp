@@ -51,6 +51,20 @@ struct SegPlan {
   std::string tag;
 };
 
+// Owner-major exchange layout for one rank (reference hook.cpp:117-166 per
+// segment; the blocks are what one grouped reduce-scatter moves): owner o's
+// float block [o*Bf, (o+1)*Bf) holds the sketches of its compressed segments
+// followed by its raw segments, its u32 block [o*Bu, (o+1)*Bu) the index
+// words.
+struct ExchangePlan {
+  std::vector<SegPlan> segs;
+  std::vector<uint64_t> skc, rawc, wc;  // per-owner sketch / raw / word totals
+  uint64_t Bf = 0, Bu = 0;
+  std::vector<uint64_t> out_off;  // per shard: offset in the owner's output, ~0 if not owned
+};
+ExchangePlan plan_exchange(const std::vector<ShardSpec>& shards, const CompressionConfig& cfg,
+                           uint32_t world, uint32_t rank);
+
 struct PlanTotals {
   uint64_t enc_tiles = 0, enc_samples = 0, cand = 0;
   uint64_t dec_word_tiles = 0, dec_slots = 0, dec_bitmap_words = 0, dec_list = 0;
