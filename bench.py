@@ -110,9 +110,12 @@ def cfg_obj():
 
 
 def algorithmic_bytes(shards, rank, world):
-    """SURVEY.md §8(d) bytes for this rank: encode reads g, acc and writes acc,
-    index (w/8) and sketch zero-fill (4/r) per compressed element plus a
-    24*d scatter RMW (d = kept density, 1 - theta/100); select reads g, acc."""
+    """SURVEY.md §8(d) bytes for this rank's dominant kernel, the fused
+    select + encode pass: per compressed element it reads g and acc (8 B) and
+    writes the residual (4 B) and the packed index (w/8 B), plus a 24*d sketch
+    read-modify-write (d = kept density = 1 - theta/100) and the 1/32 sample
+    pre-pass (8/32 B). The separate select pass of the survey's model (8 B) is
+    gone: selection rides on the same pass."""
     import paper_2504_05638_b200 as tagc
 
     comp = 0
@@ -121,9 +124,8 @@ def algorithmic_bytes(shards, rank, world):
             if tagc.kind_compressible(s.kind, "non_attention_linear", True) and s.size() >= 1024:
                 comp += s.size()
     dens = 1.0 - THETA / 100.0
-    enc = comp * (12.0 + WIDTH / 8.0 + 4.0 / RATIO + 24.0 * dens)
-    sel = comp * 8.0
-    return comp, enc, sel
+    fused = comp * (12.0 + WIDTH / 8.0 + 24.0 * dens + 8.0 / 32.0)
+    return comp, fused
 
 
 def run_b200(args):
@@ -249,12 +251,12 @@ def run_b200(args):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
 
-    comp, enc_bytes, sel_bytes = algorithmic_bytes(shards, rank, world)
+    comp, fused_bytes = algorithmic_bytes(shards, rank, world)
     hbm, peak_kind = peaks()
-    enc_ms = stage_ms[1]
-    achieved = enc_bytes / (enc_ms * 1e-3) / 1e9 if enc_ms > 0 else 0.0
+    fused_ms = stage_ms[0]
+    achieved = fused_bytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else 0.0
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "encode_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "fused_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
@@ -289,16 +291,13 @@ def run_b200(args):
         },
         "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4)},
-        "roofline": {"kernel": "k_encode (split + index + sketch scatter)", "bound": "hbm",
-                     "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
+        "roofline": {"kernel": "k_fused (sample + select + split + index + sketch scatter)",
+                     "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": int(enc_bytes)},
-        "stages_ms": {"select": round(stage_ms[0], 4), "encode": round(stage_ms[1], 4),
+                     "algorithmic_bytes_per_launch": int(fused_bytes),
+                     "timed": "sample+window+fused launches, CUDA events on the context stream"},
+        "stages_ms": {"select_encode": round(stage_ms[0], 4), "finish_select": round(stage_ms[1], 4),
                       "exchange": round(stage_ms[2], 4), "decode": round(stage_ms[3], 4)},
-        "select_roofline": {"achieved": round(sel_bytes / (stage_ms[0] * 1e-3) / 1e9, 1)
-                            if stage_ms[0] > 0 else 0.0, "unit": "GB/s",
-                            "frac": round(sel_bytes / (stage_ms[0] * 1e-3) / 1e9 / hbm, 4)
-                            if stage_ms[0] > 0 else 0.0},
         "uncompressed_rs": {"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
                             "unit": "GB/s", "ms_per_step": round(base_ms, 4)},
         "gpu_launches": int(launches_per_step * args.steps),

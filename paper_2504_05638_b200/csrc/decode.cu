@@ -80,6 +80,12 @@ __device__ __forceinline__ uint32_t present_bits(uint32_t x, bool w4) {
 
 __device__ __forceinline__ float canonical(float v) { return v == 0.0f ? 0.0f : v; }
 
+__device__ __forceinline__ uint32_t warp_sum32(uint32_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -208,6 +214,7 @@ __device__ __forceinline__ void push_slot(bool push, uint32_t s, uint32_t* s_q, 
   if (lane == leader) {
     b = atomicAdd(s_nq, cnt);
     if (b + cnt > kPushStage) {  // stage full: straight to the global frontier
+      if (b < kPushStage) atomicMin(s_nq + 1, b);  // [b, stage) stays unwritten
       direct = 1;
       b = atomicAdd(ncount, cnt);
     }
@@ -225,14 +232,17 @@ __device__ __forceinline__ void flush_pushes(uint32_t* s_q, uint32_t* s_nq, uint
                                              uint32_t* nq, uint32_t* ncount) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t n = min(*s_nq, kPushStage);
+    const uint32_t n = min(min(s_nq[0], kPushStage), s_nq[1]);
     *s_base = n ? atomicAdd(ncount, n) : 0u;
-    *s_nq = n;
+    s_nq[0] = n;
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < *s_nq; i += blockDim.x) nq[*s_base + i] = s_q[i];
+  for (uint32_t i = threadIdx.x; i < s_nq[0]; i += blockDim.x) nq[*s_base + i] = s_q[i];
   __syncthreads();
-  if (threadIdx.x == 0) *s_nq = 0;
+  if (threadIdx.x == 0) {
+    s_nq[0] = 0;
+    s_nq[1] = kPushStage;
+  }
   __syncthreads();
 }
 
@@ -256,6 +266,7 @@ __device__ __forceinline__ void peel_phase1(const DecodeWork& w, const HashParam
     if (atomicOr(word, bit) & bit) continue;  // p already claimed via another row
     __stcg(e.out + p, v);
     q[i] = slot | kWinner;
+    atomicAdd(&w.qcount[4], 1u);
   }
 }
 
@@ -294,9 +305,11 @@ __device__ __forceinline__ void peel_phase2(const DecodeWork& w, const HashParam
       if (win) {
         const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
         s = e.slot_base + local;
-        atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
-        push = st_count(old) == 2u;
+        if (s != slot) {  // the winner's own bucket held only p: leave it
+          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+          push = st_count(old) == 2u;
+        }
       }
       push_slot(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
     }
@@ -309,6 +322,7 @@ __device__ __forceinline__ void peel_phase2(const DecodeWork& w, const HashParam
 // reference's ascending seed order, decode.cpp:96-99).
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
                                               uint64_t start, uint64_t stride) {
+  uint32_t won = 0;
   for (uint32_t it = 0; it < w.n_items; ++it) {
     const DecItem e = w.items[it];
     const uint32_t np = w.stats[it].presence;
@@ -326,23 +340,37 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
       int best = -1;
       uint64_t local = 0;
       float sg = 0.0f;
+      uint32_t shared = 0;  // rows whose bucket holds other positions too
 #pragma unroll
       for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
-        if (r < hp.rows && best < 0 && st_count(st[r]) == 1u) {
+        if (r >= hp.rows) continue;
+        const uint32_t cnt = st_count(st[r]);
+        shared |= uint32_t(cnt >= 2u) << r;
+        if (best < 0 && cnt == 1u) {
           best = int(r);
           local = ls[r];
           sg = dev_sign(hp.row[r], p);
         }
       }
-      if (best < 0) continue;
+      if (best < 0) {
+        w.pinfo[e.list_off + i] = make_uint2(0u, 0u);
+        continue;
+      }
       const float v = canonical(sg * ldcg(e.sketch + local));
       __stcg(e.out + p, v);
       atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+      // phase 2 needs the value and only the rows shared with other positions
+      w.pinfo[e.list_off + i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
+      ++won;
     }
   }
+  won = warp_sum32(won);
+  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
 }
 
-// Round 0 subtraction for every position peeled in round0_phase1.
+// Round 0 subtraction for every position peeled in round0_phase1. Buckets
+// that held only the peeled position are left alone: nothing else reads them
+// (their count drops 1 -> 0 in the reference, decode.cpp:115-121).
 __device__ __forceinline__ void round0_phase2(const DecodeWork& w, const HashParams& hp,
                                               uint64_t start, uint64_t stride, uint32_t* s_q,
                                               uint32_t* s_nq, uint32_t* s_base) {
@@ -354,18 +382,20 @@ __device__ __forceinline__ void round0_phase2(const DecodeWork& w, const HashPar
     const uint32_t np = w.stats[it].presence;
     for (uint64_t base = start - lane; base < np; base += stride) {
       const uint64_t i = base + lane;
-      uint32_t p = 0;
-      bool win = false;
+      uint32_t p = 0, rows = 0;
       float v = 0.0f;
       if (i < np) {
-        p = w.plist[e.list_off + i];
-        win = (ldcg(w.bitmap + e.bitmap_off + (p >> 5)) >> (p & 31)) & 1u;
-        if (win) v = ldcg(e.out + p);
+        const uint2 info = w.pinfo[e.list_off + i];
+        if (info.y & 0x100u) {
+          rows = info.y & 0xFFu;
+          v = __uint_as_float(info.x);
+          p = w.plist[e.list_off + i];
+        }
       }
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
         bool push = false;
         uint64_t s = 0;
-        if (win) {
+        if (rows >> r & 1u) {
           const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
           s = e.slot_base + local;
           atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
@@ -381,8 +411,11 @@ __device__ __forceinline__ void round0_phase2(const DecodeWork& w, const HashPar
 
 __global__ void __launch_bounds__(256) k_peel(DecodeWork w, const HashParams hp) {
   __shared__ uint32_t s_q[kPushStage];
-  __shared__ uint32_t s_nq, s_base;
-  if (threadIdx.x == 0) s_nq = 0;
+  __shared__ uint32_t s_nq[2], s_base;  // [0] reserved, [1] end of the contiguous written prefix
+  if (threadIdx.x == 0) {
+    s_nq[0] = 0;
+    s_nq[1] = kPushStage;
+  }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -393,7 +426,7 @@ __global__ void __launch_bounds__(256) k_peel(DecodeWork w, const HashParams hp)
   PEEL_MARK(mk++);
   grid.sync();
   PEEL_MARK(mk++);
-  round0_phase2(w, hp, gtid, gstride, s_q, &s_nq, &s_base);
+  round0_phase2(w, hp, gtid, gstride, s_q, s_nq, &s_base);
   PEEL_MARK(mk++);
   if (gtid == 0) w.qcount[2] = 1;
   uint32_t cur = 1;
@@ -411,7 +444,7 @@ __global__ void __launch_bounds__(256) k_peel(DecodeWork w, const HashParams hp)
     }
     grid.sync();
     PEEL_MARK(mk++);
-    peel_phase2(w, hp, cur, qlen, gtid, gstride, s_q, &s_nq, &s_base);
+    peel_phase2(w, hp, cur, qlen, gtid, gstride, s_q, s_nq, &s_base);
     PEEL_MARK(mk++);
     cur ^= 1;
   }
@@ -430,15 +463,224 @@ __global__ void __launch_bounds__(256) k_peel(DecodeWork w, const HashParams hp)
     }
     __threadfence();
     __syncthreads();
-    peel_phase2(w, hp, cur, qlen, threadIdx.x, blockDim.x, s_q, &s_nq, &s_base);
+    peel_phase2(w, hp, cur, qlen, threadIdx.x, blockDim.x, s_q, s_nq, &s_base);
     __threadfence();
     PEEL_MARK(mk++);
     cur ^= 1;
   }
 }
 
+// ------------------------------------------------------------------ ordered peel
+// FIFO-order emulation for indices that can hide mass (1-bit merge carries
+// drop positions whose contributions stay in the sketch, so the reference's
+// values depend on its peel order, decode.cpp:96-122). Generation 0 is the
+// position-centric round above: every position peels from its lowest
+// singleton slot, exactly the reference's ascending seed order. Generation
+// g+1 is the queue of slots whose count dropped to one while generation g was
+// processed, ordered as the reference's deque orders it: by the processing
+// order of the peeled position, then by row. Pushes carry that key, the host
+// sorts each generation (cub radix sort), and a position that is a singleton
+// in several queued slots is peeled from the first of them (epoch-tagged
+// atomicMax claims).
+struct OrdPush {
+  unsigned long long* keys;
+  uint32_t* slots;
+  uint32_t* count;
+  unsigned long long* slot_key;  // per slot: (epoch << 36) | max FIFO key of this generation
+  unsigned long long tag;        // epoch << 36 of the generation doing the subtractions
+};
+constexpr unsigned long long kKeyMask = (1ull << 36) - 1ull;
+
+constexpr uint32_t kOrdStage = 2048;
+
+__device__ __forceinline__ void ord_push(bool push, unsigned long long key, uint32_t slot,
+                                         unsigned long long* s_k, uint32_t* s_s, uint32_t* s_n,
+                                         const OrdPush& o) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t mask = __ballot_sync(kFull, push);
+  if (!mask) return;
+  const uint32_t leader = __ffs(mask) - 1, cnt = __popc(mask);
+  uint32_t b = 0, direct = 0;
+  if (lane == leader) {
+    b = atomicAdd(s_n, cnt);
+    if (b + cnt > kOrdStage) {
+      if (b < kOrdStage) atomicMin(s_n + 1, b);  // [b, stage) stays unwritten
+      direct = 1;
+      b = atomicAdd(o.count, cnt);
+    }
+  }
+  b = __shfl_sync(kFull, b, leader);
+  direct = __shfl_sync(kFull, direct, leader);
+  if (push) {
+    const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
+    if (direct) {
+      o.keys[idx] = key;
+      o.slots[idx] = slot;
+    } else {
+      s_k[idx] = key;
+      s_s[idx] = slot;
+    }
+  }
+}
+
+__device__ __forceinline__ void ord_flush(unsigned long long* s_k, uint32_t* s_s, uint32_t* s_n,
+                                          uint32_t* s_b, const OrdPush& o) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t n = min(min(s_n[0], kOrdStage), s_n[1]);
+    *s_b = n ? atomicAdd(o.count, n) : 0u;
+    s_n[0] = n;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < *s_n; i += blockDim.x) {
+    o.keys[*s_b + i] = s_k[i];
+    o.slots[*s_b + i] = s_s[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
+  round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x,
+                uint64_t(gridDim.x) * blockDim.x);
+}
+
+// Generation-0 subtraction; pushes are keyed (winner slot, row).
+__global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams hp, OrdPush o) {
+  __shared__ unsigned long long s_k[kOrdStage];
+  __shared__ uint32_t s_s[kOrdStage];
+  __shared__ uint32_t s_n[2], s_b;  // [0] reserved, [1] end of the contiguous written prefix
+  if (threadIdx.x == 0) {
+    s_n[0] = 0;
+    s_n[1] = kOrdStage;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint32_t it = 0; it < w.n_items; ++it) {
+    const DecItem e = w.items[it];
+    const uint32_t np = w.stats[it].presence;
+    for (uint64_t base = start - lane; base < np; base += stride) {
+      const uint64_t i = base + lane;
+      uint32_t p = 0, rows = 0;
+      float v = 0.0f;
+      unsigned long long wkey = 0;
+      if (i < np) {
+        const uint2 info = w.pinfo[e.list_off + i];
+        if (info.y & 0x100u) {
+          rows = info.y & 0xFFu;
+          v = __uint_as_float(info.x);
+          p = w.plist[e.list_off + i];
+          const uint32_t best = (info.y >> 12) & 0xFu;
+          const uint64_t ws = e.slot_base + uint64_t(best) * e.m + dev_bucket(row_coef(hp, best), p, e.m);
+          wkey = ws * hp.rows;
+        }
+      }
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+        bool push = false;
+        uint64_t s = 0;
+        if (rows >> r & 1u) {
+          const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+          s = e.slot_base + local;
+          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+          // the reference queues a slot when its LAST subtraction of the
+          // generation (in FIFO order) leaves one position: keep the max key
+          atomicMax(o.slot_key + s, o.tag | (wkey + r));
+          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+          push = st_count(old) == 2u;
+        }
+        ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
+      }
+    }
+  }
+  ord_flush(s_k, s_s, s_n, &s_b, o);
+}
+
+__global__ void __launch_bounds__(256) k_ord_keys(unsigned long long* keys, const uint32_t* slots,
+                                                  uint32_t n, const unsigned long long* slot_key) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    keys[j] = slot_key[slots[j]] & kKeyMask;
+}
+
+__global__ void __launch_bounds__(256) k_ord_claim(DecodeWork w, const uint32_t* __restrict__ q,
+                                                   uint32_t qlen, unsigned long long* claim,
+                                                   uint32_t epoch) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < qlen; i += gridDim.x * blockDim.x) {
+    const uint32_t slot = q[i];
+    const unsigned long long st = w.slot_state[slot];
+    if (st_count(st) != 1u) continue;
+    const uint32_t it = find_slot_item(w.items, w.n_items, slot);
+    const uint64_t pos = w.items[it].bitmap_off * 32ull + st_pos(st);
+    atomicMax(claim + pos, (uint64_t(epoch) << 32) | uint64_t(~i));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams hp,
+                                                  const uint32_t* __restrict__ q, uint32_t qlen,
+                                                  const unsigned long long* __restrict__ claim,
+                                                  uint32_t epoch, OrdPush o) {
+  __shared__ unsigned long long s_k[kOrdStage];
+  __shared__ uint32_t s_s[kOrdStage];
+  __shared__ uint32_t s_n[2], s_b;  // [0] reserved, [1] end of the contiguous written prefix
+  if (threadIdx.x == 0) {
+    s_n[0] = 0;
+    s_n[1] = kOrdStage;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t won = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < qlen; base += stride) {
+    const uint32_t i = base + lane;
+    bool win = false;
+    uint32_t slot = 0, p = 0;
+    DecItem e{};
+    float v = 0.0f;
+    if (i < qlen) {
+      slot = q[i];
+      const unsigned long long st = w.slot_state[slot];
+      if (st_count(st) == 1u) {
+        p = st_pos(st);
+        const uint32_t it = find_slot_item(w.items, w.n_items, slot);
+        e = w.items[it];
+        win = claim[e.bitmap_off * 32ull + p] == ((uint64_t(epoch) << 32) | uint64_t(~i));
+        if (win) {
+          const uint64_t local = slot - e.slot_base;
+          const uint32_t row = uint32_t(local / e.m);
+          v = canonical(dev_sign(row_coef(hp, row), p) * e.sketch[local]);  // decode.cpp:110-111
+          e.out[p] = v;
+          atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+          ++won;
+        }
+      }
+    }
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      bool push = false;
+      uint64_t s = 0;
+      if (win) {
+        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        s = e.slot_base + local;
+        if (s != slot) {
+          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+          atomicMax(o.slot_key + s, o.tag | (uint64_t(i) * hp.rows + r));
+          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+          push = st_count(old) == 2u;
+        }
+      }
+      ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
+    }
+  }
+  won = warp_sum32(won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  ord_flush(s_k, s_s, s_n, &s_b, o);
+}
+
 // ------------------------------------------------------------------ estimate
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
+  {  // every present position peeled: nothing to estimate
+    uint64_t total = 0;
+    for (uint32_t it = 0; it < w.n_items; ++it) total += w.stats[it].presence;
+    if (total == w.qcount[4]) return;
+  }
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
@@ -572,6 +814,62 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
   return 3;
+}
+
+int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
+                          const OrderedBuffers& ob, cudaStream_t stream, uint32_t& epoch,
+                          uint32_t* rounds) {
+  if (w.n_items == 0) return 0;
+  int launches = 0;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_build, 256, 0);
+  uint64_t g = uint64_t(std::max(per_sm, 1)) * di.sms;
+  if (w.total_word_tiles < g) g = w.total_word_tiles;
+  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w, hp);
+  const int grid = di.sms * 4;
+  k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
+  ++epoch;
+  OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
+  cudaMemsetAsync(ob.count, 0, 4, stream);
+  k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
+  launches += 3;
+  uint32_t gen = 1;
+  unsigned long long* cur_keys = ob.keys[0];
+  uint32_t* cur_slots = ob.slots[0];
+  for (;;) {
+    uint32_t cnt = 0;
+    cudaMemcpyAsync(&cnt, ob.count, 4, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    if (cnt == 0) break;
+    k_ord_keys<<<grid, 256, 0, stream>>>(cur_keys, cur_slots, cnt, ob.slot_key);
+    cub::DoubleBuffer<unsigned long long> dk(cur_keys, cur_keys == ob.keys[0] ? ob.keys[1] : ob.keys[0]);
+    cub::DoubleBuffer<uint32_t> dv(cur_slots, cur_slots == ob.slots[0] ? ob.slots[1] : ob.slots[0]);
+    size_t tb = ob.scratch_bytes;
+    cub::DeviceRadixSort::SortPairs(ob.scratch, tb, dk, dv, int(cnt), 0, 36, stream);
+    const uint32_t* q = dv.Current();
+    // the next generation's pushes go to the buffers the sort left free
+    ++epoch;
+    OrdPush no{dk.Alternate(), dv.Alternate(), ob.count, ob.slot_key, uint64_t(epoch) << 36};
+    k_ord_claim<<<grid, 256, 0, stream>>>(w, q, cnt, ob.claim, epoch);
+    cudaMemsetAsync(ob.count, 0, 4, stream);
+    k_ord_peel<<<grid, 256, 0, stream>>>(w, hp, q, cnt, ob.claim, epoch, no);
+    cur_keys = dk.Alternate();
+    cur_slots = dv.Alternate();
+    launches += 4;
+    ++gen;
+  }
+  if (rounds) *rounds = gen;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
+  k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
+  return launches + 1;
+}
+
+size_t ordered_sort_scratch_bytes(uint32_t count) {
+  size_t temp = 0;
+  cub::DoubleBuffer<unsigned long long> dk(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> dv(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, int(count), 0, 64);
+  return temp;
 }
 
 int launch_presence_to_bitmap(const uint32_t* presence, uint32_t count, uint32_t n,

@@ -52,19 +52,22 @@ struct EncItem {
   float* sketch;    // rows*m floats
   uint64_t tile_begin;
   uint64_t sample_begin;  // first sample-work id (sample kernel)
-  uint64_t cand_off;      // offset into the candidate key pool
+  uint64_t cand_off;      // offset into the candidate pool (uint2: position, value bits)
+  uint64_t hi_off;        // offset into the speculatively-kept pool (uint2)
   uint32_t n, m, c, flags;
-  uint32_t cand_cap, sample_stride, sample_tiles, pad;
+  uint32_t cand_cap, sample_stride, sample_tiles, hi_cap;
 };
 
 // Select state per item (device; reset by the window kernel every call).
+// status: 0 tau ready, 1 fallback, 3 collect sub-bin, 4 fallback tau ready.
 struct SelState {
-  uint32_t klo, khi;            // candidate window on the 31-bit key
-  uint32_t cnt_zero, cnt_lo;    // keys == 0, 0 < key < klo
-  uint32_t cnt_in, status;      // candidates appended; 0 ok / 1 fallback / 2 NaN
-  uint32_t tau_key, prefix;     // threshold key; fallback radix prefix
-  uint32_t rank, kept;          // fallback residual rank; kept elements (zero_count)
-  uint32_t fshift, pad1;        // fine-bin shift of the window: bin = (key - klo) >> fshift
+  uint32_t klo, khi;          // candidate window on the 31-bit key
+  uint32_t cnt_zero, cnt_lo;  // keys == 0, 0 < key < klo
+  uint32_t cnt_in, cnt_hi;    // window candidates, keys above the window (kept speculatively)
+  uint32_t status, tau_key;
+  uint32_t prefix, rank;      // collect: target sub-bin / rank; fallback: radix prefix / rank
+  uint32_t kept, fshift;      // kept elements (zero_count); fine-bin shift of the window
+  uint32_t n_sel, pad;        // keys gathered from the target sub-bin
 };
 
 // One owner-side decode unit (one compressed segment).

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ item
   __shared__ uint32_t s_lo, s_hi;
   const uint32_t item = blockIdx.x;
   const EncItem e = items[item];
-  uint32_t klo = 1u, khi = 0x7F800000u;
+  uint32_t klo = 1u, khi = 0x7F800000u;  // no sample: every nonzero key is a candidate
   if (e.sample_tiles > 0) {
     uint32_t* h = sample_hist + uint64_t(item) * kSampleBins;
     constexpr int kPer = kSampleBins / 256;
@@ -170,21 +170,36 @@ __global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ item
     const double t = double(e.c > 0 ? e.c - 1 : 0) * s / double(e.n);
     const double delta = 6.0 * sqrt(fmax(s * p * (1.0 - p), 0.0)) + 16.0;
     const double lo = floor(t - delta), hi = ceil(t + delta);
+    // Window edges are interpolated linearly inside the sample bin that holds
+    // the bracketing rank (keys are close to uniform inside a 1/16-octave
+    // bin); the +-6 sigma rank margin absorbs both sampling and
+    // interpolation error, and a miss only costs the exact fallback.
     uint32_t cum = pre;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const uint32_t b = threadIdx.x * kPer + i;
       const double c0 = double(cum), c1 = double(cum + loc[i]);
-      if (lo >= 0.0 && c0 <= lo && lo < c1) s_lo = b;
-      if (hi < s && c0 <= hi && hi < c1) s_hi = b;
+      if (lo >= 0.0 && c0 <= lo && lo < c1) {
+        const double f = (lo - c0) / double(loc[i]);
+        s_lo = (b << kSampleShift) + uint32_t(floor(f * double(1u << kSampleShift)));
+      }
+      if (hi < s && c0 <= hi && hi < c1) {
+        const double f = (hi + 1.0 - c0) / double(loc[i]);
+        s_hi = (b << kSampleShift) + uint32_t(fmin(ceil(f * double(1u << kSampleShift)),
+                                                   double((1u << kSampleShift) - 1u)));
+      }
       cum += loc[i];
     }
     __syncthreads();
-    if (s_lo != 0xFFFFFFFFu) klo = max(1u, s_lo << kSampleShift);
-    if (s_hi != 0xFFFFFFFFu) khi = min(0x7F800000u, ((s_hi + 1u) << kSampleShift) - 1u);
+    if (s_lo != 0xFFFFFFFFu) klo = max(1u, s_lo);
+    if (s_hi != 0xFFFFFFFFu) khi = min(0x7F800000u, s_hi);
     // leave the histogram zeroed for the next call
 #pragma unroll
     for (int i = 0; i < kPer; ++i) h[threadIdx.x * kPer + i] = 0;
+  }
+  if (e.c == 0) {  // tau = 0 without selection: every nonzero key is kept
+    klo = 1u;
+    khi = 0u;
   }
   if (threadIdx.x == 0) {
     SelState st{};
@@ -197,11 +212,11 @@ __global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ item
   }
 }
 
-// --------------------------------------------------------------- count
+// --------------------------------------------------------------- helpers
 // Contiguous tile range of this CTA (persistent grid): consecutive tiles stay
-// in the same item, so per-item shared-memory staging is flushed rarely.
-// (32-bit arithmetic: tile counts stay far below 2^32, and a 64-bit divide
-// would pull a subroutine call into every persistent kernel.)
+// in the same item, so per-item staging is flushed rarely. 32-bit arithmetic:
+// tile counts stay far below 2^32 and a 64-bit divide would pull a subroutine
+// call into every persistent kernel.
 __device__ __forceinline__ void cta_range(uint64_t total, uint64_t& t0, uint64_t& t1) {
   const uint32_t T = uint32_t(total), G = gridDim.x;
   const uint32_t chunk = T / G, extra = T % G, b = blockIdx.x;
@@ -209,22 +224,54 @@ __device__ __forceinline__ void cta_range(uint64_t total, uint64_t& t0, uint64_t
   t1 = t0 + chunk + (b < extra ? 1u : 0u);
 }
 
-constexpr uint32_t kStageKeys = 8192;  // per-CTA candidate staging (flushed at >= 4096)
+constexpr uint32_t kStatusReady = 0, kStatusFallback = 1, kStatusCollect = 3, kStatusFbReady = 4;
 
-// One HBM pass: NaN check (sparsify.cpp:24-28), counts of zero keys and keys
-// below the window, compaction of in-window keys (staged in shared memory and
-// appended with one global atomic per flush) and a 2048-bin histogram of the
-// in-window keys that lets the finalize kernel jump to the right sub-bin.
-__global__ void __launch_bounds__(kTileThreads) k_count(const EncItem* __restrict__ items,
-                                                        SelState* __restrict__ state,
-                                                        uint32_t n_items, uint64_t total_tiles,
-                                                        uint32_t* __restrict__ cand,
-                                                        uint32_t* __restrict__ fine_hist,
-                                                        uint32_t* __restrict__ err) {
-  __shared__ uint32_t s_keys[kStageKeys];
+// Values a fallback pass reads: after k_restore an accumulator holds the
+// combined value g + acc of every element, so it is read alone.
+__device__ __forceinline__ void load_source(const EncItem& e, uint32_t pos, bool restored,
+                                            float (&v)[4]) {
+  if (restored && (e.flags & kHasAcc)) {
+    load_quad_rw(e.acc, pos, e.n, (e.flags & kAligned16) != 0, v);
+  } else {
+    load_combined(e, pos, v);
+  }
+}
+
+__device__ __forceinline__ void scatter_sketch(const EncItem& e, const HashParams& hp, uint32_t p,
+                                               float v) {
+  _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
+    atomicAdd(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m), dev_sign(hp.row[r], p) * v);
+}
+
+// --------------------------------------------------------------- fused pass
+// ONE HBM pass per element does the selection bookkeeping AND a speculative
+// encode (reference sparsify.cpp:18-49 + kernels.cpp:86-107 + index.cpp:32-41
+// + sketch.cpp:37-67). The sampled key window [klo, khi] brackets tau:
+//   key == 0 or key < klo : dropped (residual = v)
+//   key >  khi            : kept   (residual 0, index bit, sketch scatter) and
+//                           logged as (position, value) so a bracket miss can
+//                           restore the accumulator
+//   klo <= key <= khi     : undecided: written as dropped and logged as a
+//                           candidate; k_fixup keeps those with key > tau.
+// Candidates and kept elements are staged per warp in shared memory and
+// appended to global pools with one atomic per 200+ entries.
+constexpr uint32_t kWarpStage = 256;
+
+template <bool kW4>
+__global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __restrict__ items,
+                                                           SelState* __restrict__ state,
+                                                           uint32_t n_items, uint64_t total_tiles,
+                                                           const HashParams hp,
+                                                           uint2* __restrict__ cand,
+                                                           uint2* __restrict__ hi_pool,
+                                                           uint32_t* __restrict__ fine_hist,
+                                                           uint32_t* __restrict__ err) {
+  __shared__ uint2 s_cand[kTileThreads / 32][kWarpStage];
+  __shared__ uint2 s_kept[kTileThreads / 32][kWarpStage];
   __shared__ uint32_t s_hist[kRadixBins];
-  __shared__ uint32_t s_n, s_base, s_zero, s_lo;
-  const uint32_t lane = threadIdx.x & 31;
+  __shared__ uint32_t s_zero, s_lo;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
   uint64_t t0, t1;
   cta_range(total_tiles, t0, t1);
   if (t0 >= t1) return;
@@ -235,65 +282,150 @@ __global__ void __launch_bounds__(kTileThreads) k_count(const EncItem* __restric
     const uint64_t item_end = e.tile_begin + (uint64_t(e.n) + kTile - 1) / kTile;
     const uint64_t tend = item_end < t1 ? item_end : t1;
     const uint32_t klo = state[it].klo, khi = state[it].khi, fshift = state[it].fshift;
+    const bool vec = (e.flags & kAligned16) != 0;
+    const uint32_t n_words = kW4 ? (e.n + 7u) / 8u : (e.n + 31u) / 32u;
     for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) s_hist[i] = 0;
-    if (threadIdx.x == 0) s_n = s_zero = s_lo = 0;
+    if (threadIdx.x == 0) s_zero = s_lo = 0;
     __syncthreads();
-    uint32_t c_zero = 0, c_lo = 0;
-    auto flush_keys = [&]() {
-      __syncthreads();
-      if (threadIdx.x == 0) s_base = s_n ? atomicAdd(&state[it].cnt_in, s_n) : 0u;
-      __syncthreads();
-      const uint32_t nk = s_n, base = s_base, cap = e.cand_cap;
-      uint32_t* cb = cand + e.cand_off;
-      for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x)
-        if (base + i < cap) cb[base + i] = s_keys[i];
-      __syncthreads();
-      if (threadIdx.x == 0) s_n = 0;
-      __syncthreads();
+    uint32_t c_zero = 0, c_lo = 0, wc = 0, wk = 0;
+    // warp-level flushes of the staged candidates / kept elements
+    auto flush_cand = [&]() {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&state[it].cnt_in, wc);
+      base = __shfl_sync(kFull, base, 0);
+      for (uint32_t i = lane; i < wc; i += 32)
+        if (base + i < e.cand_cap) cand[e.cand_off + base + i] = s_cand[warp][i];
+      __syncwarp();
+      wc = 0;
+    };
+    auto flush_kept = [&]() {
+      __syncwarp();
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&state[it].cnt_hi, wk);
+      base = __shfl_sync(kFull, base, 0);
+      for (uint32_t i = lane; i < wk; i += 32) {
+        const uint2 kv = s_kept[warp][i];
+        const float v = __uint_as_float(kv.y);
+        if (e.flags & kWriteSketch) scatter_sketch(e, hp, kv.x, v);
+        if (base + i < e.hi_cap) {
+          hi_pool[e.hi_off + base + i] = kv;
+        } else if (e.flags & kHasAcc) {  // pool full (bracket miss): keep v recoverable
+          e.acc[kv.x] = v;
+        }
+      }
+      __syncwarp();
+      wk = 0;
     };
     for (; tile < tend; ++tile) {
       const uint32_t q0 = uint32_t(tile - e.tile_begin) * (kTile / 4);
+      float v[4][4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (pos < e.n) load_combined(e, pos, v);
+        if (pos < e.n) {
+          load_quad(e.g, pos, e.n, vec, v[k]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t key = mag_key(v[j]);
-          const bool valid = pos + j < e.n;
-          c_zero += valid && key == 0;
-          c_lo += valid && key != 0 && key < klo;
-          nan |= valid && key > 0x7F800000u;
-          const bool in = valid && key >= klo && key <= khi;
-          const uint32_t m = __ballot_sync(kFull, in);
-          if (m) {  // warp-aggregated append into the CTA stage
-            const uint32_t leader = __ffs(m) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&s_n, __popc(m));
-            base = __shfl_sync(kFull, base, leader);
-            if (in) {
-              s_keys[base + __popc(m & ((1u << lane) - 1u))] = key;
-              atomicAdd(&s_hist[(key - klo) >> fshift], 1u);
-            }
+          for (int j = 0; j < 4; ++j) v[k][j] = 0.0f;
+        }
+      }
+      if (e.flags & kHasAcc) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
+          if (pos < e.n) {
+            float a[4];
+            load_quad_rw(e.acc, pos, e.n, vec, a);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[k][j] = v[k][j] + a[j];
           }
         }
       }
-      __syncthreads();
-      if (s_n >= kStageKeys - kTile) flush_keys();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t q = q0 + k * kTileThreads + threadIdx.x;
+        const uint32_t pos = 4u * q;
+        uint32_t nib = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool valid = pos + j < e.n;
+          const uint32_t key = mag_key(v[k][j]);
+          const bool hi = valid && key > khi;
+          const bool in = valid && key >= klo && key <= khi && key != 0;
+          c_zero += valid && key == 0;
+          c_lo += valid && key != 0 && key < klo;
+          nan |= valid && key > 0x7F800000u;
+          nib |= uint32_t(hi) << j;
+          const uint32_t mi = __ballot_sync(kFull, in);
+          if (mi) {
+            if (in) {
+              s_cand[warp][wc + __popc(mi & lt)] = make_uint2(pos + j, __float_as_uint(v[k][j]));
+              atomicAdd(&s_hist[(key - klo) >> fshift], 1u);
+            }
+            wc += __popc(mi);
+            if (wc > kWarpStage - 32) {
+              __syncwarp();
+              flush_cand();
+            }
+          }
+          const uint32_t mk = __ballot_sync(kFull, hi);
+          if (mk) {
+            if (hi) s_kept[warp][wk + __popc(mk & lt)] = make_uint2(pos + j, __float_as_uint(v[k][j]));
+            wk += __popc(mk);
+            if (wk > kWarpStage - 32) flush_kept();
+          }
+        }
+        if (pos < e.n) {
+          if (e.flags & kHasAcc) {
+            float r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+            store_quad(e.acc, pos, e.n, vec, r);
+          }
+          if (e.flags & kWriteResidual) {
+            float r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+            store_quad(e.residual, pos, e.n, false, r);
+          }
+          if (e.flags & kWriteSparse) {
+            float sp[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sp[j] = (nib >> j & 1u) ? v[k][j] : 0.0f;
+            store_quad(e.sparse, pos, e.n, false, sp);
+          }
+        }
+        if (e.flags & kWriteIndex) {
+          if (kW4) {
+            if (q < 2u * n_words) {
+              const uint32_t hw = (nib & 1u) | (nib >> 1 & 1u) << 4 | (nib >> 2 & 1u) << 8 |
+                                  (nib >> 3 & 1u) << 12;
+              reinterpret_cast<uint16_t*>(e.index)[q] = uint16_t(hw);
+            }
+          } else {
+            uint32_t x = nib << (4u * (lane & 7u));
+            x |= __shfl_xor_sync(kFull, x, 1);
+            x |= __shfl_xor_sync(kFull, x, 2);
+            x |= __shfl_xor_sync(kFull, x, 4);
+            if ((lane & 7u) == 0 && q / 8u < n_words) e.index[q / 8u] = x;
+          }
+        }
+      }
     }
-    flush_keys();
-    // counts and fine histogram of this item
+    // item done: drain the warp stages, then the CTA's counts and histogram
+    __syncwarp();
+    if (wc) flush_cand();
+    if (wk) flush_kept();
     c_zero = warp_sum(c_zero);
     c_lo = warp_sum(c_lo);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       if (c_zero) atomicAdd(&s_zero, c_zero);
       if (c_lo) atomicAdd(&s_lo, c_lo);
     }
+    __syncthreads();
     uint32_t* fh = fine_hist + uint64_t(it) * kRadixBins;
     for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x)
       if (s_hist[i]) atomicAdd(fh + i, s_hist[i]);
-    __syncthreads();
     if (threadIdx.x == 0) {
       if (s_zero) atomicAdd(&state[it].cnt_zero, s_zero);
       if (s_lo) atomicAdd(&state[it].cnt_lo, s_lo);
@@ -341,14 +473,12 @@ __host__ __device__ constexpr int digit_bits(int pass) { return pass == 0 ? 11 :
 constexpr uint32_t kFinalKeys = 8192;  // per-item capacity of the target sub-bin list
 
 // --------------------------------------------------------------- finalize
-// (1) k_pick, one CTA per item: the fine histogram names the sub-bin holding
-//     the target rank; (2) k_collect, all SMs: the keys of that sub-bin
-//     (typically tens) are gathered from the candidate pool; (3) k_select,
-//     one CTA per item: exact radix select of the remaining rank in shared
-//     memory. Bit-identical to nth_element (sparsify.cpp:35-36): tau is the
-//     c-th smallest key.
-constexpr uint32_t kStatusCollect = 3;
-
+// (1) k_pick, one CTA per item: checks that tau (the c-th smallest key,
+//     sparsify.cpp:33-37) falls inside the window, so every speculative
+//     decision outside it was right, and names the fine sub-bin holding it;
+// (2) k_collect, all SMs: gathers that sub-bin's keys from the candidates;
+// (3) k_select, one CTA per item: exact radix select in shared memory.
+// Bit-identical to nth_element (sparsify.cpp:35-36).
 __global__ void __launch_bounds__(1024) k_pick(const EncItem* __restrict__ items,
                                                SelState* __restrict__ state,
                                                uint32_t* __restrict__ fine_hist,
@@ -358,52 +488,52 @@ __global__ void __launch_bounds__(1024) k_pick(const EncItem* __restrict__ items
   const EncItem e = items[item];
   const SelState s = state[item];
   uint32_t* fh = fine_hist + uint64_t(item) * kRadixBins;
-  const bool nan = (*err & 1u) != 0;
-  bool done = nan;
-  if (!done && (e.c == 0 || e.c <= s.cnt_zero)) {  // tau = 0 (c == 0, or the rank falls on zeros)
-    if (threadIdx.x == 0) {
-      state[item].tau_key = 0;
-      state[item].status = 0;
-    }
-    done = true;
+  const bool overflow = s.cnt_in > e.cand_cap || s.cnt_hi > e.hi_cap;
+  const uint32_t Z = s.cnt_zero, L = s.cnt_lo, I = s.cnt_in;
+  int action = 0;  // 0 none (NaN), 1 tau = 0, 2 collect, 3 fallback
+  if (!(*err & 1u)) {
+    if (e.c <= Z) action = (L == 0 && !overflow) ? 1 : 3;  // tau = 0: every nonzero key is kept
+    else if (!overflow && Z + L < e.c && e.c <= Z + L + I) action = 2;
+    else action = 3;
   }
-  const uint32_t r = e.c - s.cnt_zero;  // 1-based rank among nonzero keys
-  if (!done && !(s.cnt_lo < r && r <= s.cnt_lo + s.cnt_in && s.cnt_in <= e.cand_cap)) {
-    if (threadIdx.x == 0) {  // bracket missed: full radix select fallback
-      state[item].status = 1;
+  if (action == 2) {
+    find_digit<1024>(fh, kRadixBins, e.c - Z - L - 1, &s_digit, &s_below);
+    if (threadIdx.x == 0) {
+      state[item].status = kStatusCollect;
+      state[item].prefix = s_digit;  // target sub-bin
+      state[item].rank = e.c - Z - L - 1 - s_below;
+      state[item].n_sel = 0;
+    }
+  } else if (threadIdx.x == 0) {
+    if (action == 1) {
+      state[item].tau_key = 0;
+      state[item].status = kStatusReady;
+    } else if (action == 3) {  // bracket missed: restore + full radix select
+      state[item].status = kStatusFallback;
       state[item].prefix = 0;
       state[item].rank = e.c - 1;
       atomicOr(err + 1, 1u);
     }
-    done = true;
   }
-  if (!done) {
-    find_digit<1024>(fh, kRadixBins, r - s.cnt_lo - 1, &s_digit, &s_below);
-    if (threadIdx.x == 0) {
-      state[item].status = kStatusCollect;
-      state[item].prefix = s_digit;  // target sub-bin
-      state[item].rank = r - s.cnt_lo - 1 - s_below;
-      state[item].pad1 = 0;          // collected keys
-    }
-  }
+  __syncthreads();
   for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) fh[i] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_collect(const EncItem* __restrict__ items,
                                                  SelState* __restrict__ state, uint32_t n_items,
-                                                 const uint32_t* __restrict__ cand,
+                                                 const uint2* __restrict__ cand,
                                                  uint32_t* __restrict__ sel_list) {
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
   for (uint32_t it = 0; it < n_items; ++it) {
     const SelState s = state[it];
     if (s.status != kStatusCollect) continue;
-    const uint32_t* ck = cand + items[it].cand_off;
+    const uint2* ck = cand + items[it].cand_off;
     uint32_t* out = sel_list + uint64_t(it) * kFinalKeys;
     for (uint64_t i = gtid; i < s.cnt_in; i += gstride) {
-      const uint32_t key = ck[i];
+      const uint32_t key = ck[i].y & 0x7FFFFFFFu;
       if (((key - s.klo) >> s.fshift) == s.prefix) {
-        const uint32_t idx = atomicAdd(&state[it].pad1, 1u);
+        const uint32_t idx = atomicAdd(&state[it].n_sel, 1u);
         if (idx < kFinalKeys) out[idx] = key;
       }
     }
@@ -412,7 +542,7 @@ __global__ void __launch_bounds__(256) k_collect(const EncItem* __restrict__ ite
 
 __global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ items,
                                                  SelState* __restrict__ state,
-                                                 const uint32_t* __restrict__ cand,
+                                                 const uint2* __restrict__ cand,
                                                  const uint32_t* __restrict__ sel_list) {
   __shared__ uint32_t keys[kFinalKeys];
   __shared__ uint32_t hist[kRadixBins];
@@ -420,9 +550,9 @@ __global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ ite
   const uint32_t item = blockIdx.x;
   const SelState s = state[item];
   if (s.status != kStatusCollect) return;
-  const uint32_t nk = s.pad1;
+  const uint32_t nk = s.n_sel;
   const bool in_smem = nk <= kFinalKeys;
-  const uint32_t* ck = cand + items[item].cand_off;
+  const uint2* ck = cand + items[item].cand_off;
   if (in_smem)
     for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) keys[i] = sel_list[uint64_t(item) * kFinalKeys + i];
   uint32_t rank = s.rank, prefix = 0;
@@ -438,7 +568,7 @@ __global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ ite
       }
     } else {  // massive ties inside one sub-bin: stream the candidates again
       for (uint32_t i = threadIdx.x; i < s.cnt_in; i += blockDim.x) {
-        const uint32_t key = ck[i];
+        const uint32_t key = ck[i].y & 0x7FFFFFFFu;
         if (((key - s.klo) >> s.fshift) == s.prefix && (key >> hs) == (prefix >> hs))
           atomicAdd(&hist[(key >> shift) & ((1u << bits) - 1u)], 1u);
       }
@@ -451,11 +581,78 @@ __global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ ite
   }
   if (threadIdx.x == 0) {
     state[item].tau_key = prefix;
-    state[item].status = 0;
+    state[item].status = kStatusReady;
+  }
+}
+
+// --------------------------------------------------------------- fixup
+// Window candidates with key > tau were written as dropped: make them kept
+// (residual 0, index field set, sketch scatter).
+template <bool kW4>
+__global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items,
+                                               SelState* __restrict__ state, uint32_t n_items,
+                                               const uint2* __restrict__ cand, const HashParams hp,
+                                               const uint32_t* __restrict__ err) {
+  if (err[0]) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint32_t it = 0; it < n_items; ++it) {
+    const SelState s = state[it];
+    if (s.status != kStatusReady) continue;
+    const EncItem e = items[it];
+    const uint32_t cnt = min(s.cnt_in, e.cand_cap);
+    uint32_t kept = 0;
+    for (uint64_t base = gtid - lane; base < cnt; base += gstride) {
+      const uint64_t i = base + lane;
+      if (i < cnt) {
+        const uint2 kv = cand[e.cand_off + i];
+        if ((kv.y & 0x7FFFFFFFu) > s.tau_key) {
+          const uint32_t p = kv.x;
+          const float v = __uint_as_float(kv.y);
+          ++kept;
+          if (e.flags & kHasAcc) e.acc[p] = 0.0f;
+          if (e.flags & kWriteResidual) e.residual[p] = 0.0f;
+          if (e.flags & kWriteSparse) e.sparse[p] = v;
+          if (e.flags & kWriteIndex) {
+            if (kW4) atomicOr(e.index + (p >> 3), 1u << (4u * (p & 7u)));
+            else atomicOr(e.index + (p >> 5), 1u << (p & 31u));
+          }
+          if (e.flags & kWriteSketch) scatter_sketch(e, hp, p, v);
+        }
+      }
+    }
+    kept = warp_sum(kept);
+    if (lane == 0 && kept) atomicAdd(&state[it].kept, kept);
   }
 }
 
 // --------------------------------------------------------------- fallback
+// Bracket missed: put the combined value back into the accumulator of every
+// speculatively kept element, clear the sketch, and rerun an exact radix
+// select + encode for that item only.
+__global__ void __launch_bounds__(256) k_restore(const EncItem* __restrict__ items,
+                                                 SelState* __restrict__ state, uint32_t n_items,
+                                                 const uint2* __restrict__ hi_pool, uint32_t rows,
+                                                 const uint32_t* __restrict__ err) {
+  if (err[0] || !err[1]) return;
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint32_t it = 0; it < n_items; ++it) {
+    if (state[it].status != kStatusFallback) continue;
+    const EncItem e = items[it];
+    if (e.flags & kHasAcc) {
+      const uint32_t cnt = min(state[it].cnt_hi, e.hi_cap);
+      for (uint64_t i = gtid; i < cnt; i += gstride) {
+        const uint2 kv = hi_pool[e.hi_off + i];
+        e.acc[kv.x] = __uint_as_float(kv.y);
+      }
+    }
+    if (e.flags & kWriteSketch)
+      for (uint64_t i = gtid; i < uint64_t(rows) * e.m; i += gstride) e.sketch[i] = 0.0f;
+  }
+}
+
 __global__ void __launch_bounds__(kTileThreads) k_fb_hist(const EncItem* __restrict__ items,
                                                           const SelState* __restrict__ state,
                                                           uint32_t n_items, uint64_t total_tiles,
@@ -466,7 +663,7 @@ __global__ void __launch_bounds__(kTileThreads) k_fb_hist(const EncItem* __restr
   const int shift = digit_shift(pass), bits = digit_bits(pass), hs = shift + bits;
   for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const uint32_t it = find_tile_item(items, n_items, tile);
-    if (state[it].status != 1) continue;  // block-uniform
+    if (state[it].status != kStatusFallback) continue;  // block-uniform
     const EncItem e = items[it];
     const uint32_t prefix = state[it].prefix;
     for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) hist[i] = 0;
@@ -476,7 +673,7 @@ __global__ void __launch_bounds__(kTileThreads) k_fb_hist(const EncItem* __restr
       const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
       if (pos >= e.n) continue;
       float v[4];
-      load_combined(e, pos, v);
+      load_source(e, pos, true, v);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t key = mag_key(v[j]);
@@ -498,7 +695,7 @@ __global__ void __launch_bounds__(512) k_fb_scan(SelState* __restrict__ state,
   __shared__ uint32_t s_digit, s_below;
   if (err[0] || !err[1]) return;
   const uint32_t item = blockIdx.x;
-  if (state[item].status != 1) return;
+  if (state[item].status != kStatusFallback) return;
   uint32_t* h = fb_hist + uint64_t(item) * kRadixBins;
   const uint32_t rank = state[item].rank;
   find_digit<512>(h, 1u << digit_bits(pass), rank, &s_digit, &s_below);
@@ -509,32 +706,30 @@ __global__ void __launch_bounds__(512) k_fb_scan(SelState* __restrict__ state,
     state[item].rank = rank - s_below;
     if (pass == 2) {
       state[item].tau_key = prefix;
-      state[item].status = 0;
+      state[item].status = kStatusFbReady;
+      state[item].kept = 0;
     }
   }
 }
 
-// --------------------------------------------------------------- encode
-// Split (drop iff |v| <= tau: kernels.cpp:95, on the 31-bit key), residual
-// write-back, packed index (field set iff the kept value is nonzero,
-// index.cpp:35) and count-sketch scatter row[h_r(p)] += s_r(p)*v
-// (sketch.cpp:52-53) with fp32 reductions at L2. All 16 elements of a thread
-// are loaded before any is consumed (8 x 16-byte requests in flight per
-// thread); kept elements are staged in shared memory and scattered by the
-// whole CTA, so the rare hash work does not serialise the streaming loop.
+// --------------------------------------------------------------- exact encode
+// Split + index + sketch for a known tau. mode 0: every item, tau = 0
+// (CountSketch::compress / Index::create entry points); mode 1: only items
+// whose selection fell back (status 4), reading the restored values.
 constexpr uint32_t kKeptStage = 1024;  // kept elements staged per tile (overflow: direct)
 
 template <bool kW4>
 __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __restrict__ items,
-                                                         const SelState* __restrict__ state,
-                                                         uint32_t n_items, uint64_t total_tiles,
-                                                         const HashParams hp,
-                                                         const uint32_t* __restrict__ err,
-                                                         SelState* __restrict__ kept_state) {
+                                                            SelState* __restrict__ state,
+                                                            uint32_t n_items, uint64_t total_tiles,
+                                                            const HashParams hp,
+                                                            const uint32_t* __restrict__ err,
+                                                            int mode) {
   __shared__ uint32_t s_pos[kKeptStage];
   __shared__ float s_val[kKeptStage];
   __shared__ uint32_t s_n;
-  if (err && *err) return;  // NaN anywhere: no accumulator is touched
+  if (err && err[0]) return;  // NaN anywhere: nothing more is written
+  if (mode == 1 && !err[1]) return;
   const uint32_t lane = threadIdx.x & 31;
   uint64_t t0, t1;
   cta_range(total_tiles, t0, t1);
@@ -543,8 +738,9 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __res
   uint32_t it = t0 < t1 ? find_tile_item(items, n_items, t0) : 0;
   for (uint64_t tile = t0; tile < t1; ++tile) {
     while (it + 1 < n_items && items[it + 1].tile_begin <= tile) ++it;
+    if (mode == 1 && state[it].status != kStatusFbReady) continue;  // block-uniform
     const EncItem e = items[it];
-    const uint32_t tau = (e.flags & kSelect) ? state[it].tau_key : 0u;
+    const uint32_t tau = mode == 1 ? state[it].tau_key : 0u;
     const bool vec = (e.flags & kAligned16) != 0;
     const uint32_t n_words = kW4 ? (e.n + 7u) / 8u : (e.n + 31u) / 32u;
     const uint32_t q0 = uint32_t(tile - e.tile_begin) * (kTile / 4);
@@ -553,22 +749,10 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __res
     for (int k = 0; k < 4; ++k) {
       const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
       if (pos < e.n) {
-        load_quad(e.g, pos, e.n, vec, v[k]);
+        load_source(e, pos, mode == 1, v[k]);
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[k][j] = 0.0f;
-      }
-    }
-    if (e.flags & kHasAcc) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
-        if (pos < e.n) {
-          float a[4];
-          load_quad_rw(e.acc, pos, e.n, vec, a);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) v[k][j] = v[k][j] + a[j];
-        }
       }
     }
     uint32_t kept = 0;
@@ -609,9 +793,7 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __res
                 s_pos[base + o] = pos + j;
                 s_val[base + o] = v[k][j];
               } else {  // dense tile: scatter directly
-                _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
-                  atomicAdd(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], pos + j, e.m),
-                            dev_sign(hp.row[r], pos + j) * v[k][j]);
+                scatter_sketch(e, hp, pos + j, v[k][j]);
               }
               ++o;
             }
@@ -634,21 +816,12 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __res
         }
       }
     }
-    if (kept_state && (e.flags & kWriteSparse)) {
-      kept = warp_sum(kept);
-      if (lane == 0 && kept) atomicAdd(&kept_state[it].kept, kept);
-    }
+    kept = warp_sum(kept);
+    if (lane == 0 && kept) atomicAdd(&state[it].kept, kept);
     if (e.flags & kWriteSketch) {
       __syncthreads();
       const uint32_t nk = min(s_n, kKeptStage);
-      float* sk = e.sketch;
-      const uint32_t m = e.m;
-      for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) {
-        const uint32_t p = s_pos[i];
-        const float x = s_val[i];
-        _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
-          atomicAdd(sk + uint64_t(r) * m + dev_bucket(hp.row[r], p, m), dev_sign(hp.row[r], p) * x);
-      }
+      for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) scatter_sketch(e, hp, s_pos[i], s_val[i]);
       __syncthreads();
       if (threadIdx.x == 0) s_n = 0;
       __syncthreads();
@@ -773,10 +946,10 @@ int flat_grid(uint64_t n, int threads) {
 
 }  // namespace
 
-int launch_select(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
-                  uint64_t total_tiles, uint64_t total_samples, uint32_t* sample_hist,
-                  uint32_t* fb_hist, uint32_t* fine_hist, uint32_t* cand, uint32_t* sel_list,
-                  uint32_t* err, cudaStream_t stream) {
+int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                        uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
+                        uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand, uint2* hi_pool,
+                        uint32_t* err, cudaStream_t stream) {
   if (n_items == 0) return 0;
   int launches = 0;
   if (total_samples) {
@@ -785,33 +958,53 @@ int launch_select(const DevInfo& di, const EncItem* items, SelState* state, uint
     ++launches;
   }
   k_window<<<n_items, 256, 0, stream>>>(items, state, sample_hist);
-  k_count<<<persistent_grid((const void*)k_count, kTileThreads, di, total_tiles), kTileThreads, 0,
-            stream>>>(items, state, n_items, total_tiles, cand, fine_hist, err);
+  if (w4)
+    k_fused<true><<<persistent_grid((const void*)k_fused<true>, kTileThreads, di, total_tiles),
+                    kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, cand, hi_pool,
+                                               fine_hist, err);
+  else
+    k_fused<false><<<persistent_grid((const void*)k_fused<false>, kTileThreads, di, total_tiles),
+                     kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, cand, hi_pool,
+                                                fine_hist, err);
+  return launches + 2;
+}
+
+int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                         uint64_t total_tiles, const HashParams& hp, bool w4, uint32_t* fine_hist,
+                         uint32_t* fb_hist, uint2* cand, uint2* hi_pool, uint32_t* sel_list,
+                         uint32_t* err, cudaStream_t stream) {
+  if (n_items == 0) return 0;
   k_pick<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, err);
   k_collect<<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, sel_list);
   k_select<<<n_items, 1024, 0, stream>>>(items, state, cand, sel_list);
-  launches += 5;
+  if (w4) k_fixup<true><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
+  else k_fixup<false><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
+  // fallback chain: every kernel exits at once unless some item missed its bracket
+  k_restore<<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, hi_pool, hp.rows, err);
   const int fg = persistent_grid((const void*)k_fb_hist, kTileThreads, di, total_tiles);
   for (int pass = 0; pass < 3; ++pass) {
     k_fb_hist<<<fg, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, fb_hist, pass, err);
     k_fb_scan<<<n_items, 512, 0, stream>>>(state, fb_hist, pass, err);
-    launches += 2;
   }
-  return launches;
+  if (w4)
+    k_encode<true><<<persistent_grid((const void*)k_encode<true>, kTileThreads, di, total_tiles),
+                     kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 1);
+  else
+    k_encode<false><<<persistent_grid((const void*)k_encode<false>, kTileThreads, di, total_tiles),
+                      kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 1);
+  return 13;
 }
 
-int launch_encode(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
-                    uint64_t total_tiles, const HashParams& hp, const uint32_t* err,
-                    SelState* kept_state, bool w4, cudaStream_t stream) {
+int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                        uint64_t total_tiles, const HashParams& hp, const uint32_t* err, bool w4,
+                        cudaStream_t stream) {
   if (n_items == 0) return 0;
   if (w4) {
     const int g = persistent_grid((const void*)k_encode<true>, kTileThreads, di, total_tiles);
-    k_encode<true><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err,
-                                                   kept_state);
+    k_encode<true><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 0);
   } else {
     const int g = persistent_grid((const void*)k_encode<false>, kTileThreads, di, total_tiles);
-    k_encode<false><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err,
-                                                    kept_state);
+    k_encode<false><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 0);
   }
   return 1;
 }

@@ -208,8 +208,8 @@ void Engine::fetch_rounds() {
   uint32_t q[4] = {0, 0, 0, 0};
   cuda_check(cudaMemcpyAsync(q, ws_.get("qcount", 16), 16, cudaMemcpyDeviceToHost, stream_), "D2H q");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
-  rounds_[0] = q[2];
-  rounds_[1] = q[3];
+  rounds_[0] = last_ordered_ ? ordered_gens_ : q[2];
+  rounds_[1] = last_ordered_ ? 0 : q[3];
 }
 
 void Engine::sync_check() {
@@ -225,7 +225,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   const uint32_t n = uint32_t(items.size());
   if (n == 0) return;
   bool select = (items[0].flags & kSelect) != 0;
-  uint64_t tiles = 0, samples = 0, cand = 0;
+  uint64_t tiles = 0, samples = 0, cand = 0, hi = 0;
   for (EncItem& e : items) {
     if (((e.flags & kSelect) != 0) != select) throw CudaError("mixed select batch");
     const uint64_t t = (uint64_t(e.n) + kTile - 1) / kTile;
@@ -243,6 +243,10 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     e.cand_off = cand;
     e.cand_cap = select ? (e.n <= kSmallSegment ? e.n : std::max<uint32_t>(kSmallSegment, e.n / 16)) : 0;
     cand += e.cand_cap;
+    // speculatively kept elements number at most n - c when the bracket holds
+    e.hi_off = hi;
+    e.hi_cap = select ? uint32_t(std::min<uint64_t>(e.n, uint64_t(e.n - e.c) + 1024)) : 0;
+    hi += e.hi_cap;
   }
   auto* d_items = static_cast<EncItem*>(ws_.get("enc_items", n * sizeof(EncItem), false, stream_));
   upload(items.data(), n * sizeof(EncItem), d_items);
@@ -253,21 +257,28 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleBins * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
     auto* fine = static_cast<uint32_t*>(ws_.get("fine_hist", size_t(n) * kRadixBins * 4, true, stream_));
-    auto* cd = static_cast<uint32_t*>(ws_.get("cand", cand * 4, false, stream_));
+    auto* cd = static_cast<uint2*>(ws_.get("cand", cand * 8, false, stream_));
+    auto* hp_pool = static_cast<uint2*>(ws_.get("hi_pool", hi * 8, false, stream_));
     auto* sl = static_cast<uint32_t*>(ws_.get("sel_list", size_t(n) * 8192 * 4, false, stream_));
-    launches_ += launch_select(di_, d_items, state, n, tiles, samples, sh, fh, fine, cd, sl, err, stream_);
-  } else if (want_kept) {
+    launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, sh, fine, cd, hp_pool,
+                                     err, stream_);
+    ev_record(1);
+    launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
+                                      err, stream_);
+    ev_record(2);
+  } else {
     cuda_check(cudaMemsetAsync(state, 0, n * sizeof(SelState), stream_), "state reset");
+    ev_record(1);
+    launches_ += launch_encode_exact(di_, d_items, state, n, tiles, hp, err, w4, stream_);
+    ev_record(2);
   }
-  ev_record(1);
-  launches_ += launch_encode(di_, d_items, state, n, tiles, hp, err, want_kept ? state : nullptr, w4,
-                             stream_);
-  ev_record(2);
+  (void)want_kept;
   cuda_check(cudaGetLastError(), "select/encode launch");
 }
 
 // ------------------------------------------------------------------ decode
-void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved) {
+void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
+                        bool ordered) {
   const uint32_t n = uint32_t(items.size());
   dec_stats_.assign(n, DecStats{});
   if (n == 0) return;
@@ -293,22 +304,42 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.slot_state = static_cast<unsigned long long*>(ws_.get("slot_state", slots * 8, false, stream_));
   w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
+  w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
-  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 16, false, stream_));
+  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 32, false, stream_));
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", n * sizeof(DecStats), false, stream_));
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
   cuda_check(cudaMemsetAsync(w.slot_state, 0, slots * 8, stream_), "slot reset");
   cuda_check(cudaMemsetAsync(w.bitmap, 0, bm * 4, stream_), "bitmap reset");
-  cuda_check(cudaMemsetAsync(w.qcount, 0, 16, stream_), "qcount reset");
+  cuda_check(cudaMemsetAsync(w.qcount, 0, 32, stream_), "qcount reset");
   cuda_check(cudaMemsetAsync(w.stats, 0, n * sizeof(DecStats), stream_), "stats reset");
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {
     w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));
     cuda_check(cudaMemsetAsync(w.dbg, 0, 64 * 8, stream_), "dbg reset");
   }
-  launches_ += launch_decode(di_, w, hp, stream_);
+  last_ordered_ = ordered;
+  if (ordered) {
+    // 1-bit merged index over several ranks: carries can hide positions whose
+    // mass stays in the sketch, so values follow the reference's FIFO order
+    OrderedBuffers ob{};
+    ob.keys[0] = static_cast<unsigned long long*>(ws_.get("ord_k0", slots * 8, false, stream_));
+    ob.keys[1] = static_cast<unsigned long long*>(ws_.get("ord_k1", slots * 8, false, stream_));
+    ob.slots[0] = static_cast<uint32_t*>(ws_.get("ord_s0", slots * 4, false, stream_));
+    ob.slots[1] = static_cast<uint32_t*>(ws_.get("ord_s1", slots * 4, false, stream_));
+    ob.count = static_cast<uint32_t*>(ws_.get("ord_count", 16, false, stream_));
+    ob.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", bm * 32 * 8, true, stream_));
+    ob.slot_key = static_cast<unsigned long long*>(ws_.get("ord_slot_key", slots * 8, true, stream_));
+    ob.scratch_bytes = ordered_sort_scratch_bytes(uint32_t(std::min<uint64_t>(slots, 0x7FFFFFFF)));
+    ob.scratch = ws_.get("ord_scratch", ob.scratch_bytes, false, stream_);
+    uint32_t gens = 0;
+    launches_ += launch_decode_ordered(di_, w, hp, ob, stream_, epoch_, &gens);
+    ordered_gens_ = gens;
+  } else {
+    launches_ += launch_decode(di_, w, hp, stream_);
+  }
   cuda_check(cudaGetLastError(), "decode launch");
   if (dbg) {
     unsigned long long t[64];
@@ -418,7 +449,7 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
     diag.push_back(DiagItem{merged + p.word_off, p.word_off, uint32_t(p.len), p.n_words, w, 0});
     max_words = std::max(max_words, p.n_words);
   }
-  run_decode(dec, hp, false);
+  run_decode(dec, hp, false, w == 1 && world > 1);
   ev_record(4);
   unsigned long long* ls = nullptr;
   if (!diag.empty()) {
@@ -558,7 +589,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     d.n_words = p.n_words;
     dec.push_back(d);
   }
-  run_decode(dec, hp, false);
+  run_decode(dec, hp, false, w == 1 && W > 1);
   if (!unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
@@ -644,7 +675,10 @@ void Engine::sparsify(const float* g, uint32_t n, double theta, float* sparse, f
                              stream_), "D2H state");
   sync_check();
   if (tau) std::memcpy(tau, &st.tau_key, 4);
-  if (zero_count) *zero_count = uint64_t(n) - st.kept;
+  // kept = speculatively kept (above the window) + candidates kept by the
+  // fix-up; after a fallback the exact re-encode counted every kept element.
+  const uint64_t kept = st.status == 4 ? st.kept : uint64_t(st.cnt_hi) + st.kept;
+  if (zero_count) *zero_count = uint64_t(n) - kept;
 }
 
 void Engine::index_create(const float* v, uint32_t n, uint32_t width, uint32_t* words) {
@@ -727,7 +761,7 @@ void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32
   d[0].flags = 0;  // presence bitmap == width-1 index
   d[0].n_words = uint32_t(nb);
   const HashParams hp = make_hash_params(seed, rows);
-  run_decode(d, hp, true);
+  run_decode(d, hp, true, true);  // arbitrary presence/sketch pairs: FIFO-exact order
   DecStats ds{};
   uint32_t e = 0;
   cuda_check(cudaMemcpyAsync(&ds, ws_.get("dec_stats", 16), sizeof(ds), cudaMemcpyDeviceToHost, stream_), "D2H");

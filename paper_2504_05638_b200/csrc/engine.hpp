@@ -121,7 +121,8 @@ class Engine {
   struct EncBatch;
   void run_select_encode(std::vector<EncItem>& items, bool w4, const HashParams& hp,
                          bool want_kept, const char* tag);
-  void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved);
+  void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
+                  bool ordered);
   void upload(const void* host, size_t bytes, void* dev);
   void ev_record(int i);
   uint32_t* err_flag();
@@ -142,6 +143,9 @@ class Engine {
   // host mirrors of the last decode's per-item stats (device -> host)
   std::vector<DecStats> dec_stats_;
   uint32_t rounds_[2] = {0, 0};
+  uint32_t epoch_ = 0;         // ordered-peel claim epochs (monotonic per context)
+  uint32_t ordered_gens_ = 0;  // generations of the last ordered peel
+  bool last_ordered_ = false;
   void fetch_rounds();
 };
 

@@ -16,21 +16,26 @@ struct DevInfo {
   int dev = 0;
 };
 
-// ---------------------------------------------------------------- select
-// Threshold selection for `n_items` items (all with kSelect). Device arrays:
-// items[n_items], state[n_items], sample_hist[n_items * kSampleBins] (zero on
-// entry, left zero), fb_hist[n_items * kRadixBins] (same), cand pool, err flag.
-// total_tiles / total_samples are the host-known sums.
-int launch_select(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
-                  uint64_t total_tiles, uint64_t total_samples, uint32_t* sample_hist,
-                  uint32_t* fb_hist, uint32_t* fine_hist, uint32_t* cand, uint32_t* sel_list,
-                  uint32_t* err, cudaStream_t stream);
-
-// ---------------------------------------------------------------- encode
-// Split + index + sketch scatter (+ acc / sparse / residual writes).
-int launch_encode(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
-                  uint64_t total_tiles, const HashParams& hp, const uint32_t* err,
-                  SelState* kept_state, bool width4, cudaStream_t stream);
+// ---------------------------------------------------------------- select + encode
+// Speculative single-pass sparsify + encode for `n_items` items (all with
+// kSelect): sample -> window -> fused pass. Device scratch: sample_hist
+// [n_items * kSampleBins] and fine_hist [n_items * kRadixBins] (zero on entry,
+// left zero), cand / hi_pool (uint2 pools at each item's cand_off / hi_off),
+// err[4] (err[0] NaN, err[1] fallback needed).
+int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                        uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
+                        uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand, uint2* hi_pool,
+                        uint32_t* err, cudaStream_t stream);
+// Exact tau from the window candidates, fix-up of the candidates, and the
+// (normally idle) restore + radix-select + re-encode fallback chain.
+int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                         uint64_t total_tiles, const HashParams& hp, bool w4, uint32_t* fine_hist,
+                         uint32_t* fb_hist, uint2* cand, uint2* hi_pool, uint32_t* sel_list,
+                         uint32_t* err, cudaStream_t stream);
+// tau = 0 encode (CountSketch::compress / Index::create entry points).
+int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
+                        uint64_t total_tiles, const HashParams& hp, const uint32_t* err, bool w4,
+                        cudaStream_t stream);
 
 // ------------------------------------------------------- elementwise / sums
 // out[i] = sum_{r<world} in[r][i], ascending rank order (reference rank_sum,
@@ -87,8 +92,9 @@ struct DecodeWork {
   unsigned long long* slot_state;  // (count << 40) | key_sum, total_slots
   uint32_t* bitmap;                // recovered bits
   uint32_t* plist;                 // presence lists
+  uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
   uint32_t* queue[2];              // capacity total_slots each
-  uint32_t* qcount;                // [2] + rounds counter
+  uint32_t* qcount;                // [0..1] frontier sizes, [2] rounds, [3] tail rounds, [4] peeled
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
@@ -98,6 +104,23 @@ struct DecodeWork {
 // persistent kernel, and estimates the rest (decode.cpp:53-140 semantics).
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
                   cudaStream_t stream);
+
+// FIFO-order peel (see decode.cu): host-driven generations, one sort each.
+// claim: u64 per position slot (bitmap_off * 32 + p), zero-initialised once;
+// epoch is advanced per generation and persists across calls.
+struct OrderedBuffers {
+  unsigned long long* keys[2];
+  uint32_t* slots[2];  // capacity total_slots each
+  uint32_t* count;
+  unsigned long long* claim;
+  unsigned long long* slot_key;  // u64 per slot, zero-initialised once
+  void* scratch;
+  size_t scratch_bytes;
+};
+int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
+                          const OrderedBuffers& ob, cudaStream_t stream, uint32_t& epoch,
+                          uint32_t* rounds);
+size_t ordered_sort_scratch_bytes(uint32_t count);
 
 // Presence list -> bitmap (width-1 index) with bounds/duplicate checks for the
 // standalone peeling API (decode.cpp:15-20, :89-94). err bit 1 = OOB, 2 = dup.
