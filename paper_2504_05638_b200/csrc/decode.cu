@@ -172,8 +172,10 @@ __global__ void __launch_bounds__(256) k_build(DecodeWork w, const HashParams hp
         if (li < kStage) {
           s_list[li] = p;
         } else {
-          const uint32_t gi = atomicAdd(&w.stats[it].presence, 1u);
-          w.plist[e.list_off + gi] = p;
+          atomicAdd(&w.stats[it].presence, 1u);
+          const uint32_t gi = atomicAdd(&w.qcount[5], 1u);
+          w.plist[gi] = p;
+          w.pitem[gi] = it;
         }
         _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
           const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
@@ -186,11 +188,15 @@ __global__ void __launch_bounds__(256) k_build(DecodeWork w, const HashParams hp
     if (item_ends || s_nl >= kStage / 2) {  // flush the staged presence list
       if (threadIdx.x == 0) {
         const uint32_t nl = min(s_nl, kStage);
-        s_bl = nl ? atomicAdd(&w.stats[it].presence, nl) : 0;
+        if (nl) atomicAdd(&w.stats[it].presence, nl);
+        s_bl = nl ? atomicAdd(&w.qcount[5], nl) : 0;
         s_nl = nl;
       }
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < s_nl; i += blockDim.x) w.plist[e.list_off + s_bl + i] = s_list[i];
+      for (uint32_t i = threadIdx.x; i < s_nl; i += blockDim.x) {
+        w.plist[s_bl + i] = s_list[i];
+        w.pitem[s_bl + i] = it;
+      }
       __syncthreads();
       if (threadIdx.x == 0) s_nl = 0;
       __syncthreads();
@@ -323,46 +329,44 @@ __device__ __forceinline__ void peel_phase2(const DecodeWork& w, const HashParam
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
                                               uint64_t start, uint64_t stride) {
   uint32_t won = 0;
-  for (uint32_t it = 0; it < w.n_items; ++it) {
-    const DecItem e = w.items[it];
-    const uint32_t np = w.stats[it].presence;
-    for (uint64_t i = start; i < np; i += stride) {
-      const uint32_t p = w.plist[e.list_off + i];
-      uint64_t ls[kMaxRows];
-      unsigned long long st[kMaxRows];
+  const uint32_t total = ldcg(&w.qcount[5]);  // flat presence list (all items)
+  for (uint64_t i = start; i < total; i += stride) {
+    const uint32_t p = w.plist[i];
+    const DecItem e = w.items[w.pitem[i]];
+    uint64_t ls[kMaxRows];
+    unsigned long long st[kMaxRows];
 #pragma unroll
-      for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
-        if (r < hp.rows) {  // issue every row's load before inspecting any
-          ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-          st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
-        }
+    for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
+      if (r < hp.rows) {  // issue every row's load before inspecting any
+        ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
       }
-      int best = -1;
-      uint64_t local = 0;
-      float sg = 0.0f;
-      uint32_t shared = 0;  // rows whose bucket holds other positions too
-#pragma unroll
-      for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
-        if (r >= hp.rows) continue;
-        const uint32_t cnt = st_count(st[r]);
-        shared |= uint32_t(cnt >= 2u) << r;
-        if (best < 0 && cnt == 1u) {
-          best = int(r);
-          local = ls[r];
-          sg = dev_sign(hp.row[r], p);
-        }
-      }
-      if (best < 0) {
-        w.pinfo[e.list_off + i] = make_uint2(0u, 0u);
-        continue;
-      }
-      const float v = canonical(sg * ldcg(e.sketch + local));
-      __stcg(e.out + p, v);
-      atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
-      // phase 2 needs the value and only the rows shared with other positions
-      w.pinfo[e.list_off + i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
-      ++won;
     }
+    int best = -1;
+    uint64_t local = 0;
+    float sg = 0.0f;
+    uint32_t shared = 0;  // rows whose bucket holds other positions too
+#pragma unroll
+    for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
+      if (r >= hp.rows) continue;
+      const uint32_t cnt = st_count(st[r]);
+      shared |= uint32_t(cnt >= 2u) << r;
+      if (best < 0 && cnt == 1u) {
+        best = int(r);
+        local = ls[r];
+        sg = dev_sign(hp.row[r], p);
+      }
+    }
+    if (best < 0) {
+      w.pinfo[i] = make_uint2(0u, 0u);
+      continue;
+    }
+    const float v = canonical(sg * ldcg(e.sketch + local));
+    __stcg(e.out + p, v);
+    atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+    // phase 2 needs the value and only the rows shared with other positions
+    w.pinfo[i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
+    ++won;
   }
   won = warp_sum32(won);
   if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
@@ -377,33 +381,32 @@ __device__ __forceinline__ void round0_phase2(const DecodeWork& w, const HashPar
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* nq = w.queue[1];
   uint32_t* ncount = &w.qcount[1];
-  for (uint32_t it = 0; it < w.n_items; ++it) {
-    const DecItem e = w.items[it];
-    const uint32_t np = w.stats[it].presence;
-    for (uint64_t base = start - lane; base < np; base += stride) {
-      const uint64_t i = base + lane;
-      uint32_t p = 0, rows = 0;
-      float v = 0.0f;
-      if (i < np) {
-        const uint2 info = w.pinfo[e.list_off + i];
-        if (info.y & 0x100u) {
-          rows = info.y & 0xFFu;
-          v = __uint_as_float(info.x);
-          p = w.plist[e.list_off + i];
-        }
+  const uint32_t total = ldcg(&w.qcount[5]);
+  for (uint64_t base = start - lane; base < total; base += stride) {
+    const uint64_t i = base + lane;
+    uint32_t p = 0, rows = 0;
+    float v = 0.0f;
+    DecItem e{};
+    if (i < total) {
+      const uint2 info = w.pinfo[i];
+      if (info.y & 0x100u) {
+        rows = info.y & 0xFFu;
+        v = __uint_as_float(info.x);
+        p = w.plist[i];
+        e = w.items[w.pitem[i]];
       }
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-        bool push = false;
-        uint64_t s = 0;
-        if (rows >> r & 1u) {
-          const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-          s = e.slot_base + local;
-          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
-          push = st_count(old) == 2u;
-        }
-        push_slot(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
+    }
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      bool push = false;
+      uint64_t s = 0;
+      if (rows >> r & 1u) {
+        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        s = e.slot_base + local;
+        atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+        push = st_count(old) == 2u;
       }
+      push_slot(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
     }
   }
   flush_pushes(s_q, s_nq, s_base, nq, ncount);
@@ -556,40 +559,39 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint32_t it = 0; it < w.n_items; ++it) {
-    const DecItem e = w.items[it];
-    const uint32_t np = w.stats[it].presence;
-    for (uint64_t base = start - lane; base < np; base += stride) {
-      const uint64_t i = base + lane;
-      uint32_t p = 0, rows = 0;
-      float v = 0.0f;
-      unsigned long long wkey = 0;
-      if (i < np) {
-        const uint2 info = w.pinfo[e.list_off + i];
-        if (info.y & 0x100u) {
-          rows = info.y & 0xFFu;
-          v = __uint_as_float(info.x);
-          p = w.plist[e.list_off + i];
-          const uint32_t best = (info.y >> 12) & 0xFu;
-          const uint64_t ws = e.slot_base + uint64_t(best) * e.m + dev_bucket(row_coef(hp, best), p, e.m);
-          wkey = ws * hp.rows;
-        }
+  const uint32_t total = w.qcount[5];
+  for (uint64_t base = start - lane; base < total; base += stride) {
+    const uint64_t i = base + lane;
+    uint32_t p = 0, rows = 0;
+    float v = 0.0f;
+    unsigned long long wkey = 0;
+    DecItem e{};
+    if (i < total) {
+      const uint2 info = w.pinfo[i];
+      if (info.y & 0x100u) {
+        rows = info.y & 0xFFu;
+        v = __uint_as_float(info.x);
+        p = w.plist[i];
+        e = w.items[w.pitem[i]];
+        const uint32_t best = (info.y >> 12) & 0xFu;
+        const uint64_t ws = e.slot_base + uint64_t(best) * e.m + dev_bucket(row_coef(hp, best), p, e.m);
+        wkey = ws * hp.rows;
       }
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-        bool push = false;
-        uint64_t s = 0;
-        if (rows >> r & 1u) {
-          const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-          s = e.slot_base + local;
-          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-          // the reference queues a slot when its LAST subtraction of the
-          // generation (in FIFO order) leaves one position: keep the max key
-          atomicMax(o.slot_key + s, o.tag | (wkey + r));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
-          push = st_count(old) == 2u;
-        }
-        ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
+    }
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      bool push = false;
+      uint64_t s = 0;
+      if (rows >> r & 1u) {
+        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        s = e.slot_base + local;
+        atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+        // the reference queues a slot when its LAST subtraction of the
+        // generation (in FIFO order) leaves one position: keep the max key
+        atomicMax(o.slot_key + s, o.tag | (wkey + r));
+        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+        push = st_count(old) == 2u;
       }
+      ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
     }
   }
   ord_flush(s_k, s_s, s_n, &s_b, o);
@@ -676,41 +678,31 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
 
 // ------------------------------------------------------------------ estimate
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
-  {  // every present position peeled: nothing to estimate
-    uint64_t total = 0;
-    for (uint32_t it = 0; it < w.n_items; ++it) total += w.stats[it].presence;
-    if (total == w.qcount[4]) return;
-  }
+  const uint32_t total = w.qcount[5];
+  if (total == w.qcount[4]) return;  // every present position peeled: nothing to estimate
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint32_t it = 0; it < w.n_items; ++it) {
-    const DecItem e = w.items[it];
-    const uint32_t np = w.stats[it].presence;
-    for (uint64_t base = gtid - lane; base < np; base += gstride) {
-      const uint64_t i = base + lane;
-      bool unres = false;
-      uint32_t p = 0;
-      if (i < np) {
-        p = w.plist[e.list_off + i];
-        unres = !(w.bitmap[e.bitmap_off + (p >> 5)] >> (p & 31) & 1u);
-        if (unres) {  // decode.cpp:130-138 / :43-47
-          float est[kMaxRows];
+  for (uint64_t base = gtid - lane; base < total; base += gstride) {
+    const uint64_t i = base + lane;
+    bool unres = false;
+    uint32_t p = 0, it = 0;
+    DecItem e{};
+    if (i < total) {
+      p = w.plist[i];
+      it = w.pitem[i];
+      e = w.items[it];
+      unres = !(w.bitmap[e.bitmap_off + (p >> 5)] >> (p & 31) & 1u);
+      if (unres) {  // decode.cpp:130-138 / :43-47
+        float est[kMaxRows];
 #pragma unroll
-          for (uint32_t r = 0; r < kMaxRows; ++r) {
-            if (r >= hp.rows) break;
-            est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m)];
-          }
-          e.out[p] = canonical(median_rows(est, hp.rows));
+        for (uint32_t r = 0; r < kMaxRows; ++r) {
+          if (r >= hp.rows) break;
+          est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m)];
         }
-      }
-      const uint32_t mask = __ballot_sync(kFull, unres);
-      if (mask) {
-        uint32_t b = 0;
-        const uint32_t leader = __ffs(mask) - 1;
-        if (lane == leader) b = atomicAdd(&w.stats[it].unresolved, __popc(mask));
-        b = __shfl_sync(kFull, b, leader);
-        if (unres && w.unresolved) w.unresolved[e.list_off + b + __popc(mask & ((1u << lane) - 1u))] = p;
+        e.out[p] = canonical(median_rows(est, hp.rows));
+        const uint32_t b = atomicAdd(&w.stats[it].unresolved, 1u);
+        if (w.unresolved) w.unresolved[e.list_off + b] = p;
       }
     }
   }

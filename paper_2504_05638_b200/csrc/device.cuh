@@ -20,6 +20,7 @@ constexpr uint32_t kSampleBins = 4096;  // top 12 bits of the 31-bit magnitude k
 constexpr uint32_t kSampleShift = 19;
 constexpr uint32_t kRadixBins = 2048;   // 11/10/10-bit digits of the key
 constexpr uint32_t kDecWordTile = 1024; // merged-index words per decode build tile
+constexpr uint32_t kMaxFlatItems = 4096; // items per call (flattened iteration bound)
 
 // Per-row hash coefficients (reference hash.hpp:27-33), derived on the host.
 struct RowCoef {
@@ -97,6 +98,41 @@ __device__ __forceinline__ float dev_sign(const RowCoef& c, uint32_t p) {
   return (h >> 63) ? 1.0f : -1.0f;                                         // hash.hpp:42
 }
 __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+// Flattened iteration over per-item counts that live in device memory: one
+// warp builds the exclusive prefix in shared memory (pref[0..n]), then every
+// thread maps a flat index to (item, offset) by binary search. Keeps all SMs
+// busy when items (segments) are many and uneven instead of walking them one
+// after another.
+template <typename CountFn>
+__device__ __forceinline__ uint32_t flat_prefix(uint32_t n_items, CountFn count, uint32_t* pref) {
+  if (threadIdx.x < 32) {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n_items; base += 32) {
+      const uint32_t i = base + threadIdx.x;
+      uint32_t c = i < n_items ? count(i) : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, c, o);
+        if (threadIdx.x >= uint32_t(o)) c += y;
+      }
+      if (i < n_items) pref[i + 1] = carry + c;
+      carry += __shfl_sync(0xFFFFFFFFu, c, 31);
+    }
+    if (threadIdx.x == 0) pref[0] = 0;
+  }
+  __syncthreads();
+  return pref[n_items];
+}
+__device__ __forceinline__ uint32_t flat_item(const uint32_t* pref, uint32_t n_items, uint32_t j) {
+  uint32_t lo = 0, hi = n_items - 1;  // largest i with pref[i] <= j
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (pref[mid] <= j) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // Row coefficients with a runtime row index, without dynamic indexing into
 // the kernel-parameter struct (which would spill it to local memory).
 __device__ __forceinline__ RowCoef row_coef(const HashParams& hp, uint32_t row) {

@@ -255,9 +255,13 @@ __device__ __forceinline__ void scatter_sketch(const EncItem& e, const HashParam
 //                           candidate; k_fixup keeps those with key > tau.
 // Candidates and kept elements are staged per warp in shared memory and
 // appended to global pools with one atomic per 200+ entries.
-constexpr uint32_t kWarpStage = 256;
+constexpr uint32_t kWarpStage = 128;
 
-template <bool kW4>
+// kHook: the exchange path (accumulator in/out, index + sketch). !kHook: the
+// per-stage sparsify entry point (separate sparse/residual outputs). Separate
+// template instances keep the hot kernel small enough for the instruction
+// cache.
+template <bool kW4, bool kHook>
 __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __restrict__ items,
                                                            SelState* __restrict__ state,
                                                            uint32_t n_items, uint64_t total_tiles,
@@ -268,10 +272,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
                                                            uint32_t* __restrict__ err) {
   __shared__ uint2 s_cand[kTileThreads / 32][kWarpStage];
   __shared__ uint2 s_kept[kTileThreads / 32][kWarpStage];
+  __shared__ float s_v[16][kTileThreads];  // a thread's 16 values, read back by bit index
   __shared__ uint32_t s_hist[kRadixBins];
   __shared__ uint32_t s_zero, s_lo;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
   uint64_t t0, t1;
   cta_range(total_tiles, t0, t1);
   if (t0 >= t1) return;
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
     uint32_t c_zero = 0, c_lo = 0, wc = 0, wk = 0;
     // warp-level flushes of the staged candidates / kept elements
     auto flush_cand = [&]() {
+      __syncwarp();
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&state[it].cnt_in, wc);
       base = __shfl_sync(kFull, base, 0);
@@ -306,10 +311,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
       for (uint32_t i = lane; i < wk; i += 32) {
         const uint2 kv = s_kept[warp][i];
         const float v = __uint_as_float(kv.y);
-        if (e.flags & kWriteSketch) scatter_sketch(e, hp, kv.x, v);
+        if (kHook) scatter_sketch(e, hp, kv.x, v);
         if (base + i < e.hi_cap) {
           hi_pool[e.hi_off + base + i] = kv;
-        } else if (e.flags & kHasAcc) {  // pool full (bracket miss): keep v recoverable
+        } else if (kHook) {  // pool full (bracket miss): keep v recoverable
           e.acc[kv.x] = v;
         }
       }
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
           for (int j = 0; j < 4; ++j) v[k][j] = 0.0f;
         }
       }
-      if (e.flags & kHasAcc) {
+      if (kHook) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
@@ -341,61 +346,105 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
           }
         }
       }
+      // classify the thread's 16 elements into bit masks (bit 4k+j)
+      uint32_t in_m = 0, hi_m = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t q = q0 + k * kTileThreads + threadIdx.x;
-        const uint32_t pos = 4u * q;
-        uint32_t nib = 0;
+        const uint32_t pos = 4u * (q0 + k * kTileThreads + threadIdx.x);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const bool valid = pos + j < e.n;
           const uint32_t key = mag_key(v[k][j]);
-          const bool hi = valid && key > khi;
-          const bool in = valid && key >= klo && key <= khi && key != 0;
+          const uint32_t bit = 1u << (4 * k + j);
+          hi_m |= (valid && key > khi) ? bit : 0u;
+          in_m |= (valid && key >= klo && key <= khi && key != 0) ? bit : 0u;
           c_zero += valid && key == 0;
           c_lo += valid && key != 0 && key < klo;
           nan |= valid && key > 0x7F800000u;
-          nib |= uint32_t(hi) << j;
-          const uint32_t mi = __ballot_sync(kFull, in);
-          if (mi) {
-            if (in) {
-              s_cand[warp][wc + __popc(mi & lt)] = make_uint2(pos + j, __float_as_uint(v[k][j]));
-              atomicAdd(&s_hist[(key - klo) >> fshift], 1u);
-            }
-            wc += __popc(mi);
-            if (wc > kWarpStage - 32) {
-              __syncwarp();
-              flush_cand();
-            }
-          }
-          const uint32_t mk = __ballot_sync(kFull, hi);
-          if (mk) {
-            if (hi) s_kept[warp][wk + __popc(mk & lt)] = make_uint2(pos + j, __float_as_uint(v[k][j]));
-            wk += __popc(mk);
-            if (wk > kWarpStage - 32) flush_kept();
-          }
         }
+      }
+      // element b = 4k + j sits at position 4*(q0 + k*256 + tid) + j
+      const uint32_t pbase = 4u * (q0 + threadIdx.x);
+      if (in_m | hi_m) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) s_v[4 * k + j][threadIdx.x] = v[k][j];
+      }
+      // warp-level placement in the stages: one packed scan per tile
+      const uint32_t cnt = uint32_t(__popc(in_m)) | (uint32_t(__popc(hi_m)) << 16);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= uint32_t(o)) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      const uint32_t tot_c = tot & 0xFFFFu, tot_k = tot >> 16;
+      if (tot_c) {
+        if (wc + tot_c > kWarpStage) flush_cand();
+        const bool direct = tot_c > kWarpStage;  // dense tile: straight to the pool
+        uint32_t gbase = 0;
+        if (direct) {
+          if (lane == 0) gbase = atomicAdd(&state[it].cnt_in, tot_c);
+          gbase = __shfl_sync(kFull, gbase, 0);
+        }
+        uint32_t o = (incl - cnt) & 0xFFFFu;
+        for (uint32_t m = in_m; m; m &= m - 1) {
+          const uint32_t b = __ffs(m) - 1;
+          const float x = s_v[b][threadIdx.x];
+          const uint2 kv = make_uint2(pbase + (b >> 2) * 4u * kTileThreads + (b & 3u), __float_as_uint(x));
+          if (!direct) s_cand[warp][wc + o] = kv;
+          else if (gbase + o < e.cand_cap) cand[e.cand_off + gbase + o] = kv;
+          atomicAdd(&s_hist[(mag_key(x) - klo) >> fshift], 1u);
+          ++o;
+        }
+        if (!direct) wc += tot_c;
+      }
+      if (tot_k) {
+        if (wk + tot_k > kWarpStage) flush_kept();
+        const bool direct = tot_k > kWarpStage;
+        uint32_t gbase = 0;
+        if (direct) {
+          if (lane == 0) gbase = atomicAdd(&state[it].cnt_hi, tot_k);
+          gbase = __shfl_sync(kFull, gbase, 0);
+        }
+        uint32_t o = (incl - cnt) >> 16;
+        for (uint32_t m = hi_m; m; m &= m - 1) {
+          const uint32_t b = __ffs(m) - 1;
+          const float x = s_v[b][threadIdx.x];
+          const uint2 kv = make_uint2(pbase + (b >> 2) * 4u * kTileThreads + (b & 3u), __float_as_uint(x));
+          if (!direct) {
+            s_kept[warp][wk + o] = kv;
+          } else {
+            if (kHook) scatter_sketch(e, hp, kv.x, x);
+            if (gbase + o < e.hi_cap) hi_pool[e.hi_off + gbase + o] = kv;
+            else hi_m &= ~(1u << b);  // pool full: the element keeps v in place
+          }
+          ++o;
+        }
+        if (!direct) wk += tot_k;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t q = q0 + k * kTileThreads + threadIdx.x;
+        const uint32_t pos = 4u * q;
+        const uint32_t nib = (hi_m >> (4 * k)) & 0xFu;
         if (pos < e.n) {
-          if (e.flags & kHasAcc) {
-            float r[4];
+          float r[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+          for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+          if (kHook) {
             store_quad(e.acc, pos, e.n, vec, r);
-          }
-          if (e.flags & kWriteResidual) {
-            float r[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+          } else {
             store_quad(e.residual, pos, e.n, false, r);
-          }
-          if (e.flags & kWriteSparse) {
             float sp[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) sp[j] = (nib >> j & 1u) ? v[k][j] : 0.0f;
             store_quad(e.sparse, pos, e.n, false, sp);
           }
         }
-        if (e.flags & kWriteIndex) {
+        if (kHook) {
           if (kW4) {
             if (q < 2u * n_words) {
               const uint32_t hw = (nib & 1u) | (nib >> 1 & 1u) << 4 | (nib >> 2 & 1u) << 8 |
@@ -523,19 +572,17 @@ __global__ void __launch_bounds__(256) k_collect(const EncItem* __restrict__ ite
                                                  SelState* __restrict__ state, uint32_t n_items,
                                                  const uint2* __restrict__ cand,
                                                  uint32_t* __restrict__ sel_list) {
-  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint32_t it = 0; it < n_items; ++it) {
-    const SelState s = state[it];
-    if (s.status != kStatusCollect) continue;
-    const uint2* ck = cand + items[it].cand_off;
-    uint32_t* out = sel_list + uint64_t(it) * kFinalKeys;
-    for (uint64_t i = gtid; i < s.cnt_in; i += gstride) {
-      const uint32_t key = ck[i].y & 0x7FFFFFFFu;
-      if (((key - s.klo) >> s.fshift) == s.prefix) {
-        const uint32_t idx = atomicAdd(&state[it].n_sel, 1u);
-        if (idx < kFinalKeys) out[idx] = key;
-      }
+  __shared__ uint32_t pref[kMaxFlatItems + 1];
+  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) {
+    return state[i].status == kStatusCollect ? min(state[i].cnt_in, items[i].cand_cap) : 0u;
+  }, pref);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
+    const uint32_t it = flat_item(pref, n_items, j);
+    const SelState& s = state[it];
+    const uint32_t key = cand[items[it].cand_off + (j - pref[it])].y & 0x7FFFFFFFu;
+    if (((key - s.klo) >> s.fshift) == s.prefix) {
+      const uint32_t idx = atomicAdd(&state[it].n_sel, 1u);
+      if (idx < kFinalKeys) sel_list[uint64_t(it) * kFinalKeys + idx] = key;
     }
   }
 }
@@ -593,37 +640,39 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
                                                SelState* __restrict__ state, uint32_t n_items,
                                                const uint2* __restrict__ cand, const HashParams hp,
                                                const uint32_t* __restrict__ err) {
+  __shared__ uint32_t pref[kMaxFlatItems + 1];
   if (err[0]) return;
+  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) {
+    return state[i].status == kStatusReady ? min(state[i].cnt_in, items[i].cand_cap) : 0u;
+  }, pref);
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint32_t it = 0; it < n_items; ++it) {
-    const SelState s = state[it];
-    if (s.status != kStatusReady) continue;
-    const EncItem e = items[it];
-    const uint32_t cnt = min(s.cnt_in, e.cand_cap);
-    uint32_t kept = 0;
-    for (uint64_t base = gtid - lane; base < cnt; base += gstride) {
-      const uint64_t i = base + lane;
-      if (i < cnt) {
-        const uint2 kv = cand[e.cand_off + i];
-        if ((kv.y & 0x7FFFFFFFu) > s.tau_key) {
-          const uint32_t p = kv.x;
-          const float v = __uint_as_float(kv.y);
-          ++kept;
-          if (e.flags & kHasAcc) e.acc[p] = 0.0f;
-          if (e.flags & kWriteResidual) e.residual[p] = 0.0f;
-          if (e.flags & kWriteSparse) e.sparse[p] = v;
-          if (e.flags & kWriteIndex) {
-            if (kW4) atomicOr(e.index + (p >> 3), 1u << (4u * (p & 7u)));
-            else atomicOr(e.index + (p >> 5), 1u << (p & 31u));
-          }
-          if (e.flags & kWriteSketch) scatter_sketch(e, hp, p, v);
-        }
-      }
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < total;
+       base += gridDim.x * blockDim.x) {
+    const uint32_t j = base + lane;
+    uint32_t it = 0xFFFFFFFFu;
+    bool keep = false;
+    uint2 kv = make_uint2(0u, 0u);
+    if (j < total) {
+      it = flat_item(pref, n_items, j);
+      kv = cand[items[it].cand_off + (j - pref[it])];
+      keep = (kv.y & 0x7FFFFFFFu) > state[it].tau_key;
     }
-    kept = warp_sum(kept);
-    if (lane == 0 && kept) atomicAdd(&state[it].kept, kept);
+    // kept counts, aggregated over the lanes of the same item
+    const uint32_t grp = __match_any_sync(kFull, it);
+    const uint32_t km = __ballot_sync(kFull, keep) & grp;
+    if (keep && lane == __ffs(km) - 1) atomicAdd(&state[it].kept, __popc(km));
+    if (!keep) continue;
+    const EncItem& e = items[it];
+    const uint32_t p = kv.x;
+    const float v = __uint_as_float(kv.y);
+    if (e.flags & kHasAcc) e.acc[p] = 0.0f;
+    if (e.flags & kWriteResidual) e.residual[p] = 0.0f;
+    if (e.flags & kWriteSparse) e.sparse[p] = v;
+    if (e.flags & kWriteIndex) {
+      if (kW4) atomicOr(e.index + (p >> 3), 1u << (4u * (p & 7u)));
+      else atomicOr(e.index + (p >> 5), 1u << (p & 31u));
+    }
+    if (e.flags & kWriteSketch) scatter_sketch(e, hp, p, v);
   }
 }
 
@@ -948,8 +997,8 @@ int flat_grid(uint64_t n, int threads) {
 
 int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
-                        uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand, uint2* hi_pool,
-                        uint32_t* err, cudaStream_t stream) {
+                        int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
+                        uint2* hi_pool, uint32_t* err, cudaStream_t stream) {
   if (n_items == 0) return 0;
   int launches = 0;
   if (total_samples) {
@@ -958,14 +1007,16 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
     ++launches;
   }
   k_window<<<n_items, 256, 0, stream>>>(items, state, sample_hist);
-  if (w4)
-    k_fused<true><<<persistent_grid((const void*)k_fused<true>, kTileThreads, di, total_tiles),
-                    kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, cand, hi_pool,
-                                               fine_hist, err);
-  else
-    k_fused<false><<<persistent_grid((const void*)k_fused<false>, kTileThreads, di, total_tiles),
-                     kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, cand, hi_pool,
-                                                fine_hist, err);
+  // every item of a batch shares the path: hook (accumulator) or per-stage outputs
+  const bool hook = per_stage == 0;
+  auto launch = [&](auto kern) {
+    kern<<<persistent_grid((const void*)kern, kTileThreads, di, total_tiles), kTileThreads, 0, stream>>>(
+        items, state, n_items, total_tiles, hp, cand, hi_pool, fine_hist, err);
+  };
+  if (w4 && hook) launch(k_fused<true, true>);
+  else if (w4) launch(k_fused<true, false>);
+  else if (hook) launch(k_fused<false, true>);
+  else launch(k_fused<false, false>);
   return launches + 2;
 }
 

@@ -224,6 +224,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
                                bool want_kept, const char*) {
   const uint32_t n = uint32_t(items.size());
   if (n == 0) return;
+  if (n > kMaxFlatItems) throw InvalidArgument("more than 4096 compressed segments in one call");
   bool select = (items[0].flags & kSelect) != 0;
   uint64_t tiles = 0, samples = 0, cand = 0, hi = 0;
   for (EncItem& e : items) {
@@ -260,8 +261,13 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     auto* cd = static_cast<uint2*>(ws_.get("cand", cand * 8, false, stream_));
     auto* hp_pool = static_cast<uint2*>(ws_.get("hi_pool", hi * 8, false, stream_));
     auto* sl = static_cast<uint32_t*>(ws_.get("sel_list", size_t(n) * 8192 * 4, false, stream_));
-    launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, sh, fine, cd, hp_pool,
-                                     err, stream_);
+    // hook items carry an accumulator; the per-stage sparsify entry writes
+    // separate sparse/residual outputs (one kind per batch)
+    const int per_stage = (items[0].flags & kHasAcc) ? 0 : 1;
+    for (const EncItem& e : items)
+      if (((e.flags & kHasAcc) ? 0 : 1) != per_stage) throw CudaError("mixed fused batch");
+    launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
+                                     cd, hp_pool, err, stream_);
     ev_record(1);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
@@ -304,6 +310,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.slot_state = static_cast<unsigned long long*>(ws_.get("slot_state", slots * 8, false, stream_));
   w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
+  w.pitem = static_cast<uint32_t*>(ws_.get("pitem", list * 4, false, stream_));
   w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));

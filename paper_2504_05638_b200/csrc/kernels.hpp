@@ -24,8 +24,8 @@ struct DevInfo {
 // err[4] (err[0] NaN, err[1] fallback needed).
 int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
-                        uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand, uint2* hi_pool,
-                        uint32_t* err, cudaStream_t stream);
+                        int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
+                        uint2* hi_pool, uint32_t* err, cudaStream_t stream);
 // Exact tau from the window candidates, fix-up of the candidates, and the
 // (normally idle) restore + radix-select + re-encode fallback chain.
 int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
@@ -91,10 +91,12 @@ struct DecodeWork {
   uint64_t total_slots;
   unsigned long long* slot_state;  // (count << 40) | key_sum, total_slots
   uint32_t* bitmap;                // recovered bits
-  uint32_t* plist;                 // presence lists
+  uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
+  uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
   uint32_t* queue[2];              // capacity total_slots each
-  uint32_t* qcount;                // [0..1] frontier sizes, [2] rounds, [3] tail rounds, [4] peeled
+  uint32_t* qcount;                // [0..1] frontier sizes, [2] rounds, [3] tail rounds, [4] peeled,
+                                   // [5] presence total
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
