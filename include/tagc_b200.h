@@ -174,10 +174,17 @@ int tagc_ctx_ledger_csv(tagc_ctx* ctx, char* buf, size_t len, size_t* needed);
 int tagc_ctx_ledger_reset(tagc_ctx* ctx);
 /* Device bytes the context currently holds in workspaces. */
 uint64_t tagc_ctx_workspace_bytes(const tagc_ctx* ctx);
-/* Optional per-stage device timing of the last fused call (ms): select,
- * encode, exchange, decode. Enabled by tagc_ctx_set_timing(ctx, 1). */
+/* Optional per-stage device timing of the last fused call (ms): prep
+ * (descriptor uploads, sketch zeroing), the sampled select + fused
+ * split/encode pass, select finish (exact tau, fix-up), exchange, decode.
+ * Enabled by tagc_ctx_set_timing(ctx, 1). */
 int tagc_ctx_set_timing(tagc_ctx* ctx, int enabled);
-int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[4]);
+int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[5]);
+/* Timing mode: device execution spans (ms) of the last fused call's two
+ * dominant kernel chains, stamped by the kernels themselves (%globaltimer):
+ * out_ms[0] = sampled select + fused split/encode pass (k_sample start to
+ * k_fused end), out_ms[1] = decode (k_build start to k_final end). */
+int tagc_ctx_last_kernel_spans(tagc_ctx* ctx, float out_ms[2]);
 /* Kernel launches enqueued by the last fused call. */
 uint64_t tagc_ctx_last_launches(const tagc_ctx* ctx);
 /* Synchronise the context stream and surface deferred device errors (a NaN
@@ -211,6 +218,23 @@ int tagc_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shard
  * out is written on the owner rank only. */
 int tagc_reduce_shard(tagc_ctx* ctx, const tagc_shard* shard, const float* grad, float* acc,
                       float* out, tagc_peel_stats* stats);
+/* Host-buffer form of tagc_reduce_shards: the call a user makes when the
+ * gradient lives in host memory (the reference's tagc_reduce_shard takes host
+ * std::vector<float> slices, hook.hpp:76-80). host_grad: host, max(shard.end)
+ * floats; acc: dev (engine-side error-feedback state, in/out); host_out: host,
+ * the owned shards' decoded values (as `out` above). Page-locked host buffers
+ * give full overlap: the gradient is copied in on one copy stream into one of
+ * two device buffers and the result copied out on another, so consecutive
+ * calls overlap D2H(k), H2D(k+1) and the exchange. The call is asynchronous
+ * unless stats != NULL; host_out is complete after tagc_ctx_sync, or on the
+ * context stream after tagc_ctx_host_join. */
+int tagc_reduce_shards_host(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                            const float* host_grad, float* acc, float* host_out,
+                            tagc_peel_stats* stats);
+/* Make the context stream wait for every copy tagc_reduce_shards_host has
+ * enqueued (a CUDA event recorded on the context stream afterwards brackets
+ * the host copies too). */
+int tagc_ctx_host_join(tagc_ctx* ctx);
 /* The owner-major exchange layout tagc_reduce_shards uses on `rank` (pure
  * host computation; exposed so a foreign transport can reproduce the
  * exchange). Owner o's f32 block is [o*block_f32, (o+1)*block_f32) of the

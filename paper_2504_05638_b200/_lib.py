@@ -116,6 +116,7 @@ SIGNATURES = {
     "tagc_ctx_workspace_bytes": (U64, [VP]),
     "tagc_ctx_set_timing": (C.c_int, [VP, C.c_int]),
     "tagc_ctx_last_timing": (C.c_int, [VP, C.POINTER(C.c_float)]),
+    "tagc_ctx_last_kernel_spans": (C.c_int, [VP, C.POINTER(C.c_float)]),
     "tagc_ctx_last_launches": (U64, [VP]),
     "tagc_ctx_sync": (C.c_int, [VP]),
     "tagc_ctx_last_peel_rounds": (C.c_int, [VP, C.POINTER(U32)]),
@@ -123,6 +124,8 @@ SIGNATURES = {
                                         C.POINTER(PeelStats)]),
     "tagc_baseline_reduce_shard_sim": (C.c_int, [VP, C.POINTER(Shard), U32, C.POINTER(VP), VP]),
     "tagc_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats)]),
+    "tagc_reduce_shards_host": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats)]),
+    "tagc_ctx_host_join": (C.c_int, [VP]),
     "tagc_reduce_shard": (C.c_int, [VP, C.POINTER(Shard), VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_baseline_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP]),
     "tagc_plan_exchange": (C.c_int, [C.POINTER(Config), C.POINTER(Shard), U32, U32, U32,

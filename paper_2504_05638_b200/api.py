@@ -292,8 +292,14 @@ class Context:
         check(lib.tagc_ctx_set_timing(self.h, int(on)))
 
     def last_timing(self):
-        out = (C.c_float * 4)()
+        out = (C.c_float * 5)()
         check(lib.tagc_ctx_last_timing(self.h, out))
+        return list(out)
+
+    def last_kernel_spans(self):
+        """(select+fused pass, decode) device execution spans in ms (timing mode)."""
+        out = (C.c_float * 2)()
+        check(lib.tagc_ctx_last_kernel_spans(self.h, out))
         return list(out)
 
     def last_launches(self) -> int:
@@ -347,6 +353,28 @@ class Context:
         check(lib.tagc_reduce_shards(self.h, arr, len(scs), _ptr(grad), _ptr(acc), _ptr(out),
                                      C.byref(st) if stats else None), "tagc_reduce_shards")
         return out, (PeelStats(**st.as_dict()) if stats else None)
+
+    def tagc_reduce_shards_host(self, shards: Sequence[ShardSpec], host_grad, acc, host_out=None,
+                                stats=False):
+        """Host-buffer form (the end-to-end call): host_grad / host_out are CPU
+        tensors (pinned for copy/compute overlap), acc stays on the device.
+        Asynchronous unless stats: host_out is complete after sync(), or on the
+        context stream after host_join()."""
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        if host_out is None:
+            host_out = self.torch.empty(max(owned, 1), dtype=self.torch.float32, pin_memory=True)
+        for t in (host_grad, host_out):
+            if t.is_cuda:
+                raise TagcInvalidArgument(2, "host buffers must be CPU tensors")
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shards_host(self.h, arr, len(scs), _ptr(host_grad), _ptr(acc), _ptr(host_out),
+                                          C.byref(st) if stats else None), "tagc_reduce_shards_host")
+        return host_out, (PeelStats(**st.as_dict()) if stats else None)
+
+    def host_join(self):
+        check(lib.tagc_ctx_host_join(self.h), "host_join")
 
     def baseline_reduce_shards(self, shards: Sequence[ShardSpec], grad, out=None):
         L = shards[0].size()

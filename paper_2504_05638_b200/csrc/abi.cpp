@@ -247,11 +247,15 @@ int tagc_ctx_set_timing(tagc_ctx* ctx, int enabled) {
   return guarded([&] { eng(ctx).set_timing(enabled != 0); });
 }
 
-int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[4]) {
+int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[5]) {
   return guarded([&] {
     cuda_check(cudaStreamSynchronize(eng(ctx).stream()), "sync");
     eng(ctx).last_timing(out_ms);
   });
+}
+
+int tagc_ctx_last_kernel_spans(tagc_ctx* ctx, float out_ms[2]) {
+  return guarded([&] { eng(ctx).last_kernel_spans(out_ms); });
 }
 
 uint64_t tagc_ctx_last_launches(const tagc_ctx* ctx) {
@@ -299,6 +303,24 @@ int tagc_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shard
 int tagc_reduce_shard(tagc_ctx* ctx, const tagc_shard* shard, const float* grad, float* acc,
                       float* out, tagc_peel_stats* stats) {
   return tagc_reduce_shards(ctx, shard, 1, grad, acc, out, stats);
+}
+
+int tagc_reduce_shards_host(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                            const float* host_grad, float* acc, float* host_out,
+                            tagc_peel_stats* stats) {
+  return guarded([&] {
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    PeelStats st;
+    eng(ctx).reduce_shards_host(v, host_grad, acc, host_out, stats ? &st : nullptr);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
+int tagc_ctx_host_join(tagc_ctx* ctx) {
+  return guarded([&] { eng(ctx).host_join(); });
 }
 
 int tagc_plan_exchange(const tagc_config* cfg, const tagc_shard* shards, uint32_t n_shards,

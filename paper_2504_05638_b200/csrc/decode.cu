@@ -121,6 +121,7 @@ __device__ __forceinline__ float median_rows(float (&e)[kMaxRows], uint32_t k) {
 // Contiguous range of word tiles per CTA (kWordTile words per tile, 4 words
 // per thread), bucket state updated with fire-and-forget 64-bit reductions.
 __global__ void __launch_bounds__(256) k_build(DecodeWork w, const HashParams hp) {
+  span_begin(w.span);
   __shared__ uint32_t s_list[kStage];
   __shared__ uint32_t s_nl, s_bl;
   const uint32_t lane = threadIdx.x & 31;
@@ -679,7 +680,10 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
 // ------------------------------------------------------------------ estimate
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
   const uint32_t total = w.qcount[5];
-  if (total == w.qcount[4]) return;  // every present position peeled: nothing to estimate
+  if (total == w.qcount[4]) {  // every present position peeled: nothing to estimate
+    span_end(w.span);
+    return;
+  }
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
@@ -706,6 +710,7 @@ __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp
       }
     }
   }
+  span_end(w.span);
 }
 
 // ------------------------------------------------------------------ helpers

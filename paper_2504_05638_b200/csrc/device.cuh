@@ -98,6 +98,24 @@ __device__ __forceinline__ float dev_sign(const RowCoef& c, uint32_t p) {
   return (h >> 63) ? 1.0f : -1.0f;                                         // hash.hpp:42
 }
 __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+// Device-side execution spans (timing mode): span[0] = earliest CTA start,
+// span[1] = latest CTA end of a kernel chain, in %globaltimer ns. Independent
+// of where the driver stamps stream events.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void span_begin(unsigned long long* span) {
+  if (span && threadIdx.x == 0) atomicMin(span, globaltimer_ns());
+}
+// CTA-uniform call site (contains a barrier)
+__device__ __forceinline__ void span_end(unsigned long long* span) {
+  if (span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(span + 1, globaltimer_ns());
+  }
+}
 // Flattened iteration over per-item counts that live in device memory: one
 // warp builds the exclusive prefix in shared memory (pref[0..n]), then every
 // thread maps a flat index to (item, offset) by binary search. Keeps all SMs

@@ -102,7 +102,9 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
 // --------------------------------------------------------------- sampling
 __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restrict__ items,
                                                          uint32_t n_items, uint64_t total,
-                                                         uint32_t* __restrict__ sample_hist) {
+                                                         uint32_t* __restrict__ sample_hist,
+                                                         unsigned long long* span) {
+  span_begin(span);
   __shared__ uint32_t hist[kSampleBins];
   for (uint32_t i = threadIdx.x; i < kSampleBins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -141,7 +143,9 @@ __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restri
 // One CTA per item: bracket the target rank of the sample into a key window.
 __global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ items,
                                                 SelState* __restrict__ state,
-                                                uint32_t* __restrict__ sample_hist) {
+                                                uint32_t* __restrict__ sample_hist,
+                                                unsigned long long* span) {
+  span_begin(span);
   using Scan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ uint32_t s_lo, s_hi;
@@ -269,7 +273,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
                                                            uint2* __restrict__ cand,
                                                            uint2* __restrict__ hi_pool,
                                                            uint32_t* __restrict__ fine_hist,
-                                                           uint32_t* __restrict__ err) {
+                                                           uint32_t* __restrict__ err,
+                                                           unsigned long long* span) {
+  span_begin(span);
   __shared__ uint2 s_cand[kTileThreads / 32][kWarpStage];
   __shared__ uint2 s_kept[kTileThreads / 32][kWarpStage];
   __shared__ float s_v[16][kTileThreads];  // a thread's 16 values, read back by bit index
@@ -483,6 +489,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
     ++it;
   }
   if (nan) atomicOr(err, 1u);
+  span_end(span);
 }
 
 // Block-wide search over `kRadixBins` counters: finds the digit whose
@@ -980,6 +987,29 @@ __global__ void k_index_diag(const DiagItem* __restrict__ items,
   }
 }
 
+__global__ void __launch_bounds__(256) k_zero(const ZeroRanges r) {
+  for (int k = 0; k < r.n; ++k) {
+    char* p = static_cast<char*>(r.ptr[k]);
+    const uint64_t n = r.bytes[k];
+    const uint64_t mis = (16u - (reinterpret_cast<uintptr_t>(p) & 15u)) & 15u;
+    const uint64_t head = mis < n ? mis : n;
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = tid; i < head; i += stride) p[i] = 0;
+    const uint64_t nv = (n - head) / 16;
+    uint4* v = reinterpret_cast<uint4*>(p + head);
+    for (uint64_t i = tid; i < nv; i += stride) v[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (uint64_t i = head + nv * 16 + tid; i < n; i += stride) p[i] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_stage_copy(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                    uint64_t n16) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
 int persistent_grid(const void* fn, int threads, const DevInfo& di, uint64_t work) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
@@ -998,20 +1028,20 @@ int flat_grid(uint64_t n, int threads) {
 int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
                         int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
-                        uint2* hi_pool, uint32_t* err, cudaStream_t stream) {
+                        uint2* hi_pool, uint32_t* err, cudaStream_t stream, unsigned long long* span) {
   if (n_items == 0) return 0;
   int launches = 0;
   if (total_samples) {
     k_sample<<<persistent_grid((const void*)k_sample, kTileThreads, di, total_samples), kTileThreads,
-               0, stream>>>(items, n_items, total_samples, sample_hist);
+               0, stream>>>(items, n_items, total_samples, sample_hist, span);
     ++launches;
   }
-  k_window<<<n_items, 256, 0, stream>>>(items, state, sample_hist);
+  k_window<<<n_items, 256, 0, stream>>>(items, state, sample_hist, span);
   // every item of a batch shares the path: hook (accumulator) or per-stage outputs
   const bool hook = per_stage == 0;
   auto launch = [&](auto kern) {
     kern<<<persistent_grid((const void*)kern, kTileThreads, di, total_tiles), kTileThreads, 0, stream>>>(
-        items, state, n_items, total_tiles, hp, cand, hi_pool, fine_hist, err);
+        items, state, n_items, total_tiles, hp, cand, hi_pool, fine_hist, err, span);
   };
   if (w4 && hook) launch(k_fused<true, true>);
   else if (w4) launch(k_fused<true, false>);
@@ -1057,6 +1087,26 @@ int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state
     const int g = persistent_grid((const void*)k_encode<false>, kTileThreads, di, total_tiles);
     k_encode<false><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 0);
   }
+  return 1;
+}
+
+int launch_zero(const ZeroRanges& r, cudaStream_t stream) {
+  uint64_t mx = 0;
+  for (int k = 0; k < r.n; ++k) mx = std::max<uint64_t>(mx, r.bytes[k]);
+  if (!mx) return 0;
+  const uint64_t blocks = std::min<uint64_t>((mx / 16 + 255) / 256 + 1, 148ull * 8);
+  k_zero<<<int(blocks), 256, 0, stream>>>(r);
+  return 1;
+}
+
+// dst and mapped_src 16-byte aligned, bytes a multiple of 16 (the staging
+// arena rounds every upload up).
+int launch_stage_copy(void* dst, const void* mapped_src, uint64_t bytes, cudaStream_t stream) {
+  const uint64_t n16 = bytes / 16;
+  if (!n16) return 0;
+  const uint64_t blocks = std::min<uint64_t>((n16 + 255) / 256, 64);
+  k_stage_copy<<<int(blocks), 256, 0, stream>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(mapped_src),
+                                                n16);
   return 1;
 }
 

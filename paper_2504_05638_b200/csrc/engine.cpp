@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 
 namespace tagc_b200 {
 
@@ -164,8 +165,20 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
 
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
+  if (h2d_) cudaStreamSynchronize(h2d_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
+  for (Staging& s : stage_) {
+    if (s.ev) cudaEventDestroy(s.ev);
+    if (s.ptr) cudaFreeHost(s.ptr);
+  }
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {hev_in_[i], hev_gfree_[i], hev_dec_[i], hev_out_[i]})
+      if (e) cudaEventDestroy(e);
+  if (hev_join_) cudaEventDestroy(hev_join_);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   if (own_comm_ && comm_) nccl().CommDestroy(comm_);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
 }
@@ -185,19 +198,111 @@ void Engine::init_nccl(const uint8_t id[128]) {
   own_comm_ = true;
 }
 
-void Engine::last_timing(float out[4]) const {
-  for (int i = 0; i < 4; ++i) {
+void Engine::last_timing(float out[kStages]) const {
+  for (int i = 0; i < kStages; ++i) {
     out[i] = 0.f;
     if (timing_) cudaEventElapsedTime(&out[i], ev_[i], ev_[i + 1]);
   }
 }
 
+void Engine::span_reset() {
+  if (!timing_) return;
+  spans_ = static_cast<unsigned long long*>(ws_.get("kernel_spans", 4 * 8, false, stream_));
+  const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+  upload(init, sizeof(init), spans_);
+}
+
+void Engine::last_kernel_spans(float out_ms[2]) {
+  out_ms[0] = out_ms[1] = 0.f;
+  if (!timing_ || !spans_) return;
+  unsigned long long t[4];
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cuda_check(cudaMemcpy(t, spans_, sizeof(t), cudaMemcpyDeviceToHost), "D2H spans");
+  for (int i = 0; i < 2; ++i)
+    if (t[2 * i + 1] > t[2 * i] && t[2 * i] != ~0ull) out_ms[i] = float(double(t[2 * i + 1] - t[2 * i]) * 1e-6);
+}
+
 void Engine::ev_record(int i) {
   if (timing_) cuda_check(cudaEventRecord(ev_[i], stream_), "event record");
+  static const bool probe = std::getenv("TAGC_TIMING_PROBE") != nullptr;
+  if (timing_ && probe) {
+    cudaStreamSynchronize(stream_);
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    std::fprintf(stderr, "[ev%d] host %.1f us\n", i, ts.tv_sec * 1e6 + ts.tv_nsec / 1e3);
+  }
+}
+
+// One public call = one staging half (see engine.hpp). Nested public calls
+// (the host-buffer path) share the outer call's half.
+struct CallScope {
+  Engine& e;
+  explicit CallScope(Engine& en) : e(en) {
+    if (e.call_depth_++ == 0) e.call_begin();
+  }
+  ~CallScope() {
+    if (--e.call_depth_ == 0) e.call_end();
+  }
+};
+
+void Engine::call_begin() {
+  stage_cur_ ^= 1;
+  Staging& s = stage_[stage_cur_];
+  if (s.ev) cuda_check(cudaEventSynchronize(s.ev), "staging reuse");
+  s.off = 0;
+}
+
+void Engine::call_end() {
+  Staging& s = stage_[stage_cur_];
+  if (!s.ev && cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming) != cudaSuccess) {
+    s.ev = nullptr;
+    return;
+  }
+  cudaEventRecord(s.ev, stream_);
 }
 
 void Engine::upload(const void* host, size_t bytes, void* dev) {
-  if (bytes) cuda_check(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+  if (!bytes) return;
+  if (call_depth_ == 0) {  // internal helper called outside a public entry
+    CallScope scope(*this);
+    upload(host, bytes, dev);
+    return;
+  }
+  Staging& s = stage_[stage_cur_];
+  if (s.off + bytes > s.cap) {
+    // grow: earlier copies of this call may still read the old buffer
+    cuda_check(cudaStreamSynchronize(stream_), "staging grow");
+    if (s.ptr) cudaFreeHost(s.ptr);
+    s.ptr = nullptr;
+    s.cap = std::max<size_t>(std::max<size_t>(2 * s.cap, align_up(bytes, 4096)), 1 << 16);
+    s.off = 0;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s.ptr), s.cap, cudaHostAllocMapped),
+               "staging alloc");
+    void* dp = nullptr;
+    cuda_check(cudaHostGetDevicePointer(&dp, s.ptr, 0), "staging map");
+    s.dev = static_cast<char*>(dp);
+  }
+  std::memcpy(s.ptr + s.off, host, bytes);
+  // the SMs pull the descriptors over PCIe (a copy-engine H2D would queue
+  // behind the host-buffer path's bulk transfers); workspace destinations
+  // have room for the 16-byte round-up
+  launches_ += launch_stage_copy(dev, s.dev + s.off, align_up(bytes, 16), stream_);
+  s.off = align_up(s.off + bytes, 256);
+}
+
+void Engine::zero(const std::vector<std::pair<void*, uint64_t>>& ranges) {
+  ZeroRanges r{};
+  for (const auto& pr : ranges) {
+    if (!pr.second) continue;
+    if (r.n == kZeroRanges) {
+      launches_ += launch_zero(r, stream_);
+      r = ZeroRanges{};
+    }
+    r.ptr[r.n] = pr.first;
+    r.bytes[r.n] = pr.second;
+    ++r.n;
+  }
+  if (r.n) launches_ += launch_zero(r, stream_);
 }
 
 uint32_t* Engine::err_flag() {
@@ -213,6 +318,8 @@ void Engine::fetch_rounds() {
 }
 
 void Engine::sync_check() {
+  if (h2d_) cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
+  if (d2h_) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
   cuda_check(cudaStreamSynchronize(stream_), "stream sync");
   uint32_t err = 0;
   cuda_check(cudaMemcpy(&err, err_flag(), 4, cudaMemcpyDeviceToHost), "D2H err");
@@ -253,7 +360,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   upload(items.data(), n * sizeof(EncItem), d_items);
   auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
   uint32_t* err = err_flag();
-  cuda_check(cudaMemsetAsync(err, 0, 16, stream_), "err reset");
+  zero({{err, 16}});
   if (select) {
     auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleBins * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
@@ -266,17 +373,19 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     const int per_stage = (items[0].flags & kHasAcc) ? 0 : 1;
     for (const EncItem& e : items)
       if (((e.flags & kHasAcc) ? 0 : 1) != per_stage) throw CudaError("mixed fused batch");
-    launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
-                                     cd, hp_pool, err, stream_);
     ev_record(1);
+    launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
+                                     cd, hp_pool, err, stream_, timing_ ? spans_ : nullptr);
+    ev_record(2);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
-    ev_record(2);
+    ev_record(3);
   } else {
-    cuda_check(cudaMemsetAsync(state, 0, n * sizeof(SelState), stream_), "state reset");
+    zero({{state, n * sizeof(SelState)}});
     ev_record(1);
-    launches_ += launch_encode_exact(di_, d_items, state, n, tiles, hp, err, w4, stream_);
     ev_record(2);
+    launches_ += launch_encode_exact(di_, d_items, state, n, tiles, hp, err, w4, stream_);
+    ev_record(3);
   }
   (void)want_kept;
   cuda_check(cudaGetLastError(), "select/encode launch");
@@ -303,6 +412,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   auto* d_items = static_cast<DecItem*>(ws_.get("dec_items", n * sizeof(DecItem), false, stream_));
   upload(items.data(), n * sizeof(DecItem), d_items);
   DecodeWork w{};
+  w.span = timing_ ? spans_ + 2 : nullptr;
   w.items = d_items;
   w.n_items = n;
   w.total_word_tiles = wt;
@@ -318,10 +428,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", n * sizeof(DecStats), false, stream_));
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
-  cuda_check(cudaMemsetAsync(w.slot_state, 0, slots * 8, stream_), "slot reset");
-  cuda_check(cudaMemsetAsync(w.bitmap, 0, bm * 4, stream_), "bitmap reset");
-  cuda_check(cudaMemsetAsync(w.qcount, 0, 32, stream_), "qcount reset");
-  cuda_check(cudaMemsetAsync(w.stats, 0, n * sizeof(DecStats), stream_), "stats reset");
+  zero({{w.slot_state, slots * 8}, {w.bitmap, bm * 4}, {w.qcount, 32}, {w.stats, n * sizeof(DecStats)}});
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {
     w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));
@@ -361,11 +468,13 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
 // ------------------------------------------------------------ simulated world
 void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
                               float* const* accs, float* out, PeelStats* stats) {
+  CallScope scope(*this);
   if (world == 0) throw InvalidArgument("world size must be at least 1");
   cfg_.validate_for_world(world);  // hook.cpp:105
   check_shard(shard, world);
   launches_ = 0;
   ev_record(0);
+  span_reset();
   const uint32_t w = cfg_.index_width, rows = cfg_.sketch_rows;
   std::vector<SegPlan> plan;
   uint64_t NW = 0, SK = 0;
@@ -400,7 +509,7 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
   for (uint32_t r = 0; r < world; ++r) ptrs.push_back(sk_all + r * SK);
   auto* d_ptrs = static_cast<const void**>(ws_.get("sim_ptrs", ptrs.size() * 8, false, stream_));
   upload(ptrs.data(), ptrs.size() * 8, d_ptrs);
-  if (SK) cuda_check(cudaMemsetAsync(sk_all, 0, world * SK * 4, stream_), "sketch zero");
+  zero({{sk_all, world * SK * 4}});
 
   std::vector<EncItem> enc;
   for (uint32_t r = 0; r < world; ++r) {
@@ -438,7 +547,7 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
     launches_ += launch_raw_sum(d_raw, uint32_t(raw.size()), max_raw,
                                 reinterpret_cast<const float* const*>(d_ptrs), world, stream_);
   }
-  ev_record(3);
+  ev_record(4);
   std::vector<DecItem> dec;
   std::vector<DiagItem> diag;
   uint32_t max_words = 0;
@@ -457,13 +566,13 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
     max_words = std::max(max_words, p.n_words);
   }
   run_decode(dec, hp, false, w == 1 && world > 1);
-  ev_record(4);
+  ev_record(5);
   unsigned long long* ls = nullptr;
   if (!diag.empty()) {
     auto* d_diag = static_cast<DiagItem*>(ws_.get("sim_diag", diag.size() * sizeof(DiagItem), false, stream_));
     upload(diag.data(), diag.size() * sizeof(DiagItem), d_diag);
     ls = static_cast<unsigned long long*>(ws_.get("sim_ls", diag.size() * 16, false, stream_));
-    cuda_check(cudaMemsetAsync(ls, 0, diag.size() * 16, stream_), "ls reset");
+    zero({{ls, diag.size() * 16}});
     launches_ += launch_index_diag(d_diag, uint32_t(diag.size()), max_words,
                                    reinterpret_cast<const uint32_t* const*>(d_ptrs + world), world, ls,
                                    stream_);
@@ -505,6 +614,7 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
 
 void Engine::baseline_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
                           float* out) {
+  CallScope scope(*this);
   if (world == 0) throw InvalidArgument("world size must be at least 1");
   check_shard(shard, world);
   launches_ = 0;
@@ -519,11 +629,13 @@ void Engine::baseline_sim(const ShardSpec& shard, uint32_t world, const float* c
 // ------------------------------------------------------------------ NCCL world
 void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                            float* out, PeelStats* stats) {
+  CallScope scope(*this);
   cfg_.validate_for_world(world_);
   for (const ShardSpec& s : shards) check_shard(s, world_);
   if (world_ > 1 && !comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
   launches_ = 0;
   ev_record(0);
+  span_reset();
   const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
   const ExchangePlan P = plan_exchange(shards, cfg_, W, rank_);
   const std::vector<SegPlan>& plan = P.segs;
@@ -538,8 +650,11 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
     recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
   }
-  for (uint32_t o = 0; o < W; ++o)
-    if (skc[o]) cuda_check(cudaMemsetAsync(send_f + o * Bf, 0, skc[o] * 4, stream_), "sketch zero");
+  {
+    std::vector<std::pair<void*, uint64_t>> zr;
+    for (uint32_t o = 0; o < W; ++o) zr.push_back({send_f + o * Bf, skc[o] * 4});
+    zero(zr);
+  }
   const HashParams hp = make_hash_params(cfg_.seed, rows);
   std::vector<EncItem> enc;
   std::vector<CopyItem> pack, unpack;
@@ -567,12 +682,16 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     }
   }
   run_select_encode(enc, w == 4, hp, false, "nccl");
-  if (!pack.empty()) {
-    const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
-    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", pack.size() * sizeof(CopyItem), false, stream_));
-    upload(pack.data(), pack.size() * sizeof(CopyItem), d_pack);
-    launches_ += launch_copy_items(di_, d_pack, uint32_t(pack.size()), tt, stream_);
+  // raw segments: packed into the send blocks, or (W == 1) copied straight to
+  // the output; after this the gradient is no longer read
+  std::vector<CopyItem>& raw_now = W > 1 ? pack : unpack;
+  if (!raw_now.empty()) {
+    const uint64_t tt = copy_tiles(raw_now.data(), uint32_t(raw_now.size()));
+    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", raw_now.size() * sizeof(CopyItem), false, stream_));
+    upload(raw_now.data(), raw_now.size() * sizeof(CopyItem), d_pack);
+    launches_ += launch_copy_items(di_, d_pack, uint32_t(raw_now.size()), tt, stream_);
   }
+  if (grad_read_ev_) cuda_check(cudaEventRecord(grad_read_ev_, stream_), "grad-read event");
   if (W > 1) {
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
     nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
@@ -582,7 +701,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
     ledger_.wire_bytes += W * (Bf + Bu) * 4;
   }
-  ev_record(3);
+  ev_record(4);
   std::vector<DecItem> dec;
   for (const SegPlan& p : plan) {
     if (!p.compressed || shards[p.shard].owner != rank_) continue;
@@ -597,13 +716,13 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     dec.push_back(d);
   }
   run_decode(dec, hp, false, w == 1 && W > 1);
-  if (!unpack.empty()) {
+  if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
     upload(unpack.data(), unpack.size() * sizeof(CopyItem), d_un);
     launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_);
   }
-  ev_record(4);
+  ev_record(5);
   cuda_check(cudaGetLastError(), "nccl-world launch");
   uint64_t n_raw_owned = 0;
   for (const SegPlan& p : plan) {
@@ -639,6 +758,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
 }
 
 void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out) {
+  CallScope scope(*this);
   if (shards.size() != world_) throw InvalidArgument("baseline needs one shard per rank");
   const uint64_t L = shards[0].size();
   for (uint32_t i = 0; i < shards.size(); ++i) {
@@ -660,9 +780,68 @@ void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* 
                    s.size());
 }
 
+// ------------------------------------------------------------ host buffers
+void Engine::reduce_shards_host(const std::vector<ShardSpec>& shards, const float* host_grad,
+                                float* acc, float* host_out, PeelStats* stats) {
+  CallScope scope(*this);
+  if (!host_grad || !host_out) throw InvalidArgument("null host buffer");
+  if (!h2d_) {
+    cuda_check(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "h2d stream");
+    cuda_check(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "d2h stream");
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&hev_in_[i], &hev_gfree_[i], &hev_dec_[i], &hev_out_[i]})
+        cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "host event");
+    cuda_check(cudaEventCreateWithFlags(&hev_join_, cudaEventDisableTiming), "host event");
+  }
+  uint64_t total = 0, owned = 0;
+  for (const ShardSpec& sh : shards) {
+    total = std::max<uint64_t>(total, sh.end);
+    if (sh.owner == rank_) owned += sh.size();
+  }
+  if (total * 4 > host_grad_cap_ || owned * 4 > host_out_cap_) {
+    // the double buffers are about to move: nothing may still use them
+    cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
+    cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
+    cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+  }
+  const int s = int(host_calls_++ & 1);
+  auto* gdev = static_cast<float*>(ws_.get(s ? "host_grad1" : "host_grad0", total * 4, false, stream_));
+  auto* odev = static_cast<float*>(
+      ws_.get(s ? "host_out1" : "host_out0", std::max<uint64_t>(owned, 1) * 4, false, stream_));
+  host_grad_cap_ = std::max(host_grad_cap_, total * 4);
+  host_out_cap_ = std::max(host_out_cap_, owned * 4);
+  // H2D once the exchange two calls back has consumed this device buffer
+  cuda_check(cudaStreamWaitEvent(h2d_, hev_gfree_[s], 0), "wait gfree");
+  cuda_check(cudaMemcpyAsync(gdev, host_grad, total * 4, cudaMemcpyHostToDevice, h2d_), "H2D grad");
+  cuda_check(cudaEventRecord(hev_in_[s], h2d_), "record in");
+  cuda_check(cudaStreamWaitEvent(stream_, hev_in_[s], 0), "wait in");
+  cuda_check(cudaStreamWaitEvent(stream_, hev_out_[s], 0), "wait out");  // D2H two calls back done
+  grad_read_ev_ = hev_gfree_[s];
+  try {
+    reduce_shards(shards, gdev, acc, odev, stats);
+  } catch (...) {
+    grad_read_ev_ = nullptr;
+    throw;
+  }
+  grad_read_ev_ = nullptr;
+  cuda_check(cudaEventRecord(hev_dec_[s], stream_), "record dec");
+  cuda_check(cudaStreamWaitEvent(d2h_, hev_dec_[s], 0), "wait dec");
+  if (owned)
+    cuda_check(cudaMemcpyAsync(host_out, odev, owned * 4, cudaMemcpyDeviceToHost, d2h_), "D2H out");
+  cuda_check(cudaEventRecord(hev_out_[s], d2h_), "record out");
+  if (stats) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
+}
+
+void Engine::host_join() {
+  if (!d2h_) return;
+  cuda_check(cudaEventRecord(hev_join_, d2h_), "record join");
+  cuda_check(cudaStreamWaitEvent(stream_, hev_join_, 0), "wait join");
+}
+
 // ------------------------------------------------------------------ codec API
 void Engine::sparsify(const float* g, uint32_t n, double theta, float* sparse, float* residual,
                       float* tau, uint64_t* zero_count) {
+  CallScope scope(*this);
   if (!(theta >= 0.0 && theta <= 100.0))
     throw InvalidArgument("sparsification threshold must lie in [0, 100]");  // sparsify.cpp:19-20
   if (n == 0) throw InvalidArgument("sparsify: empty gradient");             // :21
@@ -689,6 +868,7 @@ void Engine::sparsify(const float* g, uint32_t n, double theta, float* sparse, f
 }
 
 void Engine::index_create(const float* v, uint32_t n, uint32_t width, uint32_t* words) {
+  CallScope scope(*this);
   if (width != 1 && width != 4) throw InvalidArgument("index width must be 1 or 4");
   if (n == 0) throw InvalidArgument("index needs at least one position");
   launches_ = 0;
@@ -702,6 +882,7 @@ void Engine::index_create(const float* v, uint32_t n, uint32_t width, uint32_t* 
 
 void Engine::merge_indices(const uint32_t* const* words, uint32_t world, uint32_t n_words,
                            uint32_t* out) {
+  CallScope scope(*this);
   if (world == 0) throw InvalidArgument("merge_indices: no inputs");
   launches_ = 0;
   auto* d = static_cast<const uint32_t**>(ws_.get("merge_ptrs", world * 8, false, stream_));
@@ -711,6 +892,7 @@ void Engine::merge_indices(const uint32_t* const* words, uint32_t world, uint32_
 
 void Engine::index_presence(const uint32_t* words, uint32_t n, uint32_t width, uint32_t* positions,
                             uint32_t* count) {
+  CallScope scope(*this);
   if (width != 1 && width != 4) throw InvalidArgument("index width must be 1 or 4");
   if (n == 0) throw InvalidArgument("index needs at least one position");
   launches_ = 0;
@@ -726,6 +908,7 @@ void Engine::index_presence(const uint32_t* words, uint32_t n, uint32_t width, u
 
 void Engine::sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t rows,
                              uint64_t seed, float* sketch) {
+  CallScope scope(*this);
   if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
   const SketchGeometry g = sketch_geometry(n, ratio, rows);
   launches_ = 0;
@@ -747,6 +930,7 @@ void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32
                                 uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
                                 float* values, uint32_t* unresolved, uint32_t* n_unresolved,
                                 double* pf) {
+  CallScope scope(*this);
   if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
   const SketchGeometry g = sketch_geometry(n, ratio, rows);
   launches_ = 0;
@@ -793,6 +977,7 @@ void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32
 void Engine::estimation_decompress(const uint32_t* presence, uint32_t count, uint32_t n,
                                    uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
                                    const uint32_t* targets, uint32_t n_targets, float* out) {
+  CallScope scope(*this);
   if (rows > kMaxRows) throw InvalidArgument("sketch_rows above 8 is not supported on device");
   const SketchGeometry g = sketch_geometry(n, ratio, rows);
   launches_ = 0;

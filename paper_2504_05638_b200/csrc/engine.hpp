@@ -83,8 +83,14 @@ class Engine {
   uint64_t workspace_bytes() const { return ws_.bytes(); }
   void init_nccl(const uint8_t id[128]);
   void set_timing(bool on) { timing_ = on; }
-  void last_timing(float out[4]) const;
+  // stage times (ms) of the last call: prep, select+fused pass, select finish, exchange, decode
+  static constexpr int kStages = 5;
+  void last_timing(float out[kStages]) const;
   uint64_t last_launches() const { return launches_; }
+  // timing mode: device execution spans (ms) of the last call's sampled
+  // select + fused pass (k_sample start .. k_fused end) and decode (k_build
+  // start .. k_final end), from %globaltimer stamps written by the kernels
+  void last_kernel_spans(float out_ms[2]);
   // peel rounds of the last decode that returned stats: {grid rounds, single-CTA tail rounds}
   void last_peel_rounds(uint32_t out[2]) const { out[0] = rounds_[0]; out[1] = rounds_[1]; }
 
@@ -97,6 +103,15 @@ class Engine {
   void reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                      float* out, PeelStats* stats);
   void baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out);
+  // Host-buffer form of reduce_shards (the end-to-end call): the gradient is
+  // copied H2D on a copy stream into one of two device buffers, the owner's
+  // decoded shard D2H on a second copy stream from one of two device buffers,
+  // so consecutive calls overlap D2H(k), H2D(k+1) and the exchange itself.
+  // host_out is complete once host_join() (or sync_check) has run.
+  void reduce_shards_host(const std::vector<ShardSpec>& shards, const float* host_grad, float* acc,
+                          float* host_out, PeelStats* stats);
+  // The context stream waits for every copy the host-buffer path enqueued.
+  void host_join();
 
   // Per-stage codec entry points (single vector).
   void sparsify(const float* g, uint32_t n, double theta, float* sparse, float* residual,
@@ -119,12 +134,35 @@ class Engine {
 
  private:
   struct EncBatch;
+  friend struct CallScope;
+  // Descriptor uploads go through pinned staging (a pageable cudaMemcpyAsync
+  // would synchronise the stream): two halves, one per public call, each
+  // reused only after the call that last filled it has finished on the GPU.
+  struct Staging {
+    char* ptr = nullptr;  // mapped pinned host memory
+    char* dev = nullptr;  // its device alias
+    size_t cap = 0, off = 0;
+    cudaEvent_t ev = nullptr;
+  };
+  Staging stage_[2];
+  int stage_cur_ = 0, call_depth_ = 0;
+  void call_begin();
+  void call_end();
+  // host-buffer path (reduce_shards_host)
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  cudaEvent_t hev_in_[2] = {}, hev_gfree_[2] = {}, hev_dec_[2] = {}, hev_out_[2] = {}, hev_join_ = nullptr;
+  uint64_t host_calls_ = 0, host_grad_cap_ = 0, host_out_cap_ = 0;
+  cudaEvent_t grad_read_ev_ = nullptr;  // recorded by reduce_shards once the gradient is consumed
   void run_select_encode(std::vector<EncItem>& items, bool w4, const HashParams& hp,
                          bool want_kept, const char* tag);
   void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
                   bool ordered);
   void upload(const void* host, size_t bytes, void* dev);
+  // zero byte ranges with one kernel launch (no copy-engine memset)
+  void zero(const std::vector<std::pair<void*, uint64_t>>& ranges);
   void ev_record(int i);
+  void span_reset();
+  unsigned long long* spans_ = nullptr;
   uint32_t* err_flag();
 
   CompressionConfig cfg_;
@@ -138,7 +176,7 @@ class Engine {
   Workspace ws_;
   TrafficLedger ledger_;
   bool timing_ = false;
-  cudaEvent_t ev_[5] = {};
+  cudaEvent_t ev_[kStages + 1] = {};
   uint64_t launches_ = 0;
   // host mirrors of the last decode's per-item stats (device -> host)
   std::vector<DecStats> dec_stats_;

@@ -25,7 +25,8 @@ struct DevInfo {
 int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
                         int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
-                        uint2* hi_pool, uint32_t* err, cudaStream_t stream);
+                        uint2* hi_pool, uint32_t* err, cudaStream_t stream,
+                        unsigned long long* span = nullptr);
 // Exact tau from the window candidates, fix-up of the candidates, and the
 // (normally idle) restore + radix-select + re-encode fallback chain.
 int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
@@ -36,6 +37,20 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
 int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, const HashParams& hp, const uint32_t* err, bool w4,
                         cudaStream_t stream);
+
+// ------------------------------------------------------- plumbing kernels
+// Zero up to kZeroRanges byte ranges in one launch, and copy bytes from mapped
+// pinned host memory. Both run on the SMs, so the context stream never queues
+// behind a bulk transfer on a copy engine (the host-buffer path keeps the
+// copy engines busy with gradient / result transfers).
+constexpr int kZeroRanges = 8;
+struct ZeroRanges {
+  void* ptr[kZeroRanges];
+  uint64_t bytes[kZeroRanges];
+  int n;
+};
+int launch_zero(const ZeroRanges& r, cudaStream_t stream);
+int launch_stage_copy(void* dst, const void* mapped_src, uint64_t bytes, cudaStream_t stream);
 
 // ------------------------------------------------------- elementwise / sums
 // out[i] = sum_{r<world} in[r][i], ascending rank order (reference rank_sum,
@@ -100,6 +115,7 @@ struct DecodeWork {
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
+  unsigned long long* span;        // optional: execution span of build .. final (timing mode)
 };
 // Peel + estimate. Zero-fills each item's `out`, rebuilds bucket state from
 // the merged index, peels in synchronous rounds inside one cooperative
