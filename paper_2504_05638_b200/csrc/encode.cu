@@ -492,6 +492,327 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
   span_end(span);
 }
 
+
+// --------------------------------------------------------------- fused pass (TMA)
+// The same single pass as k_fused for the exchange path (accumulator in/out),
+// restructured around bulk async copies (cp.async.bulk, the 1-D TMA path):
+// one persistent CTA per SM = one producer warp + kConsumerWarps consumer
+// warps sharing a kFusedStages-deep ring of 32 KB stages (a 4096-element tile
+// of g and of acc). The producer keeps the ring full (full/empty mbarriers,
+// no CTA-wide barrier per tile), so HBM sees a steady stream of 16 KB
+// requests while the consumers classify tiles out of shared memory. Items must
+// be 16-byte aligned (the host checks); a tile's last <16 bytes are read
+// directly from global memory.
+constexpr int kFusedStages = 6;
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kFusedThreads = kConsumers + 32;
+constexpr int kQuads = kTile / 4 / kConsumers;  // quads (4 elements) per consumer thread per tile
+constexpr uint32_t kWarpStageT = 64;
+struct alignas(128) FusedStage {
+  float g[kTile];
+  float a[kTile];
+};
+constexpr size_t kFusedSmem = size_t(kFusedStages) * sizeof(FusedStage) + 2 * kFusedStages * 8 + 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier; the streamed operands
+// are marked evict-first in L2 so the sketch rows being scattered into stay hot
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* b, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+template <bool kW4>
+__global__ void __launch_bounds__(kFusedThreads, 1) k_fused_tma(const EncItem* __restrict__ items,
+                                                                SelState* __restrict__ state,
+                                                                uint32_t n_items, uint64_t total_tiles,
+                                                                const HashParams hp,
+                                                                uint2* __restrict__ cand,
+                                                                uint2* __restrict__ hi_pool,
+                                                                uint32_t* __restrict__ fine_hist,
+                                                                uint32_t* __restrict__ err,
+                                                                unsigned long long* span) {
+  extern __shared__ __align__(128) unsigned char fsm[];
+  FusedStage* stg = reinterpret_cast<FusedStage*>(fsm);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(fsm + size_t(kFusedStages) * sizeof(FusedStage));
+  unsigned long long* empty = full + kFusedStages;
+  __shared__ uint2 s_cand[kConsumerWarps][kWarpStageT];
+  __shared__ uint2 s_kept[kConsumerWarps][kWarpStageT];
+  __shared__ uint32_t s_hist[kRadixBins];
+  __shared__ uint32_t s_zero, s_lo;
+  span_begin(span);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t t0, t1;
+  cta_range(total_tiles, t0, t1);
+  if (t0 >= t1) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFusedStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {  // ------------------------------ producer warp
+    if (lane == 0) {
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      uint32_t pit = find_tile_item(items, n_items, t0);
+      uint32_t i = 0;
+      for (uint64_t tile = t0; tile < t1; ++tile, ++i) {
+        while (tile >= items[pit].tile_begin + (uint64_t(items[pit].n) + kTile - 1) / kTile) ++pit;
+        const EncItem& pe = items[pit];
+        const int s = int(i % kFusedStages);
+        if (i >= uint32_t(kFusedStages)) mbar_wait(&empty[s], ((i / kFusedStages) - 1) & 1u);
+        const uint32_t start = uint32_t(tile - pe.tile_begin) * kTile;
+        const uint32_t len = min(kTile, pe.n - start);
+        const uint32_t bytes = (len * 4u) & ~15u;
+        mbar_arrive_expect_tx(&full[s], 2u * bytes);
+        if (bytes) {
+          bulk_g2s(stg[s].g, pe.g + start, bytes, &full[s], policy);
+          bulk_g2s(stg[s].a, pe.acc + start, bytes, &full[s], policy);
+        }
+      }
+    }
+    span_end(span);
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const uint32_t ctid = threadIdx.x;
+  bool nan = false;
+  uint32_t iter = 0;
+  uint32_t it = find_tile_item(items, n_items, t0);
+  for (uint64_t tile = t0; tile < t1;) {
+    const EncItem e = items[it];
+    const uint64_t item_end = e.tile_begin + (uint64_t(e.n) + kTile - 1) / kTile;
+    const uint64_t tend = item_end < t1 ? item_end : t1;
+    const uint32_t klo = state[it].klo, khi = state[it].khi, fshift = state[it].fshift;
+    const uint32_t n_words = kW4 ? (e.n + 7u) / 8u : (e.n + 31u) / 32u;
+    for (uint32_t i = ctid; i < kRadixBins; i += kConsumers) s_hist[i] = 0;
+    if (ctid == 0) s_zero = s_lo = 0;
+    consumer_sync();
+    uint32_t c_zero = 0, c_lo = 0, wc = 0, wk = 0;
+    auto flush_cand = [&]() {
+      __syncwarp();
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&state[it].cnt_in, wc);
+      base = __shfl_sync(kFull, base, 0);
+      for (uint32_t i = lane; i < wc; i += 32)
+        if (base + i < e.cand_cap) cand[e.cand_off + base + i] = s_cand[warp][i];
+      __syncwarp();
+      wc = 0;
+    };
+    auto flush_kept = [&]() {
+      __syncwarp();
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&state[it].cnt_hi, wk);
+      base = __shfl_sync(kFull, base, 0);
+      for (uint32_t i = lane; i < wk; i += 32) {
+        const uint2 kv = s_kept[warp][i];
+        const float v = __uint_as_float(kv.y);
+        scatter_sketch(e, hp, kv.x, v);
+        if (base + i < e.hi_cap) hi_pool[e.hi_off + base + i] = kv;
+        else e.acc[kv.x] = v;  // pool full (bracket miss): keep v recoverable
+      }
+      __syncwarp();
+      wk = 0;
+    };
+    for (; tile < tend; ++tile, ++iter) {
+      const int s = int(iter % kFusedStages);
+      const uint32_t start = uint32_t(tile - e.tile_begin) * kTile;
+      const uint32_t len = min(kTile, e.n - start);
+      mbar_wait(&full[s], (iter / kFusedStages) & 1u);
+      float* sg = stg[s].g;
+      const float* sa = stg[s].a;
+      float v[kQuads][4];
+      uint32_t hi_m = 0, lo_m = 0, z_m = 0, valid_m = (1u << (4 * kQuads)) - 1u;
+#pragma unroll
+      for (int k = 0; k < kQuads; ++k) {
+        const uint32_t e0 = 4u * (k * kConsumers + ctid);
+        if (e0 + 4 <= len) {
+          const float4 x = *reinterpret_cast<const float4*>(sg + e0);
+          const float4 y = *reinterpret_cast<const float4*>(sa + e0);
+          v[k][0] = x.x + y.x; v[k][1] = x.y + y.y; v[k][2] = x.z + y.z; v[k][3] = x.w + y.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool in = e0 + j < len;
+            v[k][j] = in ? __ldg(e.g + start + e0 + j) + e.acc[start + e0 + j] : 0.0f;
+            if (!in) valid_m &= ~(1u << (4 * k + j));
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t key = mag_key(v[k][j]);
+          const uint32_t bit = 1u << (4 * k + j);
+          hi_m |= key > khi ? bit : 0u;
+          lo_m |= key < klo ? bit : 0u;
+          z_m |= key == 0u ? bit : 0u;
+        }
+      }
+      hi_m &= valid_m;
+      lo_m &= valid_m;
+      z_m &= valid_m;
+      const uint32_t in_m = valid_m & ~hi_m & ~lo_m;
+      c_zero += __popc(z_m);
+      c_lo += __popc(lo_m & ~z_m);
+      // a thread with flagged elements parks its combined values in the stage
+      // (its own slots only) for the compaction below
+      if (in_m | hi_m) {
+#pragma unroll
+        for (int k = 0; k < kQuads; ++k)
+          *reinterpret_cast<float4*>(sg + 4u * (k * kConsumers + ctid)) =
+              make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+      }
+      const uint32_t cnt = uint32_t(__popc(in_m)) | (uint32_t(__popc(hi_m)) << 16);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= uint32_t(o)) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      const uint32_t tot_c = tot & 0xFFFFu, tot_k = tot >> 16;
+      const uint32_t pbase = start + 4u * ctid;  // element b = 4k + j -> pbase + k*4*kConsumers + j
+      if (tot_c) {
+        if (wc + tot_c > kWarpStageT) flush_cand();
+        const bool direct = tot_c > kWarpStageT;
+        uint32_t gbase = 0;
+        if (direct) {
+          if (lane == 0) gbase = atomicAdd(&state[it].cnt_in, tot_c);
+          gbase = __shfl_sync(kFull, gbase, 0);
+        }
+        uint32_t o = (incl - cnt) & 0xFFFFu;
+        for (uint32_t m = in_m; m; m &= m - 1) {
+          const uint32_t b = __ffs(m) - 1;
+          const uint32_t off = (b >> 2) * 4u * kConsumers + (b & 3u);
+          const float x = sg[4u * ctid + off];
+          const uint2 kv = make_uint2(pbase + off, __float_as_uint(x));
+          if (!direct) s_cand[warp][wc + o] = kv;
+          else if (gbase + o < e.cand_cap) cand[e.cand_off + gbase + o] = kv;
+          atomicAdd(&s_hist[(mag_key(x) - klo) >> fshift], 1u);
+          ++o;
+        }
+        if (!direct) wc += tot_c;
+      }
+      if (tot_k) {
+        if (wk + tot_k > kWarpStageT) flush_kept();
+        const bool direct = tot_k > kWarpStageT;
+        uint32_t gbase = 0;
+        if (direct) {
+          if (lane == 0) gbase = atomicAdd(&state[it].cnt_hi, tot_k);
+          gbase = __shfl_sync(kFull, gbase, 0);
+        }
+        uint32_t o = (incl - cnt) >> 16;
+        for (uint32_t m = hi_m; m; m &= m - 1) {
+          const uint32_t b = __ffs(m) - 1;
+          const uint32_t off = (b >> 2) * 4u * kConsumers + (b & 3u);
+          const float x = sg[4u * ctid + off];
+          nan |= mag_key(x) > 0x7F800000u;
+          const uint2 kv = make_uint2(pbase + off, __float_as_uint(x));
+          if (!direct) {
+            s_kept[warp][wk + o] = kv;
+          } else {
+            scatter_sketch(e, hp, kv.x, x);
+            if (gbase + o < e.hi_cap) hi_pool[e.hi_off + gbase + o] = kv;
+            else hi_m &= ~(1u << b);  // pool full: the element keeps v in place
+          }
+          ++o;
+        }
+        if (!direct) wk += tot_k;
+      }
+#pragma unroll
+      for (int k = 0; k < kQuads; ++k) {
+        const uint32_t qt = k * kConsumers + ctid;  // quad within the tile
+        const uint32_t e0 = 4u * qt;
+        const uint32_t nib = (hi_m >> (4 * k)) & 0xFu;
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = (nib >> j & 1u) ? 0.0f : v[k][j];
+        if (e0 + 4 <= len) {
+          __stcs(reinterpret_cast<float4*>(e.acc + start + e0), make_float4(r[0], r[1], r[2], r[3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (e0 + j < len) e.acc[start + e0 + j] = r[j];
+        }
+        const uint32_t q = start / 4u + qt;
+        if (kW4) {
+          if (q < 2u * n_words) {
+            const uint32_t hw = (nib & 1u) | (nib >> 1 & 1u) << 4 | (nib >> 2 & 1u) << 8 | (nib >> 3 & 1u) << 12;
+            reinterpret_cast<uint16_t*>(e.index)[q] = uint16_t(hw);
+          }
+        } else {
+          uint32_t x = nib << (4u * (lane & 7u));
+          x |= __shfl_xor_sync(kFull, x, 1);
+          x |= __shfl_xor_sync(kFull, x, 2);
+          x |= __shfl_xor_sync(kFull, x, 4);
+          if ((lane & 7u) == 0 && q / 8u < n_words) e.index[q / 8u] = x;
+        }
+      }
+      // parked values were generic-proxy writes into the stage: order them
+      // before the bulk copy that refills it, then release the stage
+      if (in_m | hi_m) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    __syncwarp();
+    if (wc) flush_cand();
+    if (wk) flush_kept();
+    c_zero = warp_sum(c_zero);
+    c_lo = warp_sum(c_lo);
+    if (lane == 0) {
+      if (c_zero) atomicAdd(&s_zero, c_zero);
+      if (c_lo) atomicAdd(&s_lo, c_lo);
+    }
+    consumer_sync();
+    uint32_t* fh = fine_hist + uint64_t(it) * kRadixBins;
+    for (uint32_t i = ctid; i < kRadixBins; i += kConsumers)
+      if (s_hist[i]) atomicAdd(fh + i, s_hist[i]);
+    if (ctid == 0) {
+      if (s_zero) atomicAdd(&state[it].cnt_zero, s_zero);
+      if (s_lo) atomicAdd(&state[it].cnt_lo, s_lo);
+    }
+    consumer_sync();
+    ++it;
+  }
+  if (nan) atomicOr(err, 1u);
+  span_end(span);
+}
+
 // Block-wide search over `kRadixBins` counters: finds the digit whose
 // inclusive prefix first exceeds `rank`; returns the digit and the count of
 // keys in lower digits.
@@ -1028,7 +1349,8 @@ int flat_grid(uint64_t n, int threads) {
 int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
                         int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
-                        uint2* hi_pool, uint32_t* err, cudaStream_t stream, unsigned long long* span) {
+                        uint2* hi_pool, uint32_t* err, cudaStream_t stream, unsigned long long* span,
+                        bool tma) {
   if (n_items == 0) return 0;
   int launches = 0;
   if (total_samples) {
@@ -1043,7 +1365,17 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
     kern<<<persistent_grid((const void*)kern, kTileThreads, di, total_tiles), kTileThreads, 0, stream>>>(
         items, state, n_items, total_tiles, hp, cand, hi_pool, fine_hist, err, span);
   };
-  if (w4 && hook) launch(k_fused<true, true>);
+  if (tma && hook) {
+    auto launch_tma = [&](auto kern) {
+      // opt-in to > 48 KB of dynamic shared memory (cheap; per launch keeps it per device)
+      cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
+      const uint64_t g = std::min<uint64_t>(uint64_t(di.sms), total_tiles);
+      kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
+                                                                 hi_pool, fine_hist, err, span);
+    };
+    if (w4) launch_tma(k_fused_tma<true>);
+    else launch_tma(k_fused_tma<false>);
+  } else if (w4 && hook) launch(k_fused<true, true>);
   else if (w4) launch(k_fused<true, false>);
   else if (hook) launch(k_fused<false, true>);
   else launch(k_fused<false, false>);

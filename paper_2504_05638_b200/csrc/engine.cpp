@@ -140,6 +140,7 @@ void* Workspace::get(const std::string& name, size_t bytes, bool zero_on_alloc, 
 Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int device,
                void* nccl_comm, void* stream)
     : cfg_(cfg), world_(world), rank_(rank), device_(device) {
+  if (const char* v = std::getenv("TAGC_FUSED_TMA")) use_tma_ = std::atoi(v) != 0;
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -371,11 +372,14 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     // hook items carry an accumulator; the per-stage sparsify entry writes
     // separate sparse/residual outputs (one kind per batch)
     const int per_stage = (items[0].flags & kHasAcc) ? 0 : 1;
+    bool all_aligned = true;  // bulk-copy staging needs 16-byte aligned g / acc
+    for (const EncItem& e : items) all_aligned = all_aligned && (e.flags & kAligned16);
     for (const EncItem& e : items)
       if (((e.flags & kHasAcc) ? 0 : 1) != per_stage) throw CudaError("mixed fused batch");
     ev_record(1);
     launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
-                                     cd, hp_pool, err, stream_, timing_ ? spans_ : nullptr);
+                                     cd, hp_pool, err, stream_, timing_ ? spans_ : nullptr,
+                                     use_tma_ && all_aligned);
     ev_record(2);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);

@@ -163,6 +163,7 @@ class Engine {
   void ev_record(int i);
   void span_reset();
   unsigned long long* spans_ = nullptr;
+  bool use_tma_ = true;  // TMA-staged fused pass (TAGC_FUSED_TMA=0 selects the register path)
   uint32_t* err_flag();
 
   CompressionConfig cfg_;
