@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.hpp"
@@ -118,19 +119,24 @@ __device__ __forceinline__ float median_rows(float (&e)[kMaxRows], uint32_t k) {
 }
 
 // ------------------------------------------------------------------ build
-// Contiguous range of word tiles per CTA (kWordTile words per tile, 4 words
-// per thread), bucket state updated with fire-and-forget 64-bit reductions.
-__global__ void __launch_bounds__(256) k_build(DecodeWork w, const HashParams hp) {
+// Contiguous range of word tiles per CTA (kWordTile words, 4 per thread).
+// Per tile: zero-fill the tile's output positions with coalesced 16-byte
+// streaming stores (each warp covers its 32 words' positions contiguously)
+// and append the present positions to the flat presence list in ascending
+// order (one block scan + one global atomic per tile). Bucket state is
+// accumulated from the list by k_accumulate, where every thread carries one
+// position (no per-word imbalance ahead of a block barrier).
+__global__ void __launch_bounds__(256) k_build(DecodeWork w) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_base;
   span_begin(w.span);
-  __shared__ uint32_t s_list[kStage];
-  __shared__ uint32_t s_nl, s_bl;
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t T = uint32_t(w.total_word_tiles), G = gridDim.x, b = blockIdx.x;
   const uint32_t chunk = T / G, extra = T % G;
   const uint32_t t0 = b * chunk + min(b, extra), t1 = t0 + chunk + (b < extra ? 1u : 0u);
   if (t0 >= t1) return;
-  if (threadIdx.x == 0) s_nl = 0;
-  __syncthreads();
+  constexpr uint32_t kPer = kWordTile / 256;
   uint32_t it = find_word_item(w.items, w.n_items, t0);
   for (uint32_t wt = t0; wt < t1; ++wt) {
     while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
@@ -138,195 +144,353 @@ __global__ void __launch_bounds__(256) k_build(DecodeWork w, const HashParams hp
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t P = w4 ? 8u : 32u;
     const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
-    // zero-fill the tile's positions (coalesced 4-byte stores)
-    {
-      const uint64_t p0 = uint64_t(wbase) * P;
-      const uint64_t p1 = min(uint64_t(e.n), p0 + uint64_t(kWordTile) * P);
-      for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) e.out[p] = 0.0f;
-    }
-    uint32_t bits[kWordTile / 256];
+    uint32_t bits[kPer];
+    uint32_t cnt = 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kWordTile / 256; ++k) {
+    for (uint32_t k = 0; k < kPer; ++k) {  // all word loads in flight before any store
       const uint32_t wi = wbase + k * 256 + threadIdx.x;
-      uint32_t x = 0;
-      if (wi < e.n_words) {
-        x = present_bits(__ldg(e.words + wi), w4);
-        const uint64_t first = uint64_t(wi) * P;
-        const uint64_t left = e.n > first ? e.n - first : 0;
-        if (w4) {
-          if (left < 8) x &= (1u << (4 * left)) - 1u;
-        } else if (left < 32) {
-          x &= (1u << left) - 1u;
-        }
+      bits[k] = wi < e.n_words ? __ldg(e.words + wi) : 0u;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint32_t wi = wbase + k * 256 + threadIdx.x;
+      uint32_t x = present_bits(bits[k], w4);
+      const uint64_t first = uint64_t(wi) * P;
+      const uint64_t left = e.n > first ? e.n - first : 0;
+      if (w4) {
+        if (left < 8) x &= left ? (1u << (4 * left)) - 1u : 0u;
+      } else if (left < 32) {
+        x &= left ? (1u << left) - 1u : 0u;
       }
       bits[k] = x;
+      cnt += __popc(x);
     }
+    const bool vec = (reinterpret_cast<uintptr_t>(e.out) & 15u) == 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kWordTile / 256; ++k) {
-      const uint32_t wi = wbase + k * 256 + threadIdx.x;
-      uint32_t x = bits[k];
-      while (x) {
-        const uint32_t bb = __ffs(x) - 1;
-        x &= x - 1;
-        const uint32_t p = wi * P + (w4 ? bb / 4 : bb);
-        const uint32_t li = atomicAdd(&s_nl, 1u);
-        if (li < kStage) {
-          s_list[li] = p;
+    for (uint32_t k = 0; k < kPer; ++k) {  // zero-fill this warp's 32 words' positions
+      const uint64_t r0 = uint64_t(wbase + k * 256 + warp * 32) * P;
+      const uint64_t r1 = r0 + 32ull * P;
+      if (r0 < e.n) {
+        if (vec && r1 <= e.n) {
+          float4* o = reinterpret_cast<float4*>(e.out + r0);
+          for (uint32_t q = lane; q < 8u * P; q += 32) __stcs(o + q, make_float4(0.f, 0.f, 0.f, 0.f));
         } else {
-          atomicAdd(&w.stats[it].presence, 1u);
-          const uint32_t gi = atomicAdd(&w.qcount[5], 1u);
-          w.plist[gi] = p;
-          w.pitem[gi] = it;
-        }
-        _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-          const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-          atomicAdd(w.slot_state + slot, st_add(p));  // result unused: RED.ADD.64
+          const uint64_t end = r1 < e.n ? r1 : e.n;
+          for (uint64_t p = r0 + lane; p < end; p += 32) e.out[p] = 0.0f;
         }
       }
     }
-    __syncthreads();
-    const bool item_ends = wt + 1 == t1 || (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt + 1);
-    if (item_ends || s_nl >= kStage / 2) {  // flush the staged presence list
+    uint32_t off, total;
+    Scan(scan_tmp).ExclusiveSum(cnt, off, total);
+    if (total) {
       if (threadIdx.x == 0) {
-        const uint32_t nl = min(s_nl, kStage);
-        if (nl) atomicAdd(&w.stats[it].presence, nl);
-        s_bl = nl ? atomicAdd(&w.qcount[5], nl) : 0;
-        s_nl = nl;
+        s_base = atomicAdd(&w.qcount[5], total);
+        atomicAdd(&w.stats[it].presence, total);
       }
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < s_nl; i += blockDim.x) {
-        w.plist[s_bl + i] = s_list[i];
-        w.pitem[s_bl + i] = it;
+      uint32_t j = s_base + off;
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k) {
+        const uint32_t wi = wbase + k * 256 + threadIdx.x;
+        for (uint32_t x = bits[k]; x; x &= x - 1) {
+          const uint32_t bb = __ffs(x) - 1;
+          w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
+          w.pitem[j] = it;
+          ++j;
+        }
       }
-      __syncthreads();
-      if (threadIdx.x == 0) s_nl = 0;
-      __syncthreads();
+    }
+    __syncthreads();  // scan storage / s_base reuse
+  }
+}
+
+// Bucket state from the presence list: (position, 1) into every row's bucket
+// with fire-and-forget 64-bit reductions.
+__global__ void __launch_bounds__(256) k_accumulate(DecodeWork w, const HashParams hp) {
+  const uint32_t total = w.qcount[5];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t p = w.plist[i];
+    const DecItem& e = w.items[w.pitem[i]];
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+      atomicAdd(w.slot_state + slot, st_add(p));  // result unused: RED.ADD.64
     }
   }
-  (void)lane;
 }
 
 // ------------------------------------------------------------------ peel
-// Next-frontier pushes are staged in shared memory per CTA (warp-aggregated)
-// and flushed with one global atomic per CTA per phase; a single queue
-// counter hit by every warp serialises at one L2 slice otherwise.
-constexpr uint32_t kPushStage = 8192;
-
-__device__ __forceinline__ void push_slot(bool push, uint32_t s, uint32_t* s_q, uint32_t* s_nq,
-                                          uint32_t* nq, uint32_t* ncount, uint32_t lane) {
+// Staged appends: warp-aggregated into a per-CTA shared-memory stage and
+// flushed with one global atomic per CTA; a single list counter hit by every
+// warp serialises at one L2 slice otherwise. s_n[0] = reserved entries,
+// s_n[1] = end of the contiguous written prefix (an overflowing warp goes
+// straight to the global list).
+template <typename T, uint32_t kCap>
+__device__ __forceinline__ void stage_push(bool push, T val, T* s_buf, uint32_t* s_n, T* g_buf,
+                                           uint32_t* g_count, uint32_t lane) {
   const uint32_t mask = __ballot_sync(kFull, push);
   if (!mask) return;
   const uint32_t leader = __ffs(mask) - 1, cnt = __popc(mask);
   uint32_t b = 0, direct = 0;
   if (lane == leader) {
-    b = atomicAdd(s_nq, cnt);
-    if (b + cnt > kPushStage) {  // stage full: straight to the global frontier
-      if (b < kPushStage) atomicMin(s_nq + 1, b);  // [b, stage) stays unwritten
+    b = atomicAdd(s_n, cnt);
+    if (b + cnt > kCap) {
+      if (b < kCap) atomicMin(s_n + 1, b);  // [b, cap) stays unwritten
       direct = 1;
-      b = atomicAdd(ncount, cnt);
+      b = atomicAdd(g_count, cnt);
     }
   }
   b = __shfl_sync(kFull, b, leader);
   direct = __shfl_sync(kFull, direct, leader);
   if (push) {
     const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
-    if (direct) nq[idx] = s;
-    else s_q[idx] = s;
+    if (direct) g_buf[idx] = val;
+    else s_buf[idx] = val;
   }
 }
 
-__device__ __forceinline__ void flush_pushes(uint32_t* s_q, uint32_t* s_nq, uint32_t* s_base,
-                                             uint32_t* nq, uint32_t* ncount) {
+template <typename T, uint32_t kCap>
+__device__ __forceinline__ void stage_flush(T* s_buf, uint32_t* s_n, uint32_t* s_base, T* g_buf,
+                                            uint32_t* g_count) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t n = min(min(s_nq[0], kPushStage), s_nq[1]);
-    *s_base = n ? atomicAdd(ncount, n) : 0u;
-    s_nq[0] = n;
+    const uint32_t n = min(min(s_n[0], kCap), s_n[1]);
+    *s_base = n ? atomicAdd(g_count, n) : 0u;
+    s_n[0] = n;
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < s_nq[0]; i += blockDim.x) nq[*s_base + i] = s_q[i];
+  for (uint32_t i = threadIdx.x; i < s_n[0]; i += blockDim.x) g_buf[*s_base + i] = s_buf[i];
   __syncthreads();
   if (threadIdx.x == 0) {
-    s_nq[0] = 0;
-    s_nq[1] = kPushStage;
+    s_n[0] = 0;
+    s_n[1] = kCap;
   }
   __syncthreads();
 }
 
-// Phase 1: claim singleton buckets of the current frontier.
-__device__ __forceinline__ void peel_phase1(const DecodeWork& w, const HashParams& hp,
-                                            uint32_t cur, uint32_t qlen, uint64_t start,
-                                            uint64_t stride) {
-  uint32_t* q = w.queue[cur];
-  for (uint64_t i = start; i < qlen; i += stride) {
-    const uint32_t slot = ldcg(q + i);
-    const unsigned long long st = ldcg(w.slot_state + slot);
-    if (st_count(st) != 1u) continue;  // stale (decode.cpp:106)
-    const uint32_t p = st_pos(st);
-    const uint32_t it = find_slot_item(w.items, w.n_items, slot);
-    const DecItem e = w.items[it];
-    const uint64_t local = slot - e.slot_base;
-    const uint32_t row = uint32_t(local / e.m);
-    const float v = canonical(dev_sign(row_coef(hp, row), p) * ldcg(e.sketch + local));  // :110-111
-    uint32_t* word = w.bitmap + e.bitmap_off + (p >> 5);
-    const uint32_t bit = 1u << (p & 31);
-    if (atomicOr(word, bit) & bit) continue;  // p already claimed via another row
-    __stcg(e.out + p, v);
-    q[i] = slot | kWinner;
-    atomicAdd(&w.qcount[4], 1u);
-  }
+constexpr uint32_t kPushStage = 8192;  // next-frontier slots per CTA
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// Phase 2: subtract each claimed position from all k rows (decode.cpp:115-121),
-// pushing buckets whose count drops to one onto the next frontier.
-__device__ __forceinline__ void peel_phase2(const DecodeWork& w, const HashParams& hp,
-                                            uint32_t cur, uint32_t qlen, uint64_t start,
-                                            uint64_t stride, uint32_t* s_q, uint32_t* s_nq,
-                                            uint32_t* s_base) {
+// Item of a global slot id: the items' slot bases are cached in shared
+// memory when they fit (binary search in L1/L2 otherwise).
+constexpr uint32_t kPeelItemsSmem = 512;
+struct SlotItems {
+  const unsigned long long* sbase;  // shared copy, or nullptr
+  const DecItem* items;
+  uint32_t n;
+  __device__ __forceinline__ uint32_t find(uint64_t s) const {
+    uint32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      const uint64_t b = sbase ? sbase[mid] : items[mid].slot_base;
+      if (b <= s) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+};
+
+__device__ __forceinline__ uint32_t slot_row(uint64_t local, uint32_t m) {
+  uint32_t row = 0;
+  while (local >= m) {
+    local -= m;
+    ++row;
+  }
+  return row;
+}
+
+// Round 0 runs as two ordinary (full-occupancy) kernels over the bucket
+// state as it stands after k_accumulate; the cooperative k_peel then takes
+// the frontier rounds.
+//   k_r0_phase1 (round0_phase1 below, shared with the ordered peel): every
+//     present position inspects its k buckets and peels from its lowest
+//     singleton row, recording its value and the rows it shares;
+//   k_r0_subtract: every peeled position leaves the buckets it shares
+//     (decode.cpp:115-121); buckets whose count drops to one seed round 1
+//     (queue 1, frontier counter qcount[9]). Buckets that held only the
+//     peeled position are left alone: nothing reads them again.
+__device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
+                                              uint64_t start, uint64_t stride);
+
+__global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashParams hp) {
+  __shared__ uint32_t s_q[kPushStage];
+  __shared__ uint32_t s_n[2], s_base;
+  if (threadIdx.x == 0) {
+    s_n[0] = 0;
+    s_n[1] = kPushStage;
+  }
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t* q = w.queue[cur];
-  uint32_t* nq = w.queue[cur ^ 1];
-  uint32_t* ncount = &w.qcount[cur ^ 1];
-  // warp-uniform trip count so pushes can be warp-aggregated
-  const uint64_t wstart = start - lane;
-  for (uint64_t base = wstart; base < qlen; base += stride) {
+  const uint32_t total = ldcg(&w.qcount[5]);
+  uint32_t* nq = w.queue[1];
+  uint32_t* ncount = &w.qcount[9];
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < total; base += stride) {
     const uint64_t i = base + lane;
-    uint32_t slot = 0, p = 0;
+    uint32_t p = 0, rows = 0;
     float v = 0.0f;
-    DecItem e{};
-    bool win = false;
-    if (i < qlen) {
-      const uint32_t x = ldcg(q + i);
-      if (x & kWinner) {
-        win = true;
-        slot = x & ~kWinner;
-        p = st_pos(ldcg(w.slot_state + slot));
-        const uint32_t it = find_slot_item(w.items, w.n_items, slot);
-        e = w.items[it];
-        v = ldcg(e.out + p);
+    const DecItem* e = w.items;
+    if (i < total) {
+      const uint2 info = __ldcs(w.pinfo + i);
+      if (info.y & 0x100u) {
+        rows = info.y & 0xFFu;
+        v = __uint_as_float(info.x);
+        p = __ldcs(w.plist + i);
+        e = w.items + __ldcs(w.pitem + i);
       }
+    }
+    unsigned long long old[kMaxRows];
+    uint64_t loc[kMaxRows];
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      const bool sh = (rows >> r) & 1u;
+      loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m) : 0;
+      old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(p)) : 0ull;
+      if (sh) atomicAdd(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
+    }
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
+      stage_push<uint32_t, kPushStage>(st_count(old[r]) == 2u, uint32_t(e->slot_base + loc[r]), s_q, s_n, nq,
+                                       ncount, lane);
+  }
+  stage_flush<uint32_t, kPushStage>(s_q, s_n, &s_base, nq, ncount);
+}
+
+// Rounds >= 1, single-phase over the frontier: a slot holding exactly one
+// position p (decode.cpp:104-106) claims p (a position reachable through
+// several singleton slots is claimed once), reads value = sign * residual
+// into the output and removes p from its other buckets, pushing buckets whose
+// count drops to one onto the next frontier. Claims, reads and subtractions
+// of one round run concurrently: a remover updates the residual before it
+// decrements the count (fence in between) and a reader acquires the count
+// before it reads the residual, so a bucket seen holding one position shows
+// exactly that position's residual. The peeled set is the complement of the
+// 2-core either way (order-independent); values match the reference's FIFO
+// peel within fp32 reassociation.
+__device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const HashParams& hp,
+                                                  const SlotItems& si, const uint32_t* q, uint32_t total,
+                                                  uint64_t start, uint64_t stride, uint32_t* s_q,
+                                                  uint32_t* s_nq, uint32_t* nq, uint32_t* ncount) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t won = 0;
+  for (uint64_t base = start - lane; base < total; base += stride) {
+    const uint64_t i = base + lane;
+    bool win = false;
+    uint32_t p = 0, row = 0;
+    float v = 0.0f;
+    const DecItem* e = w.items;
+    if (i < total) {
+      const uint32_t slot = ldcg(q + i);
+      const unsigned long long st = ld_acquire(w.slot_state + slot);
+      if (st_count(st) == 1u) {
+        p = st_pos(st);
+        e = w.items + si.find(slot);
+        const uint64_t local = slot - e->slot_base;
+        row = slot_row(local, e->m);
+        const uint32_t bit = 1u << (p & 31);
+        if (!(atomicOr(w.bitmap + e->bitmap_off + (p >> 5), bit) & bit)) {
+          win = true;
+          float sg = 0.0f;
+          _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
+          v = canonical(sg * ldcg(e->sketch + local));
+          __stcg(e->out + p, v);
+        }
+      }
+    }
+    if (win) {
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && r != row)
+        atomicAdd(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m), -(dev_sign(hp.row[r], p) * v));
+      __threadfence();  // residual updates before the count decrements
+      ++won;
     }
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
       bool push = false;
       uint64_t s = 0;
-      if (win) {
-        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-        s = e.slot_base + local;
-        if (s != slot) {  // the winner's own bucket held only p: leave it
-          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
-          push = st_count(old) == 2u;
-        }
+      if (win && r != row) {
+        s = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+        push = st_count(old) == 2u;
       }
-      push_slot(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
+      stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
     }
   }
-  flush_pushes(s_q, s_nq, s_base, nq, ncount);
+  return won;
 }
 
-// Round 0, position-centric: every present position inspects its k buckets
-// at round start and peels from its first singleton row (lowest slot id, the
-// reference's ascending seed order, decode.cpp:96-99).
+// Frontier counters rotate over three words (qcount[8..10]): round k reads
+// counter k%3, pushes into (k+1)%3, and thread 0 clears (k+2)%3, which no
+// thread touches during round k. Queue buffers alternate. Round 0 (k = 0)
+// was k_r0_phase1 / k_r0_subtract, which left round 1's frontier in queue 1
+// / qcount[9].
+__global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams hp) {
+  __shared__ uint32_t s_q[kPushStage];
+  __shared__ unsigned long long s_sbase[kPeelItemsSmem];
+  __shared__ uint32_t s_nq[2], s_base;
+  if (threadIdx.x == 0) {
+    s_nq[0] = 0;
+    s_nq[1] = kPushStage;
+  }
+  const bool cache = w.n_items <= kPeelItemsSmem;
+  if (cache)
+    for (uint32_t i = threadIdx.x; i < w.n_items; i += blockDim.x) s_sbase[i] = w.items[i].slot_base;
+  __syncthreads();
+  const SlotItems si{cache ? s_sbase : nullptr, w.items, w.n_items};
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t* cnt = w.qcount + 8;
+  uint32_t* const qbuf0 = w.queue[0];  // selected by value: a runtime index into the parameter
+  uint32_t* const qbuf1 = w.queue[1];  // struct would copy it to local memory
+  auto qbuf = [&](uint32_t k) { return (k & 1) ? qbuf1 : qbuf0; };
+  int mk = 0;
+  PEEL_MARK(mk++);
+  if (gtid == 0) w.qcount[2] = 1;
+  uint32_t won = 0, k = 1;
+  bool tail = false;
+  for (;; ++k) {
+    if (k > 1) grid.sync();
+    PEEL_MARK(mk++);
+    const uint32_t qlen = ldcg(&cnt[k % 3]);
+    if (qlen == 0) break;
+    if (qlen <= kTail) {  // every CTA sees the same qlen
+      tail = true;
+      break;
+    }
+    if (gtid == 0) {
+      cnt[(k + 2) % 3] = 0;
+      w.qcount[2] += 1;
+    }
+    won += frontier_pass(w, hp, si, qbuf(k), qlen, gtid, gstride, s_q, s_nq, qbuf(k + 1), &cnt[(k + 1) % 3]);
+    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf(k + 1), &cnt[(k + 1) % 3]);
+  }
+  won = warp_sum32(won);
+  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (!tail || blockIdx.x != 0) return;
+  // ---- tail: one CTA finishes with block barriers
+  won = 0;
+  for (;; ++k) {
+    __syncthreads();
+    const uint32_t qlen = ldcg(&cnt[k % 3]);
+    if (qlen == 0) break;
+    if (threadIdx.x == 0) {
+      cnt[(k + 2) % 3] = 0;
+      w.qcount[3] += 1;
+    }
+    won += frontier_pass(w, hp, si, qbuf(k), qlen, threadIdx.x, blockDim.x, s_q, s_nq, qbuf(k + 1),
+                         &cnt[(k + 1) % 3]);
+    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf(k + 1), &cnt[(k + 1) % 3]);
+    __threadfence();
+    PEEL_MARK(mk++);
+  }
+  won = warp_sum32(won);
+  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
+}
+
+// Round 0 of the ordered (FIFO-emulating) peel, position-centric: every
+// present position inspects its k buckets and peels from its first singleton
+// row (lowest slot id, the reference's ascending seed order, decode.cpp:96-99).
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
                                               uint64_t start, uint64_t stride) {
   uint32_t won = 0;
@@ -350,9 +514,9 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
 #pragma unroll
     for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
       if (r >= hp.rows) continue;
-      const uint32_t cnt = st_count(st[r]);
-      shared |= uint32_t(cnt >= 2u) << r;
-      if (best < 0 && cnt == 1u) {
+      const uint32_t c = st_count(st[r]);
+      shared |= uint32_t(c >= 2u) << r;
+      if (best < 0 && c == 1u) {
         best = int(r);
         local = ls[r];
         sg = dev_sign(hp.row[r], p);
@@ -365,113 +529,12 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
     const float v = canonical(sg * ldcg(e.sketch + local));
     __stcg(e.out + p, v);
     atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
-    // phase 2 needs the value and only the rows shared with other positions
+    // the push pass needs the value and only the rows shared with other positions
     w.pinfo[i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
     ++won;
   }
   won = warp_sum32(won);
   if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
-}
-
-// Round 0 subtraction for every position peeled in round0_phase1. Buckets
-// that held only the peeled position are left alone: nothing else reads them
-// (their count drops 1 -> 0 in the reference, decode.cpp:115-121).
-__device__ __forceinline__ void round0_phase2(const DecodeWork& w, const HashParams& hp,
-                                              uint64_t start, uint64_t stride, uint32_t* s_q,
-                                              uint32_t* s_nq, uint32_t* s_base) {
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t* nq = w.queue[1];
-  uint32_t* ncount = &w.qcount[1];
-  const uint32_t total = ldcg(&w.qcount[5]);
-  for (uint64_t base = start - lane; base < total; base += stride) {
-    const uint64_t i = base + lane;
-    uint32_t p = 0, rows = 0;
-    float v = 0.0f;
-    DecItem e{};
-    if (i < total) {
-      const uint2 info = w.pinfo[i];
-      if (info.y & 0x100u) {
-        rows = info.y & 0xFFu;
-        v = __uint_as_float(info.x);
-        p = w.plist[i];
-        e = w.items[w.pitem[i]];
-      }
-    }
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      bool push = false;
-      uint64_t s = 0;
-      if (rows >> r & 1u) {
-        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-        s = e.slot_base + local;
-        atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
-        push = st_count(old) == 2u;
-      }
-      push_slot(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
-    }
-  }
-  flush_pushes(s_q, s_nq, s_base, nq, ncount);
-}
-
-__global__ void __launch_bounds__(256) k_peel(DecodeWork w, const HashParams hp) {
-  __shared__ uint32_t s_q[kPushStage];
-  __shared__ uint32_t s_nq[2], s_base;  // [0] reserved, [1] end of the contiguous written prefix
-  if (threadIdx.x == 0) {
-    s_nq[0] = 0;
-    s_nq[1] = kPushStage;
-  }
-  __syncthreads();
-  cg::grid_group grid = cg::this_grid();
-  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
-  int mk = 0;
-  PEEL_MARK(mk++);
-  round0_phase1(w, hp, gtid, gstride);
-  PEEL_MARK(mk++);
-  grid.sync();
-  PEEL_MARK(mk++);
-  round0_phase2(w, hp, gtid, gstride, s_q, s_nq, &s_base);
-  PEEL_MARK(mk++);
-  if (gtid == 0) w.qcount[2] = 1;
-  uint32_t cur = 1;
-  for (;;) {
-    grid.sync();
-    PEEL_MARK(mk++);
-    const uint32_t qlen = ldcg(&w.qcount[cur]);
-    if (qlen == 0) return;
-    if (qlen <= kTail) break;  // every CTA sees the same qlen
-    peel_phase1(w, hp, cur, qlen, gtid, gstride);
-    PEEL_MARK(mk++);
-    if (gtid == 0) {
-      w.qcount[cur ^ 1] = 0;
-      w.qcount[2] += 1;
-    }
-    grid.sync();
-    PEEL_MARK(mk++);
-    peel_phase2(w, hp, cur, qlen, gtid, gstride, s_q, s_nq, &s_base);
-    PEEL_MARK(mk++);
-    cur ^= 1;
-  }
-  // tail: one CTA finishes with block barriers
-  if (blockIdx.x != 0) return;
-  for (;;) {
-    __syncthreads();
-    const uint32_t qlen = ldcg(&w.qcount[cur]);
-    if (qlen == 0) return;
-    peel_phase1(w, hp, cur, qlen, threadIdx.x, blockDim.x);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      w.qcount[cur ^ 1] = 0;
-      w.qcount[3] += 1;
-    }
-    __threadfence();
-    __syncthreads();
-    peel_phase2(w, hp, cur, qlen, threadIdx.x, blockDim.x, s_q, s_nq, &s_base);
-    __threadfence();
-    PEEL_MARK(mk++);
-    cur ^= 1;
-  }
 }
 
 // ------------------------------------------------------------------ ordered peel
@@ -799,7 +862,17 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_build, 256, 0);
   uint64_t g = uint64_t(std::max(per_sm, 1)) * di.sms;
   if (w.total_word_tiles < g) g = w.total_word_tiles;
-  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w, hp);
+  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w);
+  // bucket state zeroed after the streaming output fill, so it is L2-resident
+  // for the reductions and the peel
+  ZeroRanges zr{};
+  zr.ptr[0] = w.slot_state;
+  zr.bytes[0] = w.total_slots * 8;
+  zr.n = 1;
+  launch_zero(zr, stream);
+  k_accumulate<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_peel, 256, 0);
   const int pg = std::max(per_sm, 1) * di.sms;
@@ -810,7 +883,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return 3;
+  return 7;
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
@@ -822,14 +895,20 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_build, 256, 0);
   uint64_t g = uint64_t(std::max(per_sm, 1)) * di.sms;
   if (w.total_word_tiles < g) g = w.total_word_tiles;
-  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w, hp);
+  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w);
+  ZeroRanges zr{};
+  zr.ptr[0] = w.slot_state;
+  zr.bytes[0] = w.total_slots * 8;
+  zr.n = 1;
+  launch_zero(zr, stream);
+  k_accumulate<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   const int grid = di.sms * 4;
   k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
   ++epoch;
   OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
   cudaMemsetAsync(ob.count, 0, 4, stream);
   k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
-  launches += 3;
+  launches += 5;
   uint32_t gen = 1;
   unsigned long long* cur_keys = ob.keys[0];
   uint32_t* cur_slots = ob.slots[0];

@@ -428,11 +428,12 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
-  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 32, false, stream_));
+  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 64, false, stream_));
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", n * sizeof(DecStats), false, stream_));
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
-  zero({{w.slot_state, slots * 8}, {w.bitmap, bm * 4}, {w.qcount, 32}, {w.stats, n * sizeof(DecStats)}});
+  // the bucket state is zeroed inside launch_decode (after the output fill)
+  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)}});
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {
     w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));

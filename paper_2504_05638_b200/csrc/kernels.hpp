@@ -110,7 +110,7 @@ struct DecodeWork {
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
   uint32_t* queue[2];              // capacity total_slots each
-  uint32_t* qcount;                // [0..1] frontier sizes, [2] rounds, [3] tail rounds, [4] peeled,
+  uint32_t* qcount;                // [2] rounds, [3] tail rounds, [4] peeled, [8..10] frontier sizes,
                                    // [5] presence total
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
