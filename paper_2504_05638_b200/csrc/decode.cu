@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
       const bool sh = (rows >> r) & 1u;
       loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m) : 0;
       old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(p)) : 0ull;
-      if (sh) atomicAdd(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
+      if (sh) red_add_f32(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
     }
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
       stage_push<uint32_t, kPushStage>(st_count(old[r]) == 2u, uint32_t(e->slot_base + loc[r]), s_q, s_n, nq,
@@ -401,7 +401,7 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
     }
     if (win) {
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && r != row)
-        atomicAdd(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m), -(dev_sign(hp.row[r], p) * v));
+        red_add_f32(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m), -(dev_sign(hp.row[r], p) * v));
       __threadfence();  // residual updates before the count decrements
       ++won;
     }
@@ -528,7 +528,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
     }
     const float v = canonical(sg * ldcg(e.sketch + local));
     __stcg(e.out + p, v);
-    atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+    red_or_u32(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
     // the push pass needs the value and only the rows shared with other positions
     w.pinfo[i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
     ++won;
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
       if (rows >> r & 1u) {
         const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
         s = e.slot_base + local;
-        atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+        red_add_f32(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
         // the reference queues a slot when its LAST subtraction of the
         // generation (in FIFO order) leaves one position: keep the max key
         atomicMax(o.slot_key + s, o.tag | (wkey + r));
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
           const uint32_t row = uint32_t(local / e.m);
           v = canonical(dev_sign(row_coef(hp, row), p) * e.sketch[local]);  // decode.cpp:110-111
           e.out[p] = v;
-          atomicOr(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+          red_or_u32(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
           ++won;
         }
       }
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
         const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
         s = e.slot_base + local;
         if (s != slot) {
-          atomicAdd(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+          red_add_f32(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
           atomicMax(o.slot_key + s, o.tag | (uint64_t(i) * hp.rows + r));
           const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
           push = st_count(old) == 2u;

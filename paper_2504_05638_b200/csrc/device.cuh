@@ -98,6 +98,18 @@ __device__ __forceinline__ float dev_sign(const RowCoef& c, uint32_t p) {
   return (h >> 63) ? 1.0f : -1.0f;                                         // hash.hpp:42
 }
 __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+// Fire-and-forget global reductions. A plain atomicAdd(float*) through a
+// generic pointer compiles to a returning ATOM plus a shared-memory CAS
+// fallback; these name the global state space and return nothing (RED).
+// Like every GPU float atomic, red.add.f32 flushes subnormals.
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.add.f32 [ga], %1;\n}" ::"l"(p), "f"(v)
+               : "memory");
+}
+__device__ __forceinline__ void red_or_u32(uint32_t* p, uint32_t v) {
+  asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.or.b32 [ga], %1;\n}" ::"l"(p), "r"(v)
+               : "memory");
+}
 // Device-side execution spans (timing mode): span[0] = earliest CTA start,
 // span[1] = latest CTA end of a kernel chain, in %globaltimer ns. Independent
 // of where the driver stamps stream events.

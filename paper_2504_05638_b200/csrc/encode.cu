@@ -244,7 +244,7 @@ __device__ __forceinline__ void load_source(const EncItem& e, uint32_t pos, bool
 __device__ __forceinline__ void scatter_sketch(const EncItem& e, const HashParams& hp, uint32_t p,
                                                float v) {
   _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
-    atomicAdd(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m), dev_sign(hp.row[r], p) * v);
+    red_add_f32(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m), dev_sign(hp.row[r], p) * v);
 }
 
 // --------------------------------------------------------------- fused pass
@@ -503,11 +503,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
 // requests while the consumers classify tiles out of shared memory. Items must
 // be 16-byte aligned (the host checks); a tile's last <16 bytes are read
 // directly from global memory.
-constexpr int kFusedStages = 6;
-constexpr int kConsumerWarps = 16;
+constexpr int kFusedStages = 3;
+constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kFusedThreads = kConsumers + 32;
 constexpr int kQuads = kTile / 4 / kConsumers;  // quads (4 elements) per consumer thread per tile
+constexpr int kFusedCtasPerSm = 2;
 constexpr uint32_t kWarpStageT = 64;
 struct alignas(128) FusedStage {
   float g[kTile];
@@ -554,7 +555,7 @@ __device__ __forceinline__ void consumer_sync() {
 }
 
 template <bool kW4>
-__global__ void __launch_bounds__(kFusedThreads, 1) k_fused_tma(const EncItem* __restrict__ items,
+__global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* __restrict__ items,
                                                                 SelState* __restrict__ state,
                                                                 uint32_t n_items, uint64_t total_tiles,
                                                                 const HashParams hp,
@@ -697,15 +698,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_fused_tma(const EncItem* _
           *reinterpret_cast<float4*>(sg + 4u * (k * kConsumers + ctid)) =
               make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
       }
-      const uint32_t cnt = uint32_t(__popc(in_m)) | (uint32_t(__popc(hi_m)) << 16);
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= uint32_t(o)) incl += y;
+      // warp placement of the flagged elements: counts are almost always 0 or
+      // 1 per thread, so the exclusive prefix is a few ballots (one per count
+      // level present in the warp) instead of a dependent shuffle scan
+      const uint32_t n_c = __popc(in_m), n_k = __popc(hi_m);
+      const uint32_t lt = (1u << lane) - 1u;
+      uint32_t pre_c = 0, pre_k = 0, tot_c = 0, tot_k = 0;
+      const uint32_t levels = __reduce_max_sync(kFull, max(n_c, n_k));
+      for (uint32_t lv = 1; lv <= levels; ++lv) {
+        const uint32_t mc = __ballot_sync(kFull, n_c >= lv), mk = __ballot_sync(kFull, n_k >= lv);
+        pre_c += __popc(mc & lt);
+        pre_k += __popc(mk & lt);
+        tot_c += __popc(mc);
+        tot_k += __popc(mk);
       }
-      const uint32_t tot = __shfl_sync(kFull, incl, 31);
-      const uint32_t tot_c = tot & 0xFFFFu, tot_k = tot >> 16;
       const uint32_t pbase = start + 4u * ctid;  // element b = 4k + j -> pbase + k*4*kConsumers + j
       if (tot_c) {
         if (wc + tot_c > kWarpStageT) flush_cand();
@@ -715,7 +721,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_fused_tma(const EncItem* _
           if (lane == 0) gbase = atomicAdd(&state[it].cnt_in, tot_c);
           gbase = __shfl_sync(kFull, gbase, 0);
         }
-        uint32_t o = (incl - cnt) & 0xFFFFu;
+        uint32_t o = pre_c;
         for (uint32_t m = in_m; m; m &= m - 1) {
           const uint32_t b = __ffs(m) - 1;
           const uint32_t off = (b >> 2) * 4u * kConsumers + (b & 3u);
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_fused_tma(const EncItem* _
           if (lane == 0) gbase = atomicAdd(&state[it].cnt_hi, tot_k);
           gbase = __shfl_sync(kFull, gbase, 0);
         }
-        uint32_t o = (incl - cnt) >> 16;
+        uint32_t o = pre_k;
         for (uint32_t m = hi_m; m; m &= m - 1) {
           const uint32_t b = __ffs(m) - 1;
           const uint32_t off = (b >> 2) * 4u * kConsumers + (b & 3u);
@@ -997,8 +1003,8 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
     if (e.flags & kWriteResidual) e.residual[p] = 0.0f;
     if (e.flags & kWriteSparse) e.sparse[p] = v;
     if (e.flags & kWriteIndex) {
-      if (kW4) atomicOr(e.index + (p >> 3), 1u << (4u * (p & 7u)));
-      else atomicOr(e.index + (p >> 5), 1u << (p & 31u));
+      if (kW4) red_or_u32(e.index + (p >> 3), 1u << (4u * (p & 7u)));
+      else red_or_u32(e.index + (p >> 5), 1u << (p & 31u));
     }
     if (e.flags & kWriteSketch) scatter_sketch(e, hp, p, v);
   }
@@ -1369,7 +1375,7 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
     auto launch_tma = [&](auto kern) {
       // opt-in to > 48 KB of dynamic shared memory (cheap; per launch keeps it per device)
       cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
-      const uint64_t g = std::min<uint64_t>(uint64_t(di.sms), total_tiles);
+      const uint64_t g = std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
       kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
                                                                  hi_pool, fine_hist, err, span);
     };
