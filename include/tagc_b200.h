@@ -185,6 +185,12 @@ int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[5]);
  * out_ms[0] = sampled select + fused split/encode pass (k_sample start to
  * k_fused end), out_ms[1] = decode (k_build start to k_final end). */
 int tagc_ctx_last_kernel_spans(tagc_ctx* ctx, float out_ms[2]);
+/* CUDA-graph replay of tagc_reduce_shards / _host (default on; the
+ * environment variable TAGC_GRAPHS=0 turns it off): a call whose shard
+ * layout, config and buffer pointers repeat is captured on its second
+ * occurrence and replayed with one graph launch afterwards. Calls with stats,
+ * timing mode, or a 1-bit index over several ranks always run eagerly. */
+int tagc_ctx_set_graphs(tagc_ctx* ctx, int enabled);
 /* Kernel launches enqueued by the last fused call. */
 uint64_t tagc_ctx_last_launches(const tagc_ctx* ctx);
 /* Synchronise the context stream and surface deferred device errors (a NaN

@@ -117,6 +117,7 @@ SIGNATURES = {
     "tagc_ctx_set_timing": (C.c_int, [VP, C.c_int]),
     "tagc_ctx_last_timing": (C.c_int, [VP, C.POINTER(C.c_float)]),
     "tagc_ctx_last_kernel_spans": (C.c_int, [VP, C.POINTER(C.c_float)]),
+    "tagc_ctx_set_graphs": (C.c_int, [VP, C.c_int]),
     "tagc_ctx_last_launches": (U64, [VP]),
     "tagc_ctx_sync": (C.c_int, [VP]),
     "tagc_ctx_last_peel_rounds": (C.c_int, [VP, C.POINTER(U32)]),

@@ -296,6 +296,10 @@ class Context:
         check(lib.tagc_ctx_last_timing(self.h, out))
         return list(out)
 
+    def set_graphs(self, on: bool):
+        """CUDA-graph replay of repeated tagc_reduce_shards calls (default on)."""
+        check(lib.tagc_ctx_set_graphs(self.h, int(on)), "set_graphs")
+
     def last_kernel_spans(self):
         """(select+fused pass, decode) device execution spans in ms (timing mode)."""
         out = (C.c_float * 2)()

@@ -254,6 +254,10 @@ int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[5]) {
   });
 }
 
+int tagc_ctx_set_graphs(tagc_ctx* ctx, int enabled) {
+  return guarded([&] { eng(ctx).set_graphs(enabled != 0); });
+}
+
 int tagc_ctx_last_kernel_spans(tagc_ctx* ctx, float out_ms[2]) {
   return guarded([&] { eng(ctx).last_kernel_spans(out_ms); });
 }

@@ -128,6 +128,7 @@ void* Workspace::get(const std::string& name, size_t bytes, bool zero_on_alloc, 
     b.ptr = nullptr;
     b.bytes = 0;
   }
+  ++gen_;
   const size_t want = align_up(bytes + bytes / 8, 256);  // headroom against regrowth
   cuda_check(cudaMalloc(&b.ptr, want), ("workspace alloc " + name).c_str());
   b.bytes = want;
@@ -141,6 +142,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
                void* nccl_comm, void* stream)
     : cfg_(cfg), world_(world), rank_(rank), device_(device) {
   if (const char* v = std::getenv("TAGC_FUSED_TMA")) use_tma_ = std::atoi(v) != 0;
+  if (const char* v = std::getenv("TAGC_GRAPHS")) graphs_on_ = std::atoi(v) != 0;
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -166,6 +168,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
 
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
+  drop_graphs();
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& e : ev_)
@@ -267,6 +270,17 @@ void Engine::upload(const void* host, size_t bytes, void* dev) {
   if (call_depth_ == 0) {  // internal helper called outside a public entry
     CallScope scope(*this);
     upload(host, bytes, dev);
+    return;
+  }
+  if (capturing_) {  // the graph re-reads these bytes on every replay: give them their own buffer
+    char* h = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h), align_up(bytes, 16), cudaHostAllocMapped),
+               "graph staging alloc");
+    capturing_->pinned.push_back(h);
+    std::memcpy(h, host, bytes);
+    void* dp = nullptr;
+    cuda_check(cudaHostGetDevicePointer(&dp, h, 0), "graph staging map");
+    launches_ += launch_stage_copy(dev, dp, align_up(bytes, 16), stream_);
     return;
   }
   Staging& s = stage_[stage_cur_];
@@ -632,12 +646,123 @@ void Engine::baseline_sim(const ShardSpec& shard, uint32_t world, const float* c
 }
 
 // ------------------------------------------------------------------ NCCL world
+void Engine::record(CollectiveOp op, const std::string& tag, uint64_t bits, uint64_t params) {
+  ledger_.record(op, tag, bits, params);
+  if (capturing_) capturing_->ledger.push_back(LedgerEntry{op, tag, bits, params});
+}
+
+void Engine::set_graphs(bool on) {
+  graphs_on_ = on;
+  if (!on) drop_graphs();
+}
+
+void Engine::drop_graphs() {
+  if (!graphs_.empty() && stream_) cudaStreamSynchronize(stream_);
+  for (auto& [k, g] : graphs_) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (char* h : g.pinned) cudaFreeHost(h);
+  }
+  graphs_.clear();
+  graph_seen_.clear();
+}
+
 void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                            float* out, PeelStats* stats) {
   CallScope scope(*this);
   cfg_.validate_for_world(world_);
   for (const ShardSpec& s : shards) check_shard(s, world_);
   if (world_ > 1 && !comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
+  static const bool peel_dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
+  const bool legacy = stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread;
+  const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy &&  // default streams cannot be captured
+                        !(cfg_.index_width == 1 && world_ > 1);  // the ordered peel loops on the host
+  if (!eligible) {
+    enqueue_reduce_shards(shards, grad, acc, out, stats);
+    return;
+  }
+  // key: everything the enqueued work depends on
+  std::string key;
+  {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%p|%p|%p|%p|%.17g|%u|%u|%d|%d|%llu|%u|%llu|", (void*)grad, (void*)acc,
+                  (void*)out, (void*)grad_read_ev_, cfg_.theta, cfg_.ratio, cfg_.index_width, int(cfg_.policy),
+                  int(cfg_.include_out_proj), (unsigned long long)cfg_.seed, cfg_.sketch_rows,
+                  (unsigned long long)cfg_.min_compress_segment);
+    key = buf;
+    for (const ShardSpec& sh : shards) {
+      std::snprintf(buf, sizeof(buf), "S%u,%u,%llu,%llu:", sh.id, sh.owner, (unsigned long long)sh.begin,
+                    (unsigned long long)sh.end);
+      key += buf;
+      for (const LayerSegment& g : sh.segments) {
+        std::snprintf(buf, sizeof(buf), "%d,%llu,%llu,", int(g.kind), (unsigned long long)g.begin,
+                      (unsigned long long)g.end);
+        key += buf;
+        key += g.name;
+        key += ';';
+      }
+    }
+  }
+  auto it = graphs_.find(key);
+  if (it != graphs_.end() && it->second.gen != ws_.generation()) {
+    drop_graphs();  // a workspace buffer moved: every captured pointer is suspect
+    it = graphs_.end();
+  }
+  if (it != graphs_.end()) {
+    GraphEntry& g = it->second;
+    cuda_check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+    launches_ = g.launches;
+    for (const LedgerEntry& l : g.ledger) ledger_.record(l.op, l.tag, l.bits, l.params);
+    ledger_.wire_bytes += g.wire;
+    return;
+  }
+  if (graph_seen_[key]++ == 0) {  // first sighting: run eagerly (sizes the workspace)
+    enqueue_reduce_shards(shards, grad, acc, out, stats);
+    return;
+  }
+  // second sighting: capture, then replay from now on
+  GraphEntry g;
+  const uint64_t gen0 = ws_.generation(), wire0 = ledger_.wire_bytes;
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    graph_seen_[key] = -1000000;  // this stream cannot be captured: stay eager
+    enqueue_reduce_shards(shards, grad, acc, out, stats);
+    return;
+  }
+  capturing_ = &g;
+  bool ok = true;
+  try {
+    enqueue_reduce_shards(shards, grad, acc, out, nullptr);
+  } catch (...) {
+    ok = false;
+  }
+  capturing_ = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(stream_, &graph);
+  cudaGetLastError();
+  ok = ok && ce == cudaSuccess && graph && ws_.generation() == gen0;
+  if (ok && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    ok = false;
+  }
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {  // could not capture (e.g. a buffer had to grow): stay eager for this key
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (char* h : g.pinned) cudaFreeHost(h);
+    ledger_.wire_bytes = wire0;
+    for (const LedgerEntry& l : g.ledger) ledger_.unrecord(l.op, l.tag, l.bits, l.params);
+    graph_seen_[key] = -1000000;
+    enqueue_reduce_shards(shards, grad, acc, out, stats);
+    return;
+  }
+  g.gen = gen0;
+  g.launches = launches_;
+  g.wire = ledger_.wire_bytes - wire0;
+  cuda_check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+  graphs_.emplace(key, std::move(g));
+}
+
+void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
+                                   float* out, PeelStats* stats) {
   launches_ = 0;
   ev_record(0);
   span_reset();
@@ -696,7 +821,9 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     upload(raw_now.data(), raw_now.size() * sizeof(CopyItem), d_pack);
     launches_ += launch_copy_items(di_, d_pack, uint32_t(raw_now.size()), tt, stream_);
   }
-  if (grad_read_ev_) cuda_check(cudaEventRecord(grad_read_ev_, stream_), "grad-read event");
+  if (grad_read_ev_)  // an external record node when captured: the copy stream waits on it
+    cuda_check(cudaEventRecordWithFlags(grad_read_ev_, stream_, capturing_ ? cudaEventRecordExternal : 0),
+               "grad-read event");
   if (W > 1) {
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
     nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
@@ -732,10 +859,10 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   uint64_t n_raw_owned = 0;
   for (const SegPlan& p : plan) {
     if (p.compressed) {
-      ledger_.record(CollectiveOp::all_reduce, "index/" + p.tag, p.len * w, p.len);
-      ledger_.record(CollectiveOp::reduce, "sketch/" + p.tag, uint64_t(rows) * p.m * 32, p.len);
+      record(CollectiveOp::all_reduce, "index/" + p.tag, p.len * w, p.len);
+      record(CollectiveOp::reduce, "sketch/" + p.tag, uint64_t(rows) * p.m * 32, p.len);
     } else {
-      ledger_.record(CollectiveOp::reduce_scatter, "grad/" + p.tag, p.len * 32, p.len);
+      record(CollectiveOp::reduce_scatter, "grad/" + p.tag, p.len * 32, p.len);
       if (shards[p.shard].owner == rank_) ++n_raw_owned;
     }
   }

@@ -31,8 +31,11 @@ class Workspace {
   void* get(const std::string& name, size_t bytes, bool zero_on_alloc = false,
             cudaStream_t s = nullptr);
   uint64_t bytes() const { return total_; }
+  // bumped on every (re)allocation: captured graphs hold raw pointers
+  uint64_t generation() const { return gen_; }
 
  private:
+  uint64_t gen_ = 0;
   struct Buf {
     void* ptr = nullptr;
     size_t bytes = 0;
@@ -103,6 +106,10 @@ class Engine {
   void reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                      float* out, PeelStats* stats);
   void baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out);
+  // CUDA-graph replay of reduce_shards: a call whose shard layout, config and
+  // buffers repeat is captured once (on its second occurrence) and replayed
+  // with one cudaGraphLaunch. TAGC_GRAPHS=0 disables.
+  void set_graphs(bool on);
   // Host-buffer form of reduce_shards (the end-to-end call): the gradient is
   // copied H2D on a copy stream into one of two device buffers, the owner's
   // decoded shard D2H on a second copy stream from one of two device buffers,
@@ -135,6 +142,25 @@ class Engine {
  private:
   struct EncBatch;
   friend struct CallScope;
+  void enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                             PeelStats* stats);
+  struct LedgerEntry {
+    CollectiveOp op;
+    std::string tag;
+    uint64_t bits, params;
+  };
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t gen = 0, launches = 0, wire = 0;
+    std::vector<LedgerEntry> ledger;
+    std::vector<char*> pinned;  // descriptor uploads frozen into the graph
+  };
+  std::map<std::string, GraphEntry> graphs_;
+  std::map<std::string, int> graph_seen_;
+  bool graphs_on_ = true;
+  GraphEntry* capturing_ = nullptr;  // upload() / ledger record target while capturing
+  void drop_graphs();
+  void record(CollectiveOp op, const std::string& tag, uint64_t bits, uint64_t params);
   // Descriptor uploads go through pinned staging (a pageable cudaMemcpyAsync
   // would synchronise the stream): two halves, one per public call, each
   // reused only after the call that last filled it has finished on the GPU.

@@ -204,6 +204,19 @@ void TrafficLedger::record(CollectiveOp op, const std::string& tag, uint64_t pay
   row.params += params;
 }
 
+// Undo one record() (a capture that was abandoned after recording).
+void TrafficLedger::unrecord(CollectiveOp op, const std::string& tag, uint64_t payload_bits,
+                             uint64_t params) {
+  auto it = rows_.find({int(op), tag});
+  if (it == rows_.end()) return;
+  LedgerRow& row = it->second;
+  row.calls -= 1;
+  row.payload_bits -= payload_bits;
+  row.charged_bits -= (op == CollectiveOp::all_reduce ? 2u : 1u) * payload_bits;
+  row.params -= params;
+  if (row.calls == 0) rows_.erase(it);
+}
+
 // collectives.cpp:60-68
 double TrafficLedger::bits_per_param_per_rank(const std::string& prefix) const {
   uint64_t charged = 0, params = 0;

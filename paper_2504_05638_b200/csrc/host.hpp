@@ -119,6 +119,7 @@ struct LedgerRow {
 class TrafficLedger {
  public:
   void record(CollectiveOp op, const std::string& tag, uint64_t payload_bits, uint64_t params);
+  void unrecord(CollectiveOp op, const std::string& tag, uint64_t payload_bits, uint64_t params);
   std::string to_csv() const;
   double bits_per_param_per_rank(const std::string& prefix = "") const;
   void clear() { rows_.clear(); }

@@ -105,3 +105,22 @@ def test_host_entry_rejects_device_buffers():
     n = sh[0].size()
     with pytest.raises(tagc.TagcInvalidArgument):
         ctx.tagc_reduce_shards_host(sh, torch.zeros(n, device=DEV), torch.zeros(n, device=DEV))
+
+
+def test_graph_replay_matches_oracle(world1):
+    """Same buffers every step (new gradient copied in): call 1 runs eagerly,
+    call 2 is captured into a CUDA graph, call 3 replays it."""
+    shards, grads, refs = world1
+    n = shards[0].size()
+    ctx = tagc.Context(tagc.CompressionConfig(**CFG), device=0)
+    ctx.set_graphs(True)
+    acc = torch.zeros(n, device=DEV)
+    out = torch.empty(n, device=DEV)
+    g_d = torch.empty(n, device=DEV)
+    for g, (ref, _, oacc) in zip(grads, refs):
+        g_d.copy_(torch.from_numpy(g))
+        ctx.tagc_reduce_shards(shards, g_d, acc, out, stats=False)
+        ctx.sync()
+        assert np.array_equal(bits(acc.cpu().numpy()), bits(oacc))
+        check_close(out.cpu().numpy(), ref)
+    assert ctx.last_launches() > 10
