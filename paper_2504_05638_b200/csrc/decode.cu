@@ -1,21 +1,28 @@
 // decode.cu — sm_100a owner-side decode (reference decode.cpp:24-140):
-//   build    : zero-fill the dense shard, walk the merged index words and
-//              accumulate per-bucket (count, key_sum) state in one 64-bit word
-//              per bucket, collecting the presence list and first-touch
-//              singleton candidates;
-//   peel     : synchronous peeling rounds in ONE cooperative persistent kernel
-//              (phase 1 claims singleton buckets, phase 2 subtracts the peeled
-//              contributions from all k rows); when the frontier is small a
-//              single CTA finishes the remaining rounds with block barriers;
-//   estimate : median-of-rows on the residual sketch for every present
-//              position the peel could not resolve.
+//   build      : walk the merged index words and list the present positions
+//                in ascending order per word tile (plist / pitem, one block
+//                scan per tile); remember each tile's list offset;
+//   accumulate : per listed entry i, add (i, 1) into its k buckets' state;
+//   round 0    : every listed position inspects its k buckets and peels from
+//                its lowest singleton row (the reference's ascending seed
+//                order, decode.cpp:96-99), then leaves the buckets it shares;
+//   peel       : frontier rounds in ONE cooperative persistent kernel, a
+//                single CTA finishing once the frontier is small;
+//   estimate   : median-of-rows on the residual sketch for every listed
+//                position the peel could not resolve (decode.cpp:130-138);
+//   emit       : the dense shard tile by tile: zero-fill, then the tile's
+//                listed entries' values on top.
 //
-// Bucket state: (count << 40) | sum(position) in one u64, so building and
-// peeling cost one 64-bit L2 atomic per (position, row). count == 1 makes the
-// low 40 bits equal to the single remaining position (decode.cpp:104-106 uses
-// a u64 key_sum for the same reason). The sum field cannot carry for any
-// bucket holding fewer than 2^40 / n positions; the build kernel flags that
-// overflow (never reached at ratio <= 10) and the engine reports it.
+// Everything between build and emit is keyed by the presence-list index i,
+// not the position: a bucket's state is (count, sum of list indices) in one
+// u64, decoded values go to val[i] and the recovered flags to bit i. The
+// randomly accessed working set is then the bucket state plus the residual
+// sketch; the dense output is written once, at the end.
+//
+// Bucket state: (sum of list indices mod 2^40) << 24 | count (24 bits), so
+// building and peeling cost one 64-bit L2 atomic per (entry, row). count == 1
+// makes the low 32 bits of the sum the single remaining entry exactly
+// (decode.cpp:104-106 keeps a u64 key_sum for the same reason).
 //
 // Parity: the recovered/unresolved position sets are those of the reference's
 // FIFO peel (the peelable set is the complement of the 2-core, independent of
@@ -23,8 +30,9 @@
 // integer-valued inputs.
 #include <cooperative_groups.h>
 
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.hpp"
@@ -35,18 +43,12 @@ namespace tagc_b200 {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-// Bucket state word: (sum of positions mod 2^40) << 24 | count (24 bits).
-// Adding (p << 24) | 1 never carries out of the count field unless one bucket
-// holds 2^24 positions; the sum wraps harmlessly at the top, and when
-// count == 1 its low 32 bits are the remaining position exactly.
 constexpr unsigned long long kCountMask = (1ull << 24) - 1ull;
-__device__ __forceinline__ unsigned long long st_add(uint32_t p) { return (uint64_t(p) << 24) | 1ull; }
-__device__ __forceinline__ unsigned long long st_sub(uint32_t p) { return ~st_add(p) + 1ull; }
+__device__ __forceinline__ unsigned long long st_add(uint32_t i) { return (uint64_t(i) << 24) | 1ull; }
+__device__ __forceinline__ unsigned long long st_sub(uint32_t i) { return ~st_add(i) + 1ull; }
 __device__ __forceinline__ uint32_t st_count(unsigned long long s) { return uint32_t(s & kCountMask); }
-__device__ __forceinline__ uint32_t st_pos(unsigned long long s) { return uint32_t(s >> 24); }
-constexpr uint32_t kWinner = 0x80000000u;
+__device__ __forceinline__ uint32_t st_entry(unsigned long long s) { return uint32_t(s >> 24); }
 constexpr uint32_t kWordTile = kDecWordTile;
-constexpr uint32_t kStage = 4096;
 constexpr uint32_t kTail = 512;  // frontier size at which one CTA finishes
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
@@ -63,20 +65,19 @@ __device__ __forceinline__ uint32_t find_word_item(const DecItem* items, uint32_
   return lo;
 }
 
-__device__ __forceinline__ uint32_t find_slot_item(const DecItem* items, uint32_t n, uint64_t s) {
-  uint32_t lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (items[mid].slot_base <= s) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 // Presence bits of one merged word: field != 0 (index.cpp:43-57). Width 4:
-// bit 4j set iff nibble j nonzero; width 1: the word itself.
-__device__ __forceinline__ uint32_t present_bits(uint32_t x, bool w4) {
-  return w4 ? ((x | x >> 1 | x >> 2 | x >> 3) & 0x11111111u) : x;
+// bit 4j set iff nibble j nonzero; width 1: the word itself. Bits past the
+// item's last position are cleared.
+__device__ __forceinline__ uint32_t present_bits(uint32_t x, bool w4, uint32_t wi, uint32_t n) {
+  x = w4 ? ((x | x >> 1 | x >> 2 | x >> 3) & 0x11111111u) : x;
+  const uint64_t first = uint64_t(wi) * (w4 ? 8u : 32u);
+  const uint64_t left = n > first ? n - first : 0;
+  if (w4) {
+    if (left < 8) x &= left ? (1u << (4 * left)) - 1u : 0u;
+  } else if (left < 32) {
+    x &= left ? (1u << left) - 1u : 0u;
+  }
+  return x;
 }
 
 __device__ __forceinline__ float canonical(float v) { return v == 0.0f ? 0.0f : v; }
@@ -119,111 +120,143 @@ __device__ __forceinline__ float median_rows(float (&e)[kMaxRows], uint32_t k) {
 }
 
 // ------------------------------------------------------------------ build
-// Contiguous range of word tiles per CTA (kWordTile words, 4 per thread).
-// Per tile: zero-fill the tile's output positions with coalesced 16-byte
-// streaming stores (each warp covers its 32 words' positions contiguously)
-// and append the present positions to the flat presence list in ascending
-// order (one block scan + one global atomic per tile). Bucket state is
-// accumulated from the list by k_accumulate, where every thread carries one
-// position (no per-word imbalance ahead of a block barrier).
-__global__ void __launch_bounds__(256) k_build(DecodeWork w) {
-  using Scan = cub::BlockScan<uint32_t, 256>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_base;
-  span_begin(w.span);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t T = uint32_t(w.total_word_tiles), G = gridDim.x, b = blockIdx.x;
+// Word tiles of kWordTile merged-index words (16 per thread of a 256-thread
+// CTA), each CTA walking a contiguous tile range with an item cursor. Two
+// passes around a one-CTA scan, none with a latency chain per tile:
+//   k_count      : present positions per tile -> tile_base[wt]
+//   k_scan_tiles : exclusive scan of the tile counts; the presence list is
+//                  ordered by tile, ascending position inside a tile
+//   k_list       : writes the list entries (plist / pitem) at their final
+//                  index and adds (entry, 1) into each entry's k buckets with
+//                  fire-and-forget 64-bit reductions (the bucket state).
+constexpr uint32_t kPerThreadWords = kWordTile / 256;
+
+__device__ __forceinline__ void cta_tiles(uint64_t total, uint32_t& t0, uint32_t& t1) {
+  const uint32_t T = uint32_t(total), G = gridDim.x, b = blockIdx.x;
   const uint32_t chunk = T / G, extra = T % G;
-  const uint32_t t0 = b * chunk + min(b, extra), t1 = t0 + chunk + (b < extra ? 1u : 0u);
+  t0 = b * chunk + min(b, extra);
+  t1 = t0 + chunk + (b < extra ? 1u : 0u);
+}
+
+__device__ __forceinline__ void load_tile_bits(const DecItem& e, uint32_t wbase, bool w4,
+                                               uint32_t (&bits)[kPerThreadWords], uint32_t& cnt) {
+  uint32_t raw[kPerThreadWords];
+#pragma unroll
+  for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // all loads in flight first
+    const uint32_t wi = wbase + k * 256 + threadIdx.x;
+    raw[k] = wi < e.n_words ? __ldg(e.words + wi) : 0u;
+  }
+  cnt = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kPerThreadWords; ++k) {
+    bits[k] = present_bits(raw[k], w4, wbase + k * 256 + threadIdx.x, e.n);
+    cnt += __popc(bits[k]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_count(DecodeWork w) {
+  using Reduce = cub::BlockReduce<uint32_t, 256>;
+  __shared__ typename Reduce::TempStorage tmp;
+  span_begin(w.span);
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
   if (t0 >= t1) return;
-  constexpr uint32_t kPer = kWordTile / 256;
   uint32_t it = find_word_item(w.items, w.n_items, t0);
   for (uint32_t wt = t0; wt < t1; ++wt) {
     while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
-    const DecItem e = w.items[it];
+    const DecItem& e = w.items[it];
+    uint32_t bits[kPerThreadWords], cnt;
+    load_tile_bits(e, uint32_t(wt - e.word_tile_begin) * kWordTile, (e.flags & kWidth4) != 0, bits, cnt);
+    const uint32_t total = Reduce(tmp).Sum(cnt);
+    if (threadIdx.x == 0) {
+      w.tile_base[wt] = total;
+      if (total) atomicAdd(&w.stats[it].presence, total);
+    }
+    __syncthreads();
+  }
+}
+
+// Exclusive scan of the per-tile counts in place; the total is the presence
+// count (qcount[5]).
+__global__ void __launch_bounds__(1024) k_scan_tiles(DecodeWork w) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const uint32_t T = uint32_t(w.total_word_tiles);
+  for (uint32_t b0 = 0; b0 < T; b0 += 1024 * 4) {
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t t = b0 + threadIdx.x * 4 + k;
+      v[k] = t < T ? w.tile_base[t] : 0u;
+      sum += v[k];
+    }
+    uint32_t off, total;
+    Scan(tmp).ExclusiveSum(sum, off, total);
+    off += s_carry;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t t = b0 + threadIdx.x * 4 + k;
+      if (t < T) w.tile_base[t] = off;
+      off += v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) w.qcount[5] = s_carry;
+}
+
+__global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
+  if (t0 >= t1) return;
+  uint32_t it = find_word_item(w.items, w.n_items, t0);
+  for (uint32_t wt = t0; wt < t1; ++wt) {
+    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
+    const DecItem& e = w.items[it];
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t P = w4 ? 8u : 32u;
     const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
-    uint32_t bits[kPer];
-    uint32_t cnt = 0;
-#pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {  // all word loads in flight before any store
-      const uint32_t wi = wbase + k * 256 + threadIdx.x;
-      bits[k] = wi < e.n_words ? __ldg(e.words + wi) : 0u;
-    }
-#pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint32_t wi = wbase + k * 256 + threadIdx.x;
-      uint32_t x = present_bits(bits[k], w4);
-      const uint64_t first = uint64_t(wi) * P;
-      const uint64_t left = e.n > first ? e.n - first : 0;
-      if (w4) {
-        if (left < 8) x &= left ? (1u << (4 * left)) - 1u : 0u;
-      } else if (left < 32) {
-        x &= left ? (1u << left) - 1u : 0u;
-      }
-      bits[k] = x;
-      cnt += __popc(x);
-    }
-    const bool vec = (reinterpret_cast<uintptr_t>(e.out) & 15u) == 0;
-#pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {  // zero-fill this warp's 32 words' positions
-      const uint64_t r0 = uint64_t(wbase + k * 256 + warp * 32) * P;
-      const uint64_t r1 = r0 + 32ull * P;
-      if (r0 < e.n) {
-        if (vec && r1 <= e.n) {
-          float4* o = reinterpret_cast<float4*>(e.out + r0);
-          for (uint32_t q = lane; q < 8u * P; q += 32) __stcs(o + q, make_float4(0.f, 0.f, 0.f, 0.f));
-        } else {
-          const uint64_t end = r1 < e.n ? r1 : e.n;
-          for (uint64_t p = r0 + lane; p < end; p += 32) e.out[p] = 0.0f;
-        }
-      }
-    }
+    uint32_t bits[kPerThreadWords], cnt;
+    load_tile_bits(e, wbase, w4, bits, cnt);
     uint32_t off, total;
     Scan(scan_tmp).ExclusiveSum(cnt, off, total);
-    if (total) {
-      if (threadIdx.x == 0) {
-        s_base = atomicAdd(&w.qcount[5], total);
-        atomicAdd(&w.stats[it].presence, total);
-      }
-      __syncthreads();
-      uint32_t j = s_base + off;
+    const uint32_t base = __ldg(w.tile_base + wt);
+    uint32_t j = base + off;
 #pragma unroll
-      for (uint32_t k = 0; k < kPer; ++k) {
-        const uint32_t wi = wbase + k * 256 + threadIdx.x;
-        for (uint32_t x = bits[k]; x; x &= x - 1) {
-          const uint32_t bb = __ffs(x) - 1;
-          w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
-          w.pitem[j] = it;
-          ++j;
-        }
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // list entries: cheap, divergent
+      const uint32_t wi = wbase + k * 256 + threadIdx.x;
+      for (uint32_t x = bits[k]; x; x &= x - 1) {
+        const uint32_t bb = __ffs(x) - 1;
+        w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
+        w.pitem[j] = it;
+        ++j;
       }
     }
-    __syncthreads();  // scan storage / s_base reuse
-  }
-}
-
-// Bucket state from the presence list: (position, 1) into every row's bucket
-// with fire-and-forget 64-bit reductions.
-__global__ void __launch_bounds__(256) k_accumulate(DecodeWork w, const HashParams hp) {
-  const uint32_t total = w.qcount[5];
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint32_t p = w.plist[i];
-    const DecItem& e = w.items[w.pitem[i]];
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-      atomicAdd(w.slot_state + slot, st_add(p));  // result unused: RED.ADD.64
+    __syncthreads();  // the tile's entries are visible to the whole CTA
+    // bucket state, one entry per thread (hashing and reductions stay converged)
+    for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+      const uint32_t i = base + q;
+      const uint32_t p = w.plist[i];
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+        const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        atomicAdd(w.slot_state + slot, st_add(i));  // result unused: RED.ADD.64
+      }
     }
+    __syncthreads();  // scan storage reuse
   }
 }
 
-// ------------------------------------------------------------------ peel
-// Staged appends: warp-aggregated into a per-CTA shared-memory stage and
-// flushed with one global atomic per CTA; a single list counter hit by every
-// warp serialises at one L2 slice otherwise. s_n[0] = reserved entries,
-// s_n[1] = end of the contiguous written prefix (an overflowing warp goes
-// straight to the global list).
+// ------------------------------------------------------------------ staging
+// Warp-aggregated appends into a per-CTA shared-memory stage, flushed with one
+// global atomic per CTA; a single list counter hit by every warp serialises at
+// one L2 slice otherwise. s_n[0] = reserved entries, s_n[1] = end of the
+// contiguous written prefix (an overflowing warp goes straight to the list).
 template <typename T, uint32_t kCap>
 __device__ __forceinline__ void stage_push(bool push, T val, T* s_buf, uint32_t* s_n, T* g_buf,
                                            uint32_t* g_count, uint32_t lane) {
@@ -303,19 +336,73 @@ __device__ __forceinline__ uint32_t slot_row(uint64_t local, uint32_t m) {
   return row;
 }
 
-// Round 0 runs as two ordinary (full-occupancy) kernels over the bucket
-// state as it stands after k_accumulate; the cooperative k_peel then takes
-// the frontier rounds.
-//   k_r0_phase1 (round0_phase1 below, shared with the ordered peel): every
-//     present position inspects its k buckets and peels from its lowest
-//     singleton row, recording its value and the rows it shares;
-//   k_r0_subtract: every peeled position leaves the buckets it shares
-//     (decode.cpp:115-121); buckets whose count drops to one seed round 1
-//     (queue 1, frontier counter qcount[9]). Buckets that held only the
-//     peeled position are left alone: nothing reads them again.
+// ------------------------------------------------------------------ round 0
+// Every listed entry i (position p) inspects its k buckets at round start
+// and peels from its lowest singleton row (lowest slot id: the reference's
+// ascending seed order, decode.cpp:96-99), writing value = sign * residual
+// (decode.cpp:110-111) to val[i]; pinfo[i] keeps (value, rows shared with
+// other positions, peel row) for the subtraction pass. Recovered flags of a
+// warp's 32 consecutive entries are written as one word (no atomics).
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
-                                              uint64_t start, uint64_t stride);
+                                              uint64_t start, uint64_t stride) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t won = 0;
+  const uint32_t total = ldcg(&w.qcount[5]);
+  for (uint64_t base = start - lane; base < total; base += stride) {
+    const uint64_t i = base + lane;
+    bool peeled = false;
+    if (i < total) {
+      const uint32_t p = __ldcs(w.plist + i);
+      const DecItem& e = w.items[__ldcs(w.pitem + i)];
+      uint64_t ls[kMaxRows];
+      unsigned long long st[kMaxRows];
+#pragma unroll
+      for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
+        if (r < hp.rows) {  // issue every row's load before inspecting any
+          ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+          st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
+        }
+      }
+      int best = -1;
+      uint64_t local = 0;
+      float sg = 0.0f;
+      uint32_t shared = 0;  // rows whose bucket holds other positions too
+#pragma unroll
+      for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
+        if (r >= hp.rows) continue;
+        const uint32_t c = st_count(st[r]);
+        shared |= uint32_t(c >= 2u) << r;
+        if (best < 0 && c == 1u) {
+          best = int(r);
+          local = ls[r];
+          sg = dev_sign(hp.row[r], p);
+        }
+      }
+      uint2 info = make_uint2(0u, 0u);
+      if (best >= 0) {
+        const float v = canonical(sg * ldcg(e.sketch + local));
+        w.val[i] = v;
+        info = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
+        peeled = true;
+        ++won;
+      }
+      w.pinfo[i] = info;
+    }
+    const uint32_t m = __ballot_sync(kFull, peeled);
+    if (lane == 0 && base < total) w.bitmap[base >> 5] = m;  // base is a multiple of 32
+  }
+  won = warp_sum32(won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+}
 
+__global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
+  round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x);
+}
+
+// Every entry peeled in round 0 leaves the buckets it shares with other
+// positions (decode.cpp:115-121); buckets whose count drops to one seed round
+// 1 (queue 1, frontier counter qcount[9]). Buckets that held only the peeled
+// entry are left alone: nothing reads them again.
 __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashParams hp) {
   __shared__ uint32_t s_q[kPushStage];
   __shared__ uint32_t s_n[2], s_base;
@@ -348,7 +435,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
       const bool sh = (rows >> r) & 1u;
       loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m) : 0;
-      old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(p)) : 0ull;
+      old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(uint32_t(i))) : 0ull;
       if (sh) red_add_f32(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
     }
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
@@ -358,17 +445,18 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
   stage_flush<uint32_t, kPushStage>(s_q, s_n, &s_base, nq, ncount);
 }
 
+// ------------------------------------------------------------------ frontier
 // Rounds >= 1, single-phase over the frontier: a slot holding exactly one
-// position p (decode.cpp:104-106) claims p (a position reachable through
-// several singleton slots is claimed once), reads value = sign * residual
-// into the output and removes p from its other buckets, pushing buckets whose
-// count drops to one onto the next frontier. Claims, reads and subtractions
-// of one round run concurrently: a remover updates the residual before it
-// decrements the count (fence in between) and a reader acquires the count
-// before it reads the residual, so a bucket seen holding one position shows
-// exactly that position's residual. The peeled set is the complement of the
-// 2-core either way (order-independent); values match the reference's FIFO
-// peel within fp32 reassociation.
+// entry i (decode.cpp:104-106) claims i (an entry reachable through several
+// singleton slots is claimed once), reads value = sign * residual into val[i]
+// and removes i from its other buckets, pushing buckets whose count drops to
+// one onto the next frontier. Claims, reads and subtractions of one round run
+// concurrently: a remover updates the residual before it decrements the
+// count (fence in between) and a reader acquires the count before it reads
+// the residual, so a bucket seen holding one entry shows exactly that entry's
+// residual. The peeled set is the complement of the 2-core either way
+// (order-independent); values match the reference's FIFO peel within fp32
+// reassociation.
 __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const HashParams& hp,
                                                   const SlotItems& si, const uint32_t* q, uint32_t total,
                                                   uint64_t start, uint64_t stride, uint32_t* s_q,
@@ -376,26 +464,27 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
   const uint32_t lane = threadIdx.x & 31;
   uint32_t won = 0;
   for (uint64_t base = start - lane; base < total; base += stride) {
-    const uint64_t i = base + lane;
+    const uint64_t j = base + lane;
     bool win = false;
-    uint32_t p = 0, row = 0;
+    uint32_t i = 0, p = 0, row = 0;
     float v = 0.0f;
     const DecItem* e = w.items;
-    if (i < total) {
-      const uint32_t slot = ldcg(q + i);
+    if (j < total) {
+      const uint32_t slot = ldcg(q + j);
       const unsigned long long st = ld_acquire(w.slot_state + slot);
       if (st_count(st) == 1u) {
-        p = st_pos(st);
-        e = w.items + si.find(slot);
-        const uint64_t local = slot - e->slot_base;
-        row = slot_row(local, e->m);
-        const uint32_t bit = 1u << (p & 31);
-        if (!(atomicOr(w.bitmap + e->bitmap_off + (p >> 5), bit) & bit)) {
+        i = st_entry(st);
+        const uint32_t bit = 1u << (i & 31);
+        if (!(atomicOr(w.bitmap + (i >> 5), bit) & bit)) {
           win = true;
+          p = __ldg(w.plist + i);
+          e = w.items + si.find(slot);
+          const uint64_t local = slot - e->slot_base;
+          row = slot_row(local, e->m);
           float sg = 0.0f;
           _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
           v = canonical(sg * ldcg(e->sketch + local));
-          __stcg(e->out + p, v);
+          w.val[i] = v;
         }
       }
     }
@@ -410,7 +499,7 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
       uint64_t s = 0;
       if (win && r != row) {
         s = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
-        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
         push = st_count(old) == 2u;
       }
       stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
@@ -488,67 +577,18 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
   if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
 }
 
-// Round 0 of the ordered (FIFO-emulating) peel, position-centric: every
-// present position inspects its k buckets and peels from its first singleton
-// row (lowest slot id, the reference's ascending seed order, decode.cpp:96-99).
-__device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
-                                              uint64_t start, uint64_t stride) {
-  uint32_t won = 0;
-  const uint32_t total = ldcg(&w.qcount[5]);  // flat presence list (all items)
-  for (uint64_t i = start; i < total; i += stride) {
-    const uint32_t p = w.plist[i];
-    const DecItem e = w.items[w.pitem[i]];
-    uint64_t ls[kMaxRows];
-    unsigned long long st[kMaxRows];
-#pragma unroll
-    for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
-      if (r < hp.rows) {  // issue every row's load before inspecting any
-        ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-        st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
-      }
-    }
-    int best = -1;
-    uint64_t local = 0;
-    float sg = 0.0f;
-    uint32_t shared = 0;  // rows whose bucket holds other positions too
-#pragma unroll
-    for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
-      if (r >= hp.rows) continue;
-      const uint32_t c = st_count(st[r]);
-      shared |= uint32_t(c >= 2u) << r;
-      if (best < 0 && c == 1u) {
-        best = int(r);
-        local = ls[r];
-        sg = dev_sign(hp.row[r], p);
-      }
-    }
-    if (best < 0) {
-      w.pinfo[i] = make_uint2(0u, 0u);
-      continue;
-    }
-    const float v = canonical(sg * ldcg(e.sketch + local));
-    __stcg(e.out + p, v);
-    red_or_u32(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
-    // the push pass needs the value and only the rows shared with other positions
-    w.pinfo[i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
-    ++won;
-  }
-  won = warp_sum32(won);
-  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
-}
-
 // ------------------------------------------------------------------ ordered peel
 // FIFO-order emulation for indices that can hide mass (1-bit merge carries
 // drop positions whose contributions stay in the sketch, so the reference's
 // values depend on its peel order, decode.cpp:96-122). Generation 0 is the
-// position-centric round above: every position peels from its lowest
-// singleton slot, exactly the reference's ascending seed order. Generation
-// g+1 is the queue of slots whose count dropped to one while generation g was
-// processed, ordered as the reference's deque orders it: by the processing
-// order of the peeled position, then by row. Pushes carry that key, the host
-// sorts each generation (cub radix sort), and a position that is a singleton
-// in several queued slots is peeled from the first of them (epoch-tagged
-// atomicMax claims).
+// entry-centric round above: every entry peels from its lowest singleton
+// slot, exactly the reference's ascending seed order. Generation g+1 is the
+// queue of slots whose count dropped to one while generation g was processed,
+// ordered as the reference's deque orders it: by the processing order of the
+// peeled entry, then by row. Pushes carry that key, the host sorts each
+// generation (cub radix sort), and an entry that is a singleton in several
+// queued slots is peeled from the first of them (epoch-tagged atomicMax
+// claims).
 struct OrdPush {
   unsigned long long* keys;
   uint32_t* slots;
@@ -560,9 +600,8 @@ constexpr unsigned long long kKeyMask = (1ull << 36) - 1ull;
 
 constexpr uint32_t kOrdStage = 2048;
 
-__device__ __forceinline__ void ord_push(bool push, unsigned long long key, uint32_t slot,
-                                         unsigned long long* s_k, uint32_t* s_s, uint32_t* s_n,
-                                         const OrdPush& o) {
+__device__ __forceinline__ void ord_push(bool push, uint32_t slot, unsigned long long* s_k, uint32_t* s_s,
+                                         uint32_t* s_n, const OrdPush& o) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t mask = __ballot_sync(kFull, push);
   if (!mask) return;
@@ -581,10 +620,10 @@ __device__ __forceinline__ void ord_push(bool push, unsigned long long key, uint
   if (push) {
     const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
     if (direct) {
-      o.keys[idx] = key;
+      o.keys[idx] = 0ull;
       o.slots[idx] = slot;
     } else {
-      s_k[idx] = key;
+      s_k[idx] = 0ull;
       s_s[idx] = slot;
     }
   }
@@ -603,11 +642,6 @@ __device__ __forceinline__ void ord_flush(unsigned long long* s_k, uint32_t* s_s
     o.keys[*s_b + i] = s_k[i];
     o.slots[*s_b + i] = s_s[i];
   }
-}
-
-__global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
-  round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x,
-                uint64_t(gridDim.x) * blockDim.x);
 }
 
 // Generation-0 subtraction; pushes are keyed (winner slot, row).
@@ -629,16 +663,16 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
     uint32_t p = 0, rows = 0;
     float v = 0.0f;
     unsigned long long wkey = 0;
-    DecItem e{};
+    const DecItem* e = w.items;
     if (i < total) {
       const uint2 info = w.pinfo[i];
       if (info.y & 0x100u) {
         rows = info.y & 0xFFu;
         v = __uint_as_float(info.x);
         p = w.plist[i];
-        e = w.items[w.pitem[i]];
+        e = w.items + w.pitem[i];
         const uint32_t best = (info.y >> 12) & 0xFu;
-        const uint64_t ws = e.slot_base + uint64_t(best) * e.m + dev_bucket(row_coef(hp, best), p, e.m);
+        const uint64_t ws = e->slot_base + uint64_t(best) * e->m + dev_bucket(row_coef(hp, best), p, e->m);
         wkey = ws * hp.rows;
       }
     }
@@ -646,16 +680,16 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
       bool push = false;
       uint64_t s = 0;
       if (rows >> r & 1u) {
-        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-        s = e.slot_base + local;
-        red_add_f32(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
+        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        s = e->slot_base + local;
+        red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
         // the reference queues a slot when its LAST subtraction of the
         // generation (in FIFO order) leaves one position: keep the max key
         atomicMax(o.slot_key + s, o.tag | (wkey + r));
-        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(uint32_t(i)));
         push = st_count(old) == 2u;
       }
-      ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
+      ord_push(push, uint32_t(s), s_k, s_s, s_n, o);
     }
   }
   ord_flush(s_k, s_s, s_n, &s_b, o);
@@ -670,13 +704,10 @@ __global__ void __launch_bounds__(256) k_ord_keys(unsigned long long* keys, cons
 __global__ void __launch_bounds__(256) k_ord_claim(DecodeWork w, const uint32_t* __restrict__ q,
                                                    uint32_t qlen, unsigned long long* claim,
                                                    uint32_t epoch) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < qlen; i += gridDim.x * blockDim.x) {
-    const uint32_t slot = q[i];
-    const unsigned long long st = w.slot_state[slot];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < qlen; j += gridDim.x * blockDim.x) {
+    const unsigned long long st = w.slot_state[q[j]];
     if (st_count(st) != 1u) continue;
-    const uint32_t it = find_slot_item(w.items, w.n_items, slot);
-    const uint64_t pos = w.items[it].bitmap_off * 32ull + st_pos(st);
-    atomicMax(claim + pos, (uint64_t(epoch) << 32) | uint64_t(~i));
+    atomicMax(claim + st_entry(st), (uint64_t(epoch) << 32) | uint64_t(~j));
   }
 }
 
@@ -696,25 +727,25 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t won = 0;
   for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < qlen; base += stride) {
-    const uint32_t i = base + lane;
+    const uint32_t j = base + lane;
     bool win = false;
-    uint32_t slot = 0, p = 0;
-    DecItem e{};
+    uint32_t slot = 0, i = 0, p = 0;
+    const DecItem* e = w.items;
     float v = 0.0f;
-    if (i < qlen) {
-      slot = q[i];
+    if (j < qlen) {
+      slot = q[j];
       const unsigned long long st = w.slot_state[slot];
       if (st_count(st) == 1u) {
-        p = st_pos(st);
-        const uint32_t it = find_slot_item(w.items, w.n_items, slot);
-        e = w.items[it];
-        win = claim[e.bitmap_off * 32ull + p] == ((uint64_t(epoch) << 32) | uint64_t(~i));
+        i = st_entry(st);
+        win = claim[i] == ((uint64_t(epoch) << 32) | uint64_t(~j));
         if (win) {
-          const uint64_t local = slot - e.slot_base;
-          const uint32_t row = uint32_t(local / e.m);
-          v = canonical(dev_sign(row_coef(hp, row), p) * e.sketch[local]);  // decode.cpp:110-111
-          e.out[p] = v;
-          red_or_u32(w.bitmap + e.bitmap_off + (p >> 5), 1u << (p & 31));
+          p = w.plist[i];
+          e = w.items + w.pitem[i];
+          const uint64_t local = slot - e->slot_base;
+          const uint32_t row = uint32_t(local / e->m);
+          v = canonical(dev_sign(row_coef(hp, row), p) * e->sketch[local]);  // decode.cpp:110-111
+          w.val[i] = v;
+          red_or_u32(w.bitmap + (i >> 5), 1u << (i & 31));
           ++won;
         }
       }
@@ -723,16 +754,16 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
       bool push = false;
       uint64_t s = 0;
       if (win) {
-        const uint64_t local = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
-        s = e.slot_base + local;
+        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        s = e->slot_base + local;
         if (s != slot) {
-          red_add_f32(e.sketch + local, -(dev_sign(hp.row[r], p) * v));
-          atomicMax(o.slot_key + s, o.tag | (uint64_t(i) * hp.rows + r));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(p));
+          red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
+          atomicMax(o.slot_key + s, o.tag | (uint64_t(j) * hp.rows + r));
+          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
           push = st_count(old) == 2u;
         }
       }
-      ord_push(push, 0ull, uint32_t(s), s_k, s_s, s_n, o);
+      ord_push(push, uint32_t(s), s_k, s_s, s_n, o);
     }
   }
   won = warp_sum32(won);
@@ -741,37 +772,76 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
 }
 
 // ------------------------------------------------------------------ estimate
+// Median-of-rows estimate (decode.cpp:130-138 / :43-47) into val[i] for every
+// listed entry the peel left unresolved.
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
   const uint32_t total = w.qcount[5];
-  if (total == w.qcount[4]) {  // every present position peeled: nothing to estimate
+  if (total == w.qcount[4]) return;  // every listed entry peeled: nothing to estimate
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (w.bitmap[i >> 5] >> (i & 31) & 1u) continue;
+    const uint32_t p = w.plist[i], it = w.pitem[i];
+    const DecItem& e = w.items[it];
+    float est[kMaxRows];
+#pragma unroll
+    for (uint32_t r = 0; r < kMaxRows; ++r) {
+      if (r >= hp.rows) break;
+      est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m)];
+    }
+    w.val[i] = canonical(median_rows(est, hp.rows));
+    const uint32_t b = atomicAdd(&w.stats[it].unresolved, 1u);
+    if (w.unresolved) w.unresolved[e.list_off + b] = p;
+  }
+}
+
+// ------------------------------------------------------------------ emit
+// The dense shard, one word tile per CTA step (same tiles as k_list): the
+// tile's output range is zero-filled with coalesced 16-byte stores
+// (decode.cpp:61-64 zero-initialises the output), then the tile's listed
+// entries - a contiguous list range, ascending positions - drop their
+// decoded values on top; those stores hit lines the zero-fill just wrote.
+__global__ void __launch_bounds__(256) k_emit(DecodeWork w) {
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
+  if (t0 >= t1) {
     span_end(w.span);
     return;
   }
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t base = gtid - lane; base < total; base += gstride) {
-    const uint64_t i = base + lane;
-    bool unres = false;
-    uint32_t p = 0, it = 0;
-    DecItem e{};
-    if (i < total) {
-      p = w.plist[i];
-      it = w.pitem[i];
-      e = w.items[it];
-      unres = !(w.bitmap[e.bitmap_off + (p >> 5)] >> (p & 31) & 1u);
-      if (unres) {  // decode.cpp:130-138 / :43-47
-        float est[kMaxRows];
+  const uint32_t total = w.qcount[5];
+  uint32_t it = find_word_item(w.items, w.n_items, t0);
+  for (uint32_t wt = t0; wt < t1; ++wt) {
+    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
+    const DecItem& e = w.items[it];
+    const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
+    const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
+    const uint64_t p0 = wbase * P;
+    const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
+    float* out = e.out;
+    // the tile's first listed entries are fetched ahead of the zero-fill
+    const uint32_t lb = __ldg(w.tile_base + wt);
+    const uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
+    constexpr uint32_t kAhead = 2;
+    uint32_t pp[kAhead];
+    float vv[kAhead];
 #pragma unroll
-        for (uint32_t r = 0; r < kMaxRows; ++r) {
-          if (r >= hp.rows) break;
-          est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m)];
-        }
-        e.out[p] = canonical(median_rows(est, hp.rows));
-        const uint32_t b = atomicAdd(&w.stats[it].unresolved, 1u);
-        if (w.unresolved) w.unresolved[e.list_off + b] = p;
-      }
+    for (uint32_t u = 0; u < kAhead; ++u) {
+      const uint32_t i = lb + threadIdx.x + u * 256;
+      pp[u] = i < le ? __ldcs(w.plist + i) : 0xFFFFFFFFu;
+      vv[u] = i < le ? __ldcs(w.val + i) : 0.0f;
     }
+    if ((reinterpret_cast<uintptr_t>(out + p0) & 15u) == 0) {
+      const uint64_t nq = (p1 - p0) / 4;
+      float4* o = reinterpret_cast<float4*>(out + p0);
+      for (uint64_t q = threadIdx.x; q < nq; q += blockDim.x) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint64_t p = p0 + nq * 4 + threadIdx.x; p < p1; p += blockDim.x) out[p] = 0.0f;
+    } else {
+      for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) out[p] = 0.0f;
+    }
+    __syncthreads();  // zeros before values
+#pragma unroll
+    for (uint32_t u = 0; u < kAhead; ++u)
+      if (pp[u] != 0xFFFFFFFFu) out[pp[u]] = vv[u];
+    for (uint32_t i = lb + threadIdx.x + kAhead * 256; i < le; i += blockDim.x)
+      out[__ldcs(w.plist + i)] = __ldcs(w.val + i);
   }
   span_end(w.span);
 }
@@ -813,15 +883,7 @@ __global__ void k_estimate_targets(const uint32_t* __restrict__ targets, uint32_
 __global__ void k_word_counts(const uint32_t* __restrict__ words, uint32_t n, uint32_t n_words,
                               bool w4, uint32_t* __restrict__ counts) {
   for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < n_words; wi += gridDim.x * blockDim.x) {
-    uint32_t bits = present_bits(words[wi], w4);
-    const uint32_t P = w4 ? 8u : 32u;
-    const uint64_t first = uint64_t(wi) * P, left = n > first ? n - first : 0;
-    if (w4) {
-      if (left < 8) bits &= (1u << (4 * left)) - 1u;
-    } else if (left < 32) {
-      bits &= (1u << left) - 1u;
-    }
-    counts[wi] = __popc(bits);
+    counts[wi] = __popc(present_bits(words[wi], w4, wi, n));
   }
 }
 
@@ -829,14 +891,8 @@ __global__ void k_word_positions(const uint32_t* __restrict__ words, uint32_t n,
                                  bool w4, const uint32_t* __restrict__ offsets,
                                  uint32_t* __restrict__ out, uint32_t* count_dev) {
   for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < n_words; wi += gridDim.x * blockDim.x) {
-    uint32_t bits = present_bits(words[wi], w4);
+    uint32_t bits = present_bits(words[wi], w4, wi, n);
     const uint32_t P = w4 ? 8u : 32u;
-    const uint64_t first = uint64_t(wi) * P, left = n > first ? n - first : 0;
-    if (w4) {
-      if (left < 8) bits &= (1u << (4 * left)) - 1u;
-    } else if (left < 32) {
-      bits &= (1u << left) - 1u;
-    }
     uint32_t o = offsets[wi];
     const uint32_t c = __popc(bits);
     while (bits) {
@@ -853,24 +909,29 @@ int grid_for(uint64_t n, int threads) {
   return int(b < 2048 ? (b ? b : 1) : 2048);
 }
 
+// count -> scan -> list + bucket state (bucket state zeroed in between: it is
+// first touched by k_list). Returns the grid used for the word-tile passes.
+int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, cudaStream_t stream) {
+  const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
+  const int g = int(g64);
+  k_count<<<g, 256, 0, stream>>>(w);
+  k_scan_tiles<<<1, 1024, 0, stream>>>(w);
+  ZeroRanges zr{};
+  zr.ptr[0] = w.slot_state;
+  zr.bytes[0] = w.total_slots * 8;
+  zr.n = 1;
+  launch_zero(zr, stream);
+  k_list<<<g, 256, 0, stream>>>(w, hp);
+  return g;
+}
+
 }  // namespace
 
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
                   cudaStream_t stream) {
   if (w.n_items == 0) return 0;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_build, 256, 0);
-  uint64_t g = uint64_t(std::max(per_sm, 1)) * di.sms;
-  if (w.total_word_tiles < g) g = w.total_word_tiles;
-  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w);
-  // bucket state zeroed after the streaming output fill, so it is L2-resident
-  // for the reductions and the peel
-  ZeroRanges zr{};
-  zr.ptr[0] = w.slot_state;
-  zr.bytes[0] = w.total_slots * 8;
-  zr.n = 1;
-  launch_zero(zr, stream);
-  k_accumulate<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  const int g = build_passes(di, w, hp, stream);
   k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
@@ -883,7 +944,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return 7;
+  return 9;
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
@@ -892,23 +953,14 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   if (w.n_items == 0) return 0;
   int launches = 0;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_build, 256, 0);
-  uint64_t g = uint64_t(std::max(per_sm, 1)) * di.sms;
-  if (w.total_word_tiles < g) g = w.total_word_tiles;
-  k_build<<<int(g ? g : 1), 256, 0, stream>>>(w);
-  ZeroRanges zr{};
-  zr.ptr[0] = w.slot_state;
-  zr.bytes[0] = w.total_slots * 8;
-  zr.n = 1;
-  launch_zero(zr, stream);
-  k_accumulate<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  const int g = build_passes(di, w, hp, stream);
   const int grid = di.sms * 4;
   k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
   ++epoch;
   OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
   cudaMemsetAsync(ob.count, 0, 4, stream);
   k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
-  launches += 5;
+  launches += 6;
   uint32_t gen = 1;
   unsigned long long* cur_keys = ob.keys[0];
   uint32_t* cur_slots = ob.slots[0];
@@ -937,7 +989,14 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   if (rounds) *rounds = gen;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return launches + 1;
+  return launches + 2;
+}
+
+int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream) {
+  if (w.n_items == 0) return 0;
+  const uint64_t g = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 8);
+  k_emit<<<int(g), 256, 0, stream>>>(w);
+  return 1;
 }
 
 size_t ordered_sort_scratch_bytes(uint32_t count) {

@@ -19,7 +19,7 @@ constexpr uint32_t kSampleChunk = 1024;
 constexpr uint32_t kSampleBins = 4096;  // top 12 bits of the 31-bit magnitude key
 constexpr uint32_t kSampleShift = 19;
 constexpr uint32_t kRadixBins = 2048;   // 11/10/10-bit digits of the key
-constexpr uint32_t kDecWordTile = 1024; // merged-index words per decode build tile
+constexpr uint32_t kDecWordTile = 4096; // merged-index words per decode word tile (16 per thread)
 constexpr uint32_t kMaxFlatItems = 4096; // items per call (flattened iteration bound)
 
 // Per-row hash coefficients (reference hash.hpp:27-33), derived on the host.
@@ -77,7 +77,6 @@ struct DecItem {
   float* sketch;          // summed sketch rows*m (mutated into the residual)
   float* out;             // dense output for the segment (n floats)
   uint64_t slot_base;     // first global slot id (rows*m per item)
-  uint64_t bitmap_off;    // recovered-bitmap word offset
   uint64_t word_tile_begin;
   uint64_t list_off;      // presence list offset
   uint32_t n, m, flags, n_words;

@@ -1254,6 +1254,17 @@ __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__
     const CopyItem it = items[lo];
     const uint64_t b = (tile - it.tile_begin) * kCopyTile;
     const uint64_t e = min(it.n, b + kCopyTile);
+    if (!it.src) {  // zero-fill item
+      if ((reinterpret_cast<uintptr_t>(it.dst) & 15u) == 0) {
+        for (uint64_t i = b + 4ull * threadIdx.x; i < e; i += 4ull * blockDim.x) {
+          if (i + 4 <= e) __stcs(reinterpret_cast<float4*>(it.dst + i), make_float4(0.f, 0.f, 0.f, 0.f));
+          else for (uint64_t j = i; j < e; ++j) it.dst[j] = 0.0f;
+        }
+      } else {
+        for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) it.dst[i] = 0.0f;
+      }
+      continue;
+    }
     const bool vec = ((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15u) == 0;
     if (vec) {
       for (uint64_t i = b + 4ull * threadIdx.x; i < e; i += 4ull * blockDim.x) {
@@ -1478,9 +1489,12 @@ uint64_t copy_tiles(CopyItem* items, uint32_t n_items) {
 }
 
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, bool one_tile_per_cta) {
   if (!n_items || !total_tiles) return 0;
-  const uint64_t g = std::min<uint64_t>(total_tiles, uint64_t(di.sms) * 8);
+  // one tile per CTA: short CTAs that a higher-priority stream's kernels can
+  // interleave with as SMs free up (side-stream copies)
+  const uint64_t g = one_tile_per_cta ? std::min<uint64_t>(total_tiles, 0x7FFFFFFFull)
+                                      : std::min<uint64_t>(total_tiles, uint64_t(di.sms) * 8);
   k_copy_items<<<int(g), 256, 0, stream>>>(items, n_items, total_tiles);
   return 1;
 }

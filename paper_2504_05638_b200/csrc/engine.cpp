@@ -183,6 +183,12 @@ Engine::~Engine() {
   if (hev_join_) cudaEventDestroy(hev_join_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
+  if (aux_) {
+    cudaStreamSynchronize(aux_);
+    cudaEventDestroy(aux_fork_);
+    cudaEventDestroy(aux_join_);
+    cudaStreamDestroy(aux_);
+  }
   if (own_comm_ && comm_) nccl().CommDestroy(comm_);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
 }
@@ -410,8 +416,17 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
 }
 
 // ------------------------------------------------------------------ decode
+void Engine::ensure_aux() {
+  if (aux_) return;
+  int lo = 0, hi = 0;  // lowest priority: decode kernels take SMs first as side CTAs retire
+  cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, lo), "aux stream");
+  cuda_check(cudaEventCreateWithFlags(&aux_fork_, cudaEventDisableTiming), "aux event");
+  cuda_check(cudaEventCreateWithFlags(&aux_join_, cudaEventDisableTiming), "aux event");
+}
+
 void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
-                        bool ordered) {
+                        bool ordered, cudaEvent_t zero_done) {
   const uint32_t n = uint32_t(items.size());
   dec_stats_.assign(n, DecStats{});
   if (n == 0) return;
@@ -419,8 +434,6 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   for (DecItem& d : items) {
     d.slot_base = slots;
     slots += uint64_t(hp.rows) * d.m;
-    d.bitmap_off = bm;
-    bm += (uint64_t(d.n) + 31) / 32;
     d.word_tile_begin = wt;
     wt += (uint64_t(d.n_words) + kDecWordTile - 1) / kDecWordTile;
     d.list_off = list;
@@ -436,7 +449,10 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.total_word_tiles = wt;
   w.total_slots = slots;
   w.slot_state = static_cast<unsigned long long*>(ws_.get("slot_state", slots * 8, false, stream_));
+  bm = (list + 31) / 32;
   w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
+  w.val = static_cast<float*>(ws_.get("dec_val", list * 4, false, stream_));
+  w.tile_base = static_cast<uint32_t*>(ws_.get("tile_base", wt * 4, false, stream_));
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
   w.pitem = static_cast<uint32_t*>(ws_.get("pitem", list * 4, false, stream_));
   w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));
@@ -463,7 +479,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     ob.slots[0] = static_cast<uint32_t*>(ws_.get("ord_s0", slots * 4, false, stream_));
     ob.slots[1] = static_cast<uint32_t*>(ws_.get("ord_s1", slots * 4, false, stream_));
     ob.count = static_cast<uint32_t*>(ws_.get("ord_count", 16, false, stream_));
-    ob.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", bm * 32 * 8, true, stream_));
+    ob.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", list * 8, true, stream_));
     ob.slot_key = static_cast<unsigned long long*>(ws_.get("ord_slot_key", slots * 8, true, stream_));
     ob.scratch_bytes = ordered_sort_scratch_bytes(uint32_t(std::min<uint64_t>(slots, 0x7FFFFFFF)));
     ob.scratch = ws_.get("ord_scratch", ob.scratch_bytes, false, stream_);
@@ -473,6 +489,8 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   } else {
     launches_ += launch_decode(di_, w, hp, stream_);
   }
+  if (zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait side stream");
+  launches_ += launch_decode_emit(di_, w, stream_);
   cuda_check(cudaGetLastError(), "decode launch");
   if (dbg) {
     unsigned long long t[64];
@@ -812,18 +830,35 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     }
   }
   run_select_encode(enc, w == 4, hp, false, "nccl");
-  // raw segments: packed into the send blocks, or (W == 1) copied straight to
-  // the output; after this the gradient is no longer read
-  std::vector<CopyItem>& raw_now = W > 1 ? pack : unpack;
-  if (!raw_now.empty()) {
-    const uint64_t tt = copy_tiles(raw_now.data(), uint32_t(raw_now.size()));
-    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", raw_now.size() * sizeof(CopyItem), false, stream_));
-    upload(raw_now.data(), raw_now.size() * sizeof(CopyItem), d_pack);
-    launches_ += launch_copy_items(di_, d_pack, uint32_t(raw_now.size()), tt, stream_);
+  // raw segments (W > 1): packed into the send blocks before the exchange
+  if (W > 1 && !pack.empty()) {
+    const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
+    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", pack.size() * sizeof(CopyItem), false, stream_));
+    upload(pack.data(), pack.size() * sizeof(CopyItem), d_pack);
+    launches_ += launch_copy_items(di_, d_pack, uint32_t(pack.size()), tt, stream_);
   }
-  if (grad_read_ev_)  // an external record node when captured: the copy stream waits on it
-    cuda_check(cudaEventRecordWithFlags(grad_read_ev_, stream_, capturing_ ? cudaEventRecordExternal : 0),
-               "grad-read event");
+  // Side stream (W == 1), overlapping the latency-bound decode: the raw
+  // segments copied straight from the gradient to the output.
+  std::vector<CopyItem> side;
+  if (W == 1) side = unpack;
+  cudaEvent_t zero_done = nullptr;
+  const auto ev_flags = capturing_ ? cudaEventRecordExternal : 0u;  // external: waited on outside the graph
+  if (!side.empty()) {
+    ensure_aux();
+    const uint64_t tt = copy_tiles(side.data(), uint32_t(side.size()));
+    auto* d_side = static_cast<CopyItem*>(ws_.get("nc_side", side.size() * sizeof(CopyItem), false, stream_));
+    upload(side.data(), side.size() * sizeof(CopyItem), d_side);
+    cuda_check(cudaEventRecord(aux_fork_, stream_), "fork");
+    cuda_check(cudaStreamWaitEvent(aux_, aux_fork_, 0), "fork wait");
+    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true);
+    cuda_check(cudaEventRecord(aux_join_, aux_), "join");
+    zero_done = aux_join_;
+  }
+  // after this the gradient is no longer read
+  if (grad_read_ev_) {
+    if (W == 1 && zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait raw copy");
+    cuda_check(cudaEventRecordWithFlags(grad_read_ev_, stream_, ev_flags), "grad-read event");
+  }
   if (W > 1) {
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
     nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
@@ -847,7 +882,7 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     d.n_words = p.n_words;
     dec.push_back(d);
   }
-  run_decode(dec, hp, false, w == 1 && W > 1);
+  run_decode(dec, hp, false, w == 1 && W > 1, zero_done);
   if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));

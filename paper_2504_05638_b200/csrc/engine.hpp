@@ -181,8 +181,15 @@ class Engine {
   cudaEvent_t grad_read_ev_ = nullptr;  // recorded by reduce_shards once the gradient is consumed
   void run_select_encode(std::vector<EncItem>& items, bool w4, const HashParams& hp,
                          bool want_kept, const char* tag);
+  // Decode into the items' outputs; the final emit waits on `zero_done` (if
+  // set), the side stream's join event.
   void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
-                  bool ordered);
+                  bool ordered, cudaEvent_t zero_done = nullptr);
+  // Side stream for bandwidth work that overlaps the latency-bound peel
+  // (W == 1 raw-segment copies); fork/join by events.
+  cudaStream_t aux_ = nullptr;
+  cudaEvent_t aux_fork_ = nullptr, aux_join_ = nullptr;
+  void ensure_aux();
   void upload(const void* host, size_t bytes, void* dev);
   // zero byte ranges with one kernel launch (no copy-engine memset)
   void zero(const std::vector<std::pair<void*, uint64_t>>& ranges);

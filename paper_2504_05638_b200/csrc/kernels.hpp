@@ -64,7 +64,7 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
 int launch_add(const float* a, const float* b, float* out, uint64_t n, cudaStream_t stream);
 
 // Strided segment copies: dst[i] = src[i] for each item (pack/unpack raw
-// segments around the reduce-scatter).
+// segments around the reduce-scatter); src == nullptr zero-fills dst.
 struct CopyItem {
   const float* src;
   float* dst;
@@ -75,7 +75,7 @@ constexpr uint32_t kCopyTile = 4096;
 // Assigns tile_begin; returns the total tile count.
 uint64_t copy_tiles(CopyItem* items, uint32_t n_items);
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream);
+                      cudaStream_t stream, bool one_tile_per_cta = false);
 
 // Raw (uncompressed) segments in a simulated world: dst[i] = sum_r src_r[i]
 // in ascending rank order. srcs: device array [n_items * world].
@@ -104,8 +104,10 @@ struct DecodeWork {
   uint32_t n_items;
   uint64_t total_word_tiles;
   uint64_t total_slots;
-  unsigned long long* slot_state;  // (count << 40) | key_sum, total_slots
-  uint32_t* bitmap;                // recovered bits
+  unsigned long long* slot_state;  // (sum of list indices) << 24 | count, total_slots
+  uint32_t* bitmap;                // recovered flag per presence-list entry
+  float* val;                      // decoded value per presence-list entry
+  uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
@@ -117,20 +119,24 @@ struct DecodeWork {
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
   unsigned long long* span;        // optional: execution span of build .. final (timing mode)
 };
-// Peel + estimate. Zero-fills each item's `out`, rebuilds bucket state from
-// the merged index, peels in synchronous rounds inside one cooperative
-// persistent kernel, and estimates the rest (decode.cpp:53-140 semantics).
+// Presence list + bucket state from the merged index, round-0 peel, frontier
+// rounds inside one cooperative persistent kernel, estimation of the rest
+// (decode.cpp:53-140 semantics), all into the list-ordered val[]; finish
+// with launch_decode_emit.
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
                   cudaStream_t stream);
 
+// Final step of either decode: writes every item's dense output (zeros, and
+// the decoded value of each listed entry).
+int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream);
 // FIFO-order peel (see decode.cu): host-driven generations, one sort each.
-// claim: u64 per position slot (bitmap_off * 32 + p), zero-initialised once;
+// claim: u64 per presence-list entry, zero-initialised once;
 // epoch is advanced per generation and persists across calls.
 struct OrderedBuffers {
   unsigned long long* keys[2];
   uint32_t* slots[2];  // capacity total_slots each
   uint32_t* count;
-  unsigned long long* claim;
+  unsigned long long* claim;  // per presence-list entry
   unsigned long long* slot_key;  // u64 per slot, zero-initialised once
   void* scratch;
   size_t scratch_bytes;
