@@ -301,7 +301,7 @@ def run_b200(args):
         },
         "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4)},
-        "roofline": {"kernel": "k_fused (sample + select + split + index + sketch scatter)",
+        "roofline": {"kernel": "k_fused_tma (sample + window + TMA-staged select/split/index/sketch scatter)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(fused_bytes),
