@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
       const uint32_t i = base + q;
       const uint32_t p = w.plist[i];
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-        const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+        const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
         atomicAdd(w.slot_state + slot, st_add(i));  // result unused: RED.ADD.64
       }
     }
@@ -359,7 +359,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
 #pragma unroll
       for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
         if (r < hp.rows) {  // issue every row's load before inspecting any
-          ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m);
+          ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
           st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
         }
       }
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
     uint64_t loc[kMaxRows];
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
       const bool sh = (rows >> r) & 1u;
-      loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m) : 0;
+      loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul) : 0;
       old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(uint32_t(i))) : 0ull;
       if (sh) red_add_f32(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
     }
@@ -490,7 +490,7 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
     }
     if (win) {
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && r != row)
-        red_add_f32(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m), -(dev_sign(hp.row[r], p) * v));
+        red_add_f32(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul), -(dev_sign(hp.row[r], p) * v));
       __threadfence();  // residual updates before the count decrements
       ++won;
     }
@@ -498,7 +498,7 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
       bool push = false;
       uint64_t s = 0;
       if (win && r != row) {
-        s = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        s = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
         const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
         push = st_count(old) == 2u;
       }
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
         p = w.plist[i];
         e = w.items + w.pitem[i];
         const uint32_t best = (info.y >> 12) & 0xFu;
-        const uint64_t ws = e->slot_base + uint64_t(best) * e->m + dev_bucket(row_coef(hp, best), p, e->m);
+        const uint64_t ws = e->slot_base + uint64_t(best) * e->m + dev_bucket(row_coef(hp, best), p, e->m, e->mmul);
         wkey = ws * hp.rows;
       }
     }
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
       bool push = false;
       uint64_t s = 0;
       if (rows >> r & 1u) {
-        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
         s = e->slot_base + local;
         red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
         // the reference queues a slot when its LAST subtraction of the
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
       bool push = false;
       uint64_t s = 0;
       if (win) {
-        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m);
+        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
         s = e->slot_base + local;
         if (s != slot) {
           red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp
 #pragma unroll
     for (uint32_t r = 0; r < kMaxRows; ++r) {
       if (r >= hp.rows) break;
-      est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m)];
+      est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul)];
     }
     w.val[i] = canonical(median_rows(est, hp.rows));
     const uint32_t b = atomicAdd(&w.stats[it].unresolved, 1u);

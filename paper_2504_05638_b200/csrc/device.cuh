@@ -57,6 +57,7 @@ struct EncItem {
   uint64_t hi_off;        // offset into the speculatively-kept pool (uint2)
   uint32_t n, m, c, flags;
   uint32_t cand_cap, sample_stride, sample_tiles, hi_cap;
+  uint64_t mmul;  // fastmod multiplier for m (fastmod_magic), set by the engine
 };
 
 // Select state per item (device; reset by the window kernel every call).
@@ -80,6 +81,7 @@ struct DecItem {
   uint64_t word_tile_begin;
   uint64_t list_off;      // presence list offset
   uint32_t n, m, flags, n_words;
+  uint64_t mmul;          // fastmod multiplier for m (fastmod_magic), set by the engine
 };
 
 struct DecStats {  // per decode item, device
@@ -91,6 +93,15 @@ struct DecStats {  // per decode item, device
 __device__ __forceinline__ uint32_t dev_bucket(const RowCoef& c, uint32_t p, uint32_t m) {
   const uint64_t h = c.pos_a * (uint64_t(p) + 0x9E3779B9ull) + c.pos_b;  // hash.hpp:36
   return uint32_t(h >> 32) % m;                                            // hash.hpp:37
+}
+// x % m without a divide: Lemire's fastmod, exact for every 32-bit x and
+// m >= 1 with mmul = fastmod_magic(m) = floor((2^64 - 1) / m) + 1 (mod 2^64).
+__device__ __forceinline__ uint32_t fastmod(uint32_t x, uint64_t mmul, uint32_t m) {
+  return uint32_t(__umul64hi(mmul * uint64_t(x), uint64_t(m)));
+}
+__device__ __forceinline__ uint32_t dev_bucket(const RowCoef& c, uint32_t p, uint32_t m, uint64_t mmul) {
+  const uint64_t h = c.pos_a * (uint64_t(p) + 0x9E3779B9ull) + c.pos_b;  // hash.hpp:36
+  return fastmod(uint32_t(h >> 32), mmul, m);                              // hash.hpp:37
 }
 __device__ __forceinline__ float dev_sign(const RowCoef& c, uint32_t p) {
   const uint64_t h = c.sgn_a * (uint64_t(p) + 0x85EBCA77ull) + c.sgn_b;  // hash.hpp:41
@@ -172,6 +183,8 @@ __device__ __forceinline__ RowCoef row_coef(const HashParams& hp, uint32_t row) 
   return c;
 }
 #endif
+
+inline uint64_t fastmod_magic(uint32_t m) { return ~0ull / uint64_t(m ? m : 1) + 1ull; }
 
 // Host: coefficient derivation (hash.hpp:15-33).
 inline uint64_t splitmix64(uint64_t x) {

@@ -244,7 +244,7 @@ __device__ __forceinline__ void load_source(const EncItem& e, uint32_t pos, bool
 __device__ __forceinline__ void scatter_sketch(const EncItem& e, const HashParams& hp, uint32_t p,
                                                float v) {
   _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows)
-    red_add_f32(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m), dev_sign(hp.row[r], p) * v);
+    red_add_f32(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul), dev_sign(hp.row[r], p) * v);
 }
 
 // --------------------------------------------------------------- fused pass

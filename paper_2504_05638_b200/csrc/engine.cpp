@@ -377,6 +377,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     e.hi_cap = select ? uint32_t(std::min<uint64_t>(e.n, uint64_t(e.n - e.c) + 1024)) : 0;
     hi += e.hi_cap;
   }
+  for (EncItem& e : items) e.mmul = fastmod_magic(e.m);
   auto* d_items = static_cast<EncItem*>(ws_.get("enc_items", n * sizeof(EncItem), false, stream_));
   upload(items.data(), n * sizeof(EncItem), d_items);
   auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
@@ -432,6 +433,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   if (n == 0) return;
   uint64_t slots = 0, bm = 0, wt = 0, list = 0;
   for (DecItem& d : items) {
+    d.mmul = fastmod_magic(d.m);
     d.slot_base = slots;
     slots += uint64_t(hp.rows) * d.m;
     d.word_tile_begin = wt;
