@@ -379,6 +379,14 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
         }
       }
       uint2 info = make_uint2(0u, 0u);
+      if (best < 0 && w.slot_mark) {  // unresolved after round 0: its buckets still matter
+#pragma unroll
+        for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r)
+          if (r < hp.rows) {
+            const uint64_t sl = e.slot_base + ls[r];
+            red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
+          }
+      }
       if (best >= 0) {
         const float v = canonical(sg * ldcg(e.sketch + local));
         w.val[i] = v;
@@ -401,8 +409,10 @@ __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParam
 
 // Every entry peeled in round 0 leaves the buckets it shares with other
 // positions (decode.cpp:115-121); buckets whose count drops to one seed round
-// 1 (queue 1, frontier counter qcount[9]). Buckets that held only the peeled
-// entry are left alone: nothing reads them again.
+// 1 (queue 1, frontier counter qcount[9]). Only buckets that also hold an
+// entry round 0 left unresolved (slot_mark, set by round0_phase1) are
+// touched: every other bucket would only empty out, and nothing reads an
+// empty bucket again (neither the frontier nor the median estimate).
 __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashParams hp) {
   __shared__ uint32_t s_q[kPushStage];
   __shared__ uint32_t s_n[2], s_base;
@@ -433,8 +443,12 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
     unsigned long long old[kMaxRows];
     uint64_t loc[kMaxRows];
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      const bool sh = (rows >> r) & 1u;
+      bool sh = (rows >> r) & 1u;
       loc[r] = sh ? uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul) : 0;
+      if (sh) {
+        const uint64_t sl = e->slot_base + loc[r];
+        sh = (__ldg(w.slot_mark + (sl >> 5)) >> (sl & 31)) & 1u;
+      }
       old[r] = sh ? atomicAdd(w.slot_state + e->slot_base + loc[r], st_sub(uint32_t(i))) : 0ull;
       if (sh) red_add_f32(e->sketch + loc[r], -(dev_sign(hp.row[r], p) * v));
     }

@@ -454,6 +454,8 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   bm = (list + 31) / 32;
   w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
   w.val = static_cast<float*>(ws_.get("dec_val", list * 4, false, stream_));
+  const uint64_t mark_words = (slots + 31) / 32;
+  w.slot_mark = ordered ? nullptr : static_cast<uint32_t*>(ws_.get("slot_mark", mark_words * 4, false, stream_));
   w.tile_base = static_cast<uint32_t*>(ws_.get("tile_base", wt * 4, false, stream_));
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
   w.pitem = static_cast<uint32_t*>(ws_.get("pitem", list * 4, false, stream_));
@@ -465,7 +467,8 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
   // the bucket state is zeroed inside launch_decode (after the output fill)
-  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)}});
+  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)},
+        {w.slot_mark, w.slot_mark ? mark_words * 4 : 0}});
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {
     w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));

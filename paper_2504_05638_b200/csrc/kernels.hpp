@@ -107,6 +107,7 @@ struct DecodeWork {
   unsigned long long* slot_state;  // (sum of list indices) << 24 | count, total_slots
   uint32_t* bitmap;                // recovered flag per presence-list entry
   float* val;                      // decoded value per presence-list entry
+  uint32_t* slot_mark;             // per bucket: holds an entry round 0 left unresolved (or nullptr)
   uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
