@@ -10,8 +10,9 @@
 //                single CTA finishing once the frontier is small;
 //   estimate   : median-of-rows on the residual sketch for every listed
 //                position the peel could not resolve (decode.cpp:130-138);
-//   emit       : the dense shard tile by tile: zero-fill, then the tile's
-//                listed entries' values on top.
+//   emit       : the dense shard chunk by chunk: a zeroed shared-memory
+//                chunk takes the chunk's listed values and leaves by TMA
+//                bulk store.
 //
 // Everything between build and emit is keyed by the presence-list index i,
 // not the position: a bucket's state is (count, sum of list indices) in one
@@ -138,18 +139,30 @@ __device__ __forceinline__ void cta_tiles(uint64_t total, uint32_t& t0, uint32_t
   t1 = t0 + chunk + (b < extra ? 1u : 0u);
 }
 
+// Thread t of a tile owns words [wbase + 16 t, wbase + 16 t + 16): the block
+// scan over threads then lists positions in ascending order (k_emit relies on
+// it). 16-byte loads when the words are aligned.
+__device__ __forceinline__ uint32_t tile_word(uint32_t wbase, uint32_t k) {
+  return wbase + threadIdx.x * kPerThreadWords + k;
+}
 __device__ __forceinline__ void load_tile_bits(const DecItem& e, uint32_t wbase, bool w4,
                                                uint32_t (&bits)[kPerThreadWords], uint32_t& cnt) {
   uint32_t raw[kPerThreadWords];
+  const uint32_t w0 = tile_word(wbase, 0);
+  if (w0 + kPerThreadWords <= e.n_words && (reinterpret_cast<uintptr_t>(e.words + w0) & 15u) == 0) {
 #pragma unroll
-  for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // all loads in flight first
-    const uint32_t wi = wbase + k * 256 + threadIdx.x;
-    raw[k] = wi < e.n_words ? __ldg(e.words + wi) : 0u;
+    for (uint32_t k = 0; k < kPerThreadWords; k += 4) {  // streamed: keep the bucket state in L2
+      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(e.words + w0 + k));
+      raw[k] = x.x; raw[k + 1] = x.y; raw[k + 2] = x.z; raw[k + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) raw[k] = w0 + k < e.n_words ? __ldcs(e.words + w0 + k) : 0u;
   }
   cnt = 0;
 #pragma unroll
   for (uint32_t k = 0; k < kPerThreadWords; ++k) {
-    bits[k] = present_bits(raw[k], w4, wbase + k * 256 + threadIdx.x, e.n);
+    bits[k] = present_bits(raw[k], w4, w0 + k, e.n);
     cnt += __popc(bits[k]);
   }
 }
@@ -230,7 +243,7 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
     uint32_t j = base + off;
 #pragma unroll
     for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // list entries: cheap, divergent
-      const uint32_t wi = wbase + k * 256 + threadIdx.x;
+      const uint32_t wi = tile_word(wbase, k);
       for (uint32_t x = bits[k]; x; x &= x - 1) {
         const uint32_t bb = __ffs(x) - 1;
         w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
@@ -808,54 +821,76 @@ __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp
 }
 
 // ------------------------------------------------------------------ emit
-// The dense shard, one word tile per CTA step (same tiles as k_list): the
-// tile's output range is zero-filled with coalesced 16-byte stores
-// (decode.cpp:61-64 zero-initialises the output), then the tile's listed
-// entries - a contiguous list range, ascending positions - drop their
-// decoded values on top; those stores hit lines the zero-fill just wrote.
+// The dense shard, chunk by chunk (8192 positions): a shared-memory chunk is
+// zeroed (decode.cpp:61-64 zero-initialises the output), the chunk's listed
+// entries - a contiguous list range, ascending positions - drop their values
+// into it, and one bulk async copy (1-D TMA store) writes it out. Two chunk
+// buffers alternate, so a chunk is assembled while the previous one streams.
+constexpr uint32_t kEmitChunk = 8192;
+constexpr size_t kEmitSmem = 2 * kEmitChunk * sizeof(float);
+
+__device__ __forceinline__ uint32_t emit_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 __global__ void __launch_bounds__(256) k_emit(DecodeWork w) {
+  extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk]
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
-  if (t0 >= t1) {
-    span_end(w.span);
-    return;
-  }
   const uint32_t total = w.qcount[5];
-  uint32_t it = find_word_item(w.items, w.n_items, t0);
-  for (uint32_t wt = t0; wt < t1; ++wt) {
-    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
-    const DecItem& e = w.items[it];
-    const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
-    const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
-    const uint64_t p0 = wbase * P;
-    const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
-    float* out = e.out;
-    // the tile's first listed entries are fetched ahead of the zero-fill
-    const uint32_t lb = __ldg(w.tile_base + wt);
-    const uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
-    constexpr uint32_t kAhead = 2;
-    uint32_t pp[kAhead];
-    float vv[kAhead];
-#pragma unroll
-    for (uint32_t u = 0; u < kAhead; ++u) {
-      const uint32_t i = lb + threadIdx.x + u * 256;
-      pp[u] = i < le ? __ldcs(w.plist + i) : 0xFFFFFFFFu;
-      vv[u] = i < le ? __ldcs(w.val + i) : 0.0f;
+  uint32_t n_chunks = 0;  // chunks stored by this CTA (ring position)
+  if (t0 < t1) {
+    uint32_t it = find_word_item(w.items, w.n_items, t0);
+    for (uint32_t wt = t0; wt < t1; ++wt) {
+      while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
+      const DecItem& e = w.items[it];
+      const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
+      const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
+      const uint64_t p0 = wbase * P;
+      const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
+      uint32_t cur = __ldg(w.tile_base + wt);
+      const uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
+      for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
+        const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
+        float* buf = ebuf + (n_chunks & 1u) * kEmitChunk;
+        if (n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
+          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncthreads();
+        }
+        float4* b4 = reinterpret_cast<float4*>(buf);
+        for (uint32_t q = threadIdx.x; q < kEmitChunk / 4; q += blockDim.x) b4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        // this chunk's entries: positions below c0 + clen, from `cur` on
+        for (;;) {
+          const uint32_t i = cur + threadIdx.x;
+          uint32_t p = 0xFFFFFFFFu;
+          if (i < le) p = __ldcs(w.plist + i);
+          const bool in = uint64_t(p) < c0 + clen;
+          if (in) buf[p - c0] = __ldcs(w.val + i);
+          const uint32_t cnt = __syncthreads_count(in);
+          cur += cnt;
+          if (cnt < blockDim.x) break;
+        }
+        float* dst = e.out + c0;
+        const uint32_t bytes = (clen * 4u) & ~15u;
+        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"(emit_smem_u32(buf)), "r"(bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          for (uint32_t q = bytes / 4u + threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+        } else {  // unaligned output: plain coalesced stores
+          for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+          __syncthreads();
+          if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the ring count
+        }
+      }
     }
-    if ((reinterpret_cast<uintptr_t>(out + p0) & 15u) == 0) {
-      const uint64_t nq = (p1 - p0) / 4;
-      float4* o = reinterpret_cast<float4*>(out + p0);
-      for (uint64_t q = threadIdx.x; q < nq; q += blockDim.x) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint64_t p = p0 + nq * 4 + threadIdx.x; p < p1; p += blockDim.x) out[p] = 0.0f;
-    } else {
-      for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) out[p] = 0.0f;
-    }
-    __syncthreads();  // zeros before values
-#pragma unroll
-    for (uint32_t u = 0; u < kAhead; ++u)
-      if (pp[u] != 0xFFFFFFFFu) out[pp[u]] = vv[u];
-    for (uint32_t i = lb + threadIdx.x + kAhead * 256; i < le; i += blockDim.x)
-      out[__ldcs(w.plist + i)] = __ldcs(w.val + i);
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   span_end(w.span);
 }
@@ -928,13 +963,13 @@ int grid_for(uint64_t n, int threads) {
 int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, cudaStream_t stream) {
   const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
   const int g = int(g64);
-  k_count<<<g, 256, 0, stream>>>(w);
-  k_scan_tiles<<<1, 1024, 0, stream>>>(w);
   ZeroRanges zr{};
   zr.ptr[0] = w.slot_state;
   zr.bytes[0] = w.total_slots * 8;
   zr.n = 1;
   launch_zero(zr, stream);
+  k_count<<<g, 256, 0, stream>>>(w);
+  k_scan_tiles<<<1, 1024, 0, stream>>>(w);
   k_list<<<g, 256, 0, stream>>>(w, hp);
   return g;
 }
@@ -1008,8 +1043,13 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
 
 int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream) {
   if (w.n_items == 0) return 0;
-  const uint64_t g = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 8);
-  k_emit<<<int(g), 256, 0, stream>>>(w);
+  const uint64_t g = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
+    attr = true;
+  }
+  k_emit<<<int(g), 256, kEmitSmem, stream>>>(w);
   return 1;
 }
 
