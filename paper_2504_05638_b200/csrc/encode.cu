@@ -16,9 +16,12 @@
 // inside it, and a per-item CTA radix-selects tau from the compacted keys. If
 // the bracket misses (or overflows), a 3-digit radix select over the full item
 // runs instead (kernels launched unconditionally, early-exiting per item).
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace tagc_b200 {
 namespace {
@@ -856,37 +859,40 @@ __host__ __device__ constexpr int digit_bits(int pass) { return pass == 0 ? 11 :
 constexpr uint32_t kFinalKeys = 8192;  // per-item capacity of the target sub-bin list
 
 // --------------------------------------------------------------- finalize
-// (1) k_pick, one CTA per item: checks that tau (the c-th smallest key,
-//     sparsify.cpp:33-37) falls inside the window, so every speculative
-//     decision outside it was right, and names the fine sub-bin holding it;
-// (2) k_collect, all SMs: gathers that sub-bin's keys from the candidates;
-// (3) k_select, one CTA per item: exact radix select in shared memory.
+// k_finish_select, one CTA per item:
+// (1) checks that tau (the c-th smallest key, sparsify.cpp:33-37) falls
+//     inside the window, so every speculative decision outside it was right,
+//     and names the fine sub-bin holding it;
+// (2) gathers that sub-bin's keys from the item's candidates into shared
+//     memory;
+// (3) radix-selects tau exactly among them.
 // Bit-identical to nth_element (sparsify.cpp:35-36).
-__global__ void __launch_bounds__(1024) k_pick(const EncItem* __restrict__ items,
-                                               SelState* __restrict__ state,
-                                               uint32_t* __restrict__ fine_hist,
-                                               uint32_t* __restrict__ err) {
-  __shared__ uint32_t s_digit, s_below;
+__global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restrict__ items,
+                                                        SelState* __restrict__ state,
+                                                        uint32_t* __restrict__ fine_hist,
+                                                        const uint2* __restrict__ cand,
+                                                        uint32_t* __restrict__ err) {
+  __shared__ uint32_t keys[kFinalKeys];
+  __shared__ uint32_t hist[kRadixBins];
+  __shared__ uint32_t s_digit, s_below, s_n;
   const uint32_t item = blockIdx.x;
   const EncItem e = items[item];
   const SelState s = state[item];
   uint32_t* fh = fine_hist + uint64_t(item) * kRadixBins;
   const bool overflow = s.cnt_in > e.cand_cap || s.cnt_hi > e.hi_cap;
   const uint32_t Z = s.cnt_zero, L = s.cnt_lo, I = s.cnt_in;
-  int action = 0;  // 0 none (NaN), 1 tau = 0, 2 collect, 3 fallback
+  int action = 0;  // 0 none (NaN), 1 tau = 0, 2 select among candidates, 3 fallback
   if (!(*err & 1u)) {
     if (e.c <= Z) action = (L == 0 && !overflow) ? 1 : 3;  // tau = 0: every nonzero key is kept
     else if (!overflow && Z + L < e.c && e.c <= Z + L + I) action = 2;
     else action = 3;
   }
+  if (threadIdx.x == 0) s_n = 0;
+  uint32_t rank = 0, sub = 0;
   if (action == 2) {
     find_digit<1024>(fh, kRadixBins, e.c - Z - L - 1, &s_digit, &s_below);
-    if (threadIdx.x == 0) {
-      state[item].status = kStatusCollect;
-      state[item].prefix = s_digit;  // target sub-bin
-      state[item].rank = e.c - Z - L - 1 - s_below;
-      state[item].n_sel = 0;
-    }
+    sub = s_digit;  // target sub-bin
+    rank = e.c - Z - L - 1 - s_below;
   } else if (threadIdx.x == 0) {
     if (action == 1) {
       state[item].tau_key = 0;
@@ -899,44 +905,23 @@ __global__ void __launch_bounds__(1024) k_pick(const EncItem* __restrict__ items
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) fh[i] = 0;
-}
-
-__global__ void __launch_bounds__(256) k_collect(const EncItem* __restrict__ items,
-                                                 SelState* __restrict__ state, uint32_t n_items,
-                                                 const uint2* __restrict__ cand,
-                                                 uint32_t* __restrict__ sel_list) {
-  __shared__ uint32_t pref[kMaxFlatItems + 1];
-  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) {
-    return state[i].status == kStatusCollect ? min(state[i].cnt_in, items[i].cand_cap) : 0u;
-  }, pref);
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
-    const uint32_t it = flat_item(pref, n_items, j);
-    const SelState& s = state[it];
-    const uint32_t key = cand[items[it].cand_off + (j - pref[it])].y & 0x7FFFFFFFu;
-    if (((key - s.klo) >> s.fshift) == s.prefix) {
-      const uint32_t idx = atomicAdd(&state[it].n_sel, 1u);
-      if (idx < kFinalKeys) sel_list[uint64_t(it) * kFinalKeys + idx] = key;
+  for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) fh[i] = 0;  // left zero for the next call
+  if (action != 2) return;
+  // (2) the target sub-bin's keys
+  const uint2* ck = cand + e.cand_off;
+  const uint32_t nc = min(s.cnt_in, e.cand_cap);
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+    const uint32_t key = ck[i].y & 0x7FFFFFFFu;
+    if (((key - s.klo) >> s.fshift) == sub) {
+      const uint32_t idx = atomicAdd(&s_n, 1u);
+      if (idx < kFinalKeys) keys[idx] = key;
     }
   }
-}
-
-__global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ items,
-                                                 SelState* __restrict__ state,
-                                                 const uint2* __restrict__ cand,
-                                                 const uint32_t* __restrict__ sel_list) {
-  __shared__ uint32_t keys[kFinalKeys];
-  __shared__ uint32_t hist[kRadixBins];
-  __shared__ uint32_t s_digit, s_below;
-  const uint32_t item = blockIdx.x;
-  const SelState s = state[item];
-  if (s.status != kStatusCollect) return;
-  const uint32_t nk = s.n_sel;
+  __syncthreads();
+  const uint32_t nk = s_n;
   const bool in_smem = nk <= kFinalKeys;
-  const uint2* ck = cand + items[item].cand_off;
-  if (in_smem)
-    for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) keys[i] = sel_list[uint64_t(item) * kFinalKeys + i];
-  uint32_t rank = s.rank, prefix = 0;
+  // (3) exact radix select
+  uint32_t prefix = 0;
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = digit_shift(pass), bits = digit_bits(pass), hs = shift + bits;
@@ -948,9 +933,9 @@ __global__ void __launch_bounds__(1024) k_select(const EncItem* __restrict__ ite
         if ((key >> hs) == (prefix >> hs)) atomicAdd(&hist[(key >> shift) & ((1u << bits) - 1u)], 1u);
       }
     } else {  // massive ties inside one sub-bin: stream the candidates again
-      for (uint32_t i = threadIdx.x; i < s.cnt_in; i += blockDim.x) {
+      for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
         const uint32_t key = ck[i].y & 0x7FFFFFFFu;
-        if (((key - s.klo) >> s.fshift) == s.prefix && (key >> hs) == (prefix >> hs))
+        if (((key - s.klo) >> s.fshift) == sub && (key >> hs) == (prefix >> hs))
           atomicAdd(&hist[(key >> shift) & ((1u << bits) - 1u)], 1u);
       }
     }
@@ -1014,11 +999,8 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 // Bracket missed: put the combined value back into the accumulator of every
 // speculatively kept element, clear the sketch, and rerun an exact radix
 // select + encode for that item only.
-__global__ void __launch_bounds__(256) k_restore(const EncItem* __restrict__ items,
-                                                 SelState* __restrict__ state, uint32_t n_items,
-                                                 const uint2* __restrict__ hi_pool, uint32_t rows,
-                                                 const uint32_t* __restrict__ err) {
-  if (err[0] || !err[1]) return;
+__device__ __forceinline__ void restore_body(const EncItem* __restrict__ items, SelState* __restrict__ state,
+                                             uint32_t n_items, const uint2* __restrict__ hi_pool, uint32_t rows) {
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
   for (uint32_t it = 0; it < n_items; ++it) {
@@ -1036,13 +1018,10 @@ __global__ void __launch_bounds__(256) k_restore(const EncItem* __restrict__ ite
   }
 }
 
-__global__ void __launch_bounds__(kTileThreads) k_fb_hist(const EncItem* __restrict__ items,
-                                                          const SelState* __restrict__ state,
-                                                          uint32_t n_items, uint64_t total_tiles,
-                                                          uint32_t* __restrict__ fb_hist, int pass,
-                                                          const uint32_t* __restrict__ err) {
-  if (err[0] || !err[1]) return;  // NaN, or no item needs the fallback
-  __shared__ uint32_t hist[kRadixBins];
+__device__ __forceinline__ void fb_hist_body(const EncItem* __restrict__ items,
+                                             const SelState* __restrict__ state, uint32_t n_items,
+                                             uint64_t total_tiles, uint32_t* __restrict__ fb_hist, int pass,
+                                             uint32_t* hist) {
   const int shift = digit_shift(pass), bits = digit_bits(pass), hs = shift + bits;
   for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const uint32_t it = find_tile_item(items, n_items, tile);
@@ -1072,26 +1051,26 @@ __global__ void __launch_bounds__(kTileThreads) k_fb_hist(const EncItem* __restr
   }
 }
 
-__global__ void __launch_bounds__(512) k_fb_scan(SelState* __restrict__ state,
-                                                 uint32_t* __restrict__ fb_hist, int pass,
-                                                 const uint32_t* __restrict__ err) {
-  __shared__ uint32_t s_digit, s_below;
-  if (err[0] || !err[1]) return;
-  const uint32_t item = blockIdx.x;
-  if (state[item].status != kStatusFallback) return;
-  uint32_t* h = fb_hist + uint64_t(item) * kRadixBins;
-  const uint32_t rank = state[item].rank;
-  find_digit<512>(h, 1u << digit_bits(pass), rank, &s_digit, &s_below);
-  for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
-  if (threadIdx.x == 0) {
-    const uint32_t prefix = state[item].prefix | (s_digit << digit_shift(pass));
-    state[item].prefix = prefix;
-    state[item].rank = rank - s_below;
-    if (pass == 2) {
-      state[item].tau_key = prefix;
-      state[item].status = kStatusFbReady;
-      state[item].kept = 0;
+__device__ __forceinline__ void fb_scan_body(SelState* __restrict__ state, uint32_t n_items,
+                                             uint32_t* __restrict__ fb_hist, int pass, uint32_t* s_digit,
+                                             uint32_t* s_below) {
+  for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    if (state[item].status != kStatusFallback) continue;  // block-uniform
+    uint32_t* h = fb_hist + uint64_t(item) * kRadixBins;
+    const uint32_t rank = state[item].rank;
+    find_digit<kTileThreads>(h, 1u << digit_bits(pass), rank, s_digit, s_below);
+    for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
+    if (threadIdx.x == 0) {
+      const uint32_t prefix = state[item].prefix | (*s_digit << digit_shift(pass));
+      state[item].prefix = prefix;
+      state[item].rank = rank - *s_below;
+      if (pass == 2) {
+        state[item].tau_key = prefix;
+        state[item].status = kStatusFbReady;
+        state[item].kept = 0;
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -1102,17 +1081,9 @@ __global__ void __launch_bounds__(512) k_fb_scan(SelState* __restrict__ state,
 constexpr uint32_t kKeptStage = 1024;  // kept elements staged per tile (overflow: direct)
 
 template <bool kW4>
-__global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __restrict__ items,
-                                                            SelState* __restrict__ state,
-                                                            uint32_t n_items, uint64_t total_tiles,
-                                                            const HashParams hp,
-                                                            const uint32_t* __restrict__ err,
-                                                            int mode) {
-  __shared__ uint32_t s_pos[kKeptStage];
-  __shared__ float s_val[kKeptStage];
-  __shared__ uint32_t s_n;
-  if (err && err[0]) return;  // NaN anywhere: nothing more is written
-  if (mode == 1 && !err[1]) return;
+__device__ __forceinline__ void encode_body(const EncItem* __restrict__ items, SelState* __restrict__ state,
+                                            uint32_t n_items, uint64_t total_tiles, const HashParams& hp,
+                                            int mode, uint32_t* s_pos, float* s_val, uint32_t& s_n) {
   const uint32_t lane = threadIdx.x & 31;
   uint64_t t0, t1;
   cta_range(total_tiles, t0, t1);
@@ -1210,6 +1181,46 @@ __global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __res
       __syncthreads();
     }
   }
+}
+
+template <bool kW4>
+__global__ void __launch_bounds__(kTileThreads, 5) k_encode(const EncItem* __restrict__ items,
+                                                            SelState* __restrict__ state,
+                                                            uint32_t n_items, uint64_t total_tiles,
+                                                            const HashParams hp,
+                                                            const uint32_t* __restrict__ err) {
+  __shared__ uint32_t s_pos[kKeptStage];
+  __shared__ float s_val[kKeptStage];
+  __shared__ uint32_t s_n;
+  if (err && err[0]) return;  // NaN anywhere: nothing more is written
+  encode_body<kW4>(items, state, n_items, total_tiles, hp, 0, s_pos, s_val, s_n);
+}
+
+// The whole bracket-miss repair in one cooperative launch: restore, three
+// radix-select digit passes, exact re-encode of the fallen-back items. In the
+// normal case (no item fell back, or NaN) every CTA returns at once.
+template <bool kW4>
+__global__ void __launch_bounds__(kTileThreads) k_fallback(const EncItem* __restrict__ items,
+                                                           SelState* __restrict__ state, uint32_t n_items,
+                                                           uint64_t total_tiles, const HashParams hp,
+                                                           const uint2* __restrict__ hi_pool,
+                                                           uint32_t* __restrict__ fb_hist,
+                                                           const uint32_t* __restrict__ err) {
+  __shared__ uint32_t s_hist[kRadixBins];
+  __shared__ uint32_t s_pos[kKeptStage];
+  __shared__ float s_val[kKeptStage];
+  __shared__ uint32_t s_n, s_digit, s_below;
+  if (err[0] || !err[1]) return;  // grid-uniform
+  cg::grid_group grid = cg::this_grid();
+  restore_body(items, state, n_items, hi_pool, hp.rows);
+  for (int pass = 0; pass < 3; ++pass) {
+    grid.sync();
+    fb_hist_body(items, state, n_items, total_tiles, fb_hist, pass, s_hist);
+    grid.sync();
+    fb_scan_body(state, n_items, fb_hist, pass, &s_digit, &s_below);
+  }
+  grid.sync();
+  encode_body<kW4>(items, state, n_items, total_tiles, hp, 1, s_pos, s_val, s_n);
 }
 
 // --------------------------------------------------------------- folds
@@ -1404,25 +1415,29 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
                          uint32_t* fb_hist, uint2* cand, uint2* hi_pool, uint32_t* sel_list,
                          uint32_t* err, cudaStream_t stream) {
   if (n_items == 0) return 0;
-  k_pick<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, err);
-  k_collect<<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, sel_list);
-  k_select<<<n_items, 1024, 0, stream>>>(items, state, cand, sel_list);
+  k_finish_select<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, cand, err);
+  (void)sel_list;
   if (w4) k_fixup<true><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
   else k_fixup<false><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
-  // fallback chain: every kernel exits at once unless some item missed its bracket
-  k_restore<<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, hi_pool, hp.rows, err);
-  const int fg = persistent_grid((const void*)k_fb_hist, kTileThreads, di, total_tiles);
-  for (int pass = 0; pass < 3; ++pass) {
-    k_fb_hist<<<fg, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, fb_hist, pass, err);
-    k_fb_scan<<<n_items, 512, 0, stream>>>(state, fb_hist, pass, err);
-  }
-  if (w4)
-    k_encode<true><<<persistent_grid((const void*)k_encode<true>, kTileThreads, di, total_tiles),
-                     kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 1);
-  else
-    k_encode<false><<<persistent_grid((const void*)k_encode<false>, kTileThreads, di, total_tiles),
-                      kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 1);
-  return 13;
+  // bracket-miss repair: one cooperative launch that exits at once unless some item fell back
+  auto launch_fb = [&](auto kern) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, kTileThreads, 0);
+    const uint64_t g = std::min<uint64_t>(uint64_t(std::max(per_sm, 1)) * di.sms, std::max<uint64_t>(total_tiles, 1));
+    const EncItem* a0 = items;
+    SelState* a1 = state;
+    uint32_t a2 = n_items;
+    uint64_t a3 = total_tiles;
+    HashParams a4 = hp;
+    const uint2* a5 = hi_pool;
+    uint32_t* a6 = fb_hist;
+    const uint32_t* a7 = err;
+    void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &a6, &a7};
+    cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(g)), dim3(kTileThreads), args, 0, stream);
+  };
+  if (w4) launch_fb(k_fallback<true>);
+  else launch_fb(k_fallback<false>);
+  return 3;
 }
 
 int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
@@ -1431,10 +1446,10 @@ int launch_encode_exact(const DevInfo& di, const EncItem* items, SelState* state
   if (n_items == 0) return 0;
   if (w4) {
     const int g = persistent_grid((const void*)k_encode<true>, kTileThreads, di, total_tiles);
-    k_encode<true><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 0);
+    k_encode<true><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err);
   } else {
     const int g = persistent_grid((const void*)k_encode<false>, kTileThreads, di, total_tiles);
-    k_encode<false><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err, 0);
+    k_encode<false><<<g, kTileThreads, 0, stream>>>(items, state, n_items, total_tiles, hp, err);
   }
   return 1;
 }
