@@ -219,12 +219,15 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(DecodeWork w) {
     if (threadIdx.x == 0) s_carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) w.qcount[5] = s_carry;
+  // a corrupt index (NaN input aborted the encode) may list more than the
+  // capacity: then nothing is decoded (the call reports the NaN)
+  if (threadIdx.x == 0) w.qcount[5] = s_carry <= w.list_cap ? s_carry : 0u;
 }
 
 __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp) {
   using Scan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename Scan::TempStorage scan_tmp;
+  const uint32_t total_list = w.qcount[5];
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
   if (t0 >= t1) return;
@@ -240,14 +243,17 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
     uint32_t off, total;
     Scan(scan_tmp).ExclusiveSum(cnt, off, total);
     const uint32_t base = __ldg(w.tile_base + wt);
+    if (base + total > total_list) total = base < total_list ? total_list - base : 0u;
     uint32_t j = base + off;
 #pragma unroll
     for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // list entries: cheap, divergent
       const uint32_t wi = tile_word(wbase, k);
       for (uint32_t x = bits[k]; x; x &= x - 1) {
         const uint32_t bb = __ffs(x) - 1;
-        w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
-        w.pitem[j] = it;
+        if (j < total_list) {
+          w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
+          w.pitem[j] = it;
+        }
         ++j;
       }
     }
@@ -849,7 +855,8 @@ __global__ void __launch_bounds__(256) k_emit(DecodeWork w) {
       const uint64_t p0 = wbase * P;
       const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
       uint32_t cur = __ldg(w.tile_base + wt);
-      const uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
+      uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
+      le = le < total ? le : total;
       for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
         const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
         float* buf = ebuf + (n_chunks & 1u) * kEmitChunk;

@@ -81,6 +81,7 @@ struct DecItem {
   uint64_t word_tile_begin;
   uint64_t list_off;      // presence list offset
   uint32_t n, m, flags, n_words;
+  uint32_t list_cap, pad;  // bound on this item's presence (host-side sizing)
   uint64_t mmul;          // fastmod multiplier for m (fastmod_magic), set by the engine
 };
 

@@ -42,6 +42,14 @@ uint32_t threshold_rank(double theta, uint64_t n) {
   return static_cast<uint32_t>(c);
 }
 
+// Presence bound of a compressed segment: every rank keeps at most n - c
+// positions (keys above the c-th smallest), and the merged index adds rank
+// words, so popcount(sum) <= sum of popcounts bounds the present fields.
+uint32_t presence_bound(uint64_t n, double theta, uint32_t world) {
+  const uint64_t keep = n - threshold_rank(theta, n);
+  return uint32_t(std::min<uint64_t>(n, keep * world + 32));
+}
+
 std::string seg_name(const LayerSegment& s, uint32_t i) {
   return s.name.empty() ? "seg" + std::to_string(i) : s.name;
 }
@@ -439,7 +447,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     d.word_tile_begin = wt;
     wt += (uint64_t(d.n_words) + kDecWordTile - 1) / kDecWordTile;
     d.list_off = list;
-    list += d.n;
+    list += std::min(d.list_cap ? d.list_cap : d.n, d.n);
   }
   if (slots >= (1ull << 31)) throw CudaError("decode batch exceeds 2^31 sketch buckets");
   auto* d_items = static_cast<DecItem*>(ws_.get("dec_items", n * sizeof(DecItem), false, stream_));
@@ -453,6 +461,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.slot_state = static_cast<unsigned long long*>(ws_.get("slot_state", slots * 8, false, stream_));
   bm = (list + 31) / 32;
   w.bitmap = static_cast<uint32_t*>(ws_.get("bitmap", bm * 4, false, stream_));
+  w.list_cap = list;
   w.val = static_cast<float*>(ws_.get("dec_val", list * 4, false, stream_));
   const uint64_t mark_words = (slots + 31) / 32;
   w.slot_mark = ordered ? nullptr : static_cast<uint32_t*>(ws_.get("slot_mark", mark_words * 4, false, stream_));
@@ -603,6 +612,7 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
     d.m = p.m;
     d.flags = w == 4 ? kWidth4 : 0u;
     d.n_words = p.n_words;
+    d.list_cap = presence_bound(p.len, cfg_.theta, world);
     dec.push_back(d);
     diag.push_back(DiagItem{merged + p.word_off, p.word_off, uint32_t(p.len), p.n_words, w, 0});
     max_words = std::max(max_words, p.n_words);
@@ -742,7 +752,9 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     enqueue_reduce_shards(shards, grad, acc, out, stats);
     return;
   }
-  // second sighting: capture, then replay from now on
+  // second sighting: capture, then replay from now on (a bounded cache: a
+  // caller cycling through many buffer sets starts over)
+  if (graphs_.size() >= kMaxGraphs) drop_graphs();
   GraphEntry g;
   const uint64_t gen0 = ws_.generation(), wire0 = ledger_.wire_bytes;
   cudaGraph_t graph = nullptr;
@@ -885,6 +897,7 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     d.m = p.m;
     d.flags = w == 4 ? kWidth4 : 0u;
     d.n_words = p.n_words;
+    d.list_cap = presence_bound(p.len, cfg_.theta, W);
     dec.push_back(d);
   }
   run_decode(dec, hp, false, w == 1 && W > 1, zero_done);
@@ -1123,6 +1136,7 @@ void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32
   d[0].m = g.buckets_per_row;
   d[0].flags = 0;  // presence bitmap == width-1 index
   d[0].n_words = uint32_t(nb);
+  d[0].list_cap = count;
   const HashParams hp = make_hash_params(seed, rows);
   run_decode(d, hp, true, true);  // arbitrary presence/sketch pairs: FIFO-exact order
   DecStats ds{};

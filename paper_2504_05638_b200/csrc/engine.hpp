@@ -155,6 +155,7 @@ class Engine {
     std::vector<LedgerEntry> ledger;
     std::vector<char*> pinned;  // descriptor uploads frozen into the graph
   };
+  static constexpr size_t kMaxGraphs = 16;
   std::map<std::string, GraphEntry> graphs_;
   std::map<std::string, int> graph_seen_;
   bool graphs_on_ = true;

@@ -113,6 +113,7 @@ struct DecodeWork {
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
   uint32_t* queue[2];              // capacity total_slots each
+  uint64_t list_cap;               // presence-list capacity (sum of the items' bounds)
   uint32_t* qcount;                // [2] rounds, [3] tail rounds, [4] peeled, [8..10] frontier sizes,
                                    // [5] presence total
   DecStats* stats;                 // n_items
