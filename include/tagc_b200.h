@@ -241,6 +241,23 @@ int tagc_reduce_shards_host(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_
  * enqueued (a CUDA event recorded on the context stream afterwards brackets
  * the host copies too). */
 int tagc_ctx_host_join(tagc_ctx* ctx);
+/* The exchange split around its collective, for a caller-provided transport
+ * (the reference's in-process World, MPI, a test harness): _begin encodes
+ * every shard into this rank's owner-major send blocks and returns them
+ * (dev: world_size * block_f32 floats, world_size * block_u32 u32 words; the
+ * layout of tagc_plan_exchange). The caller reduce-scatters them - owner o
+ * receives the fp32 sum and the wrapping u32 sum of every rank's block o
+ * (reference World::reduce / all_reduce_sum, collectives.cpp:143-166) - and
+ * passes this rank's reduced blocks to _end, which decodes the owned shards
+ * into `out` (given to _begin). Works for any world size without NCCL.
+ * *send_f32 / *send_u32 non-NULL on input: encode straight into those
+ * caller-owned buffers (sizes from tagc_plan_exchange), e.g. registered or
+ * symmetric memory of the transport; NULL: engine workspace, returned. */
+int tagc_reduce_shards_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                             const float* grad, float* acc, float* out, float** send_f32,
+                             uint32_t** send_u32, uint64_t* block_f32, uint64_t* block_u32);
+int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
+                           tagc_peel_stats* stats);
 /* The owner-major exchange layout tagc_reduce_shards uses on `rank` (pure
  * host computation; exposed so a foreign transport can reproduce the
  * exchange). Owner o's f32 block is [o*block_f32, (o+1)*block_f32) of the

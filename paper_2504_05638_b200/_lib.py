@@ -127,6 +127,9 @@ SIGNATURES = {
     "tagc_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_reduce_shards_host": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_ctx_host_join": (C.c_int, [VP]),
+    "tagc_reduce_shards_begin": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(VP), C.POINTER(VP),
+                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "tagc_reduce_shards_end": (C.c_int, [VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_reduce_shard": (C.c_int, [VP, C.POINTER(Shard), VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_baseline_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP]),
     "tagc_plan_exchange": (C.c_int, [C.POINTER(Config), C.POINTER(Shard), U32, U32, U32,

@@ -377,6 +377,26 @@ class Context:
                                           C.byref(st) if stats else None), "tagc_reduce_shards_host")
         return host_out, (PeelStats(**st.as_dict()) if stats else None)
 
+    def reduce_shards_begin(self, shards: Sequence[ShardSpec], grad, acc, out, send_f, send_u):
+        """First half of tagc_reduce_shards for a caller-provided transport:
+        encodes into the caller's owner-major send blocks (send_f: world *
+        block_f32 floats, send_u: world * block_u32 int32 words, sizes from
+        plan_exchange). Returns (block_f32, block_u32)."""
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        pf, pu = C.c_void_p(_ptr(send_f)), C.c_void_p(_ptr(send_u))
+        bf, bu = C.c_uint64(), C.c_uint64()
+        check(lib.tagc_reduce_shards_begin(self.h, arr, len(scs), _ptr(grad), _ptr(acc), _ptr(out), C.byref(pf),
+                                           C.byref(pu), C.byref(bf), C.byref(bu)), "reduce_shards_begin")
+        return int(bf.value), int(bu.value)
+
+    def reduce_shards_end(self, recv_f, recv_u, stats=True):
+        """Second half: decode this rank's reduced blocks into the `out` given to begin."""
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shards_end(self.h, _ptr(recv_f), _ptr(recv_u), C.byref(st) if stats else None),
+              "reduce_shards_end")
+        return PeelStats(**st.as_dict()) if stats else None
+
     def host_join(self):
         check(lib.tagc_ctx_host_join(self.h), "host_join")
 

@@ -323,6 +323,33 @@ int tagc_reduce_shards_host(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_
   });
 }
 
+int tagc_reduce_shards_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad,
+                             float* acc, float* out, float** send_f32, uint32_t** send_u32, uint64_t* block_f32,
+                             uint64_t* block_u32) {
+  return guarded([&] {
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    Engine& e = eng(ctx);
+    e.config().validate_for_world(e.world());
+    e.exchange_begin(v, grad, acc, out, send_f32 ? *send_f32 : nullptr, send_u32 ? *send_u32 : nullptr);
+    if (send_f32) *send_f32 = e.exchange_send_f();
+    if (send_u32) *send_u32 = e.exchange_send_u();
+    if (block_f32) *block_f32 = e.exchange_block_f();
+    if (block_u32) *block_u32 = e.exchange_block_u();
+  });
+}
+
+int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
+                           tagc_peel_stats* stats) {
+  return guarded([&] {
+    PeelStats st;
+    eng(ctx).exchange_end(recv_f32, recv_u32, stats ? &st : nullptr);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
 int tagc_ctx_host_join(tagc_ctx* ctx) {
   return guarded([&] { eng(ctx).host_join(); });
 }

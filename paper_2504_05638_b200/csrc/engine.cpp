@@ -796,31 +796,36 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   graphs_.emplace(key, std::move(g));
 }
 
-void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
-                                   float* out, PeelStats* stats) {
+// First half of an exchange (reference hook.cpp:137-163): encode every
+// compressed segment into its owner's send blocks, pack raw segments (W > 1)
+// or copy them to the output (W == 1, side stream). State for exchange_end
+// stays in xs_.
+void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                            float* user_send_f, uint32_t* user_send_u) {
   launches_ = 0;
   ev_record(0);
   span_reset();
   const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
-  const ExchangePlan P = plan_exchange(shards, cfg_, W, rank_);
+  xs_ = ExchangeState{};
+  xs_.shards = shards;
+  xs_.out = out;
+  xs_.P = plan_exchange(shards, cfg_, W, rank_);
+  const ExchangePlan& P = xs_.P;
   const std::vector<SegPlan>& plan = P.segs;
   const std::vector<uint64_t>& skc = P.skc;
   const std::vector<uint64_t>& out_off = P.out_off;
   const uint64_t Bf = P.Bf, Bu = P.Bu;
-  auto* send_f = static_cast<float*>(ws_.get("nc_send_f", W * Bf * 4, false, stream_));
-  auto* send_u = static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
-  float* recv_f = send_f;
-  uint32_t* recv_u = send_u;
-  if (W > 1) {
-    recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
-    recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
-  }
+  auto* send_f = user_send_f ? user_send_f : static_cast<float*>(ws_.get("nc_send_f", W * Bf * 4, false, stream_));
+  auto* send_u = user_send_u ? user_send_u : static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
+  xs_.send_f = send_f;
+  xs_.send_u = send_u;
   {
     std::vector<std::pair<void*, uint64_t>> zr;
     for (uint32_t o = 0; o < W; ++o) zr.push_back({send_f + o * Bf, skc[o] * 4});
     zero(zr);
   }
   const HashParams hp = make_hash_params(cfg_.seed, rows);
+  (void)rows;
   std::vector<EncItem> enc;
   std::vector<CopyItem> pack, unpack;
   for (const SegPlan& p : plan) {
@@ -842,8 +847,6 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
       unpack.push_back(CopyItem{grad + sh.begin + p.lo, out + out_off[p.shard] + p.lo, p.len, 0});
     } else {
       pack.push_back(CopyItem{grad + sh.begin + p.lo, send_f + o * Bf + p.raw_off, p.len, 0});
-      if (o == rank_)
-        unpack.push_back(CopyItem{recv_f + p.raw_off, out + out_off[p.shard] + p.lo, p.len, 0});
     }
   }
   run_select_encode(enc, w == 4, hp, false, "nccl");
@@ -876,6 +879,23 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     if (W == 1 && zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait raw copy");
     cuda_check(cudaEventRecordWithFlags(grad_read_ev_, stream_, ev_flags), "grad-read event");
   }
+  xs_.zero_done = zero_done;
+  xs_.active = true;
+}
+
+void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
+                                   float* out, PeelStats* stats) {
+  exchange_begin(shards, grad, acc, out);
+  const uint32_t W = world_;
+  const uint64_t Bf = xs_.P.Bf, Bu = xs_.P.Bu;
+  float* send_f = xs_.send_f;
+  uint32_t* send_u = xs_.send_u;
+  float* recv_f = send_f;
+  uint32_t* recv_u = send_u;
+  if (W > 1) {
+    recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
+    recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
+  }
   if (W > 1) {
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
     nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
@@ -886,6 +906,28 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     ledger_.wire_bytes += W * (Bf + Bu) * 4;
   }
   ev_record(4);
+  exchange_end(recv_f, recv_u, stats);
+}
+
+// Second half (hook.cpp:164-189): decode this rank's owned compressed
+// segments from the reduced blocks and unpack its raw segments.
+void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, PeelStats* stats) {
+  if (!xs_.active) throw InvalidArgument("no exchange in progress");
+  xs_.active = false;
+  const std::vector<ShardSpec>& shards = xs_.shards;
+  const ExchangePlan& P = xs_.P;
+  const std::vector<SegPlan>& plan = P.segs;
+  const std::vector<uint64_t>& out_off = P.out_off;
+  const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
+  float* out = xs_.out;
+  float* recv_f = const_cast<float*>(recv_f_in);
+  uint32_t* recv_u = const_cast<uint32_t*>(recv_u_in);
+  const HashParams hp = make_hash_params(cfg_.seed, rows);
+  const cudaEvent_t zero_done = xs_.zero_done;
+  std::vector<CopyItem> unpack;
+  for (const SegPlan& p : plan)
+    if (!p.compressed && W > 1 && shards[p.shard].owner == rank_)
+      unpack.push_back(CopyItem{recv_f + p.raw_off, out + out_off[p.shard] + p.lo, p.len, 0});
   std::vector<DecItem> dec;
   for (const SegPlan& p : plan) {
     if (!p.compressed || shards[p.shard].owner != rank_) continue;

@@ -81,6 +81,8 @@ class Engine {
 
   void set_config(const CompressionConfig& cfg);
   const CompressionConfig& config() const { return cfg_; }
+  uint32_t world() const { return world_; }
+  uint32_t rank() const { return rank_; }
   cudaStream_t stream() const { return stream_; }
   TrafficLedger& ledger() { return ledger_; }
   uint64_t workspace_bytes() const { return ws_.bytes(); }
@@ -119,6 +121,18 @@ class Engine {
                           float* host_out, PeelStats* stats);
   // The context stream waits for every copy the host-buffer path enqueued.
   void host_join();
+  // The exchange split around its collective, for a caller-provided
+  // transport: exchange_begin encodes into the owner-major send blocks
+  // (world * block_f32 floats, world * block_u32 words; layout of
+  // plan_exchange), the caller reduce-scatters them (f32 sum, wrapping u32
+  // sum), exchange_end decodes this rank's block.
+  void exchange_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                      float* user_send_f = nullptr, uint32_t* user_send_u = nullptr);
+  void exchange_end(const float* recv_f, const uint32_t* recv_u, PeelStats* stats);
+  float* exchange_send_f() const { return xs_.send_f; }
+  uint32_t* exchange_send_u() const { return xs_.send_u; }
+  uint64_t exchange_block_f() const { return xs_.P.Bf; }
+  uint64_t exchange_block_u() const { return xs_.P.Bu; }
 
   // Per-stage codec entry points (single vector).
   void sparsify(const float* g, uint32_t n, double theta, float* sparse, float* residual,
@@ -144,6 +158,16 @@ class Engine {
   friend struct CallScope;
   void enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
                              PeelStats* stats);
+  struct ExchangeState {  // between exchange_begin and exchange_end
+    bool active = false;
+    std::vector<ShardSpec> shards;
+    ExchangePlan P;
+    float* out = nullptr;
+    float* send_f = nullptr;
+    uint32_t* send_u = nullptr;
+    cudaEvent_t zero_done = nullptr;
+  };
+  ExchangeState xs_;
   struct LedgerEntry {
     CollectiveOp op;
     std::string tag;

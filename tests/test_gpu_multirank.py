@@ -1,0 +1,107 @@
+"""GPU parity of the one-process-per-GPU exchange at W > 1, on one GPU: every
+rank's context runs tagc_reduce_shards_begin / _end (the NCCL-world code
+path with the collective supplied by the caller), and the test performs the
+reduce-scatter the way the reference's World does - fp32 sums of the owner
+blocks in ascending rank order and wrapping u32 sums of the index blocks
+(collectives.cpp:127-166). Compared with the CPU oracle's tagc_reduce_shard
+(reference hook.cpp:98-200) shard by shard: residual accumulators of every
+rank bit-exact, peel statistics exact, the owner's decoded shards within the
+reference's 1e-5 tolerance (roundtrip.cpp:119-137). With a 1-bit index the
+merged words carry (index.cpp:80-93) and the decoder's FIFO-ordered peel must
+reproduce the reference's carry-corrupted values."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2504_05638_b200 as tagc
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+SPECS = [
+    ("wte", "embedding", 200_000), ("wpe", "positional_embedding", 16_384),
+    ("h0.ln_1", "norm", 512), ("h0.attn.c_attn", "attention_qkv", 98_304),
+    ("h0.attn.c_proj", "attention_out_proj", 65_536), ("h0.mlp.c_fc", "feed_forward", 262_144),
+    ("h0.mlp.c_fc.bias", "bias", 1_024), ("h0.mlp.c_proj", "feed_forward", 262_144),
+    ("h1.mlp.c_fc", "feed_forward", 131_072), ("ln_f", "norm", 512), ("lm_head", "lm_head", 120_000),
+]
+
+
+def lognormal(n, seed):
+    rng = np.random.default_rng(seed)
+    mag = np.exp(rng.standard_normal(n, dtype=np.float32))
+    return np.where(rng.integers(0, 2, n, dtype=np.int8) == 1, -mag, mag).astype(np.float32)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def check_close(got, ref, tol=1e-5):
+    scale = float(np.abs(ref).max())
+    if scale == 0.0:
+        assert np.array_equal(bits(got), bits(ref))
+        return
+    err = float(np.max(np.abs(got.astype(np.float64) - ref) / np.maximum(np.abs(ref), scale)))
+    assert err <= tol, err
+
+
+@pytest.mark.parametrize("world,width,theta,steps", [
+    (2, 4, 99.0, 2), (4, 4, 99.0, 1), (8, 4, 99.5, 1), (3, 4, 98.0, 1), (2, 1, 98.75, 2), (4, 1, 99.0, 1),
+])
+def test_split_exchange_matches_oracle(orc, world, width, theta, steps):
+    specs = [tagc.LayerSpec(n, k, c) for n, k, c in SPECS]
+    shards = tagc.make_shards(specs, world, world)
+    total = shards[-1].end
+    ratio = 10 if theta >= 98.75 else 4
+    cfg = tagc.CompressionConfig(theta=theta, ratio=ratio, index_width=width, policy="non_attention_linear",
+                                 include_out_proj=True, seed=77)
+    ocfg = O.Config(cfg.theta, cfg.ratio, cfg.index_width, cfg.policy, cfg.include_out_proj, cfg.seed,
+                    cfg.sketch_rows, cfg.allow_low_theta, cfg.min_compress_segment)
+    _, Bf, Bu = tagc.plan_exchange(cfg, shards, world, 0)
+    ctxs = [tagc.Context(cfg, world_size=world, rank=r, device=0) for r in range(world)]
+    owned = [[s for s in shards if s.owner == r] for r in range(world)]
+    acc = [torch.zeros(total, device=DEV) for _ in range(world)]
+    oacc = [np.zeros(total, np.float32) for _ in range(world)]
+    for step in range(steps):
+        grads = [lognormal(total, 1000 * step + r) for r in range(world)]
+        send_f = [torch.zeros(world * Bf, device=DEV) for _ in range(world)]
+        send_u = [torch.zeros(world * Bu, dtype=torch.int32, device=DEV) for _ in range(world)]
+        outs = [torch.full((max(1, sum(s.size() for s in owned[r])),), float("nan"), device=DEV)
+                for r in range(world)]
+        for r in range(world):
+            bf, bu = ctxs[r].reduce_shards_begin(shards, torch.from_numpy(grads[r]).to(DEV), acc[r], outs[r],
+                                                 send_f[r], send_u[r])
+            assert (bf, bu) == (Bf, Bu)
+        stats = []
+        for o in range(world):  # the reduce-scatter, ascending rank order
+            rf = send_f[0][o * Bf:(o + 1) * Bf].clone()
+            ru = send_u[0][o * Bu:(o + 1) * Bu].to(torch.int64)
+            for r in range(1, world):
+                rf += send_f[r][o * Bf:(o + 1) * Bf]
+                ru += send_u[r][o * Bu:(o + 1) * Bu].to(torch.int64)
+            ru = ((ru & 0xFFFFFFFF) ^ 0x80000000).sub(0x80000000).to(torch.int32)  # wrap to u32 bits
+            stats.append(ctxs[o].reduce_shards_end(rf, ru))
+        torch.cuda.synchronize()
+        # oracle, shard by shard (accumulators are updated in place per shard slice)
+        refs, rsts = {}, {}
+        for sh in shards:
+            osh = O.Shard(sh.id, sh.owner, sh.begin, sh.end,
+                          [O.Segment(s.kind, s.begin, s.end, s.name) for s in sh.segments])
+            g = [grads[r][sh.begin:sh.end] for r in range(world)]
+            a = [oacc[r][sh.begin:sh.end].copy() for r in range(world)]
+            ref, rst = orc.tagc_reduce_shard(osh, g, a, ocfg)
+            for r in range(world):
+                oacc[r][sh.begin:sh.end] = a[r]
+            refs[sh.id], rsts[sh.id] = ref.copy(), dict(rst)
+        for r in range(world):
+            assert np.array_equal(bits(acc[r].cpu().numpy()), bits(oacc[r])), (step, r)
+        for o in range(world):
+            got = outs[o].cpu().numpy()
+            off = 0
+            for sh in owned[o]:
+                check_close(got[off:off + sh.size()], refs[sh.id])
+                off += sh.size()
+            for k in ("presence", "peeled", "unresolved"):
+                assert getattr(stats[o], k) == sum(rsts[s.id][k] for s in owned[o]), (k, o, stats[o])
