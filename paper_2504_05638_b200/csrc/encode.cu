@@ -102,6 +102,17 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
   return x;
 }
 
+// Contiguous tile range of this CTA (persistent grid): consecutive tiles stay
+// in the same item, so per-item staging is flushed rarely. 32-bit arithmetic:
+// tile counts stay far below 2^32 and a 64-bit divide would pull a subroutine
+// call into every persistent kernel.
+__device__ __forceinline__ void cta_range(uint64_t total, uint64_t& t0, uint64_t& t1) {
+  const uint32_t T = uint32_t(total), G = gridDim.x;
+  const uint32_t chunk = T / G, extra = T % G, b = blockIdx.x;
+  t0 = uint64_t(b) * chunk + min(b, extra);
+  t1 = t0 + chunk + (b < extra ? 1u : 0u);
+}
+
 // --------------------------------------------------------------- sampling
 __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restrict__ items,
                                                          uint32_t n_items, uint64_t total,
@@ -122,21 +133,39 @@ __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restri
     }
     __syncthreads();
   };
-  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const uint32_t it = find_sample_item(items, n_items, w);
-    if (int(it) != cur) {
-      if (cur >= 0) flush(cur);
-      cur = int(it);
+  // contiguous range of sample works per CTA: one histogram flush per item
+  // touched instead of one per work
+  uint64_t w0, w1;
+  cta_range(total, w0, w1);
+  uint32_t it = w0 < w1 ? find_sample_item(items, n_items, w0) : 0;
+  constexpr int kU = 4;  // sample works in flight per thread
+  for (uint64_t w = w0; w < w1; w += kU) {
+    float v[kU][4];
+    uint32_t wit[kU];
+    bool ok[kU];
+    uint64_t pos[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t wu = w + u;
+      ok[u] = wu < w1;
+      while (ok[u] && it + 1 < n_items && items[it + 1].sample_begin <= wu) ++it;
+      wit[u] = it;
+      const EncItem& e = items[it];
+      pos[u] = ok[u] ? (wu - e.sample_begin) * uint64_t(e.sample_stride) * kTile + 4ull * threadIdx.x : 0;
+      ok[u] = ok[u] && pos[u] < e.n;
+      if (ok[u]) load_combined(e, uint32_t(pos[u]), v[u]);
     }
-    const EncItem e = items[it];
-    const uint64_t start = (w - e.sample_begin) * uint64_t(e.sample_stride) * kTile;
-    const uint64_t pos = start + 4ull * threadIdx.x;
-    if (pos < e.n) {
-      float v[4];
-      load_combined(e, uint32_t(pos), v);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (int(wit[u]) != cur) {  // block-uniform (same work ids in every thread)
+        if (cur >= 0) flush(cur);
+        cur = int(wit[u]);
+      }
+      if (!ok[u]) continue;
+      const uint32_t n = items[wit[u]].n;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (pos + j < e.n) atomicAdd(&hist[mag_key(v[j]) >> kSampleShift], 1u);
+        if (pos[u] + j < n) atomicAdd(&hist[mag_key(v[u][j]) >> kSampleShift], 1u);
     }
   }
   if (cur >= 0) flush(cur);
@@ -220,17 +249,6 @@ __global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ item
 }
 
 // --------------------------------------------------------------- helpers
-// Contiguous tile range of this CTA (persistent grid): consecutive tiles stay
-// in the same item, so per-item staging is flushed rarely. 32-bit arithmetic:
-// tile counts stay far below 2^32 and a 64-bit divide would pull a subroutine
-// call into every persistent kernel.
-__device__ __forceinline__ void cta_range(uint64_t total, uint64_t& t0, uint64_t& t1) {
-  const uint32_t T = uint32_t(total), G = gridDim.x;
-  const uint32_t chunk = T / G, extra = T % G, b = blockIdx.x;
-  t0 = uint64_t(b) * chunk + min(b, extra);
-  t1 = t0 + chunk + (b < extra ? 1u : 0u);
-}
-
 constexpr uint32_t kStatusReady = 0, kStatusFallback = 1, kStatusCollect = 3, kStatusFbReady = 4;
 
 // Values a fallback pass reads: after k_restore an accumulator holds the
