@@ -258,6 +258,27 @@ int tagc_reduce_shards_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n
                              uint32_t** send_u32, uint64_t* block_f32, uint64_t* block_u32);
 int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
                            tagc_peel_stats* stats);
+/* Pull-mode exchange over peer memory (NVLink / NVSwitch) instead of NCCL.
+ * Each rank encodes into its own owner-major send blocks inside a region its
+ * peers map through CUDA IPC, raises a step flag in every peer, and reduces
+ * its own block straight out of the W regions: fp32 sums in ascending rank
+ * order (the reference World's fold, collectives.cpp:127-166, so the reduced
+ * sketch and raw segments are bit-identical to it) and wrapping u32 sums of
+ * the index words. Deterministic, no NCCL. Setup, after the shard layout is
+ * known:
+ *   tagc_ctx_peer_prepare  allocates this rank's region, returns its handle;
+ *   (the caller all-gathers the world_size handles)
+ *   tagc_ctx_peer_open     maps the peers' regions (handles: world_size x
+ *                          TAGC_PEER_HANDLE_BYTES, rank order).
+ * tagc_ctx_peer_attach_local does the same for contexts of one process (all
+ * ranks on one GPU, tests). Afterwards tagc_reduce_shards(_host) uses the
+ * peers; a rank that never signals makes the step fail with TAGC_RUNTIME
+ * after TAGC_PEER_TIMEOUT_MS (default 20000) instead of hanging. */
+#define TAGC_PEER_HANDLE_BYTES 64
+int tagc_ctx_peer_prepare(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                          uint8_t handle[TAGC_PEER_HANDLE_BYTES]);
+int tagc_ctx_peer_open(tagc_ctx* ctx, const uint8_t* handles);
+int tagc_ctx_peer_attach_local(tagc_ctx* ctx, tagc_ctx* const* ranks, uint32_t n_ranks);
 /* The owner-major exchange layout tagc_reduce_shards uses on `rank` (pure
  * host computation; exposed so a foreign transport can reproduce the
  * exchange). Owner o's f32 block is [o*block_f32, (o+1)*block_f32) of the

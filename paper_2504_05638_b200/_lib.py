@@ -130,6 +130,9 @@ SIGNATURES = {
     "tagc_reduce_shards_begin": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(VP), C.POINTER(VP),
                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "tagc_reduce_shards_end": (C.c_int, [VP, VP, VP, C.POINTER(PeelStats)]),
+    "tagc_ctx_peer_prepare": (C.c_int, [VP, C.POINTER(Shard), U32, C.c_char_p]),
+    "tagc_ctx_peer_open": (C.c_int, [VP, C.c_char_p]),
+    "tagc_ctx_peer_attach_local": (C.c_int, [VP, C.POINTER(VP), U32]),
     "tagc_reduce_shard": (C.c_int, [VP, C.POINTER(Shard), VP, VP, VP, C.POINTER(PeelStats)]),
     "tagc_baseline_reduce_shards": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP]),
     "tagc_plan_exchange": (C.c_int, [C.POINTER(Config), C.POINTER(Shard), U32, U32, U32,

@@ -397,6 +397,26 @@ class Context:
               "reduce_shards_end")
         return PeelStats(**st.as_dict()) if stats else None
 
+    def peer_prepare(self, shards: Sequence[ShardSpec]) -> bytes:
+        """Allocate this rank's peer-exchange region for the shard layout and
+        return its 64-byte CUDA IPC handle (all-gather it across ranks)."""
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        buf = C.create_string_buffer(64)
+        check(lib.tagc_ctx_peer_prepare(self.h, arr, len(scs), buf), "peer_prepare")
+        return buf.raw
+
+    def peer_open(self, handles: Sequence[bytes]):
+        """Map every rank's region (handles in rank order); reduce_shards then
+        reduces over peer memory instead of NCCL."""
+        blob = b"".join(handles)
+        check(lib.tagc_ctx_peer_open(self.h, blob), "peer_open")
+
+    def peer_attach_local(self, ranks: Sequence["Context"]):
+        """All ranks' contexts in this process (one GPU): attach their regions."""
+        arr = (C.c_void_p * len(ranks))(*[r.h for r in ranks])
+        check(lib.tagc_ctx_peer_attach_local(self.h, arr, len(ranks)), "peer_attach_local")
+
     def host_join(self):
         check(lib.tagc_ctx_host_join(self.h), "host_join")
 

@@ -350,6 +350,30 @@ int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t*
   });
 }
 
+int tagc_ctx_peer_prepare(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
+                          uint8_t handle[TAGC_PEER_HANDLE_BYTES]) {
+  return guarded([&] {
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    eng(ctx).peer_prepare(v, handle);
+  });
+}
+
+int tagc_ctx_peer_open(tagc_ctx* ctx, const uint8_t* handles) {
+  return guarded([&] {
+    if (!handles) throw InvalidArgument("null handles");
+    eng(ctx).peer_open(handles);
+  });
+}
+
+int tagc_ctx_peer_attach_local(tagc_ctx* ctx, tagc_ctx* const* ranks, uint32_t n_ranks) {
+  return guarded([&] {
+    std::vector<Engine*> v;
+    for (uint32_t i = 0; i < n_ranks; ++i) v.push_back(&eng(ranks[i]));
+    eng(ctx).peer_attach_local(v);
+  });
+}
+
 int tagc_ctx_host_join(tagc_ctx* ctx) {
   return guarded([&] { eng(ctx).host_join(); });
 }

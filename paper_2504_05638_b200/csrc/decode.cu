@@ -992,7 +992,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_peel, 256, 0);
-  const int pg = std::max(per_sm, 1) * di.sms;
+  const int pg = coop_grid(di, std::max(per_sm, 1));
   DecodeWork wc = w;
   HashParams hc = hp;
   void* args[] = {&wc, &hc};
@@ -1021,9 +1021,9 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   unsigned long long* cur_keys = ob.keys[0];
   uint32_t* cur_slots = ob.slots[0];
   for (;;) {
-    uint32_t cnt = 0;
-    cudaMemcpyAsync(&cnt, ob.count, 4, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(ob.host_count, ob.count, 4, cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
+    const uint32_t cnt = *ob.host_count;
     if (cnt == 0) break;
     k_ord_keys<<<grid, 256, 0, stream>>>(cur_keys, cur_slots, cnt, ob.slot_key);
     cub::DoubleBuffer<unsigned long long> dk(cur_keys, cur_keys == ob.keys[0] ? ob.keys[1] : ob.keys[0]);

@@ -1441,7 +1441,7 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
   auto launch_fb = [&](auto kern) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, kTileThreads, 0);
-    const uint64_t g = std::min<uint64_t>(uint64_t(std::max(per_sm, 1)) * di.sms, std::max<uint64_t>(total_tiles, 1));
+    const uint64_t g = std::min<uint64_t>(uint64_t(coop_grid(di, std::max(per_sm, 1))), std::max<uint64_t>(total_tiles, 1));
     const EncItem* a0 = items;
     SelState* a1 = state;
     uint32_t a2 = n_items;

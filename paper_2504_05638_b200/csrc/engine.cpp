@@ -177,6 +177,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   drop_graphs();
+  peer_release();
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& e : ev_)
@@ -189,6 +190,7 @@ Engine::~Engine() {
     for (cudaEvent_t e : {hev_in_[i], hev_gfree_[i], hev_dec_[i], hev_out_[i]})
       if (e) cudaEventDestroy(e);
   if (hev_join_) cudaEventDestroy(hev_join_);
+  if (ord_host_count_) cudaFreeHost(ord_host_count_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
   if (aux_) {
@@ -353,6 +355,9 @@ void Engine::sync_check() {
   uint32_t err = 0;
   cuda_check(cudaMemcpy(&err, err_flag(), 4, cudaMemcpyDeviceToHost), "D2H err");
   if (err & 1u) throw InvalidArgument("sparsify: NaN gradient value");
+  uint32_t peer_err = 0;
+  cuda_check(cudaMemcpy(&peer_err, err_flag() + 2, 4, cudaMemcpyDeviceToHost), "D2H err");
+  if (peer_err) throw CudaError("peer exchange: a rank never signalled this step (timeout)");
 }
 
 // ------------------------------------------------------------ select/encode
@@ -435,10 +440,13 @@ void Engine::ensure_aux() {
 }
 
 void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
-                        bool ordered, cudaEvent_t zero_done) {
+                        bool ordered, cudaEvent_t zero_done, const std::function<void()>& pre_launch) {
   const uint32_t n = uint32_t(items.size());
   dec_stats_.assign(n, DecStats{});
-  if (n == 0) return;
+  if (n == 0) {
+    if (pre_launch) pre_launch();
+    return;
+  }
   uint64_t slots = 0, bm = 0, wt = 0, list = 0;
   for (DecItem& d : items) {
     d.mmul = fastmod_magic(d.m);
@@ -484,6 +492,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     cuda_check(cudaMemsetAsync(w.dbg, 0, 64 * 8, stream_), "dbg reset");
   }
   last_ordered_ = ordered;
+  if (pre_launch) pre_launch();
   if (ordered) {
     // 1-bit merged index over several ranks: carries can hide positions whose
     // mass stays in the sketch, so values follow the reference's FIFO order
@@ -493,6 +502,9 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     ob.slots[0] = static_cast<uint32_t*>(ws_.get("ord_s0", slots * 4, false, stream_));
     ob.slots[1] = static_cast<uint32_t*>(ws_.get("ord_s1", slots * 4, false, stream_));
     ob.count = static_cast<uint32_t*>(ws_.get("ord_count", 16, false, stream_));
+    if (!ord_host_count_)
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ord_host_count_), 64, cudaHostAllocDefault), "pinned");
+    ob.host_count = ord_host_count_;
     ob.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", list * 8, true, stream_));
     ob.slot_key = static_cast<unsigned long long*>(ws_.get("ord_slot_key", slots * 8, true, stream_));
     ob.scratch_bytes = ordered_sort_scratch_bytes(uint32_t(std::min<uint64_t>(slots, 0x7FFFFFFF)));
@@ -704,7 +716,8 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   CallScope scope(*this);
   cfg_.validate_for_world(world_);
   for (const ShardSpec& s : shards) check_shard(s, world_);
-  if (world_ > 1 && !comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
+  if (world_ > 1 && !comm_ && !peer_.attached)
+    throw InvalidArgument("multi-rank context has no NCCL communicator or peer exchange");
   static const bool peel_dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   const bool legacy = stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread;
   const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy &&  // default streams cannot be captured
@@ -717,8 +730,8 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   std::string key;
   {
     char buf[160];
-    std::snprintf(buf, sizeof(buf), "%p|%p|%p|%p|%.17g|%u|%u|%d|%d|%llu|%u|%llu|", (void*)grad, (void*)acc,
-                  (void*)out, (void*)grad_read_ev_, cfg_.theta, cfg_.ratio, cfg_.index_width, int(cfg_.policy),
+    std::snprintf(buf, sizeof(buf), "%p|%p|%p|%p|%d|%.17g|%u|%u|%d|%d|%llu|%u|%llu|", (void*)grad, (void*)acc,
+                  (void*)out, (void*)grad_read_ev_, peer_.attached ? peer_.set : -1, cfg_.theta, cfg_.ratio, cfg_.index_width, int(cfg_.policy),
                   int(cfg_.include_out_proj), (unsigned long long)cfg_.seed, cfg_.sketch_rows,
                   (unsigned long long)cfg_.min_compress_segment);
     key = buf;
@@ -743,6 +756,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   if (it != graphs_.end()) {
     GraphEntry& g = it->second;
     cuda_check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+    if (peer_.attached && world_ > 1) peer_.set ^= 1;  // the captured call used (and flipped) this set
     launches_ = g.launches;
     for (const LedgerEntry& l : g.ledger) ledger_.record(l.op, l.tag, l.bits, l.params);
     ledger_.wire_bytes += g.wire;
@@ -885,6 +899,25 @@ void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* g
 
 void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                                    float* out, PeelStats* stats) {
+  if (peer_.attached && world_ > 1) {  // collective by pulls over peer memory
+    const int set = peer_.set;
+    exchange_begin(shards, grad, acc, out, peer_.view.send_f[set][rank_], peer_.view.send_u[set][rank_]);
+    if (xs_.P.Bf != peer_.Bf || xs_.P.Bu != peer_.Bu)
+      throw InvalidArgument("shard layout differs from the one the peer exchange was prepared for");
+    auto* recv_f = static_cast<float*>(ws_.get("nc_recv_f", peer_.Bf * 4, false, stream_));
+    auto* recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", peer_.Bu * 4, false, stream_));
+    uint32_t* err = err_flag();
+    // the signal / wait / pull go in after the decode's allocations: a
+    // cudaMalloc behind a wait for peers could stall this rank (and, with all
+    // ranks in one process, every rank)
+    exchange_end(recv_f, recv_u, stats, [&] {
+      launches_ += launch_peer_exchange(di_, peer_.view, set, recv_f, recv_u, err, stream_);
+      ledger_.wire_bytes += uint64_t(world_) * (peer_.Bf + peer_.Bu) * 4;
+      ev_record(4);
+    });
+    peer_.set ^= 1;
+    return;
+  }
   exchange_begin(shards, grad, acc, out);
   const uint32_t W = world_;
   const uint64_t Bf = xs_.P.Bf, Bu = xs_.P.Bu;
@@ -911,7 +944,8 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
 
 // Second half (hook.cpp:164-189): decode this rank's owned compressed
 // segments from the reduced blocks and unpack its raw segments.
-void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, PeelStats* stats) {
+void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, PeelStats* stats,
+                          const std::function<void()>& pre_decode) {
   if (!xs_.active) throw InvalidArgument("no exchange in progress");
   xs_.active = false;
   const std::vector<ShardSpec>& shards = xs_.shards;
@@ -942,7 +976,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     d.list_cap = presence_bound(p.len, cfg_.theta, W);
     dec.push_back(d);
   }
-  run_decode(dec, hp, false, w == 1 && W > 1, zero_done);
+  run_decode(dec, hp, false, w == 1 && W > 1, zero_done, pre_decode);
   if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
@@ -1005,6 +1039,132 @@ void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* 
   for (const ShardSpec& s : shards)
     ledger_.record(CollectiveOp::reduce_scatter, "grad/shard" + std::to_string(s.id), s.size() * 32,
                    s.size());
+}
+
+// ------------------------------------------------------------ peer memory
+void Engine::peer_release() {
+  di_.coop_headroom = 0;
+  for (void* p : peer_.opened) cudaIpcCloseMemHandle(p);
+  peer_.opened.clear();
+  if (peer_.region) cudaFree(peer_.region);
+  peer_ = PeerState{};
+}
+
+void Engine::peer_prepare(const std::vector<ShardSpec>& shards, uint8_t handle[kPeerHandleBytes]) {
+  if (world_ > uint32_t(kMaxPeers)) throw InvalidArgument("peer exchange supports at most 16 ranks");
+  for (const ShardSpec& s : shards) check_shard(s, world_);
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  drop_graphs();
+  peer_release();
+  const ExchangePlan P = plan_exchange(shards, cfg_, world_, rank_);
+  PeerState ps;
+  ps.Bf = P.Bf;
+  ps.Bu = P.Bu;
+  size_t off = 0;
+  for (int set = 0; set < 2; ++set) {
+    ps.off_f[set] = off;
+    off = align_up(off + world_ * P.Bf * 4, 256);
+    ps.off_u[set] = off;
+    off = align_up(off + world_ * P.Bu * 4, 256);
+  }
+  ps.off_flags = off;
+  off = align_up(off + world_ * 8, 256);
+  ps.off_counter = off;
+  ps.bytes = align_up(off + 8, 256);
+  void* base = nullptr;
+  cuda_check(cudaMalloc(&base, ps.bytes), "peer region alloc");
+  ps.region = static_cast<char*>(base);
+  cuda_check(cudaMemset(ps.region + ps.off_flags, 0, ps.bytes - ps.off_flags), "peer flags zero");
+  cudaIpcMemHandle_t h;
+  cuda_check(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == kPeerHandleBytes, "IPC handle size");
+  if (handle) std::memcpy(handle, &h, kPeerHandleBytes);
+  peer_ = ps;
+  // Warm-up: two local exchanges of zeros (no peers involved), so every
+  // lazily allocated workspace and both staging halves exist before this
+  // rank ever waits on a peer; allocations (cudaMalloc / cudaHostAlloc) may
+  // synchronise the device and must not sit behind such a wait.
+  uint64_t total = 0, owned = 0;
+  for (const ShardSpec& sh : shards) {
+    total = std::max<uint64_t>(total, sh.end);
+    if (sh.owner == rank_) owned += sh.size();
+  }
+  const TrafficLedger saved = ledger_;  // the warm-up is not traffic
+  float *g = nullptr, *a = nullptr, *o = nullptr;
+  cuda_check(cudaMalloc(&g, std::max<uint64_t>(total, 1) * 4), "warm-up alloc");
+  cuda_check(cudaMalloc(&a, std::max<uint64_t>(total, 1) * 4), "warm-up alloc");
+  cuda_check(cudaMalloc(&o, std::max<uint64_t>(owned, 1) * 4), "warm-up alloc");
+  cuda_check(cudaMemset(g, 0, total * 4), "warm-up zero");
+  cuda_check(cudaMemset(a, 0, total * 4), "warm-up zero");
+  for (int rep = 0; rep < 2; ++rep) {
+    CallScope scope(*this);
+    exchange_begin(shards, g, a, o, reinterpret_cast<float*>(ps.region + ps.off_f[0]),
+                   reinterpret_cast<uint32_t*>(ps.region + ps.off_u[0]));
+    auto* recv_f = static_cast<float*>(ws_.get("nc_recv_f", ps.Bf * 4, false, stream_));
+    auto* recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", ps.Bu * 4, false, stream_));
+    zero({{recv_f, ps.Bf * 4}, {recv_u, ps.Bu * 4}});
+    exchange_end(recv_f, recv_u, nullptr);
+  }
+  ensure_aux();
+  peer_preload();
+  cuda_check(cudaStreamSynchronize(stream_), "warm-up sync");
+  cudaFree(g);
+  cudaFree(a);
+  cudaFree(o);
+  ledger_ = saved;
+}
+
+void Engine::peer_fill(const std::vector<char*>& bases) {
+  PeerView& v = peer_.view;
+  v = PeerView{};
+  v.world = world_;
+  v.rank = rank_;
+  v.block_f = peer_.Bf;
+  v.block_u = peer_.Bu;
+  uint64_t ms = 20000;
+  if (const char* e = std::getenv("TAGC_PEER_TIMEOUT_MS")) ms = std::strtoull(e, nullptr, 10);
+  v.timeout_ns = ms * 1000000ull;
+  for (uint32_t q = 0; q < world_; ++q) {
+    for (int set = 0; set < 2; ++set) {
+      v.send_f[set][q] = reinterpret_cast<float*>(bases[q] + peer_.off_f[set]);
+      v.send_u[set][q] = reinterpret_cast<uint32_t*>(bases[q] + peer_.off_u[set]);
+    }
+    v.flags[q] = reinterpret_cast<unsigned long long*>(bases[q] + peer_.off_flags);
+  }
+  v.counter = reinterpret_cast<unsigned long long*>(peer_.region + peer_.off_counter);
+  peer_.attached = true;
+  di_.coop_headroom = 1;
+}
+
+void Engine::peer_open(const uint8_t* handles) {
+  if (!peer_.region) throw InvalidArgument("peer_open before peer_prepare");
+  std::vector<char*> bases(world_, nullptr);
+  for (uint32_t q = 0; q < world_; ++q) {
+    if (q == rank_) {
+      bases[q] = peer_.region;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + size_t(q) * kPeerHandleBytes, kPeerHandleBytes);
+    void* p = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    peer_.opened.push_back(p);
+    bases[q] = static_cast<char*>(p);
+  }
+  peer_fill(bases);
+}
+
+void Engine::peer_attach_local(const std::vector<Engine*>& ranks) {
+  if (!peer_.region) throw InvalidArgument("peer_attach_local before peer_prepare");
+  if (ranks.size() != world_) throw InvalidArgument("need one context per rank");
+  std::vector<char*> bases(world_, nullptr);
+  for (uint32_t q = 0; q < world_; ++q) {
+    const Engine* e = ranks[q];
+    if (!e || e->rank_ != q || e->world_ != world_ || !e->peer_.region || e->peer_.bytes != peer_.bytes)
+      throw InvalidArgument("peer contexts must be ranks 0..W-1 prepared for the same layout");
+    bases[q] = e->peer_.region;
+  }
+  peer_fill(bases);
 }
 
 // ------------------------------------------------------------ host buffers

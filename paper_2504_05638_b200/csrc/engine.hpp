@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -121,6 +122,15 @@ class Engine {
                           float* host_out, PeelStats* stats);
   // The context stream waits for every copy the host-buffer path enqueued.
   void host_join();
+  // Pull-mode exchange over peer memory instead of NCCL (peer.cu). prepare
+  // lays out and allocates this rank's exchange region for the shard layout
+  // and returns its CUDA IPC handle; open maps every peer's region from the
+  // gathered handles; attach_local takes the regions of contexts living in
+  // this process (one GPU, tests). Afterwards reduce_shards uses the peers.
+  static constexpr size_t kPeerHandleBytes = 64;
+  void peer_prepare(const std::vector<ShardSpec>& shards, uint8_t handle[kPeerHandleBytes]);
+  void peer_open(const uint8_t* handles);
+  void peer_attach_local(const std::vector<Engine*>& ranks);
   // The exchange split around its collective, for a caller-provided
   // transport: exchange_begin encodes into the owner-major send blocks
   // (world * block_f32 floats, world * block_u32 words; layout of
@@ -128,7 +138,8 @@ class Engine {
   // sum), exchange_end decodes this rank's block.
   void exchange_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
                       float* user_send_f = nullptr, uint32_t* user_send_u = nullptr);
-  void exchange_end(const float* recv_f, const uint32_t* recv_u, PeelStats* stats);
+  void exchange_end(const float* recv_f, const uint32_t* recv_u, PeelStats* stats,
+                    const std::function<void()>& pre_decode = nullptr);
   float* exchange_send_f() const { return xs_.send_f; }
   uint32_t* exchange_send_u() const { return xs_.send_u; }
   uint64_t exchange_block_f() const { return xs_.P.Bf; }
@@ -168,6 +179,20 @@ class Engine {
     cudaEvent_t zero_done = nullptr;
   };
   ExchangeState xs_;
+  struct PeerState {
+    bool attached = false;
+    char* region = nullptr;
+    size_t bytes = 0;
+    uint64_t Bf = 0, Bu = 0;
+    size_t off_f[2] = {0, 0}, off_u[2] = {0, 0}, off_flags = 0, off_counter = 0;
+    PeerView view{};
+    int set = 0;
+    std::vector<void*> opened;
+  };
+  PeerState peer_;
+  uint32_t* ord_host_count_ = nullptr;  // pinned read-back of the ordered peel's generation size
+  void peer_release();
+  void peer_fill(const std::vector<char*>& bases);
   struct LedgerEntry {
     CollectiveOp op;
     std::string tag;
@@ -208,8 +233,12 @@ class Engine {
                          bool want_kept, const char* tag);
   // Decode into the items' outputs; the final emit waits on `zero_done` (if
   // set), the side stream's join event.
+  // pre_launch (if set) is enqueued after the decode's allocations and
+  // descriptor uploads, right before its kernels (the peer exchange goes
+  // there: nothing that may synchronise the device follows its wait).
   void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
-                  bool ordered, cudaEvent_t zero_done = nullptr);
+                  bool ordered, cudaEvent_t zero_done = nullptr,
+                  const std::function<void()>& pre_launch = nullptr);
   // Side stream for bandwidth work that overlaps the latency-bound peel
   // (W == 1 raw-segment copies); fork/join by events.
   cudaStream_t aux_ = nullptr;

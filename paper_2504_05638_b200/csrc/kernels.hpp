@@ -14,7 +14,16 @@ namespace tagc_b200 {
 struct DevInfo {
   int sms = 148;
   int dev = 0;
+  // CTAs per SM a cooperative launch leaves free: 1 while a peer exchange is
+  // attached, so a peer's 1-CTA flag wait on the same GPU (all ranks in one
+  // process) can never hold back the full-occupancy grid it waits for
+  int coop_headroom = 0;
 };
+// cooperative grid: (blocks per SM - headroom) x SMs, at least one per SM
+inline int coop_grid(const DevInfo& di, int per_sm) {
+  const int b = per_sm - di.coop_headroom;
+  return (b > 0 ? b : 1) * di.sms;
+}
 
 // ---------------------------------------------------------------- select + encode
 // Speculative single-pass sparsify + encode for `n_items` items (all with
@@ -138,6 +147,7 @@ struct OrderedBuffers {
   unsigned long long* keys[2];
   uint32_t* slots[2];  // capacity total_slots each
   uint32_t* count;
+  uint32_t* host_count;       // page-locked read-back slot (a pageable read-back blocks other threads)
   unsigned long long* claim;  // per presence-list entry
   unsigned long long* slot_key;  // u64 per slot, zero-initialised once
   void* scratch;
@@ -166,5 +176,24 @@ size_t index_presence_scratch_bytes(uint32_t n, uint32_t width);
 int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* scratch,
                     size_t scratch_bytes, cudaStream_t stream);
 size_t sort_scratch_bytes(uint32_t count);
+
+// ---------------------------------------------------------------- peer exchange
+// Pull-mode collective over peer memory (peer.cu): pointers into every rank's
+// exchange region (two send sets, flags, step counter).
+constexpr int kMaxPeers = 16;
+struct PeerView {
+  float* send_f[2][kMaxPeers];
+  uint32_t* send_u[2][kMaxPeers];
+  unsigned long long* flags[kMaxPeers];  // rank q's flag array (world slots)
+  unsigned long long* counter;           // this rank's step counter
+  uint64_t block_f, block_u;             // owner block sizes (elements, multiples of 32)
+  uint64_t timeout_ns;
+  uint32_t world, rank;
+};
+// signal peers -> wait for every peer -> reduce this rank's block of `set`
+// into recv_f / recv_u (err[2] set on a peer timeout).
+int launch_peer_exchange(const DevInfo& di, const PeerView& v, int set, float* recv_f, uint32_t* recv_u,
+                         uint32_t* err, cudaStream_t stream);
+void peer_preload();
 
 }  // namespace tagc_b200

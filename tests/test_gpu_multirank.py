@@ -9,6 +9,8 @@ rank bit-exact, peel statistics exact, the owner's decoded shards within the
 reference's 1e-5 tolerance (roundtrip.cpp:119-137). With a 1-bit index the
 merged words carry (index.cpp:80-93) and the decoder's FIFO-ordered peel must
 reproduce the reference's carry-corrupted values."""
+import threading
+
 import numpy as np
 import pytest
 import torch
@@ -105,3 +107,76 @@ def test_split_exchange_matches_oracle(orc, world, width, theta, steps):
                 off += sh.size()
             for k in ("presence", "peeled", "unresolved"):
                 assert getattr(stats[o], k) == sum(rsts[s.id][k] for s in owned[o]), (k, o, stats[o])
+
+
+@pytest.mark.parametrize("world,width,steps", [(2, 4, 5), (4, 4, 2), (2, 1, 2)])
+def test_peer_exchange_matches_oracle(orc, world, width, steps):
+    """Pull-mode exchange over peer memory (tagc_ctx_peer_*): all ranks as
+    contexts of this process on one GPU, each on its own stream so that the
+    step flags are raised and awaited concurrently. Five steps at W=2 cover
+    both send sets, the CUDA-graph capture (third call) and replay (fifth)."""
+    specs = [tagc.LayerSpec(n, k, c) for n, k, c in SPECS]
+    shards = tagc.make_shards(specs, world, world)
+    total = shards[-1].end
+    theta = 99.0 if width == 4 else 98.75
+    cfg = tagc.CompressionConfig(theta=theta, ratio=10, index_width=width, policy="non_attention_linear",
+                                 include_out_proj=True, seed=77)
+    ocfg = O.Config(cfg.theta, cfg.ratio, cfg.index_width, cfg.policy, cfg.include_out_proj, cfg.seed,
+                    cfg.sketch_rows, cfg.allow_low_theta, cfg.min_compress_segment)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ctxs = []
+    for r in range(world):
+        with torch.cuda.stream(streams[r]):
+            ctxs.append(tagc.Context(cfg, world_size=world, rank=r, device=0))
+    for c in ctxs:
+        c.peer_prepare(shards)
+    for c in ctxs:
+        c.peer_attach_local(ctxs)
+    owned = [[s for s in shards if s.owner == r] for r in range(world)]
+    acc = [torch.zeros(total, device=DEV) for _ in range(world)]
+    g_d = [torch.empty(total, device=DEV) for _ in range(world)]
+    outs = [torch.empty(max(1, sum(s.size() for s in owned[r])), device=DEV) for r in range(world)]
+    oacc = [np.zeros(total, np.float32) for _ in range(world)]
+    torch.cuda.synchronize()
+    for step in range(steps):
+        grads = [lognormal(total, 7000 + 100 * step + r) for r in range(world)]
+        for r in range(world):
+            g_d[r].copy_(torch.from_numpy(grads[r]))
+        torch.cuda.synchronize()
+        # one host thread per rank, as in a real deployment (one process per
+        # GPU): the 1-bit path's ordered peel synchronises its own stream
+        # between generations, which must not stall the other ranks' enqueues
+        errs = [None] * world
+
+        def run(r):
+            try:
+                ctxs[r].tagc_reduce_shards(shards, g_d[r], acc[r], outs[r], stats=False)
+                ctxs[r].sync()
+            except Exception as e:  # surfaced below
+                errs[r] = e
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        refs = {}
+        for sh in shards:
+            osh = O.Shard(sh.id, sh.owner, sh.begin, sh.end,
+                          [O.Segment(s.kind, s.begin, s.end, s.name) for s in sh.segments])
+            a = [oacc[r][sh.begin:sh.end].copy() for r in range(world)]
+            ref, _ = orc.tagc_reduce_shard(osh, [grads[r][sh.begin:sh.end] for r in range(world)], a, ocfg)
+            for r in range(world):
+                oacc[r][sh.begin:sh.end] = a[r]
+            refs[sh.id] = ref.copy()
+        for r in range(world):
+            assert np.array_equal(bits(acc[r].cpu().numpy()), bits(oacc[r])), (step, r)
+        for o in range(world):
+            got = outs[o].cpu().numpy()
+            off = 0
+            for sh in owned[o]:
+                check_close(got[off:off + sh.size()], refs[sh.id])
+                off += sh.size()
