@@ -151,7 +151,11 @@ def run_b200(args):
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     ctx = tagc.Context(cfg, world_size=world, rank=rank, device=local, stream=stream.cuda_stream)
-    if world > 1:
+    if world > 1 and args.exchange == "peer":  # pulls over NVLink peer memory (CUDA IPC), no NCCL
+        handles = [None] * world
+        dist.all_gather_object(handles, ctx.peer_prepare(shards))
+        ctx.peer_open(handles)
+    elif world > 1:
         obj = [tagc.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx.init_nccl(obj[0])
@@ -297,7 +301,8 @@ def run_b200(args):
             "peel": {"presence": st.presence, "peeled": st.peeled, "unresolved": st.unresolved,
                      "rounds": rounds[0], "tail_rounds": rounds[1]},
             "l2": "inputs larger than L2 (498 MB per rank)",
-            "parallelism": f"dp{world} (one process per GPU, NCCL reduce-scatter)",
+            "parallelism": f"dp{world} (one process per GPU, "
+                           f"{'peer-memory pulls' if args.exchange == 'peer' else 'NCCL reduce-scatter'})",
         },
         "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4)},
@@ -420,6 +425,8 @@ def main():
                     help="params per rank in the bounded CPU-reference sample")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 collective: grouped ncclReduceScatter, or pulls over peer memory")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
