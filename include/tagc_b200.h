@@ -298,6 +298,24 @@ int tagc_plan_exchange(const tagc_config* cfg, const tagc_shard* shards, uint32_
 int tagc_baseline_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
                                 const float* grad, float* out);
 
+/* ------------------------------------------- owner-side consumer (§8f)
+ * The step after the exchange in the reference's training loop
+ * (train.cpp:355-364): the owner takes the mean over ranks of its decoded
+ * shard and updates its parameter slice, then every rank re-gathers the
+ * padded flat parameter space.
+ * tagc_apply_optimizer: decoded (dev, len, the summed shard; the mean
+ * g = decoded * (1/world) of train.cpp:356-357 is formed on the fly and not
+ * written back), params (dev, len, in/out), adam_v (dev, len,
+ * in/out, zero before step 1; NULL for sgd). kind 0 = sgd (scale_sub_inplace,
+ * kernels.cpp:32-41), 1 = adamw_nm (apply_optimizer, train.cpp:202-220; step
+ * >= 1). Bit-identical to the reference's fp32 loop. */
+int tagc_apply_optimizer(tagc_ctx* ctx, int32_t kind, double lr, double weight_decay, uint32_t world,
+                         uint32_t step, float* params, const float* decoded, float* adam_v, uint64_t len);
+/* World::all_gather of the owner slices (collectives.cpp:197-212, call site
+ * train.cpp:364): params dev, padded = world * L floats; this rank's slice
+ * [rank*L, (rank+1)*L) is gathered in place into every rank's buffer (NCCL). */
+int tagc_allgather_params(tagc_ctx* ctx, float* params, uint64_t padded);
+
 /* ------------------------------------------------- per-layer codec (device)
  * Each mirrors one reference function on one vector of n elements. */
 /* apply_accumulator (sparsify.cpp:9-16): out = g + acc */

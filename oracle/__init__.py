@@ -283,6 +283,13 @@ class Oracle:
                                            _p(out, C.c_float)), "sketch_compress")
         return out
 
+    def apply_optimizer(self, kind, lr, weight_decay, world, step, params, decoded, adam_v):
+        """train.cpp:355-359 + apply_optimizer (train.cpp:202-220); updates in place."""
+        n = params.size
+        self.lib.or_apply_optimizer(C.c_int32(kind), C.c_float(lr), C.c_float(weight_decay), C.c_uint32(world),
+                                    C.c_uint32(step), _p(params, C.c_float), _p(decoded, C.c_float),
+                                    _p(adam_v, C.c_float) if adam_v is not None else None, C.c_size_t(n))
+
     def rank_sum(self, arrays):
         arrs = [_f32(a) for a in arrays]
         out = np.empty_like(arrs[0])
@@ -442,6 +449,11 @@ class Ref:
         _check(self.lib.ref_index_presence(_p(words, C.c_uint32), C.c_uint32(n), C.c_uint32(width),
                                            _p(out, C.c_uint32), C.byref(cnt)), "ref_presence")
         return out[: cnt.value].copy()
+
+    def scale_sub_inplace(self, dst, src, scale):
+        """kernels::scale_sub_inplace (kernels.cpp:32-41), dst updated in place."""
+        _check(self.lib.ref_scale_sub_inplace(_p(dst, C.c_float), _p(_f32(src), C.c_float), C.c_size_t(dst.size),
+                                              C.c_float(scale)), "ref_scale_sub_inplace")
 
     def sketch_compress(self, values, ratio, seed, rows=3):
         v = _f32(values)

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "tagc/kernels.hpp"
 #include "tagc/collectives.hpp"
 #include "tagc/config.hpp"
 #include "tagc/decode.hpp"
@@ -158,6 +159,14 @@ int ref_sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t row
     const CountSketch s =
         CountSketch::compress(std::span<const float>(v, n), sketch_geometry(n, ratio, rows), seed);
     std::memcpy(out, s.values.data(), s.values.size() * sizeof(float));
+  });
+}
+
+// The SGD step of the owner-side consumer (train.cpp:205-207).
+int ref_scale_sub_inplace(float* dst, const float* src, size_t n, float scale) {
+  return guarded([&] {
+    tagc::kernels::scale_sub_inplace(std::span<float>(dst, n), std::span<const float>(src, n), scale,
+                                     tagc::kernels::Exec::serial);
   });
 }
 

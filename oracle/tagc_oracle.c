@@ -608,3 +608,22 @@ int or_make_shards(const uint64_t* layer_counts, const int32_t* layer_kinds, uin
   *n_segments = ns;
   return OR_OK;
 }
+
+/* train.cpp:355-359 (mean over ranks) and apply_optimizer, train.cpp:202-220. */
+void or_apply_optimizer(int32_t kind, float lr, float weight_decay, uint32_t world, uint32_t step, float* params,
+                        float* decoded, float* adam_v, size_t n) {
+  const float inv_w = 1.0f / (float)world;                    /* train.cpp:355 */
+  for (size_t i = 0; i < n; ++i) decoded[i] *= inv_w;         /* train.cpp:356 */
+  if (kind == 0) {                                            /* kernels.cpp:32-41 */
+    for (size_t i = 0; i < n; ++i) params[i] -= lr * decoded[i];
+    return;
+  }
+  const float b2 = 0.999f, eps = 1e-8f;                       /* train.cpp:209-210 */
+  const float bias_fix = 1.0f - powf(b2, (float)step);        /* train.cpp:213 */
+  for (size_t i = 0; i < n; ++i) {
+    const float g = decoded[i];
+    adam_v[i] = b2 * adam_v[i] + (1.0f - b2) * g * g;          /* train.cpp:216 */
+    const float vhat = adam_v[i] / bias_fix;
+    params[i] -= lr * (g / (sqrtf(vhat) + eps) + weight_decay * params[i]);
+  }
+}

@@ -85,6 +85,13 @@ int or_kind_compressible(int32_t kind, int32_t policy, int32_t include_out_proj)
 void or_add_inplace(float* dst, const float* src, size_t n);
 void or_rank_sum(float* out, const float* const* inputs, uint32_t world, size_t n);
 void or_rank_sum_words(uint32_t* out, const uint32_t* const* inputs, uint32_t world, size_t n);
+
+/* ---- owner-side consumer (train.cpp:355-359, 202-220) ----
+ * decoded *= 1/W, then SGD (kind 0: params -= lr * g) or the momentum-free
+ * AdamW (kind 1: v = b2 v + (1-b2) g g; params -= lr (g / (sqrt(v / (1 - b2^step)) + eps) + wd params)).
+ * decoded is scaled in place, as the reference does. */
+void or_apply_optimizer(int32_t kind, float lr, float weight_decay, uint32_t world, uint32_t step, float* params,
+                        float* decoded, float* adam_v, size_t n);
 void or_threshold_split(const float* g, size_t n, float tau, float* sparse, float* residual);
 
 /* ---- sparsify (sparsify.cpp:18-49) ---- */

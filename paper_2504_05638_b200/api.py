@@ -476,6 +476,29 @@ class Context:
         check(lib.tagc_sketch_add(self.h, _ptr(a), _ptr(b), _ptr(out), a.numel()), "sketch_add")
         return out
 
+    def apply_optimizer(self, optimizer: str, lr: float, params, decoded, world: int, step: int,
+                        adam_v=None, weight_decay: float = 0.0):
+        """Owner-side consumer (reference train.cpp:355-359, apply_optimizer
+        :202-220): params -= update(decoded / world) in place; adam_v (zeros
+        before step 1) is the adamw_nm second moment, updated in place."""
+        kinds = {"sgd": 0, "adamw_nm": 1}
+        if optimizer not in kinds:
+            raise TagcInvalidArgument(2, f"unknown optimizer: {optimizer}")
+        n = params.numel()
+        if decoded.numel() != n or (adam_v is not None and adam_v.numel() != n):
+            raise TagcInvalidArgument(2, "params, decoded and adam_v must have equal length")
+        check(lib.tagc_apply_optimizer(self.h, kinds[optimizer], float(lr), float(weight_decay), int(world),
+                                       int(step), _ptr(params), _ptr(decoded),
+                                       _ptr(adam_v) if adam_v is not None else None, n), "apply_optimizer")
+        return params
+
+    def allgather_params(self, params):
+        """World::all_gather of the owners' slices (train.cpp:364) over NCCL,
+        in place: params is the padded flat space, this rank's slice is
+        params[rank*L:(rank+1)*L]."""
+        check(lib.tagc_allgather_params(self.h, _ptr(params), params.numel()), "allgather_params")
+        return params
+
     def peeling_decompress(self, presence, sketch, n: int, ratio: int, seed: int, rows: int = 3):
         """reference peeling_decompress (decode.cpp:53-140): (values, unresolved, peeled_fraction)"""
         cnt = presence.numel()

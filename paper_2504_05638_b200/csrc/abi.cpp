@@ -444,6 +444,15 @@ int tagc_sketch_add(tagc_ctx* ctx, const float* a, const float* b, float* out, u
   return guarded([&] { eng(ctx).add(a, b, out, len); });
 }
 
+int tagc_apply_optimizer(tagc_ctx* ctx, int32_t kind, double lr, double weight_decay, uint32_t world,
+                         uint32_t step, float* params, const float* decoded, float* adam_v, uint64_t len) {
+  return guarded([&] { eng(ctx).apply_optimizer(kind, lr, weight_decay, world, step, params, decoded, adam_v, len); });
+}
+
+int tagc_allgather_params(tagc_ctx* ctx, float* params, uint64_t padded) {
+  return guarded([&] { eng(ctx).allgather_params(params, padded); });
+}
+
 int tagc_peeling_decompress(tagc_ctx* ctx, const uint32_t* presence, uint32_t count, uint32_t n,
                             uint32_t ratio, uint32_t rows, uint64_t seed, const float* sketch,
                             float* values, uint32_t* unresolved, uint32_t* n_unresolved,

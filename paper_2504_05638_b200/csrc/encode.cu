@@ -1269,6 +1269,31 @@ __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b,
     out[i] = a[i] + b[i];
 }
 
+// Owner-side consumer of the decoded shard (reference train.cpp:355-359 and
+// apply_optimizer, train.cpp:202-220): g = decoded * (1/W), then SGD or the
+// momentum-free AdamW. Explicitly rounded operations (no FMA contraction) in
+// the reference's order, so the update is bit-identical to its fp32 loop.
+template <bool kAdam>
+__global__ void __launch_bounds__(256) k_apply_optimizer(float* __restrict__ params,
+                                                         const float* __restrict__ decoded,
+                                                         float* __restrict__ adam_v, uint64_t n, float inv_w,
+                                                         float lr, float wd, float bias_fix) {
+  constexpr float kB2 = 0.999f, kOneMinusB2 = 1.0f - 0.999f, kEps = 1e-8f;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const float g = __fmul_rn(decoded[i], inv_w);
+    const float p = params[i];
+    if (!kAdam) {
+      params[i] = __fsub_rn(p, __fmul_rn(lr, g));
+    } else {
+      const float v = __fadd_rn(__fmul_rn(kB2, adam_v[i]), __fmul_rn(__fmul_rn(kOneMinusB2, g), g));
+      adam_v[i] = v;
+      const float vhat = __fdiv_rn(v, bias_fix);
+      const float upd = __fadd_rn(__fdiv_rn(g, __fadd_rn(__fsqrt_rn(vhat), kEps)), __fmul_rn(wd, p));
+      params[i] = __fsub_rn(p, __fmul_rn(lr, upd));
+    }
+  }
+}
+
 // Raw-segment pack/unpack: flat 4096-element tiles over all items, 16-byte
 // accesses when source and destination are both aligned.
 __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__ items,
@@ -1503,6 +1528,14 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
                         cudaStream_t stream) {
   if (!n) return 0;
   k_rank_sum_u32<<<flat_grid(n, 256), 256, 0, stream>>>(in_ptrs, world, out, n);
+  return 1;
+}
+
+int launch_apply_optimizer(int kind, float* params, const float* decoded, float* adam_v, uint64_t n,
+                           float inv_w, float lr, float wd, float bias_fix, cudaStream_t stream) {
+  if (!n) return 0;
+  if (kind == 0) k_apply_optimizer<false><<<flat_grid(n, 256), 256, 0, stream>>>(params, decoded, adam_v, n, inv_w, lr, wd, bias_fix);
+  else k_apply_optimizer<true><<<flat_grid(n, 256), 256, 0, stream>>>(params, decoded, adam_v, n, inv_w, lr, wd, bias_fix);
   return 1;
 }
 

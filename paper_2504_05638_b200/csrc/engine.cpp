@@ -1309,6 +1309,30 @@ void Engine::sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_
   run_select_encode(it, true, make_hash_params(seed, rows), false, "compress");
 }
 
+void Engine::apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step,
+                             float* params, const float* decoded, float* adam_v, uint64_t n) {
+  if (kind != 0 && kind != 1) throw InvalidArgument("optimizer must be sgd (0) or adamw_nm (1)");
+  if (world == 0) throw InvalidArgument("world size must be at least 1");
+  if (kind == 1 && (step == 0 || !adam_v)) throw InvalidArgument("adamw_nm needs step >= 1 and its state");
+  const float b2 = 0.999f;
+  const float bias_fix = kind == 1 ? 1.0f - std::pow(b2, static_cast<float>(step)) : 1.0f;  // train.cpp:213
+  launches_ = launch_apply_optimizer(kind, params, decoded, adam_v, n, 1.0f / static_cast<float>(world),
+                                     static_cast<float>(lr), static_cast<float>(weight_decay), bias_fix, stream_);
+  cuda_check(cudaGetLastError(), "apply_optimizer launch");
+}
+
+void Engine::allgather_params(float* params, uint64_t padded) {
+  if (padded % world_) throw InvalidArgument("padded length must be a multiple of the world size");
+  const uint64_t L = padded / world_;
+  launches_ = 0;
+  if (world_ > 1) {
+    if (!comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");
+    nccl_check(nccl().AllGather(params + rank_ * L, params, L, ncclFloat32, comm_, stream_), "ncclAllGather");
+    ledger_.wire_bytes += padded * 4;
+  }
+  ledger_.record(CollectiveOp::all_gather, "params/allgather", padded * 32, padded);
+}
+
 void Engine::add(const float* a, const float* b, float* out, uint64_t n) {
   launches_ = launch_add(a, b, out, n, stream_);
 }

@@ -155,6 +155,13 @@ class Engine {
   void sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t rows, uint64_t seed,
                        float* sketch);
   void add(const float* a, const float* b, float* out, uint64_t n);
+  // Owner-side consumer: mean over ranks + optimizer step (train.cpp:202-220, 355-359)
+  void apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step, float* params,
+                       const float* decoded, float* adam_v, uint64_t n);
+  // Parameter all-gather after the owners' updates (train.cpp:364): params is
+  // the padded flat space (padded = W * L, train.cpp:242); rank i's slice
+  // [i*L, (i+1)*L) goes to every rank, in place.
+  void allgather_params(float* params, uint64_t padded);
   void peeling_decompress(const uint32_t* presence, uint32_t count, uint32_t n, uint32_t ratio,
                           uint32_t rows, uint64_t seed, const float* sketch, float* values,
                           uint32_t* unresolved, uint32_t* n_unresolved, double* pf);

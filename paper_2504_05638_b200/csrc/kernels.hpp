@@ -69,6 +69,10 @@ int launch_rank_sum_f32(const float* const* in_ptrs, uint32_t world, float* out,
 // Wrapping u32 word sum (kernels.cpp:65-84).
 int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t* out, uint64_t n,
                         cudaStream_t stream);
+// Owner-side optimizer step on the decoded shard (train.cpp:202-220, 355-359):
+// kind 0 SGD, 1 momentum-free AdamW (adam_v in/out).
+int launch_apply_optimizer(int kind, float* params, const float* decoded, float* adam_v, uint64_t n,
+                           float inv_w, float lr, float wd, float bias_fix, cudaStream_t stream);
 // out = a + b (sketch_add / apply_accumulator).
 int launch_add(const float* a, const float* b, float* out, uint64_t n, cudaStream_t stream);
 

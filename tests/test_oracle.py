@@ -180,3 +180,44 @@ def test_oracle_vs_live_reference(orc, ref):
         assert s1 == s2
         assert np.array_equal(bits(d1), bits(d2))
         assert all(np.array_equal(bits(x), bits(y)) for x, y in zip(a1, a2))
+
+
+def _adamw_nm_f32(params, g, v, lr, wd, step):
+    """numpy float32 restatement of apply_optimizer's adamw_nm loop
+    (train.cpp:209-219): every operation rounded to fp32, in source order."""
+    f = np.float32
+    b2, eps = f(0.999), f(1e-8)
+    bias_fix = f(1.0) - np.power(b2, f(step), dtype=np.float32)
+    v[:] = b2 * v + ((f(1.0) - b2) * g) * g
+    vhat = v / bias_fix
+    params[:] = params - f(lr) * (g / (np.sqrt(vhat) + eps) + f(wd) * params)
+
+
+def test_oracle_optimizer(orc):
+    """Owner-side consumer (train.cpp:355-359): SGD pinned to the reference's
+    own scale_sub_inplace when oracle/_ref is present, adamw_nm to an
+    independent fp32 restatement; both bit-exact over several steps."""
+    from oracle import Ref
+
+    rng = np.random.default_rng(3)
+    n, world = 10_007, 3
+    p0 = rng.standard_normal(n).astype(np.float32)
+    # sgd
+    p_o, p_r = p0.copy(), p0.copy()
+    for step in range(1, 4):
+        dec = (rng.standard_normal(n) * world).astype(np.float32)
+        orc.apply_optimizer(0, 0.01, 0.0, world, step, p_o, dec.copy(), None)
+        if Ref.available():
+            mean = dec * np.float32(1.0 / np.float32(world))
+            Ref().scale_sub_inplace(p_r, mean, np.float32(0.01))
+            assert np.array_equal(bits(p_o), bits(p_r)), step
+    # adamw_nm (momentum-free: only the second moment is kept)
+    p_o, p_n = p0.copy(), p0.copy()
+    v_o, v_n = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    for step in range(1, 6):
+        dec = (rng.standard_normal(n) * world).astype(np.float32)
+        dec[rng.integers(0, n, 500)] = 0.0  # unselected positions decode to zero
+        orc.apply_optimizer(1, 0.01, 0.1, world, step, p_o, dec.copy(), v_o)
+        _adamw_nm_f32(p_n, dec * np.float32(1.0 / np.float32(world)), v_n, 0.01, 0.1, step)
+        assert np.array_equal(bits(v_o), bits(v_n)), step
+        assert np.array_equal(bits(p_o), bits(p_n)), step
