@@ -311,6 +311,17 @@ int tagc_baseline_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_
  * >= 1). Bit-identical to the reference's fp32 loop. */
 int tagc_apply_optimizer(tagc_ctx* ctx, int32_t kind, double lr, double weight_decay, uint32_t world,
                          uint32_t step, float* params, const float* decoded, float* adam_v, uint64_t len);
+/* tagc_reduce_shards followed by the owner's step, fused: the mean and the
+ * optimizer update run inside the kernels that produce the decoded values
+ * (the decode's dense emit and the owned raw segments' unpack), so the
+ * decoded shard is not written and re-read. params / adam_v (dev) are laid
+ * out like tagc_reduce_shards' out (the owned shards, concatenated); out may
+ * be NULL (decoded values not stored) or a buffer that receives them too.
+ * Bit-identical to tagc_reduce_shards + tagc_apply_optimizer(world = the
+ * context's world size). */
+int tagc_reduce_shards_step(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad,
+                            float* acc, float* out, int32_t kind, double lr, double weight_decay, uint32_t step,
+                            float* params, float* adam_v, tagc_peel_stats* stats);
 /* World::all_gather of the owner slices (collectives.cpp:197-212, call site
  * train.cpp:364): params dev, padded = world * L floats; this rank's slice
  * [rank*L, (rank+1)*L) is gathered in place into every rank's buffer (NCCL). */

@@ -148,6 +148,8 @@ SIGNATURES = {
     "tagc_sketch_add": (C.c_int, [VP, VP, VP, VP, U64]),
     "tagc_apply_optimizer": (C.c_int, [VP, C.c_int32, C.c_double, C.c_double, U32, U32, VP, VP, VP, U64]),
     "tagc_allgather_params": (C.c_int, [VP, VP, U64]),
+    "tagc_reduce_shards_step": (C.c_int, [VP, VP, U32, VP, VP, VP, C.c_int32, C.c_double, C.c_double, U32, VP, VP,
+                                          VP]),
     "tagc_peeling_decompress": (C.c_int, [VP, VP, U32, U32, U32, U32, U64, VP, VP, VP, C.POINTER(U32),
                                           C.POINTER(C.c_double)]),
     "tagc_estimation_decompress": (C.c_int, [VP, VP, U32, U32, U32, U32, U64, VP, VP, U32, VP]),

@@ -492,6 +492,24 @@ class Context:
                                        _ptr(adam_v) if adam_v is not None else None, n), "apply_optimizer")
         return params
 
+    def tagc_reduce_shards_step(self, shards: Sequence[ShardSpec], grad, acc, params, optimizer: str, lr: float,
+                                step: int, adam_v=None, weight_decay: float = 0.0, out=None, stats=False):
+        """tagc_reduce_shards + the owner's optimizer step, fused into the decode
+        (SURVEY §8f row 2): params / adam_v / out are laid out like
+        tagc_reduce_shards' out; out=None skips storing the decoded values."""
+        kinds = {"sgd": 0, "adamw_nm": 1}
+        if optimizer not in kinds:
+            raise TagcInvalidArgument(2, f"unknown optimizer: {optimizer}")
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shards_step(self.h, arr, len(scs), _ptr(grad), _ptr(acc),
+                                          _ptr(out) if out is not None else None, kinds[optimizer], float(lr),
+                                          float(weight_decay), int(step), _ptr(params),
+                                          _ptr(adam_v) if adam_v is not None else None,
+                                          C.byref(st) if stats else None), "tagc_reduce_shards_step")
+        return PeelStats(**st.as_dict()) if stats else None
+
     def allgather_params(self, params):
         """World::all_gather of the owners' slices (train.cpp:364) over NCCL,
         in place: params is the padded flat space, this rank's slice is

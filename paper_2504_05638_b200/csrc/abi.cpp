@@ -449,6 +449,21 @@ int tagc_apply_optimizer(tagc_ctx* ctx, int32_t kind, double lr, double weight_d
   return guarded([&] { eng(ctx).apply_optimizer(kind, lr, weight_decay, world, step, params, decoded, adam_v, len); });
 }
 
+int tagc_reduce_shards_step(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad,
+                            float* acc, float* out, int32_t kind, double lr, double weight_decay, uint32_t step,
+                            float* params, float* adam_v, tagc_peel_stats* stats) {
+  return guarded([&] {
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    PeelStats st;
+    eng(ctx).reduce_shards_step(v, grad, acc, out, kind, lr, weight_decay, step, params, adam_v,
+                                stats ? &st : nullptr);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
 int tagc_allgather_params(tagc_ctx* ctx, float* params, uint64_t padded) {
   return guarded([&] { eng(ctx).allgather_params(params, padded); });
 }

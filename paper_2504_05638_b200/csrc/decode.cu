@@ -839,7 +839,8 @@ __device__ __forceinline__ uint32_t emit_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(256) k_emit(DecodeWork w) {
+template <bool kOpt>
+__global__ void __launch_bounds__(256) k_emit(DecodeWork w, OptEpilogue opt) {
   extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk]
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
@@ -880,7 +881,9 @@ __global__ void __launch_bounds__(256) k_emit(DecodeWork w) {
         }
         float* dst = e.out + c0;
         const uint32_t bytes = (clen * 4u) & ~15u;
-        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
+        if (kOpt) {  // owner-side optimizer step on the chunk (no bulk store)
+          for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) opt_apply(opt, dst + q, buf[q]);
+        } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if (threadIdx.x == 0) {
@@ -1048,15 +1051,16 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   return launches + 2;
 }
 
-int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream) {
+int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream, const OptEpilogue* opt) {
   if (w.n_items == 0) return 0;
   const uint64_t g = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute((const void*)k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
-    attr = true;
+  if (opt && opt->kind >= 0) {
+    cudaFuncSetAttribute((const void*)k_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
+    k_emit<true><<<int(g), 256, kEmitSmem, stream>>>(w, *opt);
+  } else {
+    cudaFuncSetAttribute((const void*)k_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
+    k_emit<false><<<int(g), 256, kEmitSmem, stream>>>(w, OptEpilogue{-1});
   }
-  k_emit<<<int(g), 256, kEmitSmem, stream>>>(w);
   return 1;
 }
 

@@ -89,8 +89,18 @@ struct DecStats {  // per decode item, device
   uint32_t presence, unresolved, overflow, pad;
 };
 
-// -------------------------------------------------------------- device hash
+// Owner-side optimizer epilogue parameters (see opt_step below).
+struct OptEpilogue {
+  int32_t kind;       // -1: none, 0: sgd, 1: adamw_nm
+  int32_t write_out;  // also store the decoded value (else out_base aliases params, never written)
+  const float* out_base;
+  float* params;
+  float* adam_v;
+  float inv_w, lr, wd, bias_fix;
+};
+
 #ifdef __CUDACC__
+// -------------------------------------------------------------- device hash
 __device__ __forceinline__ uint32_t dev_bucket(const RowCoef& c, uint32_t p, uint32_t m) {
   const uint64_t h = c.pos_a * (uint64_t(p) + 0x9E3779B9ull) + c.pos_b;  // hash.hpp:36
   return uint32_t(h >> 32) % m;                                            // hash.hpp:37
@@ -121,6 +131,34 @@ __device__ __forceinline__ void red_or_u32(uint32_t* p, uint32_t v) {
   asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.or.b32 [ga], %1;\n}" ::"l"(p), "r"(v)
                : "memory");
 }
+// Owner-side optimizer step (reference train.cpp:355-359, apply_optimizer
+// :202-220) as an epilogue of whatever kernel produces a decoded value:
+// g = decoded * (1/W), then SGD or momentum-free AdamW on params[i], with
+// explicitly rounded operations in the reference's order (no FMA contraction)
+// so the update is bit-identical to its fp32 loop. Element i of the owner's
+// decoded output `out_base` maps to params[i] / adam_v[i].
+template <bool kAdam>
+__device__ __forceinline__ void opt_step(const OptEpilogue& o, uint64_t i, float decoded) {
+  constexpr float kB2 = 0.999f, kOneMinusB2 = 1.0f - 0.999f, kEps = 1e-8f;
+  const float g = __fmul_rn(decoded, o.inv_w);
+  const float p = o.params[i];
+  if (!kAdam) {
+    o.params[i] = __fsub_rn(p, __fmul_rn(o.lr, g));
+  } else {
+    const float v = __fadd_rn(__fmul_rn(kB2, o.adam_v[i]), __fmul_rn(__fmul_rn(kOneMinusB2, g), g));
+    o.adam_v[i] = v;
+    const float vhat = __fdiv_rn(v, o.bias_fix);
+    const float upd = __fadd_rn(__fdiv_rn(g, __fadd_rn(__fsqrt_rn(vhat), kEps)), __fmul_rn(o.wd, p));
+    o.params[i] = __fsub_rn(p, __fmul_rn(o.lr, upd));
+  }
+}
+__device__ __forceinline__ void opt_apply(const OptEpilogue& o, float* dst, float decoded) {
+  if (o.write_out) *dst = decoded;
+  const uint64_t i = uint64_t(dst - o.out_base);
+  if (o.kind == 0) opt_step<false>(o, i, decoded);
+  else opt_step<true>(o, i, decoded);
+}
+
 // Device-side execution spans (timing mode): span[0] = earliest CTA start,
 // span[1] = latest CTA end of a kernel chain, in %globaltimer ns. Independent
 // of where the driver stamps stream events.

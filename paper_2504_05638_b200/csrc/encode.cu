@@ -1269,35 +1269,20 @@ __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b,
     out[i] = a[i] + b[i];
 }
 
-// Owner-side consumer of the decoded shard (reference train.cpp:355-359 and
-// apply_optimizer, train.cpp:202-220): g = decoded * (1/W), then SGD or the
-// momentum-free AdamW. Explicitly rounded operations (no FMA contraction) in
-// the reference's order, so the update is bit-identical to its fp32 loop.
+// Owner-side consumer of the decoded shard as a standalone pass (the fused
+// form is the OptEpilogue of k_emit / k_copy_items): params / adam_v updated
+// from decoded (read only).
 template <bool kAdam>
-__global__ void __launch_bounds__(256) k_apply_optimizer(float* __restrict__ params,
-                                                         const float* __restrict__ decoded,
-                                                         float* __restrict__ adam_v, uint64_t n, float inv_w,
-                                                         float lr, float wd, float bias_fix) {
-  constexpr float kB2 = 0.999f, kOneMinusB2 = 1.0f - 0.999f, kEps = 1e-8f;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const float g = __fmul_rn(decoded[i], inv_w);
-    const float p = params[i];
-    if (!kAdam) {
-      params[i] = __fsub_rn(p, __fmul_rn(lr, g));
-    } else {
-      const float v = __fadd_rn(__fmul_rn(kB2, adam_v[i]), __fmul_rn(__fmul_rn(kOneMinusB2, g), g));
-      adam_v[i] = v;
-      const float vhat = __fdiv_rn(v, bias_fix);
-      const float upd = __fadd_rn(__fdiv_rn(g, __fadd_rn(__fsqrt_rn(vhat), kEps)), __fmul_rn(wd, p));
-      params[i] = __fsub_rn(p, __fmul_rn(lr, upd));
-    }
-  }
+__global__ void __launch_bounds__(256) k_apply_optimizer(OptEpilogue o, uint64_t n) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    opt_step<kAdam>(o, i, __ldcs(o.out_base + i));
 }
 
 // Raw-segment pack/unpack: flat 4096-element tiles over all items, 16-byte
 // accesses when source and destination are both aligned.
+template <bool kOpt>
 __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__ items,
-                                                    uint32_t n_items, uint64_t total_tiles) {
+                                                    uint32_t n_items, uint64_t total_tiles, OptEpilogue opt) {
   for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     uint32_t lo = 0, hi = n_items - 1;
     while (lo < hi) {
@@ -1317,6 +1302,10 @@ __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__
       } else {
         for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) it.dst[i] = 0.0f;
       }
+      continue;
+    }
+    if (kOpt) {  // owner's raw segment: the optimizer step on the summed value
+      for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) opt_apply(opt, it.dst + i, __ldcs(it.src + i));
       continue;
     }
     const bool vec = ((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15u) == 0;
@@ -1531,11 +1520,10 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
   return 1;
 }
 
-int launch_apply_optimizer(int kind, float* params, const float* decoded, float* adam_v, uint64_t n,
-                           float inv_w, float lr, float wd, float bias_fix, cudaStream_t stream) {
+int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream) {
   if (!n) return 0;
-  if (kind == 0) k_apply_optimizer<false><<<flat_grid(n, 256), 256, 0, stream>>>(params, decoded, adam_v, n, inv_w, lr, wd, bias_fix);
-  else k_apply_optimizer<true><<<flat_grid(n, 256), 256, 0, stream>>>(params, decoded, adam_v, n, inv_w, lr, wd, bias_fix);
+  if (o.kind == 0) k_apply_optimizer<false><<<flat_grid(n, 256), 256, 0, stream>>>(o, n);
+  else k_apply_optimizer<true><<<flat_grid(n, 256), 256, 0, stream>>>(o, n);
   return 1;
 }
 
@@ -1555,13 +1543,14 @@ uint64_t copy_tiles(CopyItem* items, uint32_t n_items) {
 }
 
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream, bool one_tile_per_cta) {
+                      cudaStream_t stream, bool one_tile_per_cta, const OptEpilogue* opt) {
   if (!n_items || !total_tiles) return 0;
   // one tile per CTA: short CTAs that a higher-priority stream's kernels can
   // interleave with as SMs free up (side-stream copies)
   const uint64_t g = one_tile_per_cta ? std::min<uint64_t>(total_tiles, 0x7FFFFFFFull)
                                       : std::min<uint64_t>(total_tiles, uint64_t(di.sms) * 8);
-  k_copy_items<<<int(g), 256, 0, stream>>>(items, n_items, total_tiles);
+  if (opt && opt->kind >= 0) k_copy_items<true><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, *opt);
+  else k_copy_items<false><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, OptEpilogue{-1});
   return 1;
 }
 

@@ -516,7 +516,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     launches_ += launch_decode(di_, w, hp, stream_);
   }
   if (zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait side stream");
-  launches_ += launch_decode_emit(di_, w, stream_);
+  launches_ += launch_decode_emit(di_, w, stream_, &opt_);
   cuda_check(cudaGetLastError(), "decode launch");
   if (dbg) {
     unsigned long long t[64];
@@ -721,6 +721,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   static const bool peel_dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   const bool legacy = stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread;
   const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy &&  // default streams cannot be captured
+                        opt_.kind < 0 &&  // the fused optimizer's scalars (bias_fix) change every step
                         !(cfg_.index_width == 1 && world_ > 1);  // the ordered peel loops on the host
   if (!eligible) {
     enqueue_reduce_shards(shards, grad, acc, out, stats);
@@ -884,7 +885,7 @@ void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* g
     upload(side.data(), side.size() * sizeof(CopyItem), d_side);
     cuda_check(cudaEventRecord(aux_fork_, stream_), "fork");
     cuda_check(cudaStreamWaitEvent(aux_, aux_fork_, 0), "fork wait");
-    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true);
+    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true, &opt_);
     cuda_check(cudaEventRecord(aux_join_, aux_), "join");
     zero_done = aux_join_;
   }
@@ -981,7 +982,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
     upload(unpack.data(), unpack.size() * sizeof(CopyItem), d_un);
-    launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_);
+    launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_, false, &opt_);
   }
   ev_record(5);
   cuda_check(cudaGetLastError(), "nccl-world launch");
@@ -1309,15 +1310,44 @@ void Engine::sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_
   run_select_encode(it, true, make_hash_params(seed, rows), false, "compress");
 }
 
-void Engine::apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step,
-                             float* params, const float* decoded, float* adam_v, uint64_t n) {
+OptEpilogue Engine::make_opt(int kind, double lr, double weight_decay, uint32_t world, uint32_t step,
+                             float* params, float* adam_v, const float* out_base, bool write_out) const {
   if (kind != 0 && kind != 1) throw InvalidArgument("optimizer must be sgd (0) or adamw_nm (1)");
   if (world == 0) throw InvalidArgument("world size must be at least 1");
+  if (!params) throw InvalidArgument("no parameter buffer");
   if (kind == 1 && (step == 0 || !adam_v)) throw InvalidArgument("adamw_nm needs step >= 1 and its state");
-  const float b2 = 0.999f;
-  const float bias_fix = kind == 1 ? 1.0f - std::pow(b2, static_cast<float>(step)) : 1.0f;  // train.cpp:213
-  launches_ = launch_apply_optimizer(kind, params, decoded, adam_v, n, 1.0f / static_cast<float>(world),
-                                     static_cast<float>(lr), static_cast<float>(weight_decay), bias_fix, stream_);
+  OptEpilogue o{};
+  o.kind = kind;
+  o.write_out = write_out ? 1 : 0;
+  o.out_base = out_base;
+  o.params = params;
+  o.adam_v = adam_v;
+  o.inv_w = 1.0f / static_cast<float>(world);  // train.cpp:356
+  o.lr = static_cast<float>(lr);
+  o.wd = static_cast<float>(weight_decay);
+  o.bias_fix = kind == 1 ? 1.0f - std::pow(0.999f, static_cast<float>(step)) : 1.0f;  // train.cpp:213
+  return o;
+}
+
+void Engine::reduce_shards_step(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                                int kind, double lr, double weight_decay, uint32_t step, float* params,
+                                float* adam_v, PeelStats* stats) {
+  // mean over this world (train.cpp:356), fused into the decode's emit and
+  // the owner's raw-segment unpack: the decoded shard is never re-read
+  opt_ = make_opt(kind, lr, weight_decay, world_, step, params, adam_v, out ? out : params, out != nullptr);
+  try {
+    reduce_shards(shards, grad, acc, out ? out : params, stats);
+  } catch (...) {
+    opt_ = OptEpilogue{-1};
+    throw;
+  }
+  opt_ = OptEpilogue{-1};
+}
+
+void Engine::apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step,
+                             float* params, const float* decoded, float* adam_v, uint64_t n) {
+  const OptEpilogue o = make_opt(kind, lr, weight_decay, world, step, params, adam_v, decoded, false);
+  launches_ = launch_apply_optimizer(o, n, stream_);
   cuda_check(cudaGetLastError(), "apply_optimizer launch");
 }
 

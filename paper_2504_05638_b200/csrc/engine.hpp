@@ -158,6 +158,12 @@ class Engine {
   // Owner-side consumer: mean over ranks + optimizer step (train.cpp:202-220, 355-359)
   void apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step, float* params,
                        const float* decoded, float* adam_v, uint64_t n);
+  // reduce_shards followed by the owner-side optimizer step, fused into the
+  // kernels that produce the decoded values. params / adam_v / out (optional)
+  // are laid out like reduce_shards' out (the owned shards, concatenated).
+  void reduce_shards_step(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                          int kind, double lr, double weight_decay, uint32_t step, float* params, float* adam_v,
+                          PeelStats* stats);
   // Parameter all-gather after the owners' updates (train.cpp:364): params is
   // the padded flat space (padded = W * L, train.cpp:242); rank i's slice
   // [i*L, (i+1)*L) goes to every rank, in place.
@@ -186,6 +192,9 @@ class Engine {
     cudaEvent_t zero_done = nullptr;
   };
   ExchangeState xs_;
+  OptEpilogue opt_{-1};  // set for the duration of reduce_shards_step
+  OptEpilogue make_opt(int kind, double lr, double weight_decay, uint32_t world, uint32_t step, float* params,
+                       float* adam_v, const float* out_base, bool write_out) const;
   struct PeerState {
     bool attached = false;
     char* region = nullptr;

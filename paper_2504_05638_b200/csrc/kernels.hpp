@@ -71,8 +71,7 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
                         cudaStream_t stream);
 // Owner-side optimizer step on the decoded shard (train.cpp:202-220, 355-359):
 // kind 0 SGD, 1 momentum-free AdamW (adam_v in/out).
-int launch_apply_optimizer(int kind, float* params, const float* decoded, float* adam_v, uint64_t n,
-                           float inv_w, float lr, float wd, float bias_fix, cudaStream_t stream);
+int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream);
 // out = a + b (sketch_add / apply_accumulator).
 int launch_add(const float* a, const float* b, float* out, uint64_t n, cudaStream_t stream);
 
@@ -88,7 +87,7 @@ constexpr uint32_t kCopyTile = 4096;
 // Assigns tile_begin; returns the total tile count.
 uint64_t copy_tiles(CopyItem* items, uint32_t n_items);
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream, bool one_tile_per_cta = false);
+                      cudaStream_t stream, bool one_tile_per_cta = false, const OptEpilogue* opt = nullptr);
 
 // Raw (uncompressed) segments in a simulated world: dst[i] = sum_r src_r[i]
 // in ascending rank order. srcs: device array [n_items * world].
@@ -143,7 +142,10 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
 // Final step of either decode: writes every item's dense output (zeros, and
 // the decoded value of each listed entry).
-int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream);
+// With opt (kind >= 0) the optimizer step runs on every decoded value
+// instead of (or, with write_out, besides) storing it.
+int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream,
+                       const OptEpilogue* opt = nullptr);
 // FIFO-order peel (see decode.cu): host-driven generations, one sort each.
 // claim: u64 per presence-list entry, zero-initialised once;
 // epoch is advanced per generation and persists across calls.
