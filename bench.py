@@ -244,6 +244,38 @@ def run_b200(args):
     barrier()
     base_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
 
+    # owner-side consumer: exchange + adamw_nm step on the
+    # owned shard, unfused (tagc_reduce_shards then tagc_apply_optimizer,
+    # which re-reads the decoded shard) vs fused (tagc_reduce_shards_step,
+    # the update inside the decode emit / raw unpack, decoded not stored)
+    params = torch.randn(max(owned, 1), device=dev)
+    adam_v = torch.zeros(max(owned, 1), device=dev)
+    opt_steps = max(3, min(args.steps, 10))
+
+    def timed(fn):
+        for i in range(max(3, args.warmup)):  # eager, capture, first replay
+            fn(i + 1)
+        barrier()
+        e0.record(stream)
+        for i in range(opt_steps):
+            fn(i + 2)
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / opt_steps
+
+    def unfused(k):
+        step()
+        ctx.apply_optimizer("adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)
+
+    def fused(k):
+        ctx.tagc_reduce_shards_step(shards, grad, acc, params, "adamw_nm", 1e-3, k, adam_v=adam_v,
+                                    weight_decay=0.01)
+
+    owner_step = {"optimizer": "adamw_nm",
+                  "apply_only_ms": round(timed(lambda k: ctx.apply_optimizer(
+                      "adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)), 4),
+                  "unfused_ms": round(timed(unfused), 4), "fused_ms": round(timed(fused), 4)}
+
     # e2e through the C-ABI host-buffer entry (tagc_reduce_shards_host): every
     # step copies this step's gradient H2D from pinned memory and the owner's
     # decoded shard D2H; consecutive calls overlap their copies with each
@@ -319,6 +351,7 @@ def run_b200(args):
                       "decode": round(stage_ms[4], 4)},
         "uncompressed_rs": {"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
                             "unit": "GB/s", "ms_per_step": round(base_ms, 4)},
+        "owner_step": owner_step,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }

@@ -839,9 +839,11 @@ __device__ __forceinline__ uint32_t emit_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// kOpt (the owner's optimizer step instead of the bulk store): one buffer,
+// 4 CTAs per SM, so more parameter / state loads are in flight.
 template <bool kOpt>
-__global__ void __launch_bounds__(256) k_emit(DecodeWork w, OptEpilogue opt) {
-  extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk]
+__global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const OptEpilogue* __restrict__ opt) {
+  extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk] ([1] with kOpt)
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
   const uint32_t total = w.qcount[5];
@@ -860,8 +862,9 @@ __global__ void __launch_bounds__(256) k_emit(DecodeWork w, OptEpilogue opt) {
       le = le < total ? le : total;
       for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
         const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
-        float* buf = ebuf + (n_chunks & 1u) * kEmitChunk;
-        if (n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
+        float* buf = kOpt ? ebuf : ebuf + (n_chunks & 1u) * kEmitChunk;
+        if (kOpt && n_chunks) __syncthreads();  // every thread is done reading the previous chunk
+        if (!kOpt && n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
           if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncthreads();
         }
@@ -882,7 +885,9 @@ __global__ void __launch_bounds__(256) k_emit(DecodeWork w, OptEpilogue opt) {
         float* dst = e.out + c0;
         const uint32_t bytes = (clen * 4u) & ~15u;
         if (kOpt) {  // owner-side optimizer step on the chunk (no bulk store)
-          for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) opt_apply(opt, dst + q, buf[q]);
+          const OptEpilogue o = *opt;
+          if (o.kind == 1) opt_range<true, false>(o, dst, buf, clen);
+          else opt_range<false, false>(o, dst, buf, clen);
         } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
@@ -1051,15 +1056,15 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   return launches + 2;
 }
 
-int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream, const OptEpilogue* opt) {
+int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream, const OptEpilogue* dev_opt) {
   if (w.n_items == 0) return 0;
   const uint64_t g = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
-  if (opt && opt->kind >= 0) {
-    cudaFuncSetAttribute((const void*)k_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
-    k_emit<true><<<int(g), 256, kEmitSmem, stream>>>(w, *opt);
+  if (dev_opt) {
+    const uint64_t go = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
+    k_emit<true><<<int(go), 256, kEmitSmem / 2, stream>>>(w, dev_opt);
   } else {
     cudaFuncSetAttribute((const void*)k_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem));
-    k_emit<false><<<int(g), 256, kEmitSmem, stream>>>(w, OptEpilogue{-1});
+    k_emit<false><<<int(g), 256, kEmitSmem, stream>>>(w, nullptr);
   }
   return 1;
 }

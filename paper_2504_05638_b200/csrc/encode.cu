@@ -1274,15 +1274,18 @@ __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b,
 // from decoded (read only).
 template <bool kAdam>
 __global__ void __launch_bounds__(256) k_apply_optimizer(OptEpilogue o, uint64_t n) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    opt_step<kAdam>(o, i, __ldcs(o.out_base + i));
+  constexpr uint64_t kChunk = 256 * 8;
+  for (uint64_t c0 = uint64_t(blockIdx.x) * kChunk; c0 < n; c0 += uint64_t(gridDim.x) * kChunk)
+    opt_range<kAdam, true>(o, const_cast<float*>(o.out_base) + c0, o.out_base + c0,
+                           uint32_t(n - c0 < kChunk ? n - c0 : kChunk));
 }
 
 // Raw-segment pack/unpack: flat 4096-element tiles over all items, 16-byte
 // accesses when source and destination are both aligned.
 template <bool kOpt>
 __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__ items,
-                                                    uint32_t n_items, uint64_t total_tiles, OptEpilogue opt) {
+                                                    uint32_t n_items, uint64_t total_tiles,
+                                                    const OptEpilogue* __restrict__ opt) {
   for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     uint32_t lo = 0, hi = n_items - 1;
     while (lo < hi) {
@@ -1305,7 +1308,9 @@ __global__ void __launch_bounds__(256) k_copy_items(const CopyItem* __restrict__
       continue;
     }
     if (kOpt) {  // owner's raw segment: the optimizer step on the summed value
-      for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) opt_apply(opt, it.dst + i, __ldcs(it.src + i));
+      const OptEpilogue o = *opt;
+      if (o.kind == 1) opt_range<true, true>(o, it.dst + b, it.src + b, uint32_t(e - b));
+      else opt_range<false, true>(o, it.dst + b, it.src + b, uint32_t(e - b));
       continue;
     }
     const bool vec = ((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15u) == 0;
@@ -1520,10 +1525,18 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
   return 1;
 }
 
+__global__ void k_set_opt(OptEpilogue* dst, OptEpilogue o) { *dst = o; }
+
+int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream) {
+  k_set_opt<<<1, 1, 0, stream>>>(dev_opt, o);
+  return 1;
+}
+
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream) {
   if (!n) return 0;
-  if (o.kind == 0) k_apply_optimizer<false><<<flat_grid(n, 256), 256, 0, stream>>>(o, n);
-  else k_apply_optimizer<true><<<flat_grid(n, 256), 256, 0, stream>>>(o, n);
+  const int g = int(std::min<uint64_t>((n + 2047) / 2048, 148ull * 16));
+  if (o.kind == 0) k_apply_optimizer<false><<<g, 256, 0, stream>>>(o, n);
+  else k_apply_optimizer<true><<<g, 256, 0, stream>>>(o, n);
   return 1;
 }
 
@@ -1543,14 +1556,14 @@ uint64_t copy_tiles(CopyItem* items, uint32_t n_items) {
 }
 
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream, bool one_tile_per_cta, const OptEpilogue* opt) {
+                      cudaStream_t stream, bool one_tile_per_cta, const OptEpilogue* dev_opt) {
   if (!n_items || !total_tiles) return 0;
   // one tile per CTA: short CTAs that a higher-priority stream's kernels can
   // interleave with as SMs free up (side-stream copies)
   const uint64_t g = one_tile_per_cta ? std::min<uint64_t>(total_tiles, 0x7FFFFFFFull)
                                       : std::min<uint64_t>(total_tiles, uint64_t(di.sms) * 8);
-  if (opt && opt->kind >= 0) k_copy_items<true><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, *opt);
-  else k_copy_items<false><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, OptEpilogue{-1});
+  if (dev_opt) k_copy_items<true><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, dev_opt);
+  else k_copy_items<false><<<int(g), 256, 0, stream>>>(items, n_items, total_tiles, nullptr);
   return 1;
 }
 

@@ -178,6 +178,7 @@ Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   drop_graphs();
   peer_release();
+  if (opt_dev_) cudaFree(opt_dev_);
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& e : ev_)
@@ -516,7 +517,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     launches_ += launch_decode(di_, w, hp, stream_);
   }
   if (zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait side stream");
-  launches_ += launch_decode_emit(di_, w, stream_, &opt_);
+  launches_ += launch_decode_emit(di_, w, stream_, opt_on_ ? opt_dev_ : nullptr);
   cuda_check(cudaGetLastError(), "decode launch");
   if (dbg) {
     unsigned long long t[64];
@@ -721,7 +722,6 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   static const bool peel_dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   const bool legacy = stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread;
   const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy &&  // default streams cannot be captured
-                        opt_.kind < 0 &&  // the fused optimizer's scalars (bias_fix) change every step
                         !(cfg_.index_width == 1 && world_ > 1);  // the ordered peel loops on the host
   if (!eligible) {
     enqueue_reduce_shards(shards, grad, acc, out, stats);
@@ -731,8 +731,8 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   std::string key;
   {
     char buf[160];
-    std::snprintf(buf, sizeof(buf), "%p|%p|%p|%p|%d|%.17g|%u|%u|%d|%d|%llu|%u|%llu|", (void*)grad, (void*)acc,
-                  (void*)out, (void*)grad_read_ev_, peer_.attached ? peer_.set : -1, cfg_.theta, cfg_.ratio, cfg_.index_width, int(cfg_.policy),
+    std::snprintf(buf, sizeof(buf), "%p|%p|%p|%p|%d|%d|%.17g|%u|%u|%d|%d|%llu|%u|%llu|", (void*)grad, (void*)acc,
+                  (void*)out, (void*)grad_read_ev_, int(opt_on_), peer_.attached ? peer_.set : -1, cfg_.theta, cfg_.ratio, cfg_.index_width, int(cfg_.policy),
                   int(cfg_.include_out_proj), (unsigned long long)cfg_.seed, cfg_.sketch_rows,
                   (unsigned long long)cfg_.min_compress_segment);
     key = buf;
@@ -794,6 +794,8 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     cudaGetLastError();
     ok = false;
   }
+  // upload now, so the first replay does not pay for it
+  if (ok && cudaGraphUpload(g.exec, stream_) != cudaSuccess) cudaGetLastError();
   if (graph) cudaGraphDestroy(graph);
   if (!ok) {  // could not capture (e.g. a buffer had to grow): stay eager for this key
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -885,7 +887,7 @@ void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* g
     upload(side.data(), side.size() * sizeof(CopyItem), d_side);
     cuda_check(cudaEventRecord(aux_fork_, stream_), "fork");
     cuda_check(cudaStreamWaitEvent(aux_, aux_fork_, 0), "fork wait");
-    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true, &opt_);
+    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true, opt_on_ ? opt_dev_ : nullptr);
     cuda_check(cudaEventRecord(aux_join_, aux_), "join");
     zero_done = aux_join_;
   }
@@ -982,7 +984,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
     upload(unpack.data(), unpack.size() * sizeof(CopyItem), d_un);
-    launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_, false, &opt_);
+    launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_, false, opt_on_ ? opt_dev_ : nullptr);
   }
   ev_record(5);
   cuda_check(cudaGetLastError(), "nccl-world launch");
@@ -1316,6 +1318,9 @@ OptEpilogue Engine::make_opt(int kind, double lr, double weight_decay, uint32_t 
   if (world == 0) throw InvalidArgument("world size must be at least 1");
   if (!params) throw InvalidArgument("no parameter buffer");
   if (kind == 1 && (step == 0 || !adam_v)) throw InvalidArgument("adamw_nm needs step >= 1 and its state");
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  if (!a16(params) || (kind == 1 && !a16(adam_v)) || !a16(out_base))
+    throw InvalidArgument("optimizer buffers (params, adam_v, decoded/out) must be 16-byte aligned");
   OptEpilogue o{};
   o.kind = kind;
   o.write_out = write_out ? 1 : 0;
@@ -1333,15 +1338,21 @@ void Engine::reduce_shards_step(const std::vector<ShardSpec>& shards, const floa
                                 int kind, double lr, double weight_decay, uint32_t step, float* params,
                                 float* adam_v, PeelStats* stats) {
   // mean over this world (train.cpp:356), fused into the decode's emit and
-  // the owner's raw-segment unpack: the decoded shard is never re-read
-  opt_ = make_opt(kind, lr, weight_decay, world_, step, params, adam_v, out ? out : params, out != nullptr);
+  // the owner's raw-segment unpack: the decoded shard is never re-read. The
+  // step's scalars go to a device slot ahead of the (possibly replayed)
+  // exchange, so a captured graph serves every step.
+  const OptEpilogue o = make_opt(kind, lr, weight_decay, world_, step, params, adam_v, out ? out : params,
+                                 out != nullptr);
+  if (!opt_dev_) cuda_check(cudaMalloc(&opt_dev_, sizeof(OptEpilogue)), "cudaMalloc optimizer slot");
+  launch_set_opt(opt_dev_, o, stream_);
+  opt_on_ = true;
   try {
     reduce_shards(shards, grad, acc, out ? out : params, stats);
   } catch (...) {
-    opt_ = OptEpilogue{-1};
+    opt_on_ = false;
     throw;
   }
-  opt_ = OptEpilogue{-1};
+  opt_on_ = false;
 }
 
 void Engine::apply_optimizer(int kind, double lr, double weight_decay, uint32_t world, uint32_t step,

@@ -192,7 +192,8 @@ class Engine {
     cudaEvent_t zero_done = nullptr;
   };
   ExchangeState xs_;
-  OptEpilogue opt_{-1};  // set for the duration of reduce_shards_step
+  OptEpilogue* opt_dev_ = nullptr;  // device slot of the fused optimizer's scalars
+  bool opt_on_ = false;             // set for the duration of reduce_shards_step
   OptEpilogue make_opt(int kind, double lr, double weight_decay, uint32_t world, uint32_t step, float* params,
                        float* adam_v, const float* out_base, bool write_out) const;
   struct PeerState {

@@ -87,7 +87,8 @@ constexpr uint32_t kCopyTile = 4096;
 // Assigns tile_begin; returns the total tile count.
 uint64_t copy_tiles(CopyItem* items, uint32_t n_items);
 int launch_copy_items(const DevInfo& di, const CopyItem* items, uint32_t n_items, uint64_t total_tiles,
-                      cudaStream_t stream, bool one_tile_per_cta = false, const OptEpilogue* opt = nullptr);
+                      cudaStream_t stream, bool one_tile_per_cta = false,
+                      const OptEpilogue* dev_opt = nullptr);
 
 // Raw (uncompressed) segments in a simulated world: dst[i] = sum_r src_r[i]
 // in ascending rank order. srcs: device array [n_items * world].
@@ -142,10 +143,14 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
 // Final step of either decode: writes every item's dense output (zeros, and
 // the decoded value of each listed entry).
-// With opt (kind >= 0) the optimizer step runs on every decoded value
-// instead of (or, with write_out, besides) storing it.
+// With dev_opt (a device-resident OptEpilogue, read when the kernel runs, so
+// a captured graph picks up each step's scalars) the optimizer step runs on
+// every decoded value instead of (or, with write_out, besides) storing it.
 int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream,
-                       const OptEpilogue* opt = nullptr);
+                       const OptEpilogue* dev_opt = nullptr);
+// Writes the step's OptEpilogue into its device slot (stream-ordered before
+// the kernels that read it; launched outside any graph).
+int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream);
 // FIFO-order peel (see decode.cu): host-driven generations, one sort each.
 // claim: u64 per presence-list entry, zero-initialised once;
 // epoch is advanced per generation and persists across calls.

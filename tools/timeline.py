@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--host", action="store_true", help="profile the host-buffer entry (e2e path)")
     ap.add_argument("--own-stream", action="store_true", help="context-owned stream instead of torch's")
     ap.add_argument("--graph", type=int, default=-1, help="force graph mode 0/1 (-1: library default)")
+    ap.add_argument("--opt", default="", choices=["", "fused", "unfused"],
+                    help="add the owner's adamw_nm step (fused: tagc_reduce_shards_step)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -43,8 +45,20 @@ def main():
     del mag, sign
     acc = torch.zeros(total, device=dev)
     out = torch.empty(total, device=dev)
-    for _ in range(5):
+    params, adam_v = torch.randn(total, device=dev), torch.zeros(total, device=dev)
+    k = [0]
+
+    def step():
+        k[0] += 1
+        if args.opt == "fused":
+            ctx.tagc_reduce_shards_step(shards, grad, acc, params, "adamw_nm", 1e-3, k[0], adam_v=adam_v)
+            return
         ctx.tagc_reduce_shards(shards, grad, acc, out, stats=False)
+        if args.opt == "unfused":
+            ctx.apply_optimizer("adamw_nm", 1e-3, params, out, 1, k[0], adam_v)
+
+    for _ in range(5):
+        step()
     torch.cuda.synchronize()
     if args.host:
         hg = grad.cpu().pin_memory()
@@ -57,7 +71,7 @@ def main():
             if args.host:
                 ctx.tagc_reduce_shards_host(shards, hg, acc, ho)
             else:
-                ctx.tagc_reduce_shards(shards, grad, acc, out, stats=False)
+                step()
         ctx.sync()
         torch.cuda.synchronize()
     ctx.set_timing(True)
