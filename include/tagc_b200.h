@@ -172,6 +172,35 @@ int tagc_ctx_init_nccl(tagc_ctx* ctx, const uint8_t unique_id[128]);
 /* Traffic ledger as CSV in the reference's format (collectives.cpp:70-78). */
 int tagc_ctx_ledger_csv(tagc_ctx* ctx, char* buf, size_t len, size_t* needed);
 int tagc_ctx_ledger_reset(tagc_ctx* ctx);
+
+/* ------------------------------------------------- traffic ledger (§8f row 3)
+ * tagc::TrafficLedger (collectives.hpp:60-81, collectives.cpp:37-93): the
+ * declared cost model, All-Reduce charged 2x, others 1x. A context records
+ * into its own ledger (tagc_ctx_ledger, borrowed, valid while the context
+ * lives) at every exchange with the reference's tags; a standalone ledger is
+ * host-only. op: 0 all_reduce, 1 reduce, 2 reduce_scatter, 3 all_gather.
+ * _csv / _json write the reference's to_csv / to_json().dump() text (NUL
+ * terminated, truncated to len; *needed = full size + 1). */
+typedef struct tagc_ledger tagc_ledger;
+tagc_ledger* tagc_ledger_create(void);
+void tagc_ledger_destroy(tagc_ledger* l);
+int tagc_ledger_record(tagc_ledger* l, int32_t op, const char* tag, uint64_t payload_bits, uint64_t params);
+int tagc_ledger_csv(tagc_ledger* l, char* buf, size_t len, size_t* needed);
+int tagc_ledger_json(tagc_ledger* l, char* buf, size_t len, size_t* needed);
+/* bits_per_param_per_rank over the rows whose tag starts with prefix
+ * (collectives.cpp:60-68); prefix NULL or "" = all rows. */
+int tagc_ledger_bits_per_param(tagc_ledger* l, const char* prefix, double* out);
+int tagc_ledger_clear(tagc_ledger* l);
+tagc_ledger* tagc_ctx_ledger(tagc_ctx* ctx);
+/* Bytes this context actually handed to the transport (NCCL or peer pulls)
+ * since creation: measured, beside the ledger's modelled bits. */
+int tagc_ctx_wire_bytes(tagc_ctx* ctx, uint64_t* out);
+/* Index::to_bytes / CountSketch::to_bytes (index.cpp:59-69, sketch.cpp:77-89):
+ * the wire format is the little-endian u32 / f32 word layout the device
+ * buffers already hold (index words, sketch rows, and the send / receive
+ * blocks of tagc_plan_exchange), so this is a stream-ordered copy of n_words
+ * words to host_out (4 * n_words bytes). */
+int tagc_wire_bytes_from_device(tagc_ctx* ctx, const void* dev, uint64_t n_words, uint8_t* host_out);
 /* Device bytes the context currently holds in workspaces. */
 uint64_t tagc_ctx_workspace_bytes(const tagc_ctx* ctx);
 /* Optional per-stage device timing of the last fused call (ms): prep

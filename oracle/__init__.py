@@ -450,6 +450,37 @@ class Ref:
                                            _p(out, C.c_uint32), C.byref(cnt)), "ref_presence")
         return out[: cnt.value].copy()
 
+    def ledger_dump(self, records, prefix=""):
+        """records: [(op, tag, payload_bits, params)] -> (csv, json, bits_per_param(prefix))."""
+        n = len(records)
+        ops = (C.c_int32 * max(1, n))(*[r[0] for r in records])
+        tags = (C.c_char_p * max(1, n))(*[r[1].encode() for r in records])
+        bits = (C.c_uint64 * max(1, n))(*[r[2] for r in records])
+        params = (C.c_uint64 * max(1, n))(*[r[3] for r in records])
+        csv = C.create_string_buffer(1 << 16)
+        js = C.create_string_buffer(1 << 16)
+        bpp = C.c_double()
+        _check(self.lib.ref_ledger_dump(ops, tags, bits, params, C.c_uint32(n), prefix.encode(), csv,
+                                        C.c_size_t(len(csv)), js, C.c_size_t(len(js)), C.byref(bpp)),
+               "ref_ledger_dump")
+        return csv.value.decode(), js.value.decode(), bpp.value
+
+    def index_to_bytes(self, values, width):
+        v = _f32(values)
+        out = (C.c_uint8 * max(1, 4 * ((v.size * width + 31) // 32)))()
+        _check(self.lib.ref_index_to_bytes(_p(v, C.c_float), C.c_uint32(v.size), C.c_uint32(width), out),
+               "ref_index_to_bytes")
+        return bytes(out)[:4 * ((v.size * width + 31) // 32)]
+
+    def sketch_to_bytes(self, values, ratio, seed, rows=3):
+        v = _f32(values)
+        m = v.size // (ratio * rows)
+        out = (C.c_uint8 * max(1, 4 * rows * m))()
+        _check(self.lib.ref_sketch_to_bytes(_p(v, C.c_float), C.c_uint32(v.size), C.c_uint32(ratio),
+                                            C.c_uint32(rows), C.c_uint64(seed & (2**64 - 1)), out),
+               "ref_sketch_to_bytes")
+        return bytes(out)[:4 * rows * m]
+
     def scale_sub_inplace(self, dst, src, scale):
         """kernels::scale_sub_inplace (kernels.cpp:32-41), dst updated in place."""
         _check(self.lib.ref_scale_sub_inplace(_p(dst, C.c_float), _p(_f32(src), C.c_float), C.c_size_t(dst.size),

@@ -162,6 +162,37 @@ int ref_sketch_compress(const float* v, uint32_t n, uint32_t ratio, uint32_t row
   });
 }
 
+// TrafficLedger::to_csv / to_json().dump() (collectives.cpp:70-93) of a
+// ledger fed the given records; also bits_per_param_per_rank(prefix).
+int ref_ledger_dump(const int32_t* ops, const char* const* tags, const uint64_t* bits, const uint64_t* params,
+                    uint32_t n, const char* prefix, char* csv, size_t csv_len, char* json, size_t json_len,
+                    double* bpp) {
+  return guarded([&] {
+    TrafficLedger l;
+    for (uint32_t i = 0; i < n; ++i) l.record(static_cast<CollectiveOp>(ops[i]), tags[i], bits[i], params[i]);
+    std::ostringstream os;
+    l.to_csv(os);
+    copy_str(os.str(), csv, csv_len);
+    copy_str(l.to_json().dump(), json, json_len);
+    *bpp = l.bits_per_param_per_rank(prefix);
+  });
+}
+
+// Index::to_bytes / CountSketch::to_bytes (index.cpp:59-69, sketch.cpp:77-89).
+int ref_index_to_bytes(const float* v, uint32_t n, uint32_t w, uint8_t* out) {
+  return guarded([&] {
+    const std::vector<uint8_t> b = Index::create(std::span<const float>(v, n), w).to_bytes();
+    std::memcpy(out, b.data(), b.size());
+  });
+}
+int ref_sketch_to_bytes(const float* v, uint32_t n, uint32_t ratio, uint32_t rows, uint64_t seed, uint8_t* out) {
+  return guarded([&] {
+    const std::vector<uint8_t> b =
+        CountSketch::compress(std::span<const float>(v, n), sketch_geometry(n, ratio, rows), seed).to_bytes();
+    std::memcpy(out, b.data(), b.size());
+  });
+}
+
 // The SGD step of the owner-side consumer (train.cpp:205-207).
 int ref_scale_sub_inplace(float* dst, const float* src, size_t n, float scale) {
   return guarded([&] {

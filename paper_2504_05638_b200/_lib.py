@@ -112,6 +112,16 @@ SIGNATURES = {
     "tagc_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "tagc_ctx_init_nccl": (C.c_int, [VP, C.POINTER(C.c_uint8)]),
     "tagc_ctx_ledger_csv": (C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "tagc_ledger_create": (VP, []),
+    "tagc_ledger_destroy": (None, [VP]),
+    "tagc_ledger_record": (C.c_int, [VP, C.c_int32, C.c_char_p, U64, U64]),
+    "tagc_ledger_csv": (C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "tagc_ledger_json": (C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "tagc_ledger_bits_per_param": (C.c_int, [VP, C.c_char_p, C.POINTER(C.c_double)]),
+    "tagc_ledger_clear": (C.c_int, [VP]),
+    "tagc_ctx_ledger": (VP, [VP]),
+    "tagc_ctx_wire_bytes": (C.c_int, [VP, C.POINTER(U64)]),
+    "tagc_wire_bytes_from_device": (C.c_int, [VP, VP, U64, VP]),
     "tagc_ctx_ledger_reset": (C.c_int, [VP]),
     "tagc_ctx_workspace_bytes": (U64, [VP]),
     "tagc_ctx_set_timing": (C.c_int, [VP, C.c_int]),

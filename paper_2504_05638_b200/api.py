@@ -34,7 +34,7 @@ __all__ = [
     "CompressionConfig", "LayerSpec", "LayerSegment", "ShardSpec", "PeelStats", "Context",
     "make_shards", "kind_compressible", "sketch_geometry", "words_needed", "theta_floor",
     "comm_volume_model", "lhc_comm_volume_model", "TagcError", "TagcInvalidArgument",
-    "device_count", "plan_exchange",
+    "device_count", "plan_exchange", "TrafficLedger",
 ]
 
 
@@ -224,6 +224,54 @@ def _ptr_array(ts):
     return (C.c_void_p * len(ts))(*[_ptr(t) for t in ts])
 
 
+def _text(fn, *args) -> str:
+    need = C.c_size_t()
+    check(fn(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(fn(*args, buf, len(buf), None))
+    return buf.value.decode()
+
+
+class TrafficLedger:
+    """tagc::TrafficLedger (collectives.hpp:60-81): record(op, tag, payload_bits,
+    params), to_csv(), to_json() (the reference's dump() text),
+    bits_per_param_per_rank(prefix). Context.ledger() returns the context's
+    own ledger (borrowed: valid while the context lives)."""
+
+    OPS = {"all_reduce": 0, "reduce": 1, "reduce_scatter": 2, "all_gather": 3}
+
+    def __init__(self, _handle=None, _owner=None):
+        self._own = _handle is None
+        self.h = lib.tagc_ledger_create() if _handle is None else _handle
+        self._owner = _owner  # keeps a borrowing context alive
+        if not self.h:
+            raise TagcError(1, "tagc_ledger_create failed")
+
+    def __del__(self):
+        if getattr(self, "_own", False) and self.h:
+            lib.tagc_ledger_destroy(self.h)
+            self.h = None
+
+    def record(self, op: str, tag: str, payload_bits: int, params: int):
+        if op not in self.OPS:
+            raise TagcInvalidArgument(2, f"unknown collective op: {op}")
+        check(lib.tagc_ledger_record(self.h, self.OPS[op], tag.encode(), int(payload_bits), int(params)))
+
+    def to_csv(self) -> str:
+        return _text(lib.tagc_ledger_csv, self.h)
+
+    def to_json(self) -> str:
+        return _text(lib.tagc_ledger_json, self.h)
+
+    def bits_per_param_per_rank(self, prefix: str = "") -> float:
+        out = C.c_double()
+        check(lib.tagc_ledger_bits_per_param(self.h, prefix.encode(), C.byref(out)))
+        return out.value
+
+    def clear(self):
+        check(lib.tagc_ledger_clear(self.h))
+
+
 class Context:
     """Owns a tagc_ctx (one CUDA stream, workspaces, ledger, optional NCCL comm).
 
@@ -281,6 +329,25 @@ class Context:
         buf = C.create_string_buffer(need.value)
         check(lib.tagc_ctx_ledger_csv(self.h, buf, len(buf), None))
         return buf.value.decode()
+
+    def ledger(self) -> TrafficLedger:
+        return TrafficLedger(_handle=lib.tagc_ctx_ledger(self.h), _owner=self)
+
+    def ledger_json(self) -> str:
+        return self.ledger().to_json()
+
+    def wire_bytes(self) -> int:
+        out = C.c_uint64()
+        check(lib.tagc_ctx_wire_bytes(self.h, C.byref(out)), "wire_bytes")
+        return out.value
+
+    def to_bytes(self, words) -> bytes:
+        """Index::to_bytes / CountSketch::to_bytes of a device u32 / f32 buffer
+        (index.cpp:59-69, sketch.cpp:77-89): its little-endian word layout."""
+        n = words.numel()
+        buf = (C.c_uint8 * max(1, 4 * n))()
+        check(lib.tagc_wire_bytes_from_device(self.h, _ptr(words), n, buf), "to_bytes")
+        return bytes(buf)[:4 * n]
 
     def ledger_reset(self):
         check(lib.tagc_ctx_ledger_reset(self.h))

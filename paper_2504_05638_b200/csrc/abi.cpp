@@ -235,6 +235,82 @@ int tagc_ctx_ledger_csv(tagc_ctx* ctx, char* buf, size_t len, size_t* needed) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+int copy_out(const std::string& s, char* buf, size_t len, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && len) {
+    const size_t k = std::min(len - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return 0;
+}
+TrafficLedger& led(tagc_ledger* l) {
+  if (!l) throw InvalidArgument("null ledger");
+  return *reinterpret_cast<TrafficLedger*>(l);
+}
+}  // namespace
+
+extern "C" {
+
+tagc_ledger* tagc_ledger_create(void) {
+  try {
+    return reinterpret_cast<tagc_ledger*>(new TrafficLedger());
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void tagc_ledger_destroy(tagc_ledger* l) { delete reinterpret_cast<TrafficLedger*>(l); }
+
+int tagc_ledger_record(tagc_ledger* l, int32_t op, const char* tag, uint64_t payload_bits, uint64_t params) {
+  return guarded([&] {
+    if (op < 0 || op > 3) throw InvalidArgument("unknown collective op");
+    led(l).record(static_cast<CollectiveOp>(op), tag ? tag : "", payload_bits, params);
+  });
+}
+
+int tagc_ledger_csv(tagc_ledger* l, char* buf, size_t len, size_t* needed) {
+  return guarded([&] { copy_out(led(l).to_csv(), buf, len, needed); });
+}
+
+int tagc_ledger_json(tagc_ledger* l, char* buf, size_t len, size_t* needed) {
+  return guarded([&] { copy_out(led(l).to_json(), buf, len, needed); });
+}
+
+int tagc_ledger_bits_per_param(tagc_ledger* l, const char* prefix, double* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("null output");
+    *out = led(l).bits_per_param_per_rank(prefix ? prefix : "");
+  });
+}
+
+int tagc_ledger_clear(tagc_ledger* l) {
+  return guarded([&] { led(l).clear(); });
+}
+
+tagc_ledger* tagc_ctx_ledger(tagc_ctx* ctx) {
+  if (!ctx || !ctx->engine) return nullptr;
+  return reinterpret_cast<tagc_ledger*>(&ctx->engine->ledger());
+}
+
+int tagc_ctx_wire_bytes(tagc_ctx* ctx, uint64_t* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("null output");
+    *out = eng(ctx).ledger().wire_bytes;
+  });
+}
+
+int tagc_wire_bytes_from_device(tagc_ctx* ctx, const void* dev, uint64_t n_words, uint8_t* host_out) {
+  return guarded([&] {
+    static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "the wire format is the little-endian word layout");
+    if (n_words && (!dev || !host_out)) throw InvalidArgument("null buffer");
+    eng(ctx).download(dev, n_words * 4, host_out);
+  });
+}
+
 int tagc_ctx_ledger_reset(tagc_ctx* ctx) {
   return guarded([&] { eng(ctx).ledger().clear(); });
 }

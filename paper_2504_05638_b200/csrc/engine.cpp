@@ -349,6 +349,15 @@ void Engine::fetch_rounds() {
   rounds_[1] = last_ordered_ ? 0 : q[3];
 }
 
+// Index::to_bytes / CountSketch::to_bytes (index.cpp:59-69, sketch.cpp:77-89)
+// are the little-endian word layout, i.e. the device buffers as they are:
+// the wire format is a copy, ordered after this context's queued work.
+void Engine::download(const void* dev, uint64_t bytes, void* host) {
+  if (!bytes) return;
+  cuda_check(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream_), "D2H wire bytes");
+  cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+}
+
 void Engine::sync_check() {
   if (h2d_) cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
   if (d2h_) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");

@@ -86,6 +86,7 @@ class Engine {
   uint32_t rank() const { return rank_; }
   cudaStream_t stream() const { return stream_; }
   TrafficLedger& ledger() { return ledger_; }
+  void download(const void* dev, uint64_t bytes, void* host);
   uint64_t workspace_bytes() const { return ws_.bytes(); }
   void init_nccl(const uint8_t id[128]);
   void set_timing(bool on) { timing_ = on; }

@@ -2,7 +2,10 @@
 #include "host.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <sstream>
 
 namespace tagc_b200 {
@@ -239,6 +242,83 @@ std::string TrafficLedger::to_csv() const {
            buf + "\n";
   }
   return out;
+}
+
+namespace {
+
+// A JSON number the way nlohmann::json's serializer writes a double: shortest
+// round-trip digits, then its format_buffer layout (kMinExp = -4, kMaxExp =
+// 15): "2.0", "0.5", "0.0001", "1e-05", "1.5e+20"; non-finite -> null.
+std::string json_double(double x) {
+  if (!std::isfinite(x)) return "null";
+  std::string out;
+  if (std::signbit(x)) {
+    out += '-';
+    x = -x;
+  }
+  if (x == 0.0) return out + "0.0";
+  char sci[64];
+  const auto r = std::to_chars(sci, sci + sizeof(sci), x, std::chars_format::scientific);
+  const std::string s(sci, r.ptr);  // d[.ddd]e[+-]XX
+  const size_t epos = s.find('e');
+  std::string digits = s.substr(0, epos);
+  digits.erase(std::remove(digits.begin(), digits.end(), '.'), digits.end());
+  const int k = int(digits.size());
+  const int n = std::atoi(s.c_str() + epos + 1) + 1;  // value = 0.digits * 10^n
+  constexpr int kMinExp = -4, kMaxExp = 15;
+  if (k <= n && n <= kMaxExp) return out + digits + std::string(size_t(n - k), '0') + ".0";
+  if (0 < n && n <= kMaxExp) return out + digits.substr(0, size_t(n)) + "." + digits.substr(size_t(n));
+  if (kMinExp < n && n <= 0) return out + "0." + std::string(size_t(-n), '0') + digits;
+  out += digits.substr(0, 1);
+  if (k > 1) out += "." + digits.substr(1);
+  int e = n - 1;
+  out += 'e';
+  out += e < 0 ? '-' : '+';
+  e = e < 0 ? -e : e;
+  char eb[8];
+  std::snprintf(eb, sizeof(eb), e < 10 ? "0%d" : "%d", e);
+  return out + eb;
+}
+
+std::string json_string(const std::string& v) {
+  std::string out = "\"";
+  for (unsigned char c : v) {
+    switch (c) {
+      case '"': out += "\\\""; break;
+      case '\\': out += "\\\\"; break;
+      case '\b': out += "\\b"; break;
+      case '\f': out += "\\f"; break;
+      case '\n': out += "\\n"; break;
+      case '\r': out += "\\r"; break;
+      case '\t': out += "\\t"; break;
+      default:
+        if (c < 0x20) {
+          char b[8];
+          std::snprintf(b, sizeof(b), "\\u%04x", c);
+          out += b;
+        } else {
+          out += char(c);
+        }
+    }
+  }
+  return out + "\"";
+}
+
+}  // namespace
+
+// collectives.cpp:80-93
+std::string TrafficLedger::to_json() const {
+  std::string out = "[";
+  bool first = true;
+  for (const auto& [k, row] : rows_) {
+    if (!first) out += ',';
+    first = false;
+    out += "{\"op\":" + json_string(to_string(row.op)) + ",\"tag\":" + json_string(row.tag) +
+           ",\"calls\":" + std::to_string(row.calls) + ",\"payload_bits\":" + std::to_string(row.payload_bits) +
+           ",\"charged_bits\":" + std::to_string(row.charged_bits) +
+           ",\"bits_per_param_per_rank\":" + json_double(row.bits_per_param_per_rank()) + "}";
+  }
+  return out + "]";
 }
 
 }  // namespace tagc_b200

@@ -121,6 +121,9 @@ class TrafficLedger {
   void record(CollectiveOp op, const std::string& tag, uint64_t payload_bits, uint64_t params);
   void unrecord(CollectiveOp op, const std::string& tag, uint64_t payload_bits, uint64_t params);
   std::string to_csv() const;
+  // collectives.cpp:80-93: the rows as a JSON array, serialised the way
+  // nlohmann::ordered_json::dump() writes it (compact, shortest doubles)
+  std::string to_json() const;
   double bits_per_param_per_rank(const std::string& prefix = "") const;
   void clear() { rows_.clear(); }
   // Bytes actually handed to NCCL (measured, not modelled).

@@ -225,3 +225,21 @@ def test_estimation_matches_oracle(ctx, orc):
     assert np.array_equal(bits(got), bits(want))
     with pytest.raises(tagc.TagcInvalidArgument):
         ctx.estimation_decompress(d(allp[:2]), d(sk), d(np.array([3], np.uint32)), n, 2, 17)
+
+
+@pytest.mark.parametrize("width", [1, 4])
+def test_wire_bytes_match_reference(ctx, ref, width):
+    """Index::to_bytes / CountSketch::to_bytes (index.cpp:59-69,
+    sketch.cpp:77-89): the device buffers' little-endian word layout is the
+    reference's wire format byte for byte. Integer-valued sparse values keep
+    the sketch sums exact, so its bytes are order-independent."""
+    rng = np.random.default_rng(21 + width)
+    n = 300_007
+    v = np.zeros(n, np.float32)
+    idx = rng.choice(n, 3000, replace=False)
+    v[idx] = rng.integers(-50, 51, idx.size).astype(np.float32)
+    vd = torch.from_numpy(v).to(DEV)
+    words = ctx.index_create(vd, width)
+    assert ctx.to_bytes(words) == ref.index_to_bytes(v, width)
+    sk = ctx.sketch_compress(vd, 10, 77)
+    assert ctx.to_bytes(sk) == ref.sketch_to_bytes(v, 10, 77)

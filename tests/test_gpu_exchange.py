@@ -244,3 +244,25 @@ def test_validation_errors():
     with pytest.raises(tagc.TagcInvalidArgument):  # 4-bit index beyond 15 ranks
         ctx.tagc_reduce_shard_sim(single(n), [torch.ones(n, device=DEV)] * 16,
                                   [torch.zeros(n, device=DEV) for _ in range(16)])
+
+
+@pytest.mark.parametrize("world,theta,ratio,width", [(2, 80.0, 2, 4), (4, 99.0, 10, 4), (3, 98.75, 10, 1)])
+def test_ledger_matches_volume_model(orc, world, theta, ratio, width):
+    """test_hook.cpp:262-278: after an exchange the context's ledger charges
+    exactly comm_volume_model's index / sketch bits per parameter, and the
+    JSON dump agrees with the CSV rows."""
+    import json
+    n = 10_000
+    rng = np.random.default_rng(world)
+    grads = [(rng.random(n) * 2 - 1).astype(np.float32) for _ in range(world)]
+    cfg = tagc.CompressionConfig(theta=theta, ratio=ratio, index_width=width, policy="all_layers",
+                                 min_compress_segment=1)
+    _, _, _, _, _, _, ctx = run_both(orc, cfg, single(n), grads)
+    model = tagc.comm_volume_model(cfg, world, n)
+    led = ctx.ledger()
+    assert led.bits_per_param_per_rank("index/") == model["index_bits"]
+    assert led.bits_per_param_per_rank("sketch/") == model["sketch_bits"]
+    rows = json.loads(led.to_json())
+    csv_rows = ctx.ledger_csv().strip().split("\n")[1:]
+    assert [f"{r['op']},{r['tag']},{r['calls']},{r['payload_bits']},{r['charged_bits']}" for r in rows] == \
+        [",".join(c.split(",")[:5]) for c in csv_rows]

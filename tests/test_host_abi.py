@@ -144,3 +144,45 @@ def test_exchange_plan_covers_every_segment_once():
                 assert not iv or iv[-1][1] <= cap
         owned = [p for p in plan if p["owner"] == rank]
         assert all(p["out_off"] != 2**64 - 1 for p in owned)
+
+
+def test_ledger_csv_json_match_reference(ref):
+    """TrafficLedger (collectives.cpp:37-93) on the host: CSV, JSON dump text
+    and bits/param aggregates identical to the compiled reference's for the
+    same records (cost factors, row order, nlohmann number formatting)."""
+    import random
+
+    rnd = random.Random(4)
+    ops = ["all_reduce", "reduce", "reduce_scatter", "all_gather"]
+    records = []
+    for i in range(60):
+        op = rnd.randrange(4)
+        tag = rnd.choice(["index/", "sketch/", "grad/", "params/"]) + f"shard{rnd.randrange(3)}/l{rnd.randrange(5)}"
+        bits = rnd.choice([0, 1, 7, 32 * 768, 3 * 559240 * 32, rnd.randrange(1 << 40), 10 ** 18])
+        params = rnd.choice([0, 1, 3, 768, 16_777_216, rnd.randrange(1 << 30), 10 ** 13])
+        records.append((op, tag, bits, params))
+    records.append((3, "params/allgather", 62_219_904 * 2 * 32, 62_219_904 * 2))
+    led = tagc.TrafficLedger()
+    for op, tag, bits, params in records:
+        led.record(ops[op], tag, bits, params)
+    for prefix in ("", "index/", "grad/shard1", "nope"):
+        csv, js, bpp = ref.ledger_dump(records, prefix)
+        assert led.to_csv() == csv
+        assert led.to_json() == js
+        assert led.bits_per_param_per_rank(prefix) == bpp
+    with pytest.raises(tagc.TagcInvalidArgument):
+        led.record("broadcast", "x", 1, 1)
+    led.clear()
+    assert led.to_json() == "[]"
+
+
+def test_ledger_json_number_format(ref):
+    """Doubles across the nlohmann formatting regimes: integral ("4.0"),
+    fixed, small ("0.0001"), exponent ("1e-05", "1.5e+17")."""
+    cases = [(0, 8, 2), (1, 32, 10), (2, 1, 10_000), (2, 1, 100_000), (2, 3, 7), (1, 15 * 10 ** 16, 1),
+             (2, 10 ** 17, 3), (3, 0, 5), (1, 2 ** 60, 3), (2, 1, 3 * 10 ** 9)]
+    for op, bits, params in cases:
+        led = tagc.TrafficLedger()
+        led.record(["all_reduce", "reduce", "reduce_scatter", "all_gather"][op], "t", bits, params)
+        _, js, _ = ref.ledger_dump([(op, "t", bits, params)])
+        assert led.to_json() == js, (bits, params, led.to_json(), js)
