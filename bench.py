@@ -276,6 +276,70 @@ def run_b200(args):
                       "adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)), 4),
                   "unfused_ms": round(timed(unfused), 4), "fused_ms": round(timed(fused), 4)}
 
+    # backward / exchange overlap: a synthetic backward
+    # pass on a producer stream (3 bf16 GEMMs 8192x768 @ 768x3072 per GPT-2
+    # block, then the block's gradient lands in the buffer), in reverse layer
+    # order. one_shot: tagc_reduce_shards after the backward; overlapped:
+    # tagc_overlap_* encoding each block as it lands. Times from backward start
+    # to the decoded shard, device events.
+    groups, off = [], 0
+    for sp in specs:
+        key = sp.name.split(".")[0] if sp.name.startswith("h") else ("final" if sp.name.startswith("ln_f") else "embed")
+        if not groups or groups[-1][0] != key:
+            groups.append([key, off, off])
+        off += sp.param_count
+        groups[-1][2] = off
+    ranges = [(lo, hi) for _, lo, hi in groups]
+    ranges[-1] = (ranges[-1][0], total)  # the make_shards pad tail lands with the last block
+    ga = torch.randn(8192, 768, device=dev, dtype=torch.bfloat16)
+    gb = torch.randn(768, 3072, device=dev, dtype=torch.bfloat16)
+    gc = torch.empty(8192, 3072, device=dev, dtype=torch.bfloat16)
+    grad_bw = torch.empty_like(grad)
+    prod = torch.cuda.Stream(device=local)
+
+    def backward(on_ready=None):
+        for lo, hi in reversed(ranges):
+            with torch.cuda.stream(prod):
+                for _ in range(3):
+                    torch.mm(ga, gb, out=gc)
+                grad_bw[lo:hi].copy_(grad[lo:hi])
+                ev = torch.cuda.Event()
+                ev.record(prod)
+            if on_ready:
+                on_ready(lo, hi, ev)
+        done = torch.cuda.Event()
+        done.record(prod)
+        return done
+
+    def run_overlap(mode):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prod.wait_stream(stream)  # iterations do not overlap each other
+        b0.record(prod)
+        if mode == "backward":
+            backward()
+            b1.record(prod)
+        elif mode == "one_shot":
+            stream.wait_event(backward())
+            ctx.tagc_reduce_shards(shards, grad_bw, acc, out, stats=False)
+            b1.record(stream)
+        else:
+            stream.wait_event(b0)
+            ctx.overlap_begin(shards, grad_bw, acc, out)
+            backward(ctx.overlap_ready)
+            ctx.overlap_finish()
+            b1.record(stream)
+        return b0, b1
+
+    overlap = {"producer": "3x bf16 mm 8192x768@768x3072 per block, 14 blocks, reverse order"}
+    for mode in ("backward", "one_shot", "overlapped"):
+        for _ in range(max(3, args.warmup)):
+            run_overlap(mode)
+        barrier()
+        evs = [run_overlap(mode) for _ in range(opt_steps)]
+        barrier()
+        overlap[mode + "_ms"] = round(max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / opt_steps), 4)
+    del ga, gb, gc, grad_bw
+
     # e2e through the C-ABI host-buffer entry (tagc_reduce_shards_host): every
     # step copies this step's gradient H2D from pinned memory and the owner's
     # decoded shard D2H; consecutive calls overlap their copies with each
@@ -352,6 +416,7 @@ def run_b200(args):
         "uncompressed_rs": {"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
                             "unit": "GB/s", "ms_per_step": round(base_ms, 4)},
         "owner_step": owner_step,
+        "overlap": overlap,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }

@@ -327,6 +327,22 @@ int tagc_plan_exchange(const tagc_config* cfg, const tagc_shard* shards, uint32_
 int tagc_baseline_reduce_shards(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
                                 const float* grad, float* out);
 
+/* ------------------------------------- backward / exchange overlap (§8f)
+ * tagc_reduce_shards split along the gradient's production (paper §3.3): the
+ * exchange is opened before the gradient exists, every segment is sparsified
+ * and encoded as soon as the flat range [begin, end) holding it is ready, and
+ * the collective + decode run at finish. cuda_event (a cudaEvent_t recorded on
+ * the producer's stream after it wrote the range, may be NULL) is waited on by
+ * the context's stream, so encoding overlaps the rest of the backward pass.
+ * A segment is encoded by the first ready call whose range contains it;
+ * finish encodes whatever no call covered. grad must stay valid and unwritten
+ * until finish has been enqueued (its reads end there). Results are those of
+ * tagc_reduce_shards on the same inputs. */
+int tagc_overlap_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad, float* acc,
+                       float* out);
+int tagc_overlap_ready(tagc_ctx* ctx, uint64_t begin, uint64_t end, void* cuda_event);
+int tagc_overlap_finish(tagc_ctx* ctx, tagc_peel_stats* stats);
+
 /* ------------------------------------------- owner-side consumer (§8f)
  * The step after the exchange in the reference's training loop
  * (train.cpp:355-364): the owner takes the mean over ranks of its decoded

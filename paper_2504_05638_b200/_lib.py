@@ -158,6 +158,9 @@ SIGNATURES = {
     "tagc_sketch_add": (C.c_int, [VP, VP, VP, VP, U64]),
     "tagc_apply_optimizer": (C.c_int, [VP, C.c_int32, C.c_double, C.c_double, U32, U32, VP, VP, VP, U64]),
     "tagc_allgather_params": (C.c_int, [VP, VP, U64]),
+    "tagc_overlap_begin": (C.c_int, [VP, VP, U32, VP, VP, VP]),
+    "tagc_overlap_ready": (C.c_int, [VP, U64, U64, VP]),
+    "tagc_overlap_finish": (C.c_int, [VP, VP]),
     "tagc_reduce_shards_step": (C.c_int, [VP, VP, U32, VP, VP, VP, C.c_int32, C.c_double, C.c_double, U32, VP, VP,
                                           VP]),
     "tagc_peeling_decompress": (C.c_int, [VP, VP, U32, U32, U32, U32, U64, VP, VP, VP, C.POINTER(U32),

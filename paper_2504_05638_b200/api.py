@@ -577,6 +577,29 @@ class Context:
                                           C.byref(st) if stats else None), "tagc_reduce_shards_step")
         return PeelStats(**st.as_dict()) if stats else None
 
+    def overlap_begin(self, shards: Sequence[ShardSpec], grad, acc, out=None):
+        """Open an exchange before the gradient exists (tagc_overlap_begin);
+        returns out (this rank's decoded shards, complete after finish)."""
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        out = self._empty(max(owned, 1)) if out is None else out
+        scs = [_ShardC(s) for s in shards]
+        self._overlap_keep = (scs, grad, acc, out)
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        check(lib.tagc_overlap_begin(self.h, arr, len(scs), _ptr(grad), _ptr(acc), _ptr(out)), "overlap_begin")
+        return out
+
+    def overlap_ready(self, begin: int, end: int, event=None):
+        """The gradient range [begin, end) is written once `event` (a
+        torch.cuda.Event recorded on the producer's stream) completes."""
+        ev = C.c_void_p(event.cuda_event) if event is not None else None
+        check(lib.tagc_overlap_ready(self.h, int(begin), int(end), ev), "overlap_ready")
+
+    def overlap_finish(self, stats=False):
+        st = _lib.PeelStats()
+        check(lib.tagc_overlap_finish(self.h, C.byref(st) if stats else None), "overlap_finish")
+        self._overlap_keep = None
+        return PeelStats(**st.as_dict()) if stats else None
+
     def allgather_params(self, params):
         """World::all_gather of the owners' slices (train.cpp:364) over NCCL,
         in place: params is the padded flat space, this rank's slice is

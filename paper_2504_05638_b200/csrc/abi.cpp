@@ -415,6 +415,29 @@ int tagc_reduce_shards_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n
   });
 }
 
+int tagc_overlap_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad, float* acc,
+                       float* out) {
+  return guarded([&] {
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    eng(ctx).overlap_begin(v, grad, acc, out);
+  });
+}
+
+int tagc_overlap_ready(tagc_ctx* ctx, uint64_t begin, uint64_t end, void* cuda_event) {
+  return guarded([&] { eng(ctx).overlap_ready(begin, end, static_cast<cudaEvent_t>(cuda_event)); });
+}
+
+int tagc_overlap_finish(tagc_ctx* ctx, tagc_peel_stats* stats) {
+  return guarded([&] {
+    PeelStats st;
+    eng(ctx).overlap_finish(stats ? &st : nullptr);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
 int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
                            tagc_peel_stats* stats) {
   return guarded([&] {

@@ -151,6 +151,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
     : cfg_(cfg), world_(world), rank_(rank), device_(device) {
   if (const char* v = std::getenv("TAGC_FUSED_TMA")) use_tma_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_GRAPHS")) graphs_on_ = std::atoi(v) != 0;
+  if (const char* v = std::getenv("TAGC_SIDE_STREAM")) side_stream_ = std::atoi(v) != 0;
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -428,6 +429,17 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
     ev_record(3);
+    static const bool sel_dbg = std::getenv("TAGC_DEBUG_SELECT") != nullptr;
+    if (sel_dbg && !capturing_) {  // per-item select outcome (debug only: synchronises)
+      std::vector<SelState> hs(n);
+      cuda_check(cudaMemcpyAsync(hs.data(), state, n * sizeof(SelState), cudaMemcpyDeviceToHost, stream_), "dbg");
+      cuda_check(cudaStreamSynchronize(stream_), "dbg");
+      for (uint32_t i = 0; i < n; ++i)
+        if (hs[i].status != 0 || std::getenv("TAGC_DEBUG_SELECT")[0] == '2')
+          std::fprintf(stderr, "select item %u n=%u c=%u Z=%u L=%u I=%u hi=%u caps=%u/%u win=[%08x,%08x] status=%u\n",
+                       i, items[i].n, items[i].c, hs[i].cnt_zero, hs[i].cnt_lo, hs[i].cnt_in, hs[i].cnt_hi,
+                       items[i].cand_cap, items[i].hi_cap, hs[i].klo, hs[i].khi, hs[i].status);
+    }
   } else {
     zero({{state, n * sizeof(SelState)}});
     ev_record(1);
@@ -758,7 +770,13 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
       }
     }
   }
+  static const bool graph_dbg = std::getenv("TAGC_DEBUG_GRAPH") != nullptr;
   auto it = graphs_.find(key);
+  if (graph_dbg)
+    std::fprintf(stderr, "graph: %s key %zx gen %llu (cached gen %lld) seen %d graphs %zu\n",
+                 it == graphs_.end() ? "miss" : "hit", std::hash<std::string>{}(key),
+                 (unsigned long long)ws_.generation(), it == graphs_.end() ? -1ll : (long long)it->second.gen,
+                 graph_seen_.count(key) ? graph_seen_[key] : 0, graphs_.size());
   if (it != graphs_.end() && it->second.gen != ws_.generation()) {
     drop_graphs();  // a workspace buffer moved: every captured pointer is suspect
     it = graphs_.end();
@@ -825,59 +843,84 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
 // First half of an exchange (reference hook.cpp:137-163): encode every
 // compressed segment into its owner's send blocks, pack raw segments (W > 1)
 // or copy them to the output (W == 1, side stream). State for exchange_end
-// stays in xs_.
+// stays in xs_. Split into prologue / encode / seal so that the overlap
+// entry points can encode segments as their gradients become ready.
 void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
                             float* user_send_f, uint32_t* user_send_u) {
+  exchange_prologue(shards, grad, acc, out, user_send_f, user_send_u);
+  exchange_encode(0, ~0ull);
+  exchange_seal();
+}
+
+void Engine::exchange_prologue(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                               float* user_send_f, uint32_t* user_send_u) {
   launches_ = 0;
   ev_record(0);
   span_reset();
-  const uint32_t W = world_, w = cfg_.index_width, rows = cfg_.sketch_rows;
+  const uint32_t W = world_;
   xs_ = ExchangeState{};
   xs_.shards = shards;
   xs_.out = out;
+  xs_.grad = grad;
+  xs_.acc = acc;
   xs_.P = plan_exchange(shards, cfg_, W, rank_);
   const ExchangePlan& P = xs_.P;
-  const std::vector<SegPlan>& plan = P.segs;
-  const std::vector<uint64_t>& skc = P.skc;
-  const std::vector<uint64_t>& out_off = P.out_off;
+  xs_.encoded.assign(P.segs.size(), 0);
   const uint64_t Bf = P.Bf, Bu = P.Bu;
   auto* send_f = user_send_f ? user_send_f : static_cast<float*>(ws_.get("nc_send_f", W * Bf * 4, false, stream_));
   auto* send_u = user_send_u ? user_send_u : static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
   xs_.send_f = send_f;
   xs_.send_u = send_u;
-  {
-    std::vector<std::pair<void*, uint64_t>> zr;
-    for (uint32_t o = 0; o < W; ++o) zr.push_back({send_f + o * Bf, skc[o] * 4});
-    zero(zr);
-  }
-  const HashParams hp = make_hash_params(cfg_.seed, rows);
-  (void)rows;
+  std::vector<std::pair<void*, uint64_t>> zr;
+  for (uint32_t o = 0; o < W; ++o) zr.push_back({send_f + o * Bf, P.skc[o] * 4});
+  zero(zr);
+  xs_.begun = true;
+}
+
+// Encodes the not yet encoded segments lying inside the flat range [lo, hi).
+void Engine::exchange_encode(uint64_t lo, uint64_t hi) {
+  if (!xs_.begun || xs_.active) throw InvalidArgument("no exchange is open for encoding");
+  const std::vector<ShardSpec>& shards = xs_.shards;
+  const ExchangePlan& P = xs_.P;
+  const std::vector<SegPlan>& plan = P.segs;
+  const uint32_t W = world_, w = cfg_.index_width;
+  const uint64_t Bf = P.Bf, Bu = P.Bu;
+  float* send_f = xs_.send_f;
+  uint32_t* send_u = xs_.send_u;
+  const float* grad = xs_.grad;
+  float* acc = xs_.acc;
+  float* out = xs_.out;
+  const HashParams hp = make_hash_params(cfg_.seed, cfg_.sketch_rows);
   std::vector<EncItem> enc;
-  std::vector<CopyItem> pack, unpack;
-  for (const SegPlan& p : plan) {
+  std::vector<CopyItem> pack, side;
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const SegPlan& p = plan[i];
     const ShardSpec& sh = shards[p.shard];
+    const uint64_t b = sh.begin + p.lo, e = b + p.len;
+    if (xs_.encoded[i] || b < lo || e > hi) continue;
+    xs_.encoded[i] = 1;
     const uint32_t o = sh.owner;
     if (p.compressed) {
-      EncItem e{};
-      e.g = grad + sh.begin + p.lo;
-      e.acc = acc + sh.begin + p.lo;
-      e.index = send_u + o * Bu + p.word_off;
-      e.sketch = send_f + o * Bf + p.sk_off;
-      e.n = uint32_t(p.len);
-      e.m = p.m;
-      e.c = threshold_rank(cfg_.theta, p.len);
-      e.flags = (w == 4 ? kWidth4 : 0u) | kHasAcc | kWriteIndex | kWriteSketch | kSelect |
-                ((aligned16(e.g) && aligned16(e.acc)) ? kAligned16 : 0u);
-      enc.push_back(e);
+      EncItem it{};
+      it.g = grad + b;
+      it.acc = acc + b;
+      it.index = send_u + o * Bu + p.word_off;
+      it.sketch = send_f + o * Bf + p.sk_off;
+      it.n = uint32_t(p.len);
+      it.m = p.m;
+      it.c = threshold_rank(cfg_.theta, p.len);
+      it.flags = (w == 4 ? kWidth4 : 0u) | kHasAcc | kWriteIndex | kWriteSketch | kSelect |
+                 ((aligned16(it.g) && aligned16(it.acc)) ? kAligned16 : 0u);
+      enc.push_back(it);
     } else if (W == 1) {  // no exchange: raw segments go straight to the output
-      unpack.push_back(CopyItem{grad + sh.begin + p.lo, out + out_off[p.shard] + p.lo, p.len, 0});
+      side.push_back(CopyItem{grad + b, out + P.out_off[p.shard] + p.lo, p.len, 0});
     } else {
-      pack.push_back(CopyItem{grad + sh.begin + p.lo, send_f + o * Bf + p.raw_off, p.len, 0});
+      pack.push_back(CopyItem{grad + b, send_f + o * Bf + p.raw_off, p.len, 0});
     }
   }
   run_select_encode(enc, w == 4, hp, false, "nccl");
   // raw segments (W > 1): packed into the send blocks before the exchange
-  if (W > 1 && !pack.empty()) {
+  if (!pack.empty()) {
     const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
     auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", pack.size() * sizeof(CopyItem), false, stream_));
     upload(pack.data(), pack.size() * sizeof(CopyItem), d_pack);
@@ -885,37 +928,72 @@ void Engine::exchange_begin(const std::vector<ShardSpec>& shards, const float* g
   }
   // Side stream (W == 1), overlapping the latency-bound decode: the raw
   // segments copied straight from the gradient to the output.
-  std::vector<CopyItem> side;
-  if (W == 1) side = unpack;
-  cudaEvent_t zero_done = nullptr;
-  const auto ev_flags = capturing_ ? cudaEventRecordExternal : 0u;  // external: waited on outside the graph
-  if (!side.empty()) {
+  if (!side.empty() && !side_stream_) {  // in order on the context stream
+    const uint64_t tt = copy_tiles(side.data(), uint32_t(side.size()));
+    auto* d_side = static_cast<CopyItem*>(ws_.get("nc_side", side.size() * sizeof(CopyItem), false, stream_));
+    upload(side.data(), side.size() * sizeof(CopyItem), d_side);
+    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, stream_, false,
+                                   opt_on_ ? opt_dev_ : nullptr);
+  } else if (!side.empty()) {
     ensure_aux();
     const uint64_t tt = copy_tiles(side.data(), uint32_t(side.size()));
     auto* d_side = static_cast<CopyItem*>(ws_.get("nc_side", side.size() * sizeof(CopyItem), false, stream_));
     upload(side.data(), side.size() * sizeof(CopyItem), d_side);
     cuda_check(cudaEventRecord(aux_fork_, stream_), "fork");
     cuda_check(cudaStreamWaitEvent(aux_, aux_fork_, 0), "fork wait");
-    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true, opt_on_ ? opt_dev_ : nullptr);
+    launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, aux_, true,
+                                   opt_on_ ? opt_dev_ : nullptr);
+    xs_.side_used = true;
+  }
+}
+
+// Encodes whatever is left, then marks the end of the gradient reads.
+void Engine::exchange_seal() {
+  exchange_encode(0, ~0ull);
+  const auto ev_flags = capturing_ ? cudaEventRecordExternal : 0u;  // external: waited on outside the graph
+  cudaEvent_t zero_done = nullptr;
+  if (xs_.side_used) {
     cuda_check(cudaEventRecord(aux_join_, aux_), "join");
     zero_done = aux_join_;
   }
   // after this the gradient is no longer read
   if (grad_read_ev_) {
-    if (W == 1 && zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait raw copy");
+    if (world_ == 1 && zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait raw copy");
     cuda_check(cudaEventRecordWithFlags(grad_read_ev_, stream_, ev_flags), "grad-read event");
   }
   xs_.zero_done = zero_done;
+  xs_.begun = false;
   xs_.active = true;
 }
 
 void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                                    float* out, PeelStats* stats) {
-  if (peer_.attached && world_ > 1) {  // collective by pulls over peer memory
+  open_exchange(shards, grad, acc, out);
+  exchange_encode(0, ~0ull);
+  finish_exchange(stats);
+}
+
+// Prologue with this context's transport buffers: the peer region's current
+// send set when the exchange runs over peer memory, else the workspace.
+void Engine::open_exchange(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out) {
+  if (peer_.attached && world_ > 1) {
     const int set = peer_.set;
-    exchange_begin(shards, grad, acc, out, peer_.view.send_f[set][rank_], peer_.view.send_u[set][rank_]);
-    if (xs_.P.Bf != peer_.Bf || xs_.P.Bu != peer_.Bu)
+    exchange_prologue(shards, grad, acc, out, peer_.view.send_f[set][rank_], peer_.view.send_u[set][rank_]);
+    if (xs_.P.Bf != peer_.Bf || xs_.P.Bu != peer_.Bu) {
+      xs_ = ExchangeState{};
       throw InvalidArgument("shard layout differs from the one the peer exchange was prepared for");
+    }
+    return;
+  }
+  exchange_prologue(shards, grad, acc, out);
+}
+
+// Seal, the collective (peer pulls or grouped NCCL reduce-scatters), decode.
+void Engine::finish_exchange(PeelStats* stats) {
+  exchange_seal();
+  const uint32_t W = world_;
+  if (peer_.attached && W > 1) {  // collective by pulls over peer memory
+    const int set = peer_.set;
     auto* recv_f = static_cast<float*>(ws_.get("nc_recv_f", peer_.Bf * 4, false, stream_));
     auto* recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", peer_.Bu * 4, false, stream_));
     uint32_t* err = err_flag();
@@ -930,18 +1008,15 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
     peer_.set ^= 1;
     return;
   }
-  exchange_begin(shards, grad, acc, out);
-  const uint32_t W = world_;
   const uint64_t Bf = xs_.P.Bf, Bu = xs_.P.Bu;
   float* send_f = xs_.send_f;
   uint32_t* send_u = xs_.send_u;
   float* recv_f = send_f;
   uint32_t* recv_u = send_u;
   if (W > 1) {
+    if (!comm_) throw InvalidArgument("multi-rank context has no NCCL communicator or peer exchange");
     recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
     recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
-  }
-  if (W > 1) {
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
     nccl_check(nccl().ReduceScatter(send_f, recv_f, Bf, ncclFloat32, ncclSum, comm_, stream_),
                "ncclReduceScatter f32");
@@ -952,6 +1027,33 @@ void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const f
   }
   ev_record(4);
   exchange_end(recv_f, recv_u, stats);
+}
+
+// Overlap entry points: the exchange opened before the
+// gradient exists, each segment encoded as soon as the range holding it is
+// ready (after `ready` on the producer's stream), the collective and decode
+// once every range is in.
+void Engine::overlap_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out) {
+  CallScope scope(*this);
+  cfg_.validate_for_world(world_);
+  for (const ShardSpec& s : shards) check_shard(s, world_);
+  if (world_ > 1 && !comm_ && !peer_.attached)
+    throw InvalidArgument("multi-rank context has no NCCL communicator or peer exchange");
+  if (xs_.begun || xs_.active) throw InvalidArgument("an exchange is already in progress on this context");
+  open_exchange(shards, grad, acc, out);
+}
+
+void Engine::overlap_ready(uint64_t lo, uint64_t hi, cudaEvent_t ready) {
+  CallScope scope(*this);
+  if (!xs_.begun) throw InvalidArgument("no overlapped exchange is open");
+  if (ready) cuda_check(cudaStreamWaitEvent(stream_, ready, 0), "wait for the gradient producer");
+  exchange_encode(lo, hi);
+}
+
+void Engine::overlap_finish(PeelStats* stats) {
+  CallScope scope(*this);
+  if (!xs_.begun) throw InvalidArgument("no overlapped exchange is open");
+  finish_exchange(stats);
 }
 
 // Second half (hook.cpp:164-189): decode this rank's owned compressed

@@ -139,6 +139,20 @@ class Engine {
   // sum), exchange_end decodes this rank's block.
   void exchange_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
                       float* user_send_f = nullptr, uint32_t* user_send_u = nullptr);
+  // Overlapped exchange: open before the gradient exists, encode each range
+  // as it becomes ready (ready: an event on the producer's stream, or null),
+  // then the collective + decode. Same results as reduce_shards.
+  void overlap_begin(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out);
+  void overlap_ready(uint64_t lo, uint64_t hi, cudaEvent_t ready);
+  void overlap_finish(PeelStats* stats);
+  void open_exchange(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out);
+  void finish_exchange(PeelStats* stats);
+  // The pieces of exchange_begin: prologue (plan, send blocks), encode of the
+  // segments inside a flat range, seal (the rest, end of gradient reads).
+  void exchange_prologue(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                         float* user_send_f = nullptr, uint32_t* user_send_u = nullptr);
+  void exchange_encode(uint64_t lo, uint64_t hi);
+  void exchange_seal();
   void exchange_end(const float* recv_f, const uint32_t* recv_u, PeelStats* stats,
                     const std::function<void()>& pre_decode = nullptr);
   float* exchange_send_f() const { return xs_.send_f; }
@@ -184,7 +198,12 @@ class Engine {
   void enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
                              PeelStats* stats);
   struct ExchangeState {  // between exchange_begin and exchange_end
-    bool active = false;
+    bool begun = false;   // prologue done, segments may still be encoded
+    bool active = false;  // sealed: waiting for exchange_end
+    bool side_used = false;
+    const float* grad = nullptr;
+    float* acc = nullptr;
+    std::vector<uint8_t> encoded;  // per plan segment
     std::vector<ShardSpec> shards;
     ExchangePlan P;
     float* out = nullptr;
@@ -268,6 +287,7 @@ class Engine {
   void ev_record(int i);
   void span_reset();
   unsigned long long* spans_ = nullptr;
+  bool side_stream_ = true;  // W = 1 raw copies on the low-priority side stream (TAGC_SIDE_STREAM=0: in order)
   bool use_tma_ = true;  // TMA-staged fused pass (TAGC_FUSED_TMA=0 selects the register path)
   uint32_t* err_flag();
 
