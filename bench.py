@@ -111,11 +111,12 @@ def cfg_obj():
 
 def algorithmic_bytes(shards, rank, world):
     """SURVEY.md §8(d) bytes for this rank's dominant kernel, the fused
-    select + encode pass: per compressed element it reads g and acc (8 B) and
-    writes the residual (4 B) and the packed index (w/8 B), plus a 24*d sketch
-    read-modify-write (d = kept density = 1 - theta/100) and the 1/32 sample
-    pre-pass (8/32 B). The separate select pass of the survey's model (8 B) is
-    gone: selection rides on the same pass."""
+    select + encode pass (k_fused_tma): per compressed element it reads g and
+    acc (8 B) and writes the residual (4 B) and the packed index (w/8 B), plus
+    a 24*d sketch read-modify-write (d = kept density = 1 - theta/100). The
+    separate select pass of the survey's model (8 B) is gone: selection rides
+    on the same pass, bracketed by two small passes over a 1/32 sample (2 x
+    8/32 B, separate kernels, not in this figure)."""
     import paper_2504_05638_b200 as tagc
 
     comp = 0
@@ -124,7 +125,7 @@ def algorithmic_bytes(shards, rank, world):
             if tagc.kind_compressible(s.kind, "non_attention_linear", True) and s.size() >= 1024:
                 comp += s.size()
     dens = 1.0 - THETA / 100.0
-    fused = comp * (12.0 + WIDTH / 8.0 + 24.0 * dens + 8.0 / 32.0)
+    fused = comp * (12.0 + WIDTH / 8.0 + 24.0 * dens)
     return comp, fused
 
 
@@ -402,13 +403,13 @@ def run_b200(args):
         },
         "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4)},
-        "roofline": {"kernel": "k_fused_tma (sample + window + TMA-staged select/split/index/sketch scatter)",
+        "roofline": {"kernel": "k_fused_tma (TMA-staged select/split/index/sketch scatter)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(fused_bytes),
                      "kernel_ms": round(fused_ms, 4),
-                     "timed": "k_sample+k_window+k_fused launches: device span from %globaltimer stamps "
-                              "written by the kernels (first CTA start to last CTA end), mean of the timed launches"},
+                     "timed": "k_fused_tma launches: device span from %globaltimer stamps written by the "
+                              "kernel (first CTA start to last CTA end), mean of the timed launches"},
         "decode_span_ms": round(span_ms[1], 4),
         "stages_ms": {"prep": round(stage_ms[0], 4), "select_fused": round(stage_ms[1], 4),
                       "select_finish": round(stage_ms[2], 4), "exchange": round(stage_ms[3], 4),

@@ -211,8 +211,8 @@ int tagc_ctx_set_timing(tagc_ctx* ctx, int enabled);
 int tagc_ctx_last_timing(tagc_ctx* ctx, float out_ms[5]);
 /* Timing mode: device execution spans (ms) of the last fused call's two
  * dominant kernel chains, stamped by the kernels themselves (%globaltimer):
- * out_ms[0] = sampled select + fused split/encode pass (k_sample start to
- * k_fused end), out_ms[1] = decode (k_build start to k_final end). */
+ * out_ms[0] = the fused select/split/encode pass (k_fused start to end),
+ * out_ms[1] = decode (k_count start to k_final end). */
 int tagc_ctx_last_kernel_spans(tagc_ctx* ctx, float out_ms[2]);
 /* CUDA-graph replay of tagc_reduce_shards / _host (default on; the
  * environment variable TAGC_GRAPHS=0 turns it off): a call whose shard

@@ -18,6 +18,11 @@ constexpr uint32_t kSmallSegment = 65536;
 constexpr uint32_t kSampleChunk = 1024;
 constexpr uint32_t kSampleBins = 4096;  // top 12 bits of the 31-bit magnitude key
 constexpr uint32_t kSampleShift = 19;
+constexpr uint32_t kFineShift = kSampleShift - 12;   // 4096 fine bins inside a sample bin
+constexpr uint32_t kSampleStride = 3 * kSampleBins;  // per item: coarse, fine (lo), fine (hi)
+// Large segments sample 1024 elements of every kSampleMaxStride-th tile
+// (1/32 of the data); the window's rank margin scales with 1/sqrt(sample).
+constexpr uint64_t kSampleMaxStride = 8;
 constexpr uint32_t kRadixBins = 2048;   // 11/10/10-bit digits of the key
 constexpr uint32_t kDecWordTile = 4096; // merged-index words per decode word tile (16 per thread)
 constexpr uint32_t kMaxFlatItems = 4096; // items per call (flattened iteration bound)

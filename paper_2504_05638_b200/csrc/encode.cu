@@ -118,14 +118,14 @@ __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restri
                                                          uint32_t n_items, uint64_t total,
                                                          uint32_t* __restrict__ sample_hist,
                                                          unsigned long long* span) {
-  span_begin(span);
+  (void)span;
   __shared__ uint32_t hist[kSampleBins];
   for (uint32_t i = threadIdx.x; i < kSampleBins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   int cur = -1;
   auto flush = [&](int item) {
     __syncthreads();
-    uint32_t* dst = sample_hist + uint64_t(item) * kSampleBins;
+    uint32_t* dst = sample_hist + uint64_t(item) * kSampleStride;
     for (uint32_t i = threadIdx.x; i < kSampleBins; i += blockDim.x) {
       const uint32_t h = hist[i];
       if (h) atomicAdd(dst + i, h);
@@ -172,66 +172,167 @@ __global__ void __launch_bounds__(kTileThreads) k_sample(const EncItem* __restri
 }
 
 // --------------------------------------------------------------- window
-// One CTA per item: bracket the target rank of the sample into a key window.
-__global__ void __launch_bounds__(256) k_window(const EncItem* __restrict__ items,
-                                                SelState* __restrict__ state,
-                                                uint32_t* __restrict__ sample_hist,
-                                                unsigned long long* span) {
-  span_begin(span);
-  using Scan = cub::BlockScan<uint32_t, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint32_t s_lo, s_hi;
+// Two levels, so the window rests on sample order statistics rather than on
+// an assumption about how keys spread inside a bin: k_window_coarse finds the
+// 1/16-octave sample bins holding the bracketing ranks t -+ 6 sigma,
+// k_sample_fine histograms the sample keys of those two bins at 128-ulp
+// resolution, and k_window_fine sets the window to the outer edges of the
+// fine bins holding the ranks. The only error left is the sample's own
+// (covered by the 6 sigma margin) whatever the keys look like inside a bin.
+// Interpolating inside a coarse bin instead assumed uniform keys there; error
+// feedback leaves a cliff near tau (the previous step's threshold) where that
+// fails, and the exact fallback then costs ~0.6 ms on GPT-2.
+
+struct RankBinSmem {
+  cub::BlockScan<uint32_t, 256>::TempStorage scan;
+  uint32_t bin[2], below[2], total;
+};
+
+// Bins of a 256-thread CTA's histogram h[kSampleBins] holding the 0-based
+// ranks r0, r1 (negative: none) into sm.bin / sm.below (bin 0xFFFFFFFF: no
+// bin holds it), plus the total count, in one scan.
+__device__ __forceinline__ void rank_bins_256(const uint32_t* h, double r0, double r1, RankBinSmem& sm) {
+  constexpr int kPer = kSampleBins / 256;
+  uint32_t loc[kPer];
+  const uint4* h4 = reinterpret_cast<const uint4*>(h + threadIdx.x * kPer);
+#pragma unroll
+  for (int i = 0; i < kPer / 4; ++i) {
+    const uint4 q = __ldcg(h4 + i);
+    loc[4 * i] = q.x;
+    loc[4 * i + 1] = q.y;
+    loc[4 * i + 2] = q.z;
+    loc[4 * i + 3] = q.w;
+  }
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) sum += loc[i];
+  uint32_t pre, total;
+  cub::BlockScan<uint32_t, 256>(sm.scan).ExclusiveSum(sum, pre, total);
+  if (threadIdx.x == 0) {
+    sm.bin[0] = sm.bin[1] = 0xFFFFFFFFu;
+    sm.below[0] = sm.below[1] = 0;
+    sm.total = total;
+  }
+  __syncthreads();
+  uint32_t cum = pre;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const double c0 = double(cum), c1 = double(cum + loc[i]);
+    if (r0 >= 0.0 && c0 <= r0 && r0 < c1) {
+      sm.bin[0] = threadIdx.x * kPer + i;
+      sm.below[0] = cum;
+    }
+    if (r1 >= 0.0 && c0 <= r1 && r1 < c1) {
+      sm.bin[1] = threadIdx.x * kPer + i;
+      sm.below[1] = cum;
+    }
+    cum += loc[i];
+  }
+  __syncthreads();
+}
+
+// One CTA per item: coarse bins of the bracketing sample ranks, kept in the
+// item's SelState until k_window_fine: prefix / kept = lo / hi coarse bin
+// (0xFFFFFFFF: no bound), rank / n_sel = the ranks inside them.
+__global__ void __launch_bounds__(256) k_window_coarse(const EncItem* __restrict__ items,
+                                                       SelState* __restrict__ state,
+                                                       const uint32_t* __restrict__ sample_hist,
+                                                       unsigned long long* span) {
+  (void)span;
+  __shared__ RankBinSmem sm;
   const uint32_t item = blockIdx.x;
   const EncItem e = items[item];
-  uint32_t klo = 1u, khi = 0x7F800000u;  // no sample: every nonzero key is a candidate
+  SelState st{};
+  st.prefix = st.kept = 0xFFFFFFFFu;
   if (e.sample_tiles > 0) {
-    uint32_t* h = sample_hist + uint64_t(item) * kSampleBins;
-    constexpr int kPer = kSampleBins / 256;
-    uint32_t loc[kPer];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      loc[i] = h[threadIdx.x * kPer + i];
-      sum += loc[i];
-    }
-    uint32_t pre, total;
-    Scan(tmp).ExclusiveSum(sum, pre, total);
-    if (threadIdx.x == 0) {
-      s_lo = 0xFFFFFFFFu;  // "below every bin"
-      s_hi = 0xFFFFFFFFu;  // "above every bin"
-    }
-    __syncthreads();
-    const double s = double(total);
+    const uint32_t* h = sample_hist + uint64_t(item) * kSampleStride;
+    rank_bins_256(h, -1.0, -1.0, sm);
+    const double s = double(sm.total);
     const double p = double(e.c) / double(e.n);
     const double t = double(e.c > 0 ? e.c - 1 : 0) * s / double(e.n);
     const double delta = 6.0 * sqrt(fmax(s * p * (1.0 - p), 0.0)) + 16.0;
     const double lo = floor(t - delta), hi = ceil(t + delta);
-    // Window edges are interpolated linearly inside the sample bin that holds
-    // the bracketing rank (keys are close to uniform inside a 1/16-octave
-    // bin); the +-6 sigma rank margin absorbs both sampling and
-    // interpolation error, and a miss only costs the exact fallback.
-    uint32_t cum = pre;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const uint32_t b = threadIdx.x * kPer + i;
-      const double c0 = double(cum), c1 = double(cum + loc[i]);
-      if (lo >= 0.0 && c0 <= lo && lo < c1) {
-        const double f = (lo - c0) / double(loc[i]);
-        s_lo = (b << kSampleShift) + uint32_t(floor(f * double(1u << kSampleShift)));
-      }
-      if (hi < s && c0 <= hi && hi < c1) {
-        const double f = (hi + 1.0 - c0) / double(loc[i]);
-        s_hi = (b << kSampleShift) + uint32_t(fmin(ceil(f * double(1u << kSampleShift)),
-                                                   double((1u << kSampleShift) - 1u)));
-      }
-      cum += loc[i];
+    rank_bins_256(h, lo, hi < s ? hi : -1.0, sm);
+    if (lo >= 0.0 && sm.bin[0] != 0xFFFFFFFFu) {
+      st.prefix = sm.bin[0];
+      st.rank = uint32_t(lo - double(sm.below[0]));
     }
-    __syncthreads();
-    if (s_lo != 0xFFFFFFFFu) klo = max(1u, s_lo);
-    if (s_hi != 0xFFFFFFFFu) khi = min(0x7F800000u, s_hi);
-    // leave the histogram zeroed for the next call
+    if (hi < s && sm.bin[1] != 0xFFFFFFFFu) {
+      st.kept = sm.bin[1];
+      st.n_sel = uint32_t(hi - double(sm.below[1]));
+    }
+  }
+  if (threadIdx.x == 0) state[item] = st;
+}
+
+// Fine histograms (128-ulp bins) of the sample keys inside the two coarse
+// bins, over the same sample works as k_sample.
+__global__ void __launch_bounds__(kTileThreads) k_sample_fine(const EncItem* __restrict__ items,
+                                                              const SelState* __restrict__ state,
+                                                              uint32_t n_items, uint64_t total,
+                                                              uint32_t* __restrict__ sample_hist) {
+  uint64_t w0, w1;
+  cta_range(total, w0, w1);
+  uint32_t it = w0 < w1 ? find_sample_item(items, n_items, w0) : 0;
+  constexpr int kU = 4;
+  for (uint64_t w = w0; w < w1; w += kU) {
+    float v[kU][4];
+    uint32_t wit[kU];
+    bool ok[kU];
+    uint64_t pos[kU];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) h[threadIdx.x * kPer + i] = 0;
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t wu = w + u;
+      ok[u] = wu < w1;
+      while (ok[u] && it + 1 < n_items && items[it + 1].sample_begin <= wu) ++it;
+      wit[u] = it;
+      const EncItem& e = items[it];
+      pos[u] = ok[u] ? (wu - e.sample_begin) * uint64_t(e.sample_stride) * kTile + 4ull * threadIdx.x : 0;
+      ok[u] = ok[u] && pos[u] < e.n;
+      if (ok[u]) load_combined(e, uint32_t(pos[u]), v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!ok[u]) continue;
+      const uint32_t n = items[wit[u]].n;
+      const uint32_t blo = __ldg(&state[wit[u]].prefix), bhi = __ldg(&state[wit[u]].kept);
+      uint32_t* h = sample_hist + uint64_t(wit[u]) * kSampleStride;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (pos[u] + j >= n) continue;
+        const uint32_t key = mag_key(v[u][j]);
+        const uint32_t cb = key >> kSampleShift, fb = (key >> kFineShift) & (kSampleBins - 1u);
+        if (cb == blo) atomicAdd(h + kSampleBins + fb, 1u);
+        if (cb == bhi) atomicAdd(h + 2 * kSampleBins + fb, 1u);
+      }
+    }
+  }
+}
+
+// One CTA per item: the window from the fine bins (sampled items) or the
+// default window, and the fused pass's fine-bin shift. Leaves the item's
+// histograms zeroed for the next call.
+__global__ void __launch_bounds__(256) k_window_fine(const EncItem* __restrict__ items,
+                                                     SelState* __restrict__ state,
+                                                     uint32_t* __restrict__ sample_hist) {
+  __shared__ RankBinSmem sm;
+  const uint32_t item = blockIdx.x;
+  const EncItem e = items[item];
+  uint32_t klo = 1u, khi = 0x7F800000u;  // no sample: every nonzero key is a candidate
+  if (e.sample_tiles > 0) {
+    uint32_t* h = sample_hist + uint64_t(item) * kSampleStride;
+    const SelState sc = state[item];
+    if (sc.prefix != 0xFFFFFFFFu) {
+      rank_bins_256(h + kSampleBins, double(sc.rank), -1.0, sm);
+      if (sm.bin[0] != 0xFFFFFFFFu) klo = max(1u, (sc.prefix << kSampleShift) | (sm.bin[0] << kFineShift));
+    }
+    if (sc.kept != 0xFFFFFFFFu) {
+      rank_bins_256(h + 2 * kSampleBins, double(sc.n_sel), -1.0, sm);
+      if (sm.bin[0] != 0xFFFFFFFFu)
+        khi = min(0x7F800000u, (sc.kept << kSampleShift) | (sm.bin[0] << kFineShift) | ((1u << kFineShift) - 1u));
+    }
+    uint4* h4 = reinterpret_cast<uint4*>(h);
+    for (uint32_t i = threadIdx.x; i < kSampleStride / 4; i += blockDim.x) h4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (e.c == 0) {  // tau = 0 without selection: every nonzero key is kept
     klo = 1u;
@@ -928,11 +1029,20 @@ __global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restric
   // (2) the target sub-bin's keys
   const uint2* ck = cand + e.cand_off;
   const uint32_t nc = min(s.cnt_in, e.cand_cap);
-  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
-    const uint32_t key = ck[i].y & 0x7FFFFFFFu;
-    if (((key - s.klo) >> s.fshift) == sub) {
-      const uint32_t idx = atomicAdd(&s_n, 1u);
-      if (idx < kFinalKeys) keys[idx] = key;
+  constexpr uint32_t kB = 8;  // candidate loads in flight per thread
+  for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += kB * blockDim.x) {
+    uint32_t kk[kB];
+#pragma unroll
+    for (uint32_t b = 0; b < kB; ++b) {
+      const uint32_t i = i0 + b * blockDim.x;
+      kk[b] = i < nc ? (__ldcs(&ck[i].y) & 0x7FFFFFFFu) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (uint32_t b = 0; b < kB; ++b) {
+      if (kk[b] != 0xFFFFFFFFu && ((kk[b] - s.klo) >> s.fshift) == sub) {
+        const uint32_t idx = atomicAdd(&s_n, 1u);
+        if (idx < kFinalKeys) keys[idx] = kk[b];
+      }
     }
   }
   __syncthreads();
@@ -978,7 +1088,9 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
                                                const uint2* __restrict__ cand, const HashParams hp,
                                                const uint32_t* __restrict__ err) {
   __shared__ uint32_t pref[kMaxFlatItems + 1];
+  __shared__ uint32_t s_tau[kMaxFlatItems];
   if (err[0]) return;
+  for (uint32_t i = threadIdx.x; i < n_items; i += blockDim.x) s_tau[i] = state[i].tau_key;
   const uint32_t total = flat_prefix(n_items, [&](uint32_t i) {
     return state[i].status == kStatusReady ? min(state[i].cnt_in, items[i].cand_cap) : 0u;
   }, pref);
@@ -992,7 +1104,7 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
     if (j < total) {
       it = flat_item(pref, n_items, j);
       kv = cand[items[it].cand_off + (j - pref[it])];
-      keep = (kv.y & 0x7FFFFFFFu) > state[it].tau_key;
+      keep = (kv.y & 0x7FFFFFFFu) > s_tau[it];
     }
     // kept counts, aggregated over the lanes of the same item
     const uint32_t grp = __match_any_sync(kFull, it);
@@ -1423,7 +1535,13 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
                0, stream>>>(items, n_items, total_samples, sample_hist, span);
     ++launches;
   }
-  k_window<<<n_items, 256, 0, stream>>>(items, state, sample_hist, span);
+  if (total_samples) {
+    k_window_coarse<<<n_items, 256, 0, stream>>>(items, state, sample_hist, span);
+    k_sample_fine<<<persistent_grid((const void*)k_sample_fine, kTileThreads, di, total_samples), kTileThreads,
+                    0, stream>>>(items, state, n_items, total_samples, sample_hist);
+    launches += 2;
+  }
+  k_window_fine<<<n_items, 256, 0, stream>>>(items, state, sample_hist);
   // every item of a batch shares the path: hook (accumulator) or per-stage outputs
   const bool hook = per_stage == 0;
   auto launch = [&](auto kern) {
@@ -1454,8 +1572,8 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
   if (n_items == 0) return 0;
   k_finish_select<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, cand, err);
   (void)sel_list;
-  if (w4) k_fixup<true><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
-  else k_fixup<false><<<di.sms * 2, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
+  if (w4) k_fixup<true><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
+  else k_fixup<false><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
   // bracket-miss repair: one cooperative launch that exits at once unless some item fell back
   auto launch_fb = [&](auto kern) {
     int per_sm = 0;

@@ -388,7 +388,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     e.sample_stride = 0;
     e.sample_tiles = 0;
     if (select && e.n > kSmallSegment) {
-      const uint64_t stride = std::max<uint64_t>(1, std::min<uint64_t>(8, t / 16));
+      const uint64_t stride = std::max<uint64_t>(1, std::min<uint64_t>(kSampleMaxStride, t / 16));
       e.sample_stride = uint32_t(stride);
       e.sample_tiles = uint32_t((t + stride - 1) / stride);
       samples += e.sample_tiles;
@@ -408,7 +408,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   uint32_t* err = err_flag();
   zero({{err, 16}});
   if (select) {
-    auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleBins * 4, true, stream_));
+    auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleStride * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
     auto* fine = static_cast<uint32_t*>(ws_.get("fine_hist", size_t(n) * kRadixBins * 4, true, stream_));
     auto* cd = static_cast<uint2*>(ws_.get("cand", cand * 8, false, stream_));
