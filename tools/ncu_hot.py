@@ -1,12 +1,13 @@
 """Top source lines / SASS instructions by stall samples from an .ncu-rep source page.
-usage: ncu_hot.py REP [cuda|sass] [N]"""
+usage: ncu_hot.py REP [cuda|sass] [N] [KERNEL_REGEX]"""
 import csv
 import subprocess
 import sys
 
 rep, view = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else "cuda")
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+kfilter = ["-k", "regex:" + sys.argv[4]] if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep] + kfilter + ["--page", "source", "--csv", "--print-source",
                       "cuda,sass" if view == "cuda" else view],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
