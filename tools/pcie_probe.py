@@ -1,0 +1,46 @@
+"""PCIe bandwidth of this box: pinned H2D, D2H and both at once (two
+streams), 498 MB each (the bench's per-step gradient / decoded shard)."""
+import torch
+
+n = 124_439_808
+h_in = torch.empty(n, dtype=torch.float32, pin_memory=True)
+h_out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+d_in = torch.empty(n, device="cuda")
+d_out = torch.zeros(n, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def timed(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    torch.cuda.current_stream().wait_stream(s1)
+    torch.cuda.current_stream().wait_stream(s2)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def h2d():
+    with torch.cuda.stream(s1):
+        d_in.copy_(h_in, non_blocking=True)
+
+
+def d2h():
+    with torch.cuda.stream(s2):
+        h_out.copy_(d_out, non_blocking=True)
+
+
+def both():
+    h2d()
+    d2h()
+
+
+for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    ms = timed(fn)
+    print(f"{name}: {ms:.3f} ms per copy set = {n * 4 / ms / 1e6:.1f} GB/s per direction")
