@@ -33,7 +33,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 THETA, RATIO, WIDTH, SEED = 99.0, 10, 4, 77
-WORKLOAD = "gpt2-small-124M-tied/non_attention_linear/theta99/r10/w4"
+WORKLOADS = {  # --workload: BASELINE config 2 (default) and config 3's layer layout
+    "gpt2": "gpt2-small-124M-tied/non_attention_linear/theta99/r10/w4",
+    "llama3-8b": "llama3-8b-8.03B/non_attention_linear/theta99/r10/w4",
+}
+WORKLOAD = WORKLOADS["gpt2"]
 METRIC = "uncompressed-equivalent gradient GB/s per sync (encode+RS+decode)"
 
 
@@ -96,10 +100,10 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload_specs():
+def workload_specs(name="gpt2"):
     import paper_2504_05638_b200 as tagc
 
-    return tagc.gpt2_specs()
+    return tagc.llama3_8b_specs() if name == "llama3-8b" else tagc.gpt2_specs()
 
 
 def cfg_obj():
@@ -129,109 +133,10 @@ def algorithmic_bytes(shards, rank, world):
     return comp, fused
 
 
-def run_b200(args):
-    import numpy as np
+def extra_sections(args, tagc, ctx, shards, grad, acc, out, owned, total, n_params, specs, stream, dev, local,
+                   world, step, barrier, max_over_ranks, e0, e1):
+    """Uncompressed comparator, owner step, overlap and e2e (GPT-2 workload)."""
     import torch
-    import torch.distributed as dist
-
-    import paper_2504_05638_b200 as tagc
-
-    world = args.gpus
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = f"cuda:{local}"
-    specs = workload_specs()
-    shards = tagc.make_shards(specs, world, world)
-    total = shards[-1].end
-    n_params = sum(s.param_count for s in specs)
-    cfg = cfg_obj()
-
-    stream = torch.cuda.Stream(device=local)
-    torch.cuda.set_stream(stream)
-    ctx = tagc.Context(cfg, world_size=world, rank=rank, device=local, stream=stream.cuda_stream)
-    if world > 1 and args.exchange == "peer":  # pulls over NVLink peer memory (CUDA IPC), no NCCL
-        handles = [None] * world
-        dist.all_gather_object(handles, ctx.peer_prepare(shards))
-        ctx.peer_open(handles)
-    elif world > 1:
-        obj = [tagc.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.init_nccl(obj[0])
-
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 + rank)
-    grad = torch.empty(total, device=dev)
-    mag = torch.randn(total, device=dev, generator=gen).exp_()
-    sign = torch.randint(0, 2, (total,), device=dev, generator=gen, dtype=torch.int8)
-    grad.copy_(torch.where(sign.bool(), -mag, mag))
-    del mag, sign
-    if total > n_params:
-        grad[n_params:] = 0.0  # make_shards pad tail
-    acc = torch.zeros(total, device=dev)
-    owned = sum(s.size() for s in shards if s.owner == rank)
-    out = torch.empty(max(owned, 1), device=dev)
-    torch.cuda.synchronize()
-
-    def step(stats=False):
-        return ctx.tagc_reduce_shards(shards, grad, acc, out, stats=stats)
-
-    for _ in range(args.warmup):
-        step()
-    _, st = step(stats=True)  # untimed: peel statistics of this config
-    rounds = ctx.last_peel_rounds()
-    ctx.set_timing(True)
-    step()
-    stage_ms = ctx.last_timing()
-    launches_per_step = ctx.last_launches()
-    ctx.set_timing(False)
-
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    clocks = ClockSampler(local)
-    barrier()
-    clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    clk = clocks.stop()
-
-    # per-stage device time of one step with stage events (prep, sampled select +
-    # fused split/encode, select finish, exchange, decode)
-    # (each timed call starts on an idle stream: stage events recorded behind a
-    # queue of earlier calls were seen to be stamped late)
-    # The roofline kernel's duration comes from device-side %globaltimer
-    # stamps the kernels write in timing mode (earliest CTA start of k_sample
-    # to latest CTA end of k_fused), averaged over the timed launches.
-    ctx.set_timing(True)
-    stage_acc = [0.0] * 5
-    span_acc = [0.0, 0.0]
-    for _ in range(args.steps):
-        ctx.sync()
-        step()
-        t = ctx.last_timing()
-        stage_acc = [a + b for a, b in zip(stage_acc, t)]
-        span_acc = [a + b for a, b in zip(span_acc, ctx.last_kernel_spans())]
-    ctx.set_timing(False)
-    stage_ms = [a / args.steps for a in stage_acc]
-    span_ms = [a / args.steps for a in span_acc]
 
     # uncompressed comparator: ncclReduceScatter fp32 of the same shards
     base_out = torch.empty(shards[0].size(), device=dev)
@@ -381,13 +286,134 @@ def run_b200(args):
     pcie_ms = max_over_ranks(pc0.elapsed_time(pc1))
     del grad_bw_probe
 
+    uncompressed = n_params * 4.0
+    e2e = {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4), "steps": e2e_steps,
+           "pcie_bound": round(world * uncompressed / (pcie_ms * 1e-3) / 1e9, 3),
+           "pcie_bound_note": "the same H2D + D2H bytes as plain concurrent copies, no exchange"}
+    return base_ms, owner_step, overlap, e2e
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_05638_b200 as tagc
+
+    world = args.gpus
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = f"cuda:{local}"
+    specs = workload_specs(args.workload)
+    big = args.workload != "gpt2"  # 8B parameters: no room for the owner-step / overlap / e2e buffers
+    shards = tagc.make_shards(specs, world, world)
+    total = shards[-1].end
+    n_params = sum(s.param_count for s in specs)
+    cfg = cfg_obj()
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    ctx = tagc.Context(cfg, world_size=world, rank=rank, device=local, stream=stream.cuda_stream)
+    if world > 1 and args.exchange == "peer":  # pulls over NVLink peer memory (CUDA IPC), no NCCL
+        handles = [None] * world
+        dist.all_gather_object(handles, ctx.peer_prepare(shards))
+        ctx.peer_open(handles)
+    elif world > 1:
+        obj = [tagc.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_nccl(obj[0])
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    grad = torch.empty(total, device=dev)
+    chunk = 1 << 26  # generated in chunks: the temporaries of an 8B-element draw would not fit
+    for c0 in range(0, total, chunk):
+        c1 = min(total, c0 + chunk)
+        mag = torch.randn(c1 - c0, device=dev, generator=gen).exp_()
+        sign = torch.randint(0, 2, (c1 - c0,), device=dev, generator=gen, dtype=torch.int8)
+        grad[c0:c1] = torch.where(sign.bool(), -mag, mag)
+    del mag, sign
+    if total > n_params:
+        grad[n_params:] = 0.0  # make_shards pad tail
+    acc = torch.zeros(total, device=dev)
+    owned = sum(s.size() for s in shards if s.owner == rank)
+    out = torch.empty(max(owned, 1), device=dev)
+    torch.cuda.synchronize()
+
+    def step(stats=False):
+        return ctx.tagc_reduce_shards(shards, grad, acc, out, stats=stats)
+
+    for _ in range(args.warmup):
+        step()
+    _, st = step(stats=True)  # untimed: peel statistics of this config
+    rounds = ctx.last_peel_rounds()
+    ctx.set_timing(True)
+    step()
+    stage_ms = ctx.last_timing()
+    launches_per_step = ctx.last_launches()
+    ctx.set_timing(False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    clk = clocks.stop()
+
+    # per-stage device time of one step with stage events (prep, sampled select +
+    # fused split/encode, select finish, exchange, decode)
+    # (each timed call starts on an idle stream: stage events recorded behind a
+    # queue of earlier calls were seen to be stamped late)
+    # The roofline kernel's duration comes from device-side %globaltimer
+    # stamps the kernels write in timing mode (earliest CTA start of k_sample
+    # to latest CTA end of k_fused), averaged over the timed launches.
+    ctx.set_timing(True)
+    stage_acc = [0.0] * 5
+    span_acc = [0.0, 0.0]
+    for _ in range(args.steps):
+        ctx.sync()
+        step()
+        t = ctx.last_timing()
+        stage_acc = [a + b for a, b in zip(stage_acc, t)]
+        span_acc = [a + b for a, b in zip(span_acc, ctx.last_kernel_spans())]
+    ctx.set_timing(False)
+    stage_ms = [a / args.steps for a in stage_acc]
+    span_ms = [a / args.steps for a in span_acc]
+
+    base_ms = owner_step = overlap = e2e = None
+    if not big:
+        base_ms, owner_step, overlap, e2e = extra_sections(
+            args, tagc, ctx, shards, grad, acc, out, owned, total, n_params, specs, stream, dev, local, world,
+            step, barrier, max_over_ranks, e0, e1)
     comp, fused_bytes = algorithmic_bytes(shards, rank, world)
     hbm, peak_kind = peaks()
     fused_ms = span_ms[0]
     achieved = fused_bytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fused_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.workload == "gpt2":  # captured on the default workload
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get("bytes_per_launch")
@@ -410,20 +436,17 @@ def run_b200(args):
         "dtype": "f32",
         "data": "synthetic log-normal gradients (SyntheticStream distribution), generated on device",
         "config": {
-            "workload": WORKLOAD,
+            "workload": WORKLOADS[args.workload],
             "params_per_rank": n_params,
-            "shards": f"make_shards(gpt2_small, {world}, {world})",
+            "shards": f"make_shards({args.workload}, {world}, {world})",
             "compressed_params_per_rank": comp,
             "peel": {"presence": st.presence, "peeled": st.peeled, "unresolved": st.unresolved,
                      "rounds": rounds[0], "tail_rounds": rounds[1]},
-            "l2": "inputs larger than L2 (498 MB per rank)",
+            "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per rank)",
             "parallelism": f"dp{world} (one process per GPU, "
                            f"{'peer-memory pulls' if args.exchange == 'peer' else 'NCCL reduce-scatter'})",
         },
-        "e2e": {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-                "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4), "steps": e2e_steps,
-                "pcie_bound": round(world * uncompressed / (pcie_ms * 1e-3) / 1e9, 3),
-                "pcie_bound_note": "the same H2D + D2H bytes as plain concurrent copies, no exchange"},
+        "e2e": e2e if e2e is not None else {"skipped": "8B-parameter workload: host buffers not allocated"},
         "roofline": {"kernel": "k_fused_tma (TMA-staged select/split/index/sketch scatter)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
@@ -435,14 +458,14 @@ def run_b200(args):
         "stages_ms": {"prep": round(stage_ms[0], 4), "select_fused": round(stage_ms[1], 4),
                       "select_finish": round(stage_ms[2], 4), "exchange": round(stage_ms[3], 4),
                       "decode": round(stage_ms[4], 4)},
-        "uncompressed_rs": {"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
-                            "unit": "GB/s", "ms_per_step": round(base_ms, 4)},
+        "uncompressed_rs": ({"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
+                             "unit": "GB/s", "ms_per_step": round(base_ms, 4)} if base_ms else None),
         "owner_step": owner_step,
         "overlap": overlap,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
         result["cpu_baseline"] = cpu_baseline(args, specs, world, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -545,6 +568,8 @@ def main():
                     help="params per rank in the bounded CPU-reference sample")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="gpt2", choices=sorted(WORKLOADS),
+                    help="gpt2 (BASELINE config 2, the default line) or llama3-8b (config 3's layout)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N>1 collective: grouped ncclReduceScatter, or pulls over peer memory")
     args = ap.parse_args()

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtagc_b200.so")
+LIB_PATH = os.environ.get("TAGC_LIB_PATH", os.path.join(HERE, "libtagc_b200.so"))  # override: A/B experiments
 
 OK, RUNTIME, INVALID = 0, 1, 2
 

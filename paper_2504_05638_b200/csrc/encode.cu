@@ -635,7 +635,9 @@ constexpr uint32_t kWarpStageT = 64;
 struct alignas(128) FusedStage {
   float g[kTile];
   float a[kTile];
+  unsigned long long tile;  // which tile the stage holds (kNoTile: the producer is done)
 };
+constexpr unsigned long long kNoTile = ~0ull;
 constexpr size_t kFusedSmem = size_t(kFusedStages) * sizeof(FusedStage) + 2 * kFusedStages * 8 + 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
                                                                 uint2* __restrict__ hi_pool,
                                                                 uint32_t* __restrict__ fine_hist,
                                                                 uint32_t* __restrict__ err,
-                                                                unsigned long long* span) {
+                                                                unsigned long long* span, uint32_t chunk) {
   extern __shared__ __align__(128) unsigned char fsm[];
   FusedStage* stg = reinterpret_cast<FusedStage*>(fsm);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(fsm + size_t(kFusedStages) * sizeof(FusedStage));
@@ -696,9 +698,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
   __shared__ uint32_t s_zero, s_lo;
   span_begin(span);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t t0, t1;
-  cta_range(total_tiles, t0, t1);
-  if (t0 >= t1) return;
+  // Tile order. chunk == 0: the contiguous balanced range of cta_range (every
+  // sketch fits in L2 together). Otherwise the producer claims `chunk`-tile
+  // chunks from a global counter (err[3]), so all CTAs advance through the
+  // shard together inside a window of about G x chunk tiles and the sketch
+  // rows being scattered into stay L2-resident even when the shard's
+  // sketches total GBs (Llama-3-8B: 2.9 GB per rank). Consumers read each
+  // stage's tile id from the stage itself.
+  uint64_t t0 = 0, t1 = 0;
+  if (chunk == 0) {
+    cta_range(total_tiles, t0, t1);
+    if (t0 >= t1) return;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&full[s], 1);
@@ -712,13 +723,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
     if (lane == 0) {
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      uint32_t pit = find_tile_item(items, n_items, t0);
+      uint32_t pit = 0;
       uint32_t i = 0;
-      for (uint64_t tile = t0; tile < t1; ++tile, ++i) {
-        while (tile >= items[pit].tile_begin + (uint64_t(items[pit].n) + kTile - 1) / kTile) ++pit;
-        const EncItem& pe = items[pit];
+      auto push = [&](uint64_t tile) {
         const int s = int(i % kFusedStages);
         if (i >= uint32_t(kFusedStages)) mbar_wait(&empty[s], ((i / kFusedStages) - 1) & 1u);
+        ++i;
+        stg[s].tile = tile;
+        if (tile == kNoTile) {
+          mbar_arrive(&full[s]);
+          return;
+        }
+        while (tile >= items[pit].tile_begin + (uint64_t(items[pit].n) + kTile - 1) / kTile) ++pit;
+        const EncItem& pe = items[pit];
         const uint32_t start = uint32_t(tile - pe.tile_begin) * kTile;
         const uint32_t len = min(kTile, pe.n - start);
         const uint32_t bytes = (len * 4u) & ~15u;
@@ -727,7 +744,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
           bulk_g2s(stg[s].g, pe.g + start, bytes, &full[s], policy);
           bulk_g2s(stg[s].a, pe.acc + start, bytes, &full[s], policy);
         }
+      };
+      if (chunk == 0) {
+        pit = find_tile_item(items, n_items, t0);
+        for (uint64_t tile = t0; tile < t1; ++tile) push(tile);
+      } else {
+        for (;;) {
+          const uint64_t c0 = uint64_t(atomicAdd(err + 3, 1u)) * chunk;
+          if (c0 >= total_tiles) break;
+          const uint64_t c1 = min(total_tiles, c0 + chunk);
+          for (uint64_t tile = c0; tile < c1; ++tile) push(tile);
+        }
       }
+      push(kNoTile);
     }
     span_end(span);
     return;
@@ -737,11 +766,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
   const uint32_t ctid = threadIdx.x;
   bool nan = false;
   uint32_t iter = 0;
-  uint32_t it = find_tile_item(items, n_items, t0);
-  for (uint64_t tile = t0; tile < t1;) {
+  // the first tile (tiles arrive in increasing order, items with it); the
+  // contiguous order is known here, the claimed one is read from the stage
+  uint64_t tile = t0;
+  if (chunk != 0) {
+    mbar_wait(&full[0], 0u);
+    tile = *reinterpret_cast<volatile unsigned long long*>(&stg[0].tile);
+  }
+  uint32_t it = tile == kNoTile ? 0u : find_tile_item(items, n_items, tile);
+  while (tile != kNoTile) {
+    while (tile >= items[it].tile_begin + (uint64_t(items[it].n) + kTile - 1) / kTile) ++it;  // skip items with no tile here
     const EncItem e = items[it];
     const uint64_t item_end = e.tile_begin + (uint64_t(e.n) + kTile - 1) / kTile;
-    const uint64_t tend = item_end < t1 ? item_end : t1;
     const uint32_t klo = state[it].klo, khi = state[it].khi, fshift = state[it].fshift;
     const uint32_t n_words = kW4 ? (e.n + 7u) / 8u : (e.n + 31u) / 32u;
     for (uint32_t i = ctid; i < kRadixBins; i += kConsumers) s_hist[i] = 0;
@@ -773,11 +809,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
       __syncwarp();
       wk = 0;
     };
-    for (; tile < tend; ++tile, ++iter) {
+    for (;;) {  // stage `iter` holds `tile`
       const int s = int(iter % kFusedStages);
       const uint32_t start = uint32_t(tile - e.tile_begin) * kTile;
       const uint32_t len = min(kTile, e.n - start);
-      mbar_wait(&full[s], (iter / kFusedStages) & 1u);
+      mbar_wait(&full[s], (iter / kFusedStages) & 1u);  // returns at once after a peek
       float* sg = stg[s].g;
       const float* sa = stg[s].a;
       float v[kQuads][4];
@@ -916,6 +952,16 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
       if (in_m | hi_m) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      // the next tile: same item, or the end of this item's run
+      ++iter;
+      if (chunk == 0) {
+        tile = tile + 1 < t1 ? tile + 1 : kNoTile;
+      } else {  // peek at the next stage
+        const int ns = int(iter % kFusedStages);
+        mbar_wait(&full[ns], (iter / kFusedStages) & 1u);
+        tile = *reinterpret_cast<volatile unsigned long long*>(&stg[ns].tile);
+      }
+      if (tile >= item_end) break;  // kNoTile included
     }
     __syncwarp();
     if (wc) flush_cand();
@@ -1527,7 +1573,7 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
                         int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
                         uint2* hi_pool, uint32_t* err, cudaStream_t stream, unsigned long long* span,
-                        bool tma) {
+                        bool tma, uint64_t sketch_bytes) {
   if (n_items == 0) return 0;
   int launches = 0;
   if (total_samples) {
@@ -1553,8 +1599,13 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       // opt-in to > 48 KB of dynamic shared memory (cheap; per launch keeps it per device)
       cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
       const uint64_t g = std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
+      // one contiguous range per CTA while every sketch fits in L2 together;
+      // beyond that, 64-tile chunks dealt round-robin keep the active window
+      // (G x 64 tiles = 77M elements, ~31 MB of sketch) L2-resident
+      const uint64_t contiguous = (total_tiles + (g ? g : 1) - 1) / (g ? g : 1);
+      const uint32_t chunk = uint32_t(sketch_bytes <= (48ull << 20) ? 0 : std::min<uint64_t>(64, contiguous));
       kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
-                                                                 hi_pool, fine_hist, err, span);
+                                                                 hi_pool, fine_hist, err, span, chunk);
     };
     if (w4) launch_tma(k_fused_tma<true>);
     else launch_tma(k_fused_tma<false>);

@@ -422,9 +422,11 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     for (const EncItem& e : items)
       if (((e.flags & kHasAcc) ? 0 : 1) != per_stage) throw CudaError("mixed fused batch");
     ev_record(1);
+    uint64_t sketch_bytes = 0;  // scattered-into footprint of the batch
+    for (const EncItem& e : items) sketch_bytes += (e.flags & kWriteSketch) ? uint64_t(hp.rows) * e.m * 4 : 0;
     launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
                                      cd, hp_pool, err, stream_, timing_ ? spans_ : nullptr,
-                                     use_tma_ && all_aligned);
+                                     use_tma_ && all_aligned, sketch_bytes);
     ev_record(2);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);

@@ -35,7 +35,7 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
                         uint64_t total_tiles, uint64_t total_samples, const HashParams& hp, bool w4,
                         int per_stage, uint32_t* sample_hist, uint32_t* fine_hist, uint2* cand,
                         uint2* hi_pool, uint32_t* err, cudaStream_t stream,
-                        unsigned long long* span = nullptr, bool tma = false);
+                        unsigned long long* span = nullptr, bool tma = false, uint64_t sketch_bytes = 0);
 // Exact tau from the window candidates, fix-up of the candidates, and the
 // (normally idle) restore + radix-select + re-encode fallback chain.
 int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* state, uint32_t n_items,
