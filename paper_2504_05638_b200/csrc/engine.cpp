@@ -463,8 +463,40 @@ void Engine::ensure_aux() {
   cuda_check(cudaEventCreateWithFlags(&aux_join_, cudaEventDisableTiming), "aux event");
 }
 
+// Decode of a batch of segments whose bucket states are far beyond L2
+// (Llama-3-8B: 5.8 GB at W = 1) in groups of <= kDecodeGroupBytes of state:
+// each group's list build, round-0 peel and frontier rounds then hit a bucket
+// state the group's own REDs just left in L2. Results are those of one batch
+// (segments decode independently); statistics land per item as before.
+void Engine::run_decode_grouped(std::vector<DecItem>& items, const HashParams& hp, bool ordered,
+                                cudaEvent_t zero_done, const std::function<void()>& pre_launch) {
+  constexpr uint64_t kDecodeGroupBytes = 48ull << 20, kGroupAbove = 128ull << 20;
+  uint64_t state_bytes = 0;
+  for (const DecItem& d : items) state_bytes += uint64_t(hp.rows) * d.m * 8;
+  if (ordered || items.size() < 2 || state_bytes <= kGroupAbove) {
+    run_decode(items, hp, false, ordered, zero_done, pre_launch);
+    return;
+  }
+  const uint32_t n = uint32_t(items.size());
+  ws_.get("dec_stats", n * sizeof(DecStats), false, stream_);  // sized once for every group
+  size_t b = 0;
+  bool first = true;
+  while (b < items.size()) {
+    size_t e = b;
+    uint64_t bytes = 0;
+    while (e < items.size() && (e == b || bytes + uint64_t(hp.rows) * items[e].m * 8 <= kDecodeGroupBytes))
+      bytes += uint64_t(hp.rows) * items[e++].m * 8;
+    std::vector<DecItem> group(items.begin() + b, items.begin() + e);
+    run_decode(group, hp, false, false, zero_done, first ? pre_launch : std::function<void()>(), uint32_t(b));
+    first = false;
+    b = e;
+  }
+  dec_stats_.assign(n, DecStats{});
+}
+
 void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
-                        bool ordered, cudaEvent_t zero_done, const std::function<void()>& pre_launch) {
+                        bool ordered, cudaEvent_t zero_done, const std::function<void()>& pre_launch,
+                        uint32_t stats_base) {
   const uint32_t n = uint32_t(items.size());
   dec_stats_.assign(n, DecStats{});
   if (n == 0) {
@@ -504,7 +536,8 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
   w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 64, false, stream_));
-  w.stats = static_cast<DecStats*>(ws_.get("dec_stats", n * sizeof(DecStats), false, stream_));
+  w.stats = static_cast<DecStats*>(ws_.get("dec_stats", (stats_base + n) * sizeof(DecStats), false, stream_)) +
+            stats_base;
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
   // the bucket state is zeroed inside launch_decode (after the output fill)
@@ -1092,7 +1125,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     d.list_cap = presence_bound(p.len, cfg_.theta, W);
     dec.push_back(d);
   }
-  run_decode(dec, hp, false, w == 1 && W > 1, zero_done, pre_decode);
+  run_decode_grouped(dec, hp, w == 1 && W > 1, zero_done, pre_decode);
   if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));

@@ -275,7 +275,9 @@ class Engine {
   // there: nothing that may synchronise the device follows its wait).
   void run_decode(std::vector<DecItem>& items, const HashParams& hp, bool want_unresolved,
                   bool ordered, cudaEvent_t zero_done = nullptr,
-                  const std::function<void()>& pre_launch = nullptr);
+                  const std::function<void()>& pre_launch = nullptr, uint32_t stats_base = 0);
+  void run_decode_grouped(std::vector<DecItem>& items, const HashParams& hp, bool ordered,
+                          cudaEvent_t zero_done, const std::function<void()>& pre_launch);
   // Side stream for bandwidth work that overlaps the latency-bound peel
   // (W == 1 raw-segment copies); fork/join by events.
   cudaStream_t aux_ = nullptr;

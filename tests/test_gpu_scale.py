@@ -68,3 +68,38 @@ def test_density_sweep_256m(theta, ratio):
 def test_one_billion_single_bucket():
     # BASELINE config 5: 2^30-element single bucket, theta 99.9, ratio 10
     check_exchange(1 << 30, 99.9, 10)
+
+
+def test_grouped_decode_many_segments():
+    """Bucket states beyond 128 MB in total (here 3 x 80M-element segments,
+    192 MB of state) are decoded in groups (Engine::run_decode_grouped); the
+    result must be the same property-exact exchange, per segment."""
+    seg = 80 << 20
+    n = 3 * seg
+    cfg = tagc.CompressionConfig(theta=99.0, ratio=10, index_width=4, policy="all_layers", seed=77,
+                                 min_compress_segment=1)
+    shards = [tagc.ShardSpec(0, 0, 0, n, [tagc.LayerSegment(f"s{i}", "feed_forward", i * seg, (i + 1) * seg)
+                                         for i in range(3)])]
+    ctx = tagc.Context(cfg, device=0)
+    grad = lognormal(n, 17)
+    acc = torch.zeros(n, device=DEV)
+    out = torch.empty(n, device=DEV)
+    _, st = ctx.tagc_reduce_shards(shards, grad, acc, out, stats=True)
+    zero = torch.zeros((), device=DEV)
+    n_kept = 0
+    for i in range(3):
+        g, a, o = grad[i * seg:(i + 1) * seg], acc[i * seg:(i + 1) * seg], out[i * seg:(i + 1) * seg]
+        c = math.ceil(99.0 * seg / 100.0)  # sparsify.cpp:30
+        tau = float(a.abs().max())
+        assert int((g.abs() < tau).sum()) < c <= int((g.abs() <= tau).sum())
+        kept = g.abs() > tau
+        assert torch.equal(a.view(torch.int32), torch.where(kept, zero, g).view(torch.int32))
+        ref = torch.where(kept, g, zero)
+        assert torch.equal(o[~kept].view(torch.int32), torch.zeros_like(o[~kept]).view(torch.int32))
+        scale = float(ref.abs().max())
+        assert float(((o - ref).abs() / torch.clamp(ref.abs(), min=scale)).max()) <= 1e-5
+        n_kept += int(kept.sum())
+    assert st.presence == n_kept and st.peeled == n_kept and st.unresolved == 0, st
+    assert st.compressed_segments == 3
+    del grad, acc, out
+    torch.cuda.empty_cache()
