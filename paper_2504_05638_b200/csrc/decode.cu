@@ -224,16 +224,21 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(DecodeWork w) {
   if (threadIdx.x == 0) w.qcount[5] = s_carry <= w.list_cap ? s_carry : 0u;
 }
 
+// Word tiles are claimed one at a time from a counter (qcount[12]), so the
+// CTAs insert into the bucket states of neighbouring tiles together and the
+// REDs meet an L2-resident window of the state instead of all of it.
 __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp) {
   using Scan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_wt;
   const uint32_t total_list = w.qcount[5];
-  uint32_t t0, t1;
-  cta_tiles(w.total_word_tiles, t0, t1);
-  if (t0 >= t1) return;
-  uint32_t it = find_word_item(w.items, w.n_items, t0);
-  for (uint32_t wt = t0; wt < t1; ++wt) {
-    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
+  const uint32_t T = uint32_t(w.total_word_tiles);
+  for (;;) {
+    if (threadIdx.x == 0) s_wt = atomicAdd(&w.qcount[12], 1u);
+    __syncthreads();
+    const uint32_t wt = s_wt;
+    if (wt >= T) break;
+    const uint32_t it = find_word_item(w.items, w.n_items, wt);
     const DecItem& e = w.items[it];
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t P = w4 ? 8u : 32u;
