@@ -46,6 +46,7 @@ enum : uint32_t {
   kSelect = 1u << 5,      // tau from the select pipeline; else tau = 0
   kWriteSparse = 1u << 6, // per-stage sparsify outputs
   kWriteResidual = 1u << 7,
+  kDeferScatter = 1u << 8,  // sketch bigger than L2: kept entries are logged, scattered region by region later
 };
 
 // One (rank, segment) unit of sparsify + encode work.

@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
       for (uint32_t i = lane; i < wk; i += 32) {
         const uint2 kv = s_kept[warp][i];
         const float v = __uint_as_float(kv.y);
-        if (kHook) scatter_sketch(e, hp, kv.x, v);
+        if (kHook && !(e.flags & kDeferScatter)) scatter_sketch(e, hp, kv.x, v);
         if (base + i < e.hi_cap) {
           hi_pool[e.hi_off + base + i] = kv;
         } else if (kHook) {  // pool full (bracket miss): keep v recoverable
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_fused(const EncItem* __rest
           if (!direct) {
             s_kept[warp][wk + o] = kv;
           } else {
-            if (kHook) scatter_sketch(e, hp, kv.x, x);
+            if (kHook && !(e.flags & kDeferScatter)) scatter_sketch(e, hp, kv.x, x);
             if (gbase + o < e.hi_cap) hi_pool[e.hi_off + gbase + o] = kv;
             else hi_m &= ~(1u << b);  // pool full: the element keeps v in place
           }
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
       for (uint32_t i = lane; i < wk; i += 32) {
         const uint2 kv = s_kept[warp][i];
         const float v = __uint_as_float(kv.y);
-        scatter_sketch(e, hp, kv.x, v);
+        if (!(e.flags & kDeferScatter)) scatter_sketch(e, hp, kv.x, v);
         if (base + i < e.hi_cap) hi_pool[e.hi_off + base + i] = kv;
         else e.acc[kv.x] = v;  // pool full (bracket miss): keep v recoverable
       }
@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
           if (!direct) {
             s_kept[warp][wk + o] = kv;
           } else {
-            scatter_sketch(e, hp, kv.x, x);
+            if (!(e.flags & kDeferScatter)) scatter_sketch(e, hp, kv.x, x);
             if (gbase + o < e.hi_cap) hi_pool[e.hi_off + gbase + o] = kv;
             else hi_m &= ~(1u << b);  // pool full: the element keeps v in place
           }
@@ -1132,7 +1132,7 @@ template <bool kW4>
 __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items,
                                                SelState* __restrict__ state, uint32_t n_items,
                                                const uint2* __restrict__ cand, const HashParams hp,
-                                               const uint32_t* __restrict__ err) {
+                                               const uint32_t* __restrict__ err, uint2* __restrict__ hi_pool) {
   __shared__ uint32_t pref[kMaxFlatItems + 1];
   __shared__ uint32_t s_tau[kMaxFlatItems];
   if (err[0]) return;
@@ -1167,7 +1167,127 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
       if (kW4) red_or_u32(e.index + (p >> 3), 1u << (4u * (p & 7u)));
       else red_or_u32(e.index + (p >> 5), 1u << (p & 31u));
     }
-    if (e.flags & kWriteSketch) scatter_sketch(e, hp, p, v);
+    if ((e.flags & kWriteSketch) && !(e.flags & kDeferScatter)) {
+      scatter_sketch(e, hp, p, v);
+    } else if (e.flags & kWriteSketch) {  // log it with the speculatively kept: the deferred scatter takes both
+      const uint32_t dm = km;  // the kept lanes of this item, all on this branch
+      const uint32_t leader = __ffs(dm) - 1;
+      uint32_t b0 = 0;
+      if (lane == leader) b0 = atomicAdd(&state[it].cnt_hi, __popc(dm));
+      b0 = __shfl_sync(dm, b0, leader);
+      const uint32_t slot = b0 + __popc(dm & ((1u << lane) - 1u));
+      if (slot < e.hi_cap) hi_pool[e.hi_off + slot] = kv;  // kept <= n - c < hi_cap
+    }
+  }
+}
+
+// --------------------------------------------------------------- deferred scatter
+// Items whose sketch is far bigger than L2 (kDeferScatter) skip the sketch
+// REDs in the fused pass and in k_fixup: every kept entry (pos, v) is logged
+// in the item's hi_pool instead. Once tau is final, the (entry, row) updates
+// are bucketed by 16 MB region of the sketch address space (a counting sort)
+// and applied region by region, so the REDs hit L2 instead of
+// read-modify-writing random DRAM sectors. Same sums as the direct scatter;
+// only the float summation order differs, as it does between any two runs
+// of the direct scatter.
+constexpr uint32_t kRegionShift = 22;  // 4M floats = 16 MB per region
+constexpr uint32_t kMaxRegions = 4096;
+
+__device__ __forceinline__ uint32_t ds_entries(const EncItem& e, const SelState& st) {
+  return (st.status == kStatusReady && (e.flags & kDeferScatter) && (e.flags & kWriteSketch))
+             ? min(st.cnt_hi, e.hi_cap) : 0u;
+}
+
+// Per-CTA contiguous range of the flattened entries; every CTA reserves
+// its region slices with one atomic per region, then places its records.
+__global__ void __launch_bounds__(256) k_ds_count(const EncItem* __restrict__ items,
+                                                  const SelState* __restrict__ state, uint32_t n_items,
+                                                  const uint2* __restrict__ hi_pool, const HashParams hp,
+                                                  const float* base, uint32_t* __restrict__ region_count) {
+  __shared__ uint32_t pref[kMaxFlatItems + 1];
+  __shared__ uint32_t hist[kMaxRegions];
+  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x) hist[i] = 0;
+  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i]); }, pref);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
+    const uint32_t it = flat_item(pref, n_items, j);
+    const EncItem& e = items[it];
+    const uint32_t p = hi_pool[e.hi_off + (j - pref[it])].x;
+    const uint64_t sk = uint64_t(e.sketch - base);
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      const uint64_t off = sk + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
+      atomicAdd(&hist[off >> kRegionShift], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x)
+    if (hist[i]) atomicAdd(region_count + i, hist[i]);
+}
+
+// Exclusive scan of the region counts into cursors (one CTA); counts are
+// left zeroed for the next call.
+__global__ void __launch_bounds__(1024) k_ds_scan(uint32_t* __restrict__ region_count,
+                                                  uint32_t* __restrict__ cursor, uint32_t* __restrict__ n_records) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int kPer = kMaxRegions / 1024;
+  uint32_t v[kPer], sum = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    v[k] = region_count[threadIdx.x * kPer + k];
+    region_count[threadIdx.x * kPer + k] = 0;
+    sum += v[k];
+  }
+  uint32_t off, total;
+  Scan(tmp).ExclusiveSum(sum, off, total);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    cursor[threadIdx.x * kPer + k] = off;
+    off += v[k];
+  }
+  if (threadIdx.x == 0) *n_records = total;
+}
+
+__global__ void __launch_bounds__(256) k_ds_place(const EncItem* __restrict__ items,
+                                                  const SelState* __restrict__ state, uint32_t n_items,
+                                                  const uint2* __restrict__ hi_pool, const HashParams hp,
+                                                  const float* base, uint32_t* __restrict__ cursor,
+                                                  uint2* __restrict__ records) {
+  __shared__ uint32_t pref[kMaxFlatItems + 1];
+  __shared__ uint32_t hist[kMaxRegions];
+  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x) hist[i] = 0;
+  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i]); }, pref);
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t j0 = min(total, blockIdx.x * per), j1 = min(total, j0 + per);
+  auto each = [&](auto&& f) {
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const uint32_t it = flat_item(pref, n_items, j);
+      const EncItem& e = items[it];
+      const uint2 kv = hi_pool[e.hi_off + (j - pref[it])];
+      const uint64_t sk = uint64_t(e.sketch - base);
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+        const uint64_t off = sk + uint64_t(r) * e.m + dev_bucket(hp.row[r], kv.x, e.m, e.mmul);
+        f(off, dev_sign(hp.row[r], kv.x) * __uint_as_float(kv.y));
+      }
+    }
+  };
+  each([&](uint64_t off, float) { atomicAdd(&hist[off >> kRegionShift], 1u); });
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x)
+    if (hist[i]) hist[i] = atomicAdd(cursor + i, hist[i]);  // this CTA's slice of region i
+  __syncthreads();
+  each([&](uint64_t off, float x) {
+    const uint32_t slot = atomicAdd(&hist[off >> kRegionShift], 1u);
+    records[slot] = make_uint2(uint32_t(off), __float_as_uint(x));
+  });
+}
+
+// Records in region order, grid-stride: all CTAs sweep the regions together.
+__global__ void __launch_bounds__(256) k_ds_apply(const uint2* __restrict__ records,
+                                                  const uint32_t* __restrict__ n_records, float* base) {
+  const uint32_t total = *n_records;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint2 r = __ldcs(records + i);
+    red_add_f32(base + r.x, __uint_as_float(r.y));
   }
 }
 
@@ -1623,8 +1743,8 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
   if (n_items == 0) return 0;
   k_finish_select<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, cand, err);
   (void)sel_list;
-  if (w4) k_fixup<true><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
-  else k_fixup<false><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err);
+  if (w4) k_fixup<true><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err, hi_pool);
+  else k_fixup<false><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err, hi_pool);
   // bracket-miss repair: one cooperative launch that exits at once unless some item fell back
   auto launch_fb = [&](auto kern) {
     int per_sm = 0;
@@ -1699,6 +1819,21 @@ __global__ void k_set_opt(OptEpilogue* dst, OptEpilogue o) { *dst = o; }
 int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream) {
   k_set_opt<<<1, 1, 0, stream>>>(dev_opt, o);
   return 1;
+}
+
+int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
+                            const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
+                            uint32_t* region_count, uint32_t* cursor, uint32_t* n_records, uint2* records,
+                            cudaStream_t stream) {
+  if (!n_items) return 0;
+  if (span_floats > (uint64_t(kMaxRegions) << kRegionShift) || span_floats > 0xFFFFFFFFull)
+    return -1;  // caller scatters directly
+  const int g = di.sms * 4;
+  k_ds_count<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, region_count);
+  k_ds_scan<<<1, 1024, 0, stream>>>(region_count, cursor, n_records);
+  k_ds_place<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, cursor, records);
+  k_ds_apply<<<di.sms * 8, 256, 0, stream>>>(records, n_records, base);
+  return 4;
 }
 
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream) {

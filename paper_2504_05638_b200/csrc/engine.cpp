@@ -152,6 +152,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
   if (const char* v = std::getenv("TAGC_FUSED_TMA")) use_tma_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_GRAPHS")) graphs_on_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_SIDE_STREAM")) side_stream_ = std::atoi(v) != 0;
+  if (const char* v = std::getenv("TAGC_DEFER_SCATTER_BYTES")) defer_scatter_bytes_ = std::strtoull(v, nullptr, 10);
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -402,6 +403,32 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     hi += e.hi_cap;
   }
   for (EncItem& e : items) e.mmul = fastmod_magic(e.m);
+  // Sketches far beyond L2: defer their scatter to the region-ordered pass
+  // (exchange path only, with selection; one span of < 2^32 floats).
+  float* ds_base = nullptr;
+  uint64_t ds_span = 0, ds_cap = 0;
+  {
+    const float* lo = nullptr;
+    const float* hi_end = nullptr;
+    auto big = [&](const EncItem& e) {
+      return select && (e.flags & kHasAcc) && (e.flags & kWriteSketch) &&
+             uint64_t(hp.rows) * e.m * 4 > defer_scatter_bytes_;
+    };
+    for (const EncItem& e : items)
+      if (big(e)) {
+        if (!lo || e.sketch < lo) lo = e.sketch;
+        if (!hi_end || e.sketch + uint64_t(hp.rows) * e.m > hi_end) hi_end = e.sketch + uint64_t(hp.rows) * e.m;
+      }
+    if (lo && uint64_t(hi_end - lo) < (uint64_t(4096) << 22) && uint64_t(hi_end - lo) <= 0xFFFFFFFFull) {
+      ds_base = const_cast<float*>(lo);
+      ds_span = uint64_t(hi_end - lo);
+      for (EncItem& e : items)
+        if (big(e)) {
+          e.flags |= kDeferScatter;
+          ds_cap += uint64_t(hp.rows) * e.hi_cap;
+        }
+    }
+  }
   auto* d_items = static_cast<EncItem*>(ws_.get("enc_items", n * sizeof(EncItem), false, stream_));
   upload(items.data(), n * sizeof(EncItem), d_items);
   auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
@@ -423,13 +450,23 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
       if (((e.flags & kHasAcc) ? 0 : 1) != per_stage) throw CudaError("mixed fused batch");
     ev_record(1);
     uint64_t sketch_bytes = 0;  // scattered-into footprint of the batch
-    for (const EncItem& e : items) sketch_bytes += (e.flags & kWriteSketch) ? uint64_t(hp.rows) * e.m * 4 : 0;
+    for (const EncItem& e : items)  // deferred sketches are not scattered into by the fused pass
+      sketch_bytes += ((e.flags & kWriteSketch) && !(e.flags & kDeferScatter)) ? uint64_t(hp.rows) * e.m * 4 : 0;
     launches_ += launch_select_fused(di_, d_items, state, n, tiles, samples, hp, w4, per_stage, sh, fine,
                                      cd, hp_pool, err, stream_, timing_ ? spans_ : nullptr,
                                      use_tma_ && all_aligned, sketch_bytes);
     ev_record(2);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
+    if (ds_base) {
+      auto* rc = static_cast<uint32_t*>(ws_.get("ds_count", 4096 * 4, true, stream_));
+      auto* cur = static_cast<uint32_t*>(ws_.get("ds_cursor", 4096 * 4 + 16, false, stream_));
+      auto* rec = static_cast<uint2*>(ws_.get("ds_records", ds_cap * 8, false, stream_));
+      const int l = launch_deferred_scatter(di_, d_items, state, n, hp_pool, hp, ds_base, ds_span, rc, cur,
+                                            cur + 4096, rec, stream_);
+      if (l < 0) throw CudaError("deferred sketch scatter: span too large");
+      launches_ += l;
+    }
     ev_record(3);
     static const bool sel_dbg = std::getenv("TAGC_DEBUG_SELECT") != nullptr;
     if (sel_dbg && !capturing_) {  // per-item select outcome (debug only: synchronises)

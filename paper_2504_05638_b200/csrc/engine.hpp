@@ -289,6 +289,9 @@ class Engine {
   void ev_record(int i);
   void span_reset();
   unsigned long long* spans_ = nullptr;
+  // sketches above this size are scattered by the region-ordered pass
+  // (TAGC_DEFER_SCATTER_BYTES; 0 defers every compressed segment's)
+  uint64_t defer_scatter_bytes_ = 32ull << 20;
   bool side_stream_ = true;  // W = 1 raw copies on the low-priority side stream (TAGC_SIDE_STREAM=0: in order)
   bool use_tma_ = true;  // TMA-staged fused pass (TAGC_FUSED_TMA=0 selects the register path)
   uint32_t* err_flag();

@@ -69,6 +69,15 @@ int launch_rank_sum_f32(const float* const* in_ptrs, uint32_t world, float* out,
 // Wrapping u32 word sum (kernels.cpp:65-84).
 int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t* out, uint64_t n,
                         cudaStream_t stream);
+// Sketch scatter of the kDeferScatter items' logged kept entries, bucketed by
+// 16 MB region of [base, base + span_floats) (after launch_select_finish).
+// region_count: kMaxRegions (4096) u32, zero on entry (left zero); cursor:
+// 4096 u32; records: 3 x (sum of the items' hi_cap) uint2. Returns -1 when
+// the span is too large (then nothing was launched).
+int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
+                            const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
+                            uint32_t* region_count, uint32_t* cursor, uint32_t* n_records, uint2* records,
+                            cudaStream_t stream);
 // Owner-side optimizer step on the decoded shard (train.cpp:202-220, 355-359):
 // kind 0 SGD, 1 momentum-free AdamW (adam_v in/out).
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream);
