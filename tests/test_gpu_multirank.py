@@ -180,3 +180,11 @@ def test_peer_exchange_matches_oracle(orc, world, width, steps):
             for sh in owned[o]:
                 check_close(got[off:off + sh.size()], refs[sh.id])
                 off += sh.size()
+
+
+@pytest.mark.parametrize("world,width,theta,steps", [(2, 4, 99.0, 2), (3, 1, 98.75, 1)])
+def test_split_exchange_deferred_scatter(orc, monkeypatch, world, width, theta, steps):
+    """The region-ordered sketch scatter (kDeferScatter, used for sketches
+    beyond L2) forced on every segment: same parity bar against the oracle."""
+    monkeypatch.setenv("TAGC_DEFER_SCATTER_BYTES", "0")
+    test_split_exchange_matches_oracle(orc, world, width, theta, steps)
