@@ -138,17 +138,21 @@ def extra_sections(args, tagc, ctx, shards, grad, acc, out, owned, total, n_para
     """Uncompressed comparator, owner step, overlap and e2e (GPT-2 workload)."""
     import torch
 
-    # uncompressed comparator: ncclReduceScatter fp32 of the same shards
-    base_out = torch.empty(shards[0].size(), device=dev)
-    for _ in range(args.warmup):
-        ctx.baseline_reduce_shards(shards, grad, base_out)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        ctx.baseline_reduce_shards(shards, grad, base_out)
-    e1.record(stream)
-    barrier()
-    base_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    # uncompressed comparator: ncclReduceScatter fp32 of the same shards (a
+    # peer-exchange context has no NCCL communicator: no comparator then)
+    base_ms = None
+    if world == 1 or args.exchange == "nccl":
+        base_out = torch.empty(shards[0].size(), device=dev)
+        for _ in range(args.warmup):
+            ctx.baseline_reduce_shards(shards, grad, base_out)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.baseline_reduce_shards(shards, grad, base_out)
+        e1.record(stream)
+        barrier()
+        base_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+        del base_out
 
     # owner-side consumer (SURVEY §8f row 2): exchange + adamw_nm step on the
     # owned shard, unfused (tagc_reduce_shards then tagc_apply_optimizer,
@@ -304,9 +308,18 @@ def run_b200(args):
     world = args.gpus
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # TAGC_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo host plumbing -
+    # a plumbing check of the N > 1 code on a one-GPU box (--exchange peer;
+    # NCCL refuses two ranks on one device). Never a measurement.
+    share = world > 1 and os.environ.get("TAGC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = f"cuda:{local}"
     specs = workload_specs(args.workload)
     big = args.workload != "gpt2"  # 8B parameters: no room for the owner-step / overlap / e2e buffers
@@ -358,14 +371,18 @@ def run_b200(args):
     ctx.set_timing(False)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if share:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -465,12 +482,14 @@ def run_b200(args):
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
+    if share:
+        result["config"]["shared_gpu_plumbing_check"] = "all ranks on cuda:0 (TAGC_BENCH_SHARE_GPU=1): not a measurement"
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
         result["cpu_baseline"] = cpu_baseline(args, specs, world, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 

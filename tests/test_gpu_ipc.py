@@ -27,3 +27,21 @@ def test_peer_exchange_across_processes(nproc, width):
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "IPC peer exchange OK" in r.stdout, r.stdout[-2000:]
+
+
+def test_bench_two_ranks_plumbing():
+    """bench.py's N > 1 code (rank timing, max over ranks, owner step,
+    overlap, e2e, one JSON line from rank 0) with 2 ranks sharing cuda:0 over
+    the peer exchange (TAGC_BENCH_SHARE_GPU=1: a plumbing check only)."""
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3", "--exchange", "peer"]
+    env = dict(os.environ, TAGC_BENCH_SHARE_GPU="1", TAGC_PEER_TIMEOUT_MS="60000")
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["peel"]["unresolved"] == 0
+    assert d["owner_step"]["fused_ms"] > 0 and d["overlap"]["overlapped_ms"] > 0 and d["e2e"]["value"] > 0
