@@ -258,7 +258,7 @@ def extra_sections(args, tagc, ctx, shards, grad, acc, out, owned, total, n_para
     host_grad = torch.empty(total, dtype=torch.float32, pin_memory=True)
     host_grad.copy_(grad.cpu())
     host_out = torch.empty(max(owned, 1), dtype=torch.float32, pin_memory=True)
-    e2e_steps = min(max(10, args.steps), 50)  # ~10 ms a step (PCIe-bound): pipeline fill + drain once
+    e2e_steps = min(max(30, args.steps), 60)  # ~10 ms a step (PCIe-bound): pipeline fill + drain once
     for _ in range(2):
         ctx.tagc_reduce_shards_host(shards, host_grad, acc, host_out)
     ctx.host_join()
