@@ -122,14 +122,11 @@ __device__ __forceinline__ float median_rows(float (&e)[kMaxRows], uint32_t k) {
 
 // ------------------------------------------------------------------ build
 // Word tiles of kWordTile merged-index words (16 per thread of a 256-thread
-// CTA), each CTA walking a contiguous tile range with an item cursor. Two
-// passes around a one-CTA scan, none with a latency chain per tile:
-//   k_count      : present positions per tile -> tile_base[wt]
-//   k_scan_tiles : exclusive scan of the tile counts; the presence list is
-//                  ordered by tile, ascending position inside a tile
-//   k_list       : writes the list entries (plist / pitem) at their final
-//                  index and adds (entry, 1) into each entry's k buckets with
-//                  fire-and-forget 64-bit reductions (the bucket state).
+// CTA). One pass, k_list: each tile's present positions are counted, its
+// list offset found by decoupled look-back (tile_base[wt]; the presence list
+// is ordered by tile, ascending position inside a tile), the list entries
+// (plist / pitem) written at their final index and (entry, 1) added into each
+// entry's k buckets with fire-and-forget 64-bit reductions (the bucket state).
 constexpr uint32_t kPerThreadWords = kWordTile / 256;
 
 __device__ __forceinline__ void cta_tiles(uint64_t total, uint32_t& t0, uint32_t& t1) {
@@ -167,71 +164,25 @@ __device__ __forceinline__ void load_tile_bits(const DecItem& e, uint32_t wbase,
   }
 }
 
-__global__ void __launch_bounds__(256) k_count(DecodeWork w) {
-  using Reduce = cub::BlockReduce<uint32_t, 256>;
-  __shared__ typename Reduce::TempStorage tmp;
-  span_begin(w.span);
-  uint32_t t0, t1;
-  cta_tiles(w.total_word_tiles, t0, t1);
-  if (t0 >= t1) return;
-  uint32_t it = find_word_item(w.items, w.n_items, t0);
-  for (uint32_t wt = t0; wt < t1; ++wt) {
-    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
-    const DecItem& e = w.items[it];
-    uint32_t bits[kPerThreadWords], cnt;
-    load_tile_bits(e, uint32_t(wt - e.word_tile_begin) * kWordTile, (e.flags & kWidth4) != 0, bits, cnt);
-    const uint32_t total = Reduce(tmp).Sum(cnt);
-    if (threadIdx.x == 0) {
-      w.tile_base[wt] = total;
-      if (total) atomicAdd(&w.stats[it].presence, total);
-    }
-    __syncthreads();
-  }
+// List build in ONE pass over the merged index: word tiles are claimed in
+// order from a counter (qcount[12]); each CTA publishes its tile's count and
+// finds its list offset by a warp-wide decoupled look-back over the preceding
+// tiles' published counts / inclusive prefixes (tile_state), then writes its
+// list entries and inserts them into the bucket state. In-order claiming keeps
+// the look-back deadlock-free (predecessors belong to running CTAs that
+// publish their counts without waiting) and the REDs inside an L2-resident
+// window of the state.
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// Exclusive scan of the per-tile counts in place; the total is the presence
-// count (qcount[5]).
-__global__ void __launch_bounds__(1024) k_scan_tiles(DecodeWork w) {
-  using Scan = cub::BlockScan<uint32_t, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint32_t s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  const uint32_t T = uint32_t(w.total_word_tiles);
-  for (uint32_t b0 = 0; b0 < T; b0 += 1024 * 4) {
-    uint32_t v[4], sum = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t t = b0 + threadIdx.x * 4 + k;
-      v[k] = t < T ? w.tile_base[t] : 0u;
-      sum += v[k];
-    }
-    uint32_t off, total;
-    Scan(tmp).ExclusiveSum(sum, off, total);
-    off += s_carry;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t t = b0 + threadIdx.x * 4 + k;
-      if (t < T) w.tile_base[t] = off;
-      off += v[k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry += total;
-    __syncthreads();
-  }
-  // a corrupt index (NaN input aborted the encode) may list more than the
-  // capacity: then nothing is decoded (the call reports the NaN)
-  if (threadIdx.x == 0) w.qcount[5] = s_carry <= w.list_cap ? s_carry : 0u;
-}
-
-// Word tiles are claimed one at a time from a counter (qcount[12]), so the
-// CTAs insert into the bucket states of neighbouring tiles together and the
-// REDs meet an L2-resident window of the state instead of all of it.
 __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp) {
   using Scan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_wt;
-  const uint32_t total_list = w.qcount[5];
+  __shared__ uint32_t s_wt, s_base;
+  span_begin(w.span);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cap = uint32_t(w.list_cap < 0xFFFFFFFFull ? w.list_cap : 0xFFFFFFFFull);
   const uint32_t T = uint32_t(w.total_word_tiles);
   for (;;) {
     if (threadIdx.x == 0) s_wt = atomicAdd(&w.qcount[12], 1u);
@@ -247,15 +198,43 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
     load_tile_bits(e, wbase, w4, bits, cnt);
     uint32_t off, total;
     Scan(scan_tmp).ExclusiveSum(cnt, off, total);
-    const uint32_t base = __ldg(w.tile_base + wt);
-    if (base + total > total_list) total = base < total_list ? total_list - base : 0u;
+    if (threadIdx.x < 32) {  // warp 0: publish, look back, publish
+      unsigned long long* ts = w.tile_state;
+      uint64_t prefix = 0;
+      if (wt > 0) {
+        if (lane == 0) atomicExch(ts + wt, (1ull << 32) | total);  // aggregate
+        for (int k0 = int(wt) - 1;; k0 -= 32) {
+          const int k = k0 - int(lane);
+          unsigned long long v = 2ull << 32;  // before tile 0: an inclusive zero
+          if (k >= 0) {
+            do { v = ld_volatile_u64(ts + k); } while ((v >> 32) == 0);
+          }
+          const uint32_t incl = __ballot_sync(kFull, (v >> 32) == 2);
+          const uint32_t stop = incl ? uint32_t(__ffs(incl) - 1) : 31u;  // nearest inclusive prefix
+          prefix += warp_sum32(lane <= stop ? uint32_t(v) : 0u);
+          if (incl) break;
+        }
+      }
+      if (lane == 0) {
+        atomicExch(ts + wt, (2ull << 32) | uint32_t(prefix + total));  // inclusive prefix
+        s_base = uint32_t(prefix);
+        w.tile_base[wt] = uint32_t(prefix);
+        if (total) atomicAdd(&w.stats[it].presence, total);
+        // a corrupt index (NaN input aborted the encode) may list more than the
+        // capacity: then nothing is decoded (the call reports the NaN)
+        if (wt == T - 1) w.qcount[5] = prefix + total <= cap ? uint32_t(prefix + total) : 0u;
+      }
+    }
+    __syncthreads();
+    const uint32_t base = s_base;
+    const uint32_t n_in = base + total <= cap ? total : (base < cap ? cap - base : 0u);
     uint32_t j = base + off;
 #pragma unroll
     for (uint32_t k = 0; k < kPerThreadWords; ++k) {  // list entries: cheap, divergent
       const uint32_t wi = tile_word(wbase, k);
       for (uint32_t x = bits[k]; x; x &= x - 1) {
         const uint32_t bb = __ffs(x) - 1;
-        if (j < total_list) {
+        if (j < cap) {
           w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
           w.pitem[j] = it;
         }
@@ -264,7 +243,7 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
     }
     __syncthreads();  // the tile's entries are visible to the whole CTA
     // bucket state, one entry per thread (hashing and reductions stay converged)
-    for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+    for (uint32_t q = threadIdx.x; q < n_in; q += blockDim.x) {
       const uint32_t i = base + q;
       const uint32_t p = w.plist[i];
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
@@ -986,10 +965,10 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
   ZeroRanges zr{};
   zr.ptr[0] = w.slot_state;
   zr.bytes[0] = w.total_slots * 8;
-  zr.n = 1;
+  zr.ptr[1] = w.tile_state;
+  zr.bytes[1] = w.total_word_tiles * 8;
+  zr.n = 2;
   launch_zero(zr, stream);
-  k_count<<<g, 256, 0, stream>>>(w);
-  k_scan_tiles<<<1, 1024, 0, stream>>>(w);
   k_list<<<g, 256, 0, stream>>>(w, hp);
   return g;
 }
@@ -1013,7 +992,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return 9;
+  return 6;  // zero, list, round 0 (2), peel, final
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
@@ -1029,7 +1008,7 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
   cudaMemsetAsync(ob.count, 0, 4, stream);
   k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
-  launches += 6;
+  launches += 4;  // zero, list, round 0, push
   uint32_t gen = 1;
   unsigned long long* cur_keys = ob.keys[0];
   uint32_t* cur_slots = ob.slots[0];

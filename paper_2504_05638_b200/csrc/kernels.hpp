@@ -131,6 +131,7 @@ struct DecodeWork {
   float* val;                      // decoded value per presence-list entry
   uint32_t* slot_mark;             // per bucket: holds an entry round 0 left unresolved (or nullptr)
   uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
+  unsigned long long* tile_state;  // single-pass scan: per word tile, flag << 32 | count (zeroed per call)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
