@@ -181,6 +181,7 @@ Engine::~Engine() {
   drop_graphs();
   peer_release();
   if (opt_dev_) cudaFree(opt_dev_);
+  if (desc_stream_) cudaStreamDestroy(desc_stream_);
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& e : ev_)
@@ -289,6 +290,13 @@ void Engine::upload(const void* host, size_t bytes, void* dev) {
   if (call_depth_ == 0) {  // internal helper called outside a public entry
     CallScope scope(*this);
     upload(host, bytes, dev);
+    return;
+  }
+  if (capturing_ && std::find(capturing_->dev.begin(), capturing_->dev.end(), dev) != capturing_->dev.end()) {
+    // a graph-private descriptor buffer: filled now, once, outside the graph
+    if (!desc_stream_) cuda_check(cudaStreamCreateWithFlags(&desc_stream_, cudaStreamNonBlocking), "desc stream");
+    cuda_check(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, desc_stream_), "descriptor copy");
+    cuda_check(cudaStreamSynchronize(desc_stream_), "descriptor copy");
     return;
   }
   if (capturing_) {  // the graph re-reads these bytes on every replay: give them their own buffer
@@ -429,7 +437,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
         }
     }
   }
-  auto* d_items = static_cast<EncItem*>(ws_.get("enc_items", n * sizeof(EncItem), false, stream_));
+  auto* d_items = static_cast<EncItem*>(desc_buffer("enc_items", n * sizeof(EncItem)));
   upload(items.data(), n * sizeof(EncItem), d_items);
   auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
   uint32_t* err = err_flag();
@@ -551,7 +559,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     list += std::min(d.list_cap ? d.list_cap : d.n, d.n);
   }
   if (slots >= (1ull << 31)) throw CudaError("decode batch exceeds 2^31 sketch buckets");
-  auto* d_items = static_cast<DecItem*>(ws_.get("dec_items", n * sizeof(DecItem), false, stream_));
+  auto* d_items = static_cast<DecItem*>(desc_buffer("dec_items", n * sizeof(DecItem)));
   upload(items.data(), n * sizeof(DecItem), d_items);
   DecodeWork w{};
   w.span = timing_ ? spans_ + 2 : nullptr;
@@ -796,12 +804,26 @@ void Engine::set_graphs(bool on) {
   if (!on) drop_graphs();
 }
 
+void Engine::free_graph(GraphEntry& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+  for (char* h : g.pinned) cudaFreeHost(h);
+  for (void* d : g.dev) cudaFree(d);
+  g.pinned.clear();
+  g.dev.clear();
+}
+
+void* Engine::desc_buffer(const char* name, size_t bytes) {
+  if (!capturing_) return ws_.get(name, bytes, false, stream_);
+  void* d = nullptr;
+  cuda_check(cudaMalloc(&d, align_up(std::max<size_t>(bytes, 16), 256)), "graph descriptor buffer");
+  capturing_->dev.push_back(d);
+  return d;
+}
+
 void Engine::drop_graphs() {
   if (!graphs_.empty() && stream_) cudaStreamSynchronize(stream_);
-  for (auto& [k, g] : graphs_) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (char* h : g.pinned) cudaFreeHost(h);
-  }
+  for (auto& [k, g] : graphs_) free_graph(g);
   graphs_.clear();
   graph_seen_.clear();
 }
@@ -898,8 +920,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   if (ok && cudaGraphUpload(g.exec, stream_) != cudaSuccess) cudaGetLastError();
   if (graph) cudaGraphDestroy(graph);
   if (!ok) {  // could not capture (e.g. a buffer had to grow): stay eager for this key
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (char* h : g.pinned) cudaFreeHost(h);
+    free_graph(g);
     ledger_.wire_bytes = wire0;
     for (const LedgerEntry& l : g.ledger) ledger_.unrecord(l.op, l.tag, l.bits, l.params);
     graph_seen_[key] = -1000000;
@@ -995,7 +1016,7 @@ void Engine::exchange_encode(uint64_t lo, uint64_t hi) {
   // raw segments (W > 1): packed into the send blocks before the exchange
   if (!pack.empty()) {
     const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
-    auto* d_pack = static_cast<CopyItem*>(ws_.get("nc_pack", pack.size() * sizeof(CopyItem), false, stream_));
+    auto* d_pack = static_cast<CopyItem*>(desc_buffer("nc_pack", pack.size() * sizeof(CopyItem)));
     upload(pack.data(), pack.size() * sizeof(CopyItem), d_pack);
     launches_ += launch_copy_items(di_, d_pack, uint32_t(pack.size()), tt, stream_);
   }
@@ -1003,14 +1024,14 @@ void Engine::exchange_encode(uint64_t lo, uint64_t hi) {
   // segments copied straight from the gradient to the output.
   if (!side.empty() && !side_stream_) {  // in order on the context stream
     const uint64_t tt = copy_tiles(side.data(), uint32_t(side.size()));
-    auto* d_side = static_cast<CopyItem*>(ws_.get("nc_side", side.size() * sizeof(CopyItem), false, stream_));
+    auto* d_side = static_cast<CopyItem*>(desc_buffer("nc_side", side.size() * sizeof(CopyItem)));
     upload(side.data(), side.size() * sizeof(CopyItem), d_side);
     launches_ += launch_copy_items(di_, d_side, uint32_t(side.size()), tt, stream_, false,
                                    opt_on_ ? opt_dev_ : nullptr);
   } else if (!side.empty()) {
     ensure_aux();
     const uint64_t tt = copy_tiles(side.data(), uint32_t(side.size()));
-    auto* d_side = static_cast<CopyItem*>(ws_.get("nc_side", side.size() * sizeof(CopyItem), false, stream_));
+    auto* d_side = static_cast<CopyItem*>(desc_buffer("nc_side", side.size() * sizeof(CopyItem)));
     upload(side.data(), side.size() * sizeof(CopyItem), d_side);
     cuda_check(cudaEventRecord(aux_fork_, stream_), "fork");
     cuda_check(cudaStreamWaitEvent(aux_, aux_fork_, 0), "fork wait");
@@ -1166,7 +1187,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
   run_decode_grouped(dec, hp, w == 1 && W > 1, zero_done, pre_decode);
   if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
-    auto* d_un = static_cast<CopyItem*>(ws_.get("nc_unpack", unpack.size() * sizeof(CopyItem), false, stream_));
+    auto* d_un = static_cast<CopyItem*>(desc_buffer("nc_unpack", unpack.size() * sizeof(CopyItem)));
     upload(unpack.data(), unpack.size() * sizeof(CopyItem), d_un);
     launches_ += launch_copy_items(di_, d_un, uint32_t(unpack.size()), tt, stream_, false, opt_on_ ? opt_dev_ : nullptr);
   }

@@ -240,7 +240,13 @@ class Engine {
     uint64_t gen = 0, launches = 0, wire = 0;
     std::vector<LedgerEntry> ledger;
     std::vector<char*> pinned;  // descriptor uploads frozen into the graph
+    std::vector<void*> dev;     // graph-private descriptor buffers, filled once at capture
   };
+  cudaStream_t desc_stream_ = nullptr;  // capture-time descriptor copies (never captured)
+  // A descriptor buffer: the workspace's, or while capturing a graph-private
+  // one that upload() fills once (no copy kernel in the replayed graph).
+  void* desc_buffer(const char* name, size_t bytes);
+  static void free_graph(GraphEntry& g);
   static constexpr size_t kMaxGraphs = 16;
   std::map<std::string, GraphEntry> graphs_;
   std::map<std::string, int> graph_seen_;
