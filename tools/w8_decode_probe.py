@@ -47,5 +47,6 @@ for step in range(3):
         torch.cuda.synchronize()
         times.append(a.elapsed_time(b))
         stats.append(st)
+    print("unresolved per owner", [s.unresolved for s in stats], "presence", [s.presence for s in stats])
     print(f"step {step}: decode ms per owner {[round(t, 3) for t in times]}; presence {stats[0].presence} "
           f"unresolved {stats[0].unresolved} rounds {ctxs[0].last_peel_rounds()}", flush=True)
