@@ -794,19 +794,36 @@ __global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
   const uint32_t total = w.qcount[5];
   if (total == w.qcount[4]) return;  // every listed entry peeled: nothing to estimate
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    if (w.bitmap[i >> 5] >> (i & 31) & 1u) continue;
-    const uint32_t p = w.plist[i], it = w.pitem[i];
-    const DecItem& e = w.items[it];
-    float est[kMaxRows];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < total; base += stride) {
+    const uint32_t i = uint32_t(base) + lane;
+    // a warp's 32 entries share one recovered-bit word (base is a multiple of 32)
+    const uint32_t word = ldcg(w.bitmap + (base >> 5));
+    const bool todo = i < total && !(word >> lane & 1u);
+    uint32_t it = 0xFFFFFFFFu, p = 0;
+    if (todo) {
+      p = w.plist[i];
+      it = w.pitem[i];
+      const DecItem& e = w.items[it];
+      float est[kMaxRows];
 #pragma unroll
-    for (uint32_t r = 0; r < kMaxRows; ++r) {
-      if (r >= hp.rows) break;
-      est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul)];
+      for (uint32_t r = 0; r < kMaxRows; ++r) {
+        if (r >= hp.rows) break;
+        est[r] = dev_sign(hp.row[r], p) * e.sketch[uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul)];
+      }
+      w.val[i] = canonical(median_rows(est, hp.rows));
     }
-    w.val[i] = canonical(median_rows(est, hp.rows));
-    const uint32_t b = atomicAdd(&w.stats[it].unresolved, 1u);
-    if (w.unresolved) w.unresolved[e.list_off + b] = p;
+    // unresolved counts, one atomic per item group of the warp (a stalled
+    // item's counter would otherwise take one atomic per entry)
+    const uint32_t grp = __match_any_sync(kFull, it);
+    if (todo) {
+      const uint32_t leader = __ffs(grp) - 1;
+      uint32_t b0 = 0;
+      if (lane == leader) b0 = atomicAdd(&w.stats[it].unresolved, uint32_t(__popc(grp)));
+      b0 = __shfl_sync(grp, b0, leader);
+      if (w.unresolved) w.unresolved[w.items[it].list_off + b0 + __popc(grp & ((1u << lane) - 1u))] = p;
+    }
   }
 }
 
