@@ -491,16 +491,22 @@ __device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const Has
       const unsigned long long st = ld_acquire(w.slot_state + slot);
       if (st_count(st) == 1u) {
         i = st_entry(st);
+        // the entry's position and the bucket's residual are read before the
+        // claim resolves (the count was acquired: the residual is the single
+        // entry's); a lost claim just discards them - one L2 round trip less
+        // on the round's dependency chain
+        e = w.items + si.find(slot);
+        const uint64_t local = slot - e->slot_base;
+        const uint32_t pp = __ldg(w.plist + i);
+        const float resid = ldcg(e->sketch + local);
         const uint32_t bit = 1u << (i & 31);
         if (!(atomicOr(w.bitmap + (i >> 5), bit) & bit)) {
           win = true;
-          p = __ldg(w.plist + i);
-          e = w.items + si.find(slot);
-          const uint64_t local = slot - e->slot_base;
+          p = pp;
           row = slot_row(local, e->m);
           float sg = 0.0f;
           _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
-          v = canonical(sg * ldcg(e->sketch + local));
+          v = canonical(sg * resid);
           w.val[i] = v;
         }
       }
