@@ -304,6 +304,7 @@ __device__ __forceinline__ void stage_flush(T* s_buf, uint32_t* s_n, uint32_t* s
 }
 
 constexpr uint32_t kPushStage = 8192;  // next-frontier slots per CTA
+constexpr uint32_t kR0Stage = 1024;    // round-0 subtraction entries per phase-1 CTA
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -347,13 +348,14 @@ __device__ __forceinline__ uint32_t slot_row(uint64_t local, uint32_t m) {
 // other positions, peel row) for the subtraction pass. Recovered flags of a
 // warp's 32 consecutive entries are written as one word (no atomics).
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
-                                              uint64_t start, uint64_t stride) {
+                                              uint64_t start, uint64_t stride, uint32_t* s_q = nullptr,
+                                              uint32_t* s_n = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t won = 0;
   const uint32_t total = ldcg(&w.qcount[5]);
   for (uint64_t base = start - lane; base < total; base += stride) {
     const uint64_t i = base + lane;
-    bool peeled = false;
+    bool peeled = false, sub = false;  // sub: peeled with a shared bucket (k_r0_subtract's work)
     if (i < total) {
       const uint32_t p = __ldcs(w.plist + i);
       const DecItem& e = w.items[__ldcs(w.pitem + i)];
@@ -395,19 +397,33 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
         w.val[i] = v;
         info = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
         peeled = true;
+        sub = shared != 0u;
         ++won;
       }
       w.pinfo[i] = info;
     }
     const uint32_t m = __ballot_sync(kFull, peeled);
     if (lane == 0 && base < total) w.bitmap[base >> 5] = m;  // base is a multiple of 32
+    if (s_q) stage_push<uint32_t, kR0Stage>(sub, uint32_t(i), s_q, s_n, w.r0_list, &w.qcount[13], lane);
   }
   won = warp_sum32(won);
   if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
 }
 
 __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
-  round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x);
+  __shared__ uint32_t s_q[kR0Stage];
+  __shared__ uint32_t s_n[2], s_base;
+  const bool compact = w.r0_list != nullptr;
+  if (compact) {
+    if (threadIdx.x == 0) {
+      s_n[0] = 0;
+      s_n[1] = kR0Stage;
+    }
+    __syncthreads();
+  }
+  round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x,
+                compact ? s_q : nullptr, s_n);
+  if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
 }
 
 // Every entry peeled in round 0 leaves the buckets it shares with other
@@ -425,16 +441,20 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
   }
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t total = ldcg(&w.qcount[5]);
+  // only the round-0 peeled entries that share a bucket (compacted by
+  // k_r0_phase1); the whole list when no compact list was built
+  const bool compact = w.r0_list != nullptr;
+  const uint32_t total = compact ? ldcg(&w.qcount[13]) : ldcg(&w.qcount[5]);
   uint32_t* nq = w.queue[1];
   uint32_t* ncount = &w.qcount[9];
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < total; base += stride) {
-    const uint64_t i = base + lane;
+    const uint64_t j = base + lane;
+    const uint64_t i = compact && j < total ? uint64_t(ldcg(w.r0_list + j)) : j;
     uint32_t p = 0, rows = 0;
     float v = 0.0f;
     const DecItem* e = w.items;
-    if (i < total) {
+    if (j < total) {
       const uint2 info = __ldcs(w.pinfo + i);
       if (info.y & 0x100u) {
         rows = info.y & 0xFFu;

@@ -131,6 +131,7 @@ struct DecodeWork {
   float* val;                      // decoded value per presence-list entry
   uint32_t* slot_mark;             // per bucket: holds an entry round 0 left unresolved (or nullptr)
   uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
+  uint32_t* r0_list;               // round-0 peeled entries sharing a bucket (count qcount[13]), or nullptr
   unsigned long long* tile_state;  // single-pass scan: per word tile, flag << 32 | count (zeroed per call)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
