@@ -1005,14 +1005,7 @@ int grid_for(uint64_t n, int threads) {
 int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, cudaStream_t stream) {
   const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
   const int g = int(g64);
-  ZeroRanges zr{};
-  zr.ptr[0] = w.slot_state;
-  zr.bytes[0] = w.total_slots * 8;
-  zr.ptr[1] = w.tile_state;
-  zr.bytes[1] = w.total_word_tiles * 8;
-  zr.n = 2;
-  launch_zero(zr, stream);
-  k_list<<<g, 256, 0, stream>>>(w, hp);
+  k_list<<<g, 256, 0, stream>>>(w, hp);  // bucket and tile state were zeroed by the caller
   return g;
 }
 
@@ -1035,7 +1028,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return 6;  // zero, list, round 0 (2), peel, final
+  return 5;  // list, round 0 (2), peel, final
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
@@ -1051,7 +1044,7 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
   cudaMemsetAsync(ob.count, 0, 4, stream);
   k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
-  launches += 4;  // zero, list, round 0, push
+  launches += 3;  // list, round 0, push
   uint32_t gen = 1;
   unsigned long long* cur_keys = ob.keys[0];
   uint32_t* cur_slots = ob.slots[0];

@@ -587,9 +587,9 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
             stats_base;
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
-  // the bucket state is zeroed inside launch_decode (after the output fill)
   zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)},
-        {w.slot_mark, w.slot_mark ? mark_words * 4 : 0}});
+        {w.slot_mark, w.slot_mark ? mark_words * 4 : 0}, {w.slot_state, slots * 8},
+        {w.tile_state, wt * 8}});  // one launch for every decode scratch reset
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {
     w.dbg = static_cast<unsigned long long*>(ws_.get("peel_dbg", 64 * 8, false, stream_));
