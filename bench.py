@@ -2,29 +2,40 @@
 """Benchmark: uncompressed-equivalent gradient GB/s per sync (encode + exchange +
 decode) of the B200 TAGC exchange, BASELINE.json's metric.
 
-Workload (BASELINE config 2, "GPT-2 small (124M) shaped per-layer gradient
-buckets, layer-selective compression"): every rank holds a full GPT-2-small
-(tied head, 124,439,808 fp32) gradient laid out by the reference's own layer
-list (model.cpp:39-64); make_shards(specs, N, N) gives one shard per rank;
-non_attention_linear policy (+ out-proj), theta = 99 per rank, ratio 10,
-4-bit index, seed 77. A step is one full exchange: every rank sparsifies and
-encodes all shards, the index/sketch/raw blocks are reduce-scattered over
-NCCL, and every owner peels its shard back to dense fp32. Accumulators carry
-error feedback across steps. Gradients are synthetic log-normal magnitudes with
-fair signs (the distribution of the reference's SyntheticStream,
-train.cpp:445-459), generated on device; 498 MB per rank, > L2 (126 MB).
+Headline workload (BASELINE config 4, the largest single-GPU configuration):
+every rank holds ONE 2^28-element fp32 gradient bucket (a single
+`feed_forward` segment, min_compress_segment = 1), theta = 99 per rank
+(1 % density), ratio 10, 4-bit index, seed 77; make_shards(bucket, N, N)
+gives one shard per rank. A step is one full exchange: every rank sparsifies
+and encodes its whole bucket, the index / sketch blocks are reduce-scattered
+(NCCL over NVLink), and every owner peels its shard back to dense fp32.
+Accumulators carry error feedback across steps. Gradients are synthetic
+log-normal magnitudes with fair signs (the distribution of the reference's
+SyntheticStream, train.cpp:445-459), generated on device; 1 GiB per rank,
+> L2 (126 MB), so every step streams from HBM.
 
-value = N * 124,439,808 * 4 B / (device time per step, max over ranks).
+value = N * 2^28 * 4 B / (device time per step, max over ranks).
+
+Extra keys (same line): the GPT-2-small layer layout (config 2) at theta 99 /
+4-bit and at the paper setting theta 98.75 / 1-bit, the uncompressed
+ncclReduceScatter comparator with its bus bandwidth, the owner step and the
+backward overlap. --workload llama3-8b runs config 3's layout as the headline.
 
 --impl reference times the reference's own CPU implementation
-(oracle/_ref/libtagc_ref.so: tagc_reduce_shard with World(N, parallel), all
-host threads) on a bounded sample of the same workload, rank 0 only.
+(oracle/_ref/libtagc_ref.so, compiled from /root/reference by
+oracle/Makefile: tagc_reduce_shard with World(N, parallel), all host threads)
+on a bounded sample of the same workload, rank 0 only. That arm never imports
+the product package: its shard plan comes from the reference's own
+make_shards.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -32,13 +43,61 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-THETA, RATIO, WIDTH, SEED = 99.0, 10, 4, 77
-WORKLOADS = {  # --workload: BASELINE config 2 (default) and config 3's layer layout
-    "gpt2": "gpt2-small-124M-tied/non_attention_linear/theta99/r10/w4",
-    "llama3-8b": "llama3-8b-8.03B/non_attention_linear/theta99/r10/w4",
-}
-WORKLOAD = WORKLOADS["gpt2"]
 METRIC = "uncompressed-equivalent gradient GB/s per sync (encode+RS+decode)"
+SEED = 77
+C4_N = 1 << 28
+
+
+# --------------------------------------------------------------------------- workloads
+# Pure host data (name, kind, count) so the reference arm never loads the
+# product library.
+def gpt2_layers(layers=12, d=768, mu=4, vocab=50257, ctx=1024):
+    """GPT-2 small, tied head (reference model.cpp:39-64 order): 124,439,808."""
+    out = [("wte", "embedding", vocab * d), ("wpe", "positional_embedding", ctx * d)]
+    for l in range(layers):
+        p = f"h{l}."
+        out += [(p + "ln1.g", "norm", d), (p + "ln1.b", "norm", d),
+                (p + "attn.qkv.w", "attention_qkv", d * 3 * d), (p + "attn.qkv.b", "bias", 3 * d),
+                (p + "attn.proj.w", "attention_out_proj", d * d), (p + "attn.proj.b", "bias", d),
+                (p + "ln2.g", "norm", d), (p + "ln2.b", "norm", d),
+                (p + "mlp.fc.w", "feed_forward", d * mu * d), (p + "mlp.fc.b", "bias", mu * d),
+                (p + "mlp.proj.w", "feed_forward", mu * d * d), (p + "mlp.proj.b", "bias", d)]
+    return out + [("ln_f.g", "norm", d), ("ln_f.b", "norm", d)]
+
+
+def llama3_8b_layers(layers=32, d=4096, kv=1024, ffn=14336, vocab=128256):
+    out = [("embed_tokens", "embedding", vocab * d)]
+    for l in range(layers):
+        p = f"layers.{l}."
+        out += [(p + "q_proj", "attention_qkv", d * d), (p + "k_proj", "attention_qkv", d * kv),
+                (p + "v_proj", "attention_qkv", d * kv), (p + "o_proj", "attention_out_proj", d * d),
+                (p + "gate_proj", "feed_forward", d * ffn), (p + "up_proj", "feed_forward", d * ffn),
+                (p + "down_proj", "feed_forward", ffn * d),
+                (p + "input_layernorm", "norm", d), (p + "post_attention_layernorm", "norm", d)]
+    return out + [("norm", "norm", d), ("lm_head", "lm_head", d * vocab)]
+
+
+WORKLOADS = {
+    # name: (description, layers(), theta, ratio, width, policy, min_compress_segment)
+    "c4": ("bucket-2^28-f32/feed_forward/theta99/r10/w4",
+           lambda: [("bucket", "feed_forward", C4_N)], 99.0, 10, 4, "all_layers", 1),
+    "gpt2": ("gpt2-small-124M-tied/non_attention_linear/theta99/r10/w4",
+             gpt2_layers, 99.0, 10, 4, "non_attention_linear", 1024),
+    "gpt2-paper": ("gpt2-small-124M-tied/non_attention_linear/theta98.75/r10/w1 (paper setting)",
+                   gpt2_layers, 98.75, 10, 1, "non_attention_linear", 1024),
+    "llama3-8b": ("llama3-8b-8.03B/non_attention_linear/theta99/r10/w4",
+                  llama3_8b_layers, 99.0, 10, 4, "non_attention_linear", 1024),
+}
+
+
+def workload_config(name, world):
+    """The `config` object of the JSON line: identical in both arms."""
+    desc, layers, theta, ratio, width, policy, mcs = WORKLOADS[name]
+    n = sum(c for _, _, c in layers())
+    return {"workload": desc, "params_per_rank": n, "shards": f"make_shards({name}, {world}, {world})",
+            "theta": theta, "ratio": ratio, "index_width": width, "policy": policy,
+            "include_out_proj": True, "min_compress_segment": mcs, "seed": SEED,
+            "l2": f"inputs larger than L2 ({n * 4 / 1e6:.0f} MB of gradient per rank, streamed every step)"}
 
 
 def env_int(k, d):
@@ -48,13 +107,24 @@ def env_int(k, d):
         return d
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -72,7 +142,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -100,112 +170,305 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload_specs(name="gpt2"):
-    import paper_2504_05638_b200 as tagc
+# --------------------------------------------------------------------------- B200 arm
+class Rig:
+    """Per-rank plumbing: device, stream, context, barrier, max over ranks."""
 
-    return tagc.llama3_8b_specs() if name == "llama3-8b" else tagc.gpt2_specs()
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.world = args.gpus
+        self.rank = env_int("RANK", 0)
+        self.local = env_int("LOCAL_RANK", 0)
+        # TAGC_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo host plumbing
+        # and the peer-memory exchange - a check of the N > 1 code on a one-GPU
+        # box (NCCL refuses two ranks on one device). Never a measurement.
+        self.share = self.world > 1 and os.environ.get("TAGC_BENCH_SHARE_GPU") == "1"
+        if self.share:
+            self.local = 0
+            args.exchange = "peer"
+        self.exchange = args.exchange
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+        self.dev = f"cuda:{self.local}"
+        self.stream = torch.cuda.Stream(device=self.local)
+        torch.cuda.set_stream(self.stream)
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.world > 1:
+            if self.share:
+                self.dist.barrier()
+            else:
+                self.dist.barrier(device_ids=[self.local])
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], device="cpu" if self.share else self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(self, fn, steps):
+        """Device time of `steps` calls (ms per call), CUDA events on the
+        context stream bracketed by barrier + synchronize, max over ranks."""
+        self.barrier()
+        self.e0.record(self.stream)
+        for i in range(steps):
+            fn(i)
+        self.e1.record(self.stream)
+        self.barrier()
+        return self.max_over_ranks(self.e0.elapsed_time(self.e1)) / steps
+
+    def context(self, tagc, cfg, shards):
+        ctx = tagc.Context(cfg, world_size=self.world, rank=self.rank, device=self.local,
+                           stream=self.stream.cuda_stream)
+        if self.world > 1 and self.exchange == "peer":  # pulls over NVLink peer memory (CUDA IPC)
+            handles = [None] * self.world
+            self.dist.all_gather_object(handles, ctx.peer_prepare(shards))
+            ctx.peer_open(handles)
+        elif self.world > 1:
+            obj = [tagc.Context.nccl_unique_id() if self.rank == 0 else None]
+            self.dist.broadcast_object_list(obj, src=0)
+            ctx.init_nccl(obj[0])
+        return ctx
 
 
-def cfg_obj():
-    import paper_2504_05638_b200 as tagc
+def make_workload(tagc, name, world):
+    desc, layers, theta, ratio, width, policy, mcs = WORKLOADS[name]
+    specs = [tagc.LayerSpec(nm, kind, cnt) for nm, kind, cnt in layers()]
+    cfg = tagc.CompressionConfig(theta=theta, ratio=ratio, index_width=width, policy=policy,
+                                 include_out_proj=True, seed=SEED, min_compress_segment=mcs)
+    shards = tagc.make_shards(specs, world, world)
+    return specs, cfg, shards
 
-    return tagc.CompressionConfig(theta=THETA, ratio=RATIO, index_width=WIDTH,
-                                  policy="non_attention_linear", include_out_proj=True, seed=SEED)
+
+def synthetic_grad(torch, total, n_params, dev, seed):
+    """Log-normal magnitudes with fair signs (SyntheticStream's distribution),
+    drawn on the device in chunks; the make_shards pad tail is zero."""
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    grad = torch.empty(total, device=dev)
+    chunk = 1 << 26
+    for c0 in range(0, total, chunk):
+        c1 = min(total, c0 + chunk)
+        mag = torch.randn(c1 - c0, device=dev, generator=gen).exp_()
+        sign = torch.randint(0, 2, (c1 - c0,), device=dev, generator=gen, dtype=torch.int8)
+        grad[c0:c1] = torch.where(sign.bool(), -mag, mag)
+    if total > n_params:
+        grad[n_params:] = 0.0
+    return grad
 
 
-def algorithmic_bytes(shards, rank, world):
-    """SURVEY.md §8(d) bytes for this rank's dominant kernel, the fused
-    select + encode pass (k_fused_tma): per compressed element it reads g and
-    acc (8 B) and writes the residual (4 B) and the packed index (w/8 B), plus
-    a 24*d sketch read-modify-write (d = kept density = 1 - theta/100). The
-    separate select pass of the survey's model (8 B) is gone: selection rides
-    on the same pass, bracketed by two small passes over a 1/32 sample (2 x
-    8/32 B, separate kernels, not in this figure)."""
-    import paper_2504_05638_b200 as tagc
-
-    comp = 0
+def compressed_elems(tagc, shards, cfg):
+    n = 0
     for sh in shards:
         for s in sh.segments:
-            if tagc.kind_compressible(s.kind, "non_attention_linear", True) and s.size() >= 1024:
-                comp += s.size()
-    dens = 1.0 - THETA / 100.0
-    fused = comp * (12.0 + WIDTH / 8.0 + 24.0 * dens)
-    return comp, fused
+            if tagc.kind_compressible(s.kind, cfg.policy, cfg.include_out_proj) and \
+                    s.size() >= cfg.min_compress_segment and cfg.ratio > 1:
+                n += s.size()
+    return n
 
 
-def extra_sections(args, tagc, ctx, shards, grad, acc, out, owned, total, n_params, specs, stream, dev, local,
-                   world, step, barrier, max_over_ranks, e0, e1):
-    """Uncompressed comparator, owner step, overlap and e2e (GPT-2 workload)."""
-    import torch
+def fused_bytes_per_elem(cfg):
+    """SURVEY.md §8(d) bytes per compressed element of the dominant kernel, the
+    fused select + split + encode pass (k_fused_tma): read g and acc (8 B),
+    write the residual (4 B) and the packed index (w/8 B), plus a 24*d sketch
+    read-modify-write (d = 1 - theta/100). The separate select pass of the
+    survey's model (8 B) is gone: selection rides on the same pass, bracketed
+    by two small passes over a 1/32 sample (separate kernels, not counted)."""
+    return 12.0 + cfg.index_width / 8.0 + 24.0 * (1.0 - cfg.theta / 100.0)
 
-    # uncompressed comparator: ncclReduceScatter fp32 of the same shards (a
-    # peer-exchange context has no NCCL communicator: no comparator then)
-    base_ms = None
-    if world == 1 or args.exchange == "nccl":
-        base_out = torch.empty(shards[0].size(), device=dev)
-        for _ in range(args.warmup):
-            ctx.baseline_reduce_shards(shards, grad, base_out)
-        barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            ctx.baseline_reduce_shards(shards, grad, base_out)
-        e1.record(stream)
-        barrier()
-        base_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-        del base_out
 
-    # owner-side consumer (SURVEY §8f row 2): exchange + adamw_nm step on the
-    # owned shard, unfused (tagc_reduce_shards then tagc_apply_optimizer,
-    # which re-reads the decoded shard) vs fused (tagc_reduce_shards_step,
-    # the update inside the decode emit / raw unpack, decoded not stored)
-    params = torch.randn(max(owned, 1), device=dev)
-    adam_v = torch.zeros(max(owned, 1), device=dev)
-    opt_steps = max(3, min(args.steps, 10))
+def decode_bytes_per_elem(cfg):
+    """SURVEY.md §8(d) decode bytes per owned compressed element: read the
+    merged index (w/8 B) and the reduced sketch (4/r B), write the dense
+    shard (4 B)."""
+    return cfg.index_width / 8.0 + 4.0 / cfg.ratio + 4.0
+
+
+def measure_exchange(rig, tagc, name, args, full=True):
+    """One workload: warm-up, peel statistics, K timed steps (+ clocks), then
+    the per-stage and kernel-span breakdown. Returns (result dict, state)."""
+    torch = rig.torch
+    specs, cfg, shards = make_workload(tagc, name, rig.world)
+    total = shards[-1].end
+    n_params = sum(s.param_count for s in specs)
+    ctx = rig.context(tagc, cfg, shards)
+    grad = synthetic_grad(torch, total, n_params, rig.dev, 1000 + rig.rank)
+    acc = torch.zeros(total, device=rig.dev)
+    owned = sum(s.size() for s in shards if s.owner == rig.rank)
+    out = torch.empty(max(owned, 1), device=rig.dev)
+    torch.cuda.synchronize()
+
+    def step(i=0):
+        ctx.tagc_reduce_shards(shards, grad, acc, out, stats=False)
+
+    for _ in range(args.warmup):
+        step()
+    _, st = ctx.tagc_reduce_shards(shards, grad, acc, out, stats=True)  # untimed: peel statistics
+    rounds = ctx.last_peel_rounds()
+
+    clocks = ClockSampler(rig.local) if full else None
+    if clocks:
+        rig.barrier()
+        clocks.start()
+    ms = rig.timed(step, args.steps)
+    clk = clocks.stop() if clocks else None
+    launches = ctx.last_launches()
+
+    # stage breakdown and kernel-written spans (each timed call starts on an
+    # idle stream: stage events recorded behind a queue were stamped late)
+    ctx.set_timing(True)
+    stage_acc, span_acc = [0.0] * 5, [0.0, 0.0]
+    reps = max(3, min(args.steps, 10))
+    for _ in range(reps):
+        ctx.sync()
+        step()
+        stage_acc = [a + b for a, b in zip(stage_acc, ctx.last_timing())]
+        span_acc = [a + b for a, b in zip(span_acc, ctx.last_kernel_spans())]
+    ctx.set_timing(False)
+    stage_ms = [a / reps for a in stage_acc]
+    span_ms = [rig.max_over_ranks(a / reps) for a in span_acc]
+
+    comp = compressed_elems(tagc, shards, cfg)
+    owned_comp = compressed_elems(tagc, [s for s in shards if s.owner == rig.rank], cfg)
+    value = rig.world * n_params * 4.0 / (ms * 1e-3) / 1e9
+    res = {
+        "value": round(value, 3), "ms_per_step": round(ms, 4),
+        "peel": {"presence": st.presence, "peeled": st.peeled, "unresolved": st.unresolved,
+                 "index_lost": st.index_lost, "index_spurious": st.index_spurious,
+                 "grid_rounds": rounds[0], "tail_rounds": rounds[1]},
+        "k_fused_tma_ms": round(span_ms[0], 4), "decode_span_ms": round(span_ms[1], 4),
+        "stages_ms": dict(zip(("prep", "select_fused", "select_finish", "exchange", "decode"),
+                              (round(x, 4) for x in stage_ms))),
+        "launches_per_step": int(launches),
+    }
+    state = dict(specs=specs, cfg=cfg, shards=shards, total=total, n_params=n_params, ctx=ctx, grad=grad,
+                 acc=acc, out=out, owned=owned, comp=comp, owned_comp=owned_comp, ms=ms, span_ms=span_ms,
+                 clk=clk, step=step)
+    return res, state
+
+
+def uncompressed_comparator(rig, S, args):
+    """ncclReduceScatter fp32 of the same shards (baseline_reduce_shard,
+    hook.cpp:90-96): time and NCCL bus bandwidth ((W-1)/W x payload / t)."""
+    if rig.world > 1 and rig.exchange != "nccl":
+        return None  # a peer-exchange context has no NCCL communicator
+    torch, ctx, shards = rig.torch, S["ctx"], S["shards"]
+    base_out = torch.empty(max(S["owned"], 1), device=rig.dev)
+    for _ in range(args.warmup):
+        ctx.baseline_reduce_shards(shards, S["grad"], base_out)
+    ms = rig.timed(lambda i: ctx.baseline_reduce_shards(shards, S["grad"], base_out), args.steps)
+    payload = S["total"] * 4.0
+    bus = (rig.world - 1) / rig.world * payload / (ms * 1e-3) / 1e9 if rig.world > 1 else None
+    return {"value": round(rig.world * S["n_params"] * 4.0 / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "ms_per_step": round(ms, 4),
+            "nccl_bus_gbs": round(bus, 1) if bus is not None else None,
+            "what": "ncclReduceScatter fp32 of the same buffers" if rig.world > 1
+                    else "N=1: the reduce-scatter degenerates to a device copy"}
+
+
+def end_to_end(rig, S, args):
+    """The same metric through the C-ABI host-buffer entry
+    (tagc_reduce_shards_host): every step copies this step's gradient H2D from
+    pinned memory and the owner's decoded shard D2H; consecutive calls overlap
+    their copies with each other and with the exchange (two copy streams,
+    double-buffered device buffers). host_join() makes the timing stream wait
+    for the last D2H."""
+    torch, ctx, shards = rig.torch, S["ctx"], S["shards"]
+    host_grad = torch.empty(S["total"], dtype=torch.float32, pin_memory=True)
+    host_grad.copy_(S["grad"].cpu())
+    host_out = torch.empty(max(S["owned"], 1), dtype=torch.float32, pin_memory=True)
+    steps = max(args.steps, 10)
+    for _ in range(2):
+        ctx.tagc_reduce_shards_host(shards, host_grad, S["acc"], host_out)
+    ctx.host_join()
+
+    def one(i):
+        ctx.tagc_reduce_shards_host(shards, host_grad, S["acc"], host_out)
+        if i == steps - 1:
+            ctx.host_join()
+
+    ms = rig.timed(one, steps)
+    # the PCIe bound of that path: both directions at once (plain copies of
+    # the same buffers on two streams)
+    s_in, s_out = torch.cuda.Stream(device=rig.local), torch.cuda.Stream(device=rig.local)
+    scratch = torch.empty_like(S["grad"])
+
+    def copies(i):
+        s_in.wait_stream(rig.stream)
+        s_out.wait_stream(rig.stream)
+        with torch.cuda.stream(s_in):
+            scratch.copy_(host_grad, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            host_out.copy_(S["out"], non_blocking=True)
+        rig.stream.wait_stream(s_in)
+        rig.stream.wait_stream(s_out)
+
+    pcie_ms = rig.timed(copies, 3)
+    del scratch
+    u = rig.world * S["n_params"] * 4.0
+    return {"value": round(u / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(S["total"] * 4), "d2h_bytes_per_step": int(S["owned"] * 4),
+            "steps": steps, "ms_per_step": round(ms, 3),
+            "pcie_bound": round(u / (pcie_ms * 1e-3) / 1e9, 3),
+            "pcie_bound_note": "the same H2D + D2H bytes as plain concurrent copies, no exchange"}
+
+
+def owner_step_and_overlap(rig, tagc, S, args):
+    """SURVEY §8f rows 2 and 4 on the GPT-2 layout: exchange + adamw_nm step
+    on the owned shard, unfused vs fused into the decode emit; and a synthetic
+    backward pass (3 bf16 GEMMs per block) with the exchange one-shot after it
+    vs overlapped with it (tagc_overlap_*)."""
+    torch, ctx, shards, world = rig.torch, S["ctx"], S["shards"], rig.world
+    grad, acc, out, owned = S["grad"], S["acc"], S["out"], S["owned"]
+    params = torch.randn(max(owned, 1), device=rig.dev)
+    adam_v = torch.zeros(max(owned, 1), device=rig.dev)
+    reps = max(3, min(args.steps, 10))
 
     def timed(fn):
         for i in range(max(3, args.warmup)):  # eager, capture, first replay
             fn(i + 1)
-        barrier()
-        e0.record(stream)
-        for i in range(opt_steps):
-            fn(i + 2)
-        e1.record(stream)
-        barrier()
-        return max_over_ranks(e0.elapsed_time(e1)) / opt_steps
+        return rig.timed(lambda i: fn(i + 2), reps)
+
+    def apply_only(k):
+        ctx.apply_optimizer("adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)
 
     def unfused(k):
-        step()
-        ctx.apply_optimizer("adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)
+        S["step"]()
+        apply_only(k)
 
     def fused(k):
         ctx.tagc_reduce_shards_step(shards, grad, acc, params, "adamw_nm", 1e-3, k, adam_v=adam_v,
                                     weight_decay=0.01)
 
-    owner_step = {"optimizer": "adamw_nm",
-                  "apply_only_ms": round(timed(lambda k: ctx.apply_optimizer(
-                      "adamw_nm", 1e-3, params, out, world, k, adam_v, weight_decay=0.01)), 4),
-                  "unfused_ms": round(timed(unfused), 4), "fused_ms": round(timed(fused), 4)}
+    owner = {"optimizer": "adamw_nm", "apply_only_ms": round(timed(apply_only), 4),
+             "unfused_ms": round(timed(unfused), 4), "fused_ms": round(timed(fused), 4)}
 
-    # backward / exchange overlap (SURVEY §8f row 4): a synthetic backward
-    # pass on a producer stream (3 bf16 GEMMs 8192x768 @ 768x3072 per GPT-2
-    # block, then the block's gradient lands in the buffer), in reverse layer
-    # order. one_shot: tagc_reduce_shards after the backward; overlapped:
-    # tagc_overlap_* encoding each block as it lands. Times from backward start
-    # to the decoded shard, device events.
     groups, off = [], 0
-    for sp in specs:
+    for sp in S["specs"]:
         key = sp.name.split(".")[0] if sp.name.startswith("h") else ("final" if sp.name.startswith("ln_f") else "embed")
         if not groups or groups[-1][0] != key:
             groups.append([key, off, off])
         off += sp.param_count
         groups[-1][2] = off
     ranges = [(lo, hi) for _, lo, hi in groups]
-    ranges[-1] = (ranges[-1][0], total)  # the make_shards pad tail lands with the last block
-    ga = torch.randn(8192, 768, device=dev, dtype=torch.bfloat16)
-    gb = torch.randn(768, 3072, device=dev, dtype=torch.bfloat16)
-    gc = torch.empty(8192, 3072, device=dev, dtype=torch.bfloat16)
+    ranges[-1] = (ranges[-1][0], S["total"])  # the make_shards pad tail lands with the last block
+    ga = torch.randn(8192, 768, device=rig.dev, dtype=torch.bfloat16)
+    gb = torch.randn(768, 3072, device=rig.dev, dtype=torch.bfloat16)
+    gc = torch.empty(8192, 3072, device=rig.dev, dtype=torch.bfloat16)
     grad_bw = torch.empty_like(grad)
-    prod = torch.cuda.Stream(device=local)
+    prod = torch.cuda.Stream(device=rig.local)
 
     def backward(on_ready=None):
         for lo, hi in reversed(ranges):
@@ -221,360 +484,235 @@ def extra_sections(args, tagc, ctx, shards, grad, acc, out, owned, total, n_para
         done.record(prod)
         return done
 
-    def run_overlap(mode):
+    def run(mode):
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        prod.wait_stream(stream)  # iterations do not overlap each other
+        prod.wait_stream(rig.stream)
         b0.record(prod)
         if mode == "backward":
             backward()
             b1.record(prod)
         elif mode == "one_shot":
-            stream.wait_event(backward())
+            rig.stream.wait_event(backward())
             ctx.tagc_reduce_shards(shards, grad_bw, acc, out, stats=False)
-            b1.record(stream)
+            b1.record(rig.stream)
         else:
-            stream.wait_event(b0)
+            rig.stream.wait_event(b0)
             ctx.overlap_begin(shards, grad_bw, acc, out)
             backward(ctx.overlap_ready)
             ctx.overlap_finish()
-            b1.record(stream)
+            b1.record(rig.stream)
         return b0, b1
 
     overlap = {"producer": "3x bf16 mm 8192x768@768x3072 per block, 14 blocks, reverse order"}
     for mode in ("backward", "one_shot", "overlapped"):
         for _ in range(max(3, args.warmup)):
-            run_overlap(mode)
-        barrier()
-        evs = [run_overlap(mode) for _ in range(opt_steps)]
-        barrier()
-        overlap[mode + "_ms"] = round(max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / opt_steps), 4)
-    del ga, gb, gc, grad_bw
+            run(mode)
+        rig.barrier()
+        evs = [run(mode) for _ in range(reps)]
+        rig.barrier()
+        overlap[mode + "_ms"] = round(rig.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / reps), 4)
+    return owner, overlap
 
-    # e2e through the C-ABI host-buffer entry (tagc_reduce_shards_host): every
-    # step copies this step's gradient H2D from pinned memory and the owner's
-    # decoded shard D2H; consecutive calls overlap their copies with each
-    # other and with the exchange (two copy streams, double-buffered device
-    # buffers). host_join() makes the timing stream wait for the last D2H.
-    host_grad = torch.empty(total, dtype=torch.float32, pin_memory=True)
-    host_grad.copy_(grad.cpu())
-    host_out = torch.empty(max(owned, 1), dtype=torch.float32, pin_memory=True)
-    e2e_steps = min(max(30, args.steps), 60)  # ~10 ms a step (PCIe-bound): pipeline fill + drain once
-    for _ in range(2):
-        ctx.tagc_reduce_shards_host(shards, host_grad, acc, host_out)
-    ctx.host_join()
-    barrier()
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        ctx.tagc_reduce_shards_host(shards, host_grad, acc, host_out)
-    ctx.host_join()
-    e1.record(stream)
-    barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
-    # the PCIe bound of that path: both directions at once (torch copies of the
-    # same buffers on two streams), gradient-equivalent GB/s
-    s_in, s_out = torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)
-    pc0, pc1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for rep in range(3):
-        barrier()
-        pc0.record(stream)
-        s_in.wait_stream(stream)
-        s_out.wait_stream(stream)
-        with torch.cuda.stream(s_in):
-            grad_bw_probe = grad.copy_(host_grad, non_blocking=True)
-        with torch.cuda.stream(s_out):
-            host_out.copy_(out, non_blocking=True)
-        stream.wait_stream(s_in)
-        stream.wait_stream(s_out)
-        pc1.record(stream)
-        barrier()
-    pcie_ms = max_over_ranks(pc0.elapsed_time(pc1))
-    del grad_bw_probe
 
-    uncompressed = n_params * 4.0
-    e2e = {"value": round(world * uncompressed / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": int(total * 4), "d2h_bytes_per_step": int(owned * 4), "steps": e2e_steps,
-           "pcie_bound": round(world * uncompressed / (pcie_ms * 1e-3) / 1e9, 3),
-           "pcie_bound_note": "the same H2D + D2H bytes as plain concurrent copies, no exchange"}
-    return base_ms, owner_step, overlap, e2e
+def free_state(rig, S):
+    S["ctx"].sync()
+    S["ctx"].close()
+    S.clear()
+    rig.torch.cuda.synchronize()
+    rig.torch.cuda.empty_cache()
 
 
 def run_b200(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
+    rig = Rig(args)
+    torch = rig.torch
     import paper_2504_05638_b200 as tagc
 
-    world = args.gpus
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
-    # TAGC_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo host plumbing -
-    # a plumbing check of the N > 1 code on a one-GPU box (--exchange peer;
-    # NCCL refuses two ranks on one device). Never a measurement.
-    share = world > 1 and os.environ.get("TAGC_BENCH_SHARE_GPU") == "1"
-    if share:
-        local = 0
-    torch.cuda.set_device(local)
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = f"cuda:{local}"
-    specs = workload_specs(args.workload)
-    big = args.workload != "gpt2"  # 8B parameters: no room for the owner-step / overlap / e2e buffers
-    shards = tagc.make_shards(specs, world, world)
-    total = shards[-1].end
-    n_params = sum(s.param_count for s in specs)
-    cfg = cfg_obj()
-
-    stream = torch.cuda.Stream(device=local)
-    torch.cuda.set_stream(stream)
-    ctx = tagc.Context(cfg, world_size=world, rank=rank, device=local, stream=stream.cuda_stream)
-    if world > 1 and args.exchange == "peer":  # pulls over NVLink peer memory (CUDA IPC), no NCCL
-        handles = [None] * world
-        dist.all_gather_object(handles, ctx.peer_prepare(shards))
-        ctx.peer_open(handles)
-    elif world > 1:
-        obj = [tagc.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.init_nccl(obj[0])
-
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 + rank)
-    grad = torch.empty(total, device=dev)
-    chunk = 1 << 26  # generated in chunks: the temporaries of an 8B-element draw would not fit
-    for c0 in range(0, total, chunk):
-        c1 = min(total, c0 + chunk)
-        mag = torch.randn(c1 - c0, device=dev, generator=gen).exp_()
-        sign = torch.randint(0, 2, (c1 - c0,), device=dev, generator=gen, dtype=torch.int8)
-        grad[c0:c1] = torch.where(sign.bool(), -mag, mag)
-    del mag, sign
-    if total > n_params:
-        grad[n_params:] = 0.0  # make_shards pad tail
-    acc = torch.zeros(total, device=dev)
-    owned = sum(s.size() for s in shards if s.owner == rank)
-    out = torch.empty(max(owned, 1), device=dev)
-    torch.cuda.synchronize()
-
-    def step(stats=False):
-        return ctx.tagc_reduce_shards(shards, grad, acc, out, stats=stats)
-
-    for _ in range(args.warmup):
-        step()
-    _, st = step(stats=True)  # untimed: peel statistics of this config
-    rounds = ctx.last_peel_rounds()
-    ctx.set_timing(True)
-    step()
-    stage_ms = ctx.last_timing()
-    launches_per_step = ctx.last_launches()
-    ctx.set_timing(False)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            if share:
-                dist.barrier()
-            else:
-                dist.barrier(device_ids=[local])
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], device="cpu" if share else dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    clocks = ClockSampler(local)
-    barrier()
-    clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    clk = clocks.stop()
-
-    # per-stage device time of one step with stage events (prep, sampled select +
-    # fused split/encode, select finish, exchange, decode)
-    # (each timed call starts on an idle stream: stage events recorded behind a
-    # queue of earlier calls were seen to be stamped late)
-    # The roofline kernel's duration comes from device-side %globaltimer
-    # stamps the kernels write in timing mode (earliest CTA start of k_sample
-    # to latest CTA end of k_fused), averaged over the timed launches.
-    ctx.set_timing(True)
-    stage_acc = [0.0] * 5
-    span_acc = [0.0, 0.0]
-    for _ in range(args.steps):
-        ctx.sync()
-        step()
-        t = ctx.last_timing()
-        stage_acc = [a + b for a, b in zip(stage_acc, t)]
-        span_acc = [a + b for a, b in zip(span_acc, ctx.last_kernel_spans())]
-    ctx.set_timing(False)
-    stage_ms = [a / args.steps for a in stage_acc]
-    span_ms = [a / args.steps for a in span_acc]
-
-    base_ms = owner_step = overlap = e2e = None
-    if not big:
-        base_ms, owner_step, overlap, e2e = extra_sections(
-            args, tagc, ctx, shards, grad, acc, out, owned, total, n_params, specs, stream, dev, local, world,
-            step, barrier, max_over_ranks, e0, e1)
-    comp, fused_bytes = algorithmic_bytes(shards, rank, world)
+    head, S = measure_exchange(rig, tagc, args.workload, args)
+    cfg, world = S["cfg"], rig.world
     hbm, peak_kind = peaks()
-    fused_ms = span_ms[0]
+    fused_ms = S["span_ms"][0]
+    fused_bytes = S["comp"] * fused_bytes_per_elem(cfg)
     achieved = fused_bytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else 0.0
+    dec_bytes = S["owned_comp"] * decode_bytes_per_elem(cfg)
+    dec_ms = S["span_ms"][1]
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "fused_traffic.json")
-    if os.path.exists(tpath) and args.workload == "gpt2":  # captured on the default workload
+    tpath = os.path.join(ROOT, "profiles", f"fused_traffic_{args.workload}.json")
+    if os.path.exists(tpath) and world == 1:  # captured on this workload at N=1
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get("bytes_per_launch")
         except Exception:
             traffic = None
+    comparator = uncompressed_comparator(rig, S, args)
+    e2e = end_to_end(rig, S, args) if not args.no_e2e and args.workload != "llama3-8b" else None
+    clk = S["clk"]
+    launches = head["launches_per_step"]
+    config = workload_config(args.workload, world)
+    config["parallelism"] = (f"dp{world}: one process per GPU, "
+                             f"{'peer-memory pulls' if rig.exchange == 'peer' else 'NCCL reduce-scatter'}")
+    free_state(rig, S)
 
-    uncompressed = n_params * 4.0
-    value = world * uncompressed / (ms * 1e-3) / 1e9
+    extras = {}
+    if not args.no_extras and args.workload == "c4":
+        for name in ("gpt2", "gpt2-paper"):
+            r, S2 = measure_exchange(rig, tagc, name, args, full=False)
+            r["workload"] = WORKLOADS[name][0]
+            if name == "gpt2" and not args.no_owner_step:
+                r["owner_step"], r["overlap"] = owner_step_and_overlap(rig, tagc, S2, args)
+            free_state(rig, S2)
+            extras[name] = r
+
     result = {
-        "metric": METRIC,
-        "value": round(value, 3),
-        "unit": "GB/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(ms, 4),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
+        "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic log-normal gradients (SyntheticStream distribution), generated on device",
-        "config": {
-            "workload": WORKLOADS[args.workload],
-            "params_per_rank": n_params,
-            "shards": f"make_shards({args.workload}, {world}, {world})",
-            "compressed_params_per_rank": comp,
-            "peel": {"presence": st.presence, "peeled": st.peeled, "unresolved": st.unresolved,
-                     "rounds": rounds[0], "tail_rounds": rounds[1]},
-            "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per rank)",
-            "parallelism": f"dp{world} (one process per GPU, "
-                           f"{'peer-memory pulls' if args.exchange == 'peer' else 'NCCL reduce-scatter'})",
-        },
-        "e2e": e2e if e2e is not None else {"skipped": "8B-parameter workload: host buffers not allocated"},
-        "roofline": {"kernel": "k_fused_tma (TMA-staged select/split/index/sketch scatter)",
+        "config": config,
+        "peel": head["peel"],
+        "e2e": e2e if e2e is not None else {"skipped": "host buffers not allocated for this workload"},
+        "roofline": {"kernel": "k_fused_tma (TMA-staged select / split / index / sketch scatter)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(fused_bytes),
+                     "bytes_per_elem": round(fused_bytes_per_elem(cfg), 4),
                      "kernel_ms": round(fused_ms, 4),
                      "timed": "k_fused_tma launches: device span from %globaltimer stamps written by the "
-                              "kernel (first CTA start to last CTA end), mean of the timed launches"},
-        "decode_span_ms": round(span_ms[1], 4),
-        "stages_ms": {"prep": round(stage_ms[0], 4), "select_fused": round(stage_ms[1], 4),
-                      "select_finish": round(stage_ms[2], 4), "exchange": round(stage_ms[3], 4),
-                      "decode": round(stage_ms[4], 4)},
-        "uncompressed_rs": ({"value": round(world * uncompressed / (base_ms * 1e-3) / 1e9, 3),
-                             "unit": "GB/s", "ms_per_step": round(base_ms, 4)} if base_ms else None),
-        "owner_step": owner_step,
-        "overlap": overlap,
-        "gpu_launches": int(launches_per_step * args.steps),
+                              "kernel (first CTA start to last CTA end), mean of the timed launches, max "
+                              "over ranks"},
+        "decode_roofline": {"kernels": "k_list .. k_emit (owner decode chain)", "bound": "hbm",
+                            "achieved": round(dec_bytes / (dec_ms * 1e-3) / 1e9, 1) if dec_ms > 0 else None,
+                            "peak": hbm, "unit": "GB/s",
+                            "frac": round(dec_bytes / (dec_ms * 1e-3) / 1e9 / hbm, 4) if dec_ms > 0 else None,
+                            "algorithmic_bytes": int(dec_bytes), "span_ms": round(dec_ms, 4)},
+        "stages_ms": head["stages_ms"],
+        "uncompressed_rs": comparator,
+        "extras": extras,
+        "gpu_launches": int(launches * args.steps),
         "clocks": clk,
     }
-    if share:
-        result["config"]["shared_gpu_plumbing_check"] = "all ranks on cuda:0 (TAGC_BENCH_SHARE_GPU=1): not a measurement"
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
-        result["cpu_baseline"] = cpu_baseline(args, specs, world, budget_s=args.cpu_budget)
-    if rank == 0:
+    if rig.share:
+        result["config"]["shared_gpu_plumbing_check"] = \
+            "all ranks on cuda:0 (TAGC_BENCH_SHARE_GPU=1): not a measurement"
+    if not args.no_cpu_baseline:
+        # rank 0 times the reference's CPU path on the host cores while the
+        # other ranks wait (a reported baseline, outside every timed region)
+        cb = cpu_baseline(args, world) if rig.rank == 0 else None
+        rig.barrier()
+        if cb is not None:
+            result["cpu_baseline"] = cb
+    if rig.rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
-        barrier()
-        dist.destroy_process_group()
+        rig.barrier()
+        rig.dist.destroy_process_group()
 
 
-def sample_shards(specs, world, budget_elems):
-    """A bounded sample of the workload: the shard plan of make_shards(specs,
-    W, W) restricted to its first segments up to ~budget_elems per rank."""
+# --------------------------------------------------------------------------- reference arm
+def reference_plan(name, world, sample_elems):
+    """The reference's own make_shards (hook.cpp:30-61, through oracle/_ref) on
+    the workload's layer list; for the single-bucket workload a bounded sample
+    is the first `sample_elems` elements of each rank's bucket, sharded the
+    same way. Returns (oracle Shards, elements per rank)."""
     import oracle as O
-    import paper_2504_05638_b200 as tagc
 
-    shards = tagc.make_shards(specs, world, world)
-    out, used = [], 0
-    for sh in shards:
-        segs = []
-        for s in sh.segments:
-            if used >= budget_elems:
-                break
-            segs.append(O.Segment(s.kind, s.begin, s.end, s.name))
-            used += s.size()
-        if segs:
-            out.append(O.Shard(sh.id, sh.owner, segs[0].begin, segs[-1].end, segs))
-    return out, used
+    ref = O.Ref()
+    desc, layers, theta, ratio, width, policy, mcs = WORKLOADS[name]
+    lay = layers()
+    if name == "c4":
+        lay = [("bucket", "feed_forward", min(sample_elems, C4_N))]
+    counts = [c for _, _, c in lay]
+    kinds = [O.KIND[k] for _, k, _ in lay]
+    inv = {v: k for k, v in O.KIND.items()}
+    slen, segs = ref.make_shards(counts, kinds, world, world)
+    shards = []
+    for sid in range(world):
+        ss = [O.Segment(inv[k], b, e) for (s, k, b, e) in segs if s == sid]
+        shards.append(O.Shard(sid, sid % world, sid * slen, (sid + 1) * slen, ss))
+    per_rank = world * slen
+    if name != "c4":  # layered workloads: the first segments up to the sample size
+        out, used = [], 0
+        for sh in shards:
+            keep = []
+            for s in sh.segments:
+                if used >= sample_elems:
+                    break
+                keep.append(s)
+                used += s.size
+            if keep:
+                out.append(O.Shard(sh.id, sh.owner, keep[0].begin, keep[-1].end, keep))
+        shards, per_rank = out, used
+    cfg = O.Config(theta, ratio, width, policy, True, SEED, 3, False, mcs)
+    return ref, shards, per_rank, cfg
 
 
-def cpu_baseline(args, specs, world, budget_s=20.0):
+def reference_sample_elems(world):
+    # ~2-3 s of reference work per step on 16 host cores: a quarter of the
+    # 2^28 bucket at N = 1, the same total at every N
+    return max(1 << 22, (1 << 26) // world)
+
+
+def time_reference(name, world, steps, warmup, sample_elems):
+    import oracle as O
+
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    ref, shards, per_rank, cfg = reference_plan(name, world, sample_elems)
+    end = max(s.end for s in shards)
+    grads = list(ref.stream(end, 2024, count=world))  # the reference's SyntheticStream
+    if warmup:
+        ref.time_reduce_shards(shards, grads, cfg, reps=warmup)
+    secs = ref.time_reduce_shards(shards, grads, cfg, reps=steps)
+    t = float(secs.mean())
+    value = world * per_rank * 4 / t / 1e9
+    sample = (f"{'first ' if name != 'c4' else ''}{per_rank} elements per rank of {WORKLOADS[name][0]} "
+              f"({'a 2^' + str(per_rank.bit_length() - 1) + '-element bucket' if name == 'c4' else 'leading segments'}"
+              f", make_shards({world}, {world}) by the reference), tagc_reduce_shard with World({world}, "
+              f"parallel), OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}")
+    return value, t, sample
+
+
+def cpu_baseline(args, world):
     """The reference's own CPU path (oracle/_ref) on the host cores, bounded."""
-    import numpy as np
-
     import oracle as O
 
     if not O.Ref.available():
         return {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    ref = O.Ref()
-    budget = args.cpu_elems
-    shards, used = sample_shards(specs, world, budget)
-    end = max(s.end for s in shards)
-    grads = list(O.Oracle().stream(end, 2024, count=world))
-    cfg = O.Config(THETA, RATIO, WIDTH, "non_attention_linear", True, SEED, 3, False, 1024)
-    # each shard's grads are sliced by the reference wrapper from the flat buffers
-    secs = ref.time_reduce_shards(shards, grads, cfg, reps=1)
-    t = float(secs.min())
-    return {"value": round(world * used * 4 / t / 1e9, 5), "unit": "GB/s",
-            "cores": os.cpu_count(), "kind": "reference",
-            "sample": f"first {used} params per rank of the workload ({len(shards)} shard(s)), "
-                      f"tagc_reduce_shard World({world}, parallel), OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}",
-            "seconds": round(t, 3)}
+    value, t, sample = time_reference(args.workload, world, 2, 0, reference_sample_elems(world))
+    return {"value": round(value, 5), "unit": "GB/s", "cores": int(os.environ.get("OMP_NUM_THREADS")),
+            "cpu_model": cpu_model(), "kind": "reference", "sample": sample, "seconds_per_step": round(t, 3)}
 
 
 def run_reference(args):
     world = args.gpus
-    rank = env_int("RANK", 0)
-    if rank != 0:
+    if env_int("RANK", 0) != 0:
         return
-    import numpy as np
-
     import oracle as O
 
     if not O.Ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtagc_ref.so not built"}))
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    specs = workload_specs()
-    shards, used = sample_shards(specs, world, args.cpu_elems)
-    end = max(s.end for s in shards)
-    grads = list(O.Oracle().stream(end, 2024, count=world))
-    cfg = O.Config(THETA, RATIO, WIDTH, "non_attention_linear", True, SEED, 3, False, 1024)
-    ref = O.Ref()
-    ref.time_reduce_shards(shards, grads, cfg, reps=max(0, min(args.warmup, 1)) or 1)
-    secs = ref.time_reduce_shards(shards, grads, cfg, reps=args.steps)
-    t = float(secs.mean())
-    value = world * used * 4 / t / 1e9
-    sample = (f"first {used} params per rank of {WORKLOAD} ({len(shards)} shard(s)), "
-              f"tagc_reduce_shard World({world}, parallel)")
+    value, t, sample = time_reference(args.workload, world, args.steps, max(0, min(args.warmup, 1)),
+                                      reference_sample_elems(world))
+    config = workload_config(args.workload, world)
+    config["parallelism"] = f"reference World({world}, parallel): in-process ranks on the host cores"
+    cores = int(os.environ.get("OMP_NUM_THREADS"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic SyntheticStream gradients (reference generator)",
-        "config": {"workload": WORKLOAD, "sample_params_per_rank": used},
-        "cpu_baseline": {"value": round(value, 5), "unit": "GB/s", "cores": os.cpu_count(),
+        "data": "synthetic SyntheticStream gradients (the reference's own generator)",
+        "config": config,
+        "cpu_baseline": {"value": round(value, 5), "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(),
                          "kind": "reference", "sample": sample},
-        "e2e": {"value": round(value, 5), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "e2e": {"value": round(value, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+# --------------------------------------------------------------------------- launch
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -583,17 +721,23 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-elems", type=int, default=24_000_000,
-                    help="params per rank in the bounded CPU-reference sample")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="gpt2", choices=sorted(WORKLOADS),
-                    help="gpt2 (BASELINE config 2, the default line) or llama3-8b (config 3's layout)")
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS),
+                    help="c4 (BASELINE config 4: one 2^28 bucket, the default line), gpt2 / gpt2-paper "
+                         "(config 2's layout), llama3-8b (config 3's layout)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N>1 collective: grouped ncclReduceScatter, or pulls over peer memory")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the GPT-2 extra lines")
+    ap.add_argument("--no-owner-step", action="store_true", help="skip the owner-step / overlap timings")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # self-launch: one process per GPU under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+        sys.exit(subprocess.call(cmd + sys.argv[1:]))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -93,7 +93,10 @@ typedef struct tagc_shard {
   uint32_t num_segments;
 } tagc_shard;
 
-/* reference PeelStats, hook.hpp:45-59 */
+/* reference PeelStats, hook.hpp:45-59. index_lost / index_spurious are
+ * TAGC_STAT_UNAVAILABLE when a 1-bit-index split exchange (_begin / _end)
+ * was not given the ranks' support blocks (tagc_reduce_shards_support). */
+#define TAGC_STAT_UNAVAILABLE UINT64_MAX
 typedef struct tagc_peel_stats {
   uint64_t presence, peeled, unresolved, index_lost, index_spurious, compressed_segments,
       baseline_segments;
@@ -237,6 +240,14 @@ int tagc_ctx_last_peel_rounds(tagc_ctx* ctx, uint32_t out[2]);
 int tagc_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
                           const float* const* grads, float* const* accs, float* out,
                           tagc_peel_stats* stats);
+/* tagc_reduce_shard(..., collect_audit = true) (hook.cpp:98-200): as
+ * tagc_reduce_shard_sim, plus audit (dev, shard.size() floats) =
+ * ShardReduceResult::audit_exchanged_sum (hook.hpp:61-68, hook.cpp:191-195):
+ * the ascending-rank sum of the exchanged (post-sparsify) vectors over
+ * compressed segments, zeros over raw segments. */
+int tagc_reduce_shard_sim_audit(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
+                                const float* const* grads, float* const* accs, float* out,
+                                tagc_peel_stats* stats, float* audit);
 /* baseline_reduce_shard (hook.cpp:90-96): ascending-rank fp32 sum. */
 int tagc_baseline_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
                                    const float* const* grads, float* out);
@@ -285,6 +296,22 @@ int tagc_ctx_host_join(tagc_ctx* ctx);
 int tagc_reduce_shards_begin(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards,
                              const float* grad, float* acc, float* out, float** send_f32,
                              uint32_t** send_u32, uint64_t* block_f32, uint64_t* block_u32);
+/* 1-bit index only (index_lost / index_spurious, hook.cpp:176-188): after
+ * _begin, this rank's index support as one byte (0/1) per position in
+ * owner-major blocks of *block_bytes = 32 * block_u32 bytes (dev; into
+ * *send_support when non-NULL on input, else engine workspace, returned).
+ * The caller max-reduce-scatters them (max of 0/1 bytes = OR) and passes its
+ * reduced block to _end_support. */
+int tagc_reduce_shards_support(tagc_ctx* ctx, uint8_t** send_support, uint64_t* block_bytes);
+int tagc_reduce_shards_end_support(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
+                                   const uint8_t* recv_support, tagc_peel_stats* stats);
+/* tagc_reduce_shards with collect_audit = true: audit (dev, laid out like
+ * out) = audit_exchanged_sum of the owned shards (hook.cpp:191-195), zeros
+ * over raw segments. NCCL world or world_size 1 (a peer-exchange context
+ * returns TAGC_INVALID). Diagnostic: one extra fp32 reduce-scatter of the
+ * sparse vectors, and the call synchronises. */
+int tagc_reduce_shards_audit(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad,
+                             float* acc, float* out, tagc_peel_stats* stats, float* audit);
 int tagc_reduce_shards_end(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
                            tagc_peel_stats* stats);
 /* Pull-mode exchange over peer memory (NVLink / NVSwitch) instead of NCCL.

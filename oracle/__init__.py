@@ -531,6 +531,18 @@ class Ref:
                "ref_tagc_reduce_shard")
         return out, st.as_dict(), csv.value.decode()
 
+    def tagc_reduce_shard_audit(self, shard: Shard, grads, accs, cfg: Config):
+        """tagc_reduce_shard(..., collect_audit=true): (decoded, audit_exchanged_sum)."""
+        gs = [_f32(g) for g in grads]
+        sc = _ShardC(shard)
+        out = np.empty(shard.size, np.float32)
+        audit = np.empty(shard.size, np.float32)
+        _check(self.lib.ref_tagc_reduce_shard_audit(C.byref(sc.c), _ptr_array(gs, C.c_float),
+                                                    _ptr_array(accs, C.c_float), C.c_uint32(len(gs)),
+                                                    C.byref(cfg.c()), _p(out, C.c_float), _p(audit, C.c_float)),
+               "ref_tagc_reduce_shard_audit")
+        return out, audit
+
     def time_reduce_shards(self, shards, grads, cfg: Config, reps=1):
         """Times tagc_reduce_shard over every shard with World(W, parallel);
         returns per-rep seconds (conversion to reference containers untimed)."""
@@ -587,6 +599,16 @@ class Ref:
                                         C.c_uint32(cap), C.byref(ns)), "ref_make_shards")
         return int(slen.value), [(int(sh[i]), int(segs[i].kind), int(segs[i].begin), int(segs[i].end))
                                  for i in range(ns.value)]
+
+    def roundtrip_trial(self, n, theta, world, seed, t):
+        """Trial t of roundtrip_experiment's generator (roundtrip.cpp:65-95):
+        (grads [world x n] float32, the trial's compression seed)."""
+        g = np.empty((world, n), np.float32)
+        ts = C.c_uint64()
+        _check(self.lib.ref_roundtrip_trial(C.c_uint32(n), C.c_double(theta), C.c_uint32(world),
+                                            C.c_uint64(seed), C.c_uint32(t), _p(g, C.c_float), C.byref(ts)),
+               "ref_roundtrip_trial")
+        return g, int(ts.value)
 
     def roundtrip(self, n, trials, theta, ratio, width, world, rows=3, seed=1):
         out = np.zeros(4, np.float64)

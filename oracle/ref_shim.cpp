@@ -8,6 +8,7 @@
 // box's host cores. Struct types are borrowed from tagc_oracle.h (plain C).
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <optional>
 #include <sstream>
@@ -267,6 +268,27 @@ int ref_tagc_reduce_shard(const or_shard* shard, const float* const* grads, floa
   });
 }
 
+// tagc_reduce_shard(..., collect_audit = true): the decoded shard and
+// ShardReduceResult::audit_exchanged_sum (hook.cpp:191-195).
+int ref_tagc_reduce_shard_audit(const or_shard* shard, const float* const* grads, float* const* accs,
+                                uint32_t world, const or_config* config, float* decoded, float* audit) {
+  return guarded([&] {
+    const ShardSpec sh = to_shard(shard);
+    const uint64_t len = sh.size();
+    std::vector<std::vector<float>> g(world);
+    std::vector<ResidualAccumulator> acc(world, ResidualAccumulator(len));
+    for (uint32_t r = 0; r < world; ++r) {
+      g[r].assign(grads[r], grads[r] + len);
+      std::memcpy(acc[r].values.data(), accs[r], len * sizeof(float));
+    }
+    World w(world, WorldMode::sequential);
+    const ShardReduceResult res = tagc_reduce_shard(sh, g, acc, to_config(config), w, true);
+    for (uint32_t r = 0; r < world; ++r) std::memcpy(accs[r], acc[r].values.data(), len * sizeof(float));
+    std::memcpy(decoded, res.decoded->data(), len * sizeof(float));
+    std::memcpy(audit, res.audit_exchanged_sum->data(), len * sizeof(float));
+  });
+}
+
 // Timing entry for bench.py --impl reference: the caller's buffers are
 // converted to the reference's containers OUTSIDE the timed region, and only
 // tagc_reduce_shard itself is timed (BASELINE.md §2 "What is timed").
@@ -374,6 +396,48 @@ int ref_make_shards(const uint64_t* counts, const int32_t* kinds, uint32_t n_lay
 // roundtrip.cpp:31-144 — out: mean_pf, min_pf, max_rel_resolved, max_rel_any;
 // counts: trials_fully_peeled, presence_total, unresolved_total, index_lost,
 // index_spurious, integer_exact, pass
+// Trial t of roundtrip_experiment (roundtrip.cpp:65-95): the per-rank
+// gradients and the trial's compression seed, drawn with the reference's own
+// Rng / splitmix64 in the reference's draw order. sample_support
+// (roundtrip.cpp:17-28) is file-static in the reference, so its partial
+// Fisher-Yates is restated here; tests pin this generator by reproducing the
+// reference's roundtrip reports from it (tests/test_oracle.py).
+int ref_roundtrip_trial(uint32_t n, double theta, uint32_t world, uint64_t seed, uint32_t t, float* grads,
+                        uint64_t* trial_seed) {
+  return guarded([&] {
+    const uint32_t zeros = static_cast<uint32_t>(std::ceil(theta * static_cast<double>(n) / 100.0));
+    const uint32_t support = n - std::min(zeros, n);
+    Rng rng(splitmix64(seed + 0x9E3779B97F4A7C15ULL * (t + 1)));
+    const bool integer_trial = (t % 2 == 0);
+    std::vector<uint32_t> all(n);
+    for (uint32_t i = 0; i < n; ++i) all[i] = i;
+    for (uint32_t i = 0; i < support; ++i) {
+      const uint32_t j = i + static_cast<uint32_t>(rng.next_below(n - i));
+      std::swap(all[i], all[j]);
+    }
+    all.resize(support);
+    std::sort(all.begin(), all.end());
+    std::memset(grads, 0, sizeof(float) * size_t(world) * n);
+    for (uint32_t p : all) {
+      const uint64_t mask = rng.next_below((1ull << world) - 1) + 1;
+      for (uint32_t r = 0; r < world; ++r) {
+        if (!(mask >> r & 1)) continue;
+        float v;
+        if (integer_trial) {
+          v = static_cast<float>(1 + static_cast<int>(rng.next_below(16)));
+          if (rng.next_u64() & 1) v = -v;
+        } else {
+          do {
+            v = static_cast<float>(rng.next_double() * 2.0 - 1.0);
+          } while (v == 0.0f);
+        }
+        grads[size_t(r) * n + p] = v;
+      }
+    }
+    *trial_seed = rng.next_u64();
+  });
+}
+
 int ref_roundtrip(uint32_t n, uint32_t trials, double theta, uint32_t ratio, uint32_t width,
                   uint32_t world, uint32_t rows, uint64_t seed, double* out4, uint64_t* counts7) {
   return guarded([&] {

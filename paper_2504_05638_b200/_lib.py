@@ -140,6 +140,11 @@ SIGNATURES = {
     "tagc_reduce_shards_begin": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(VP), C.POINTER(VP),
                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "tagc_reduce_shards_end": (C.c_int, [VP, VP, VP, C.POINTER(PeelStats)]),
+    "tagc_reduce_shards_support": (C.c_int, [VP, C.POINTER(VP), C.POINTER(C.c_uint64)]),
+    "tagc_reduce_shards_end_support": (C.c_int, [VP, VP, VP, VP, C.POINTER(PeelStats)]),
+    "tagc_reduce_shards_audit": (C.c_int, [VP, C.POINTER(Shard), U32, VP, VP, VP, C.POINTER(PeelStats), VP]),
+    "tagc_reduce_shard_sim_audit": (C.c_int, [VP, C.POINTER(Shard), U32, C.POINTER(VP), C.POINTER(VP), VP,
+                                              C.POINTER(PeelStats), VP]),
     "tagc_ctx_peer_prepare": (C.c_int, [VP, C.POINTER(Shard), U32, C.c_char_p]),
     "tagc_ctx_peer_open": (C.c_int, [VP, C.c_char_p]),
     "tagc_ctx_peer_attach_local": (C.c_int, [VP, C.POINTER(VP), U32]),

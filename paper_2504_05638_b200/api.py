@@ -34,7 +34,7 @@ __all__ = [
     "CompressionConfig", "LayerSpec", "LayerSegment", "ShardSpec", "PeelStats", "Context",
     "make_shards", "kind_compressible", "sketch_geometry", "words_needed", "theta_floor",
     "comm_volume_model", "lhc_comm_volume_model", "TagcError", "TagcInvalidArgument",
-    "device_count", "plan_exchange", "TrafficLedger",
+    "device_count", "plan_exchange", "TrafficLedger", "STAT_UNAVAILABLE",
 ]
 
 
@@ -220,6 +220,25 @@ def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+STAT_UNAVAILABLE = 2**64 - 1  # index_lost / index_spurious without the ranks' supports
+
+
+def _dev_f32(t, n: int, name: str, device: int):
+    """The kernels take raw pointers and trust the sizes: check a device
+    buffer before its pointer crosses the C-ABI (float32, contiguous, on the
+    context's device, at least n elements)."""
+    if t is None:
+        raise TagcInvalidArgument(2, f"{name}: missing buffer")
+    if not t.is_cuda or t.device.index != device:
+        raise TagcInvalidArgument(2, f"{name}: must be a CUDA tensor on cuda:{device}")
+    if str(t.dtype) != "torch.float32":
+        raise TagcInvalidArgument(2, f"{name}: must be float32")
+    if not t.is_contiguous():
+        raise TagcInvalidArgument(2, f"{name}: must be contiguous")
+    if t.numel() < n:
+        raise TagcInvalidArgument(2, f"{name}: {t.numel()} elements, needs {n}")
+
+
 def _ptr_array(ts):
     return (C.c_void_p * len(ts))(*[_ptr(t) for t in ts])
 
@@ -398,11 +417,34 @@ class Context:
             if g.numel() != shard.size() or a.numel() != shard.size():
                 raise TagcInvalidArgument(2, "gradient slice length does not match the shard")
         out = self._empty(shard.size()) if out is None else out
+        for i, (g, a) in enumerate(zip(grads, accs)):
+            _dev_f32(g, shard.size(), f"grads[{i}]", self.device)
+            _dev_f32(a, shard.size(), f"accs[{i}]", self.device)
+        _dev_f32(out, shard.size(), "out", self.device)
         sc = _ShardC(shard)
         st = _lib.PeelStats()
         check(lib.tagc_reduce_shard_sim(self.h, C.byref(sc.c), w, _ptr_array(grads), _ptr_array(accs),
                                         _ptr(out), C.byref(st) if stats else None), "tagc_reduce_shard")
         return out, (PeelStats(**st.as_dict()) if stats else None)
+
+    def tagc_reduce_shard_sim_audit(self, shard: ShardSpec, grads, accs, out=None, stats=True):
+        """tagc_reduce_shard(..., collect_audit=true): (out, stats, audit),
+        audit = audit_exchanged_sum (hook.cpp:191-195)."""
+        w = len(grads)
+        if len(accs) != w:
+            raise TagcInvalidArgument(2, "need one accumulator per rank")
+        out = self._empty(shard.size()) if out is None else out
+        for i, (g, a) in enumerate(zip(grads, accs)):
+            _dev_f32(g, shard.size(), f"grads[{i}]", self.device)
+            _dev_f32(a, shard.size(), f"accs[{i}]", self.device)
+        _dev_f32(out, shard.size(), "out", self.device)
+        audit = self._empty(max(1, shard.size()))
+        sc = _ShardC(shard)
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shard_sim_audit(self.h, C.byref(sc.c), w, _ptr_array(grads), _ptr_array(accs),
+                                              _ptr(out), C.byref(st) if stats else None, _ptr(audit)),
+              "tagc_reduce_shard")
+        return out, (PeelStats(**st.as_dict()) if stats else None), audit
 
     def baseline_reduce_shard_sim(self, shard: ShardSpec, grads, out=None):
         for g in grads:
@@ -414,10 +456,19 @@ class Context:
                                                  _ptr(out)), "baseline_reduce_shard")
         return out
 
+    def _check_exchange(self, shards, grad, acc, out, owned):
+        end = max((s.end for s in shards), default=0)
+        if grad is not None:
+            _dev_f32(grad, end, "grad", self.device)
+        _dev_f32(acc, end, "acc", self.device)
+        if out is not None:
+            _dev_f32(out, owned, "out", self.device)
+
     def tagc_reduce_shards(self, shards: Sequence[ShardSpec], grad, acc, out=None, stats=True):
         """One process per GPU: exchange every shard, decode the owned ones."""
         owned = sum(s.size() for s in shards if s.owner == self.rank)
         out = self._empty(max(owned, 1)) if out is None else out
+        self._check_exchange(shards, grad, acc, out, owned)
         scs = [_ShardC(s) for s in shards]
         arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
         st = _lib.PeelStats()
@@ -437,6 +488,11 @@ class Context:
         for t in (host_grad, host_out):
             if t.is_cuda:
                 raise TagcInvalidArgument(2, "host buffers must be CPU tensors")
+            if t.dtype != self.torch.float32 or not t.is_contiguous():
+                raise TagcInvalidArgument(2, "host buffers must be contiguous float32")
+        if host_grad.numel() < max((s.end for s in shards), default=0) or host_out.numel() < owned:
+            raise TagcInvalidArgument(2, "host buffer too short for the shard layout")
+        self._check_exchange(shards, None, acc, None, owned)
         scs = [_ShardC(s) for s in shards]
         arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
         st = _lib.PeelStats()
@@ -449,6 +505,8 @@ class Context:
         encodes into the caller's owner-major send blocks (send_f: world *
         block_f32 floats, send_u: world * block_u32 int32 words, sizes from
         plan_exchange). Returns (block_f32, block_u32)."""
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        self._check_exchange(shards, grad, acc, out, owned)
         scs = [_ShardC(s) for s in shards]
         arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
         pf, pu = C.c_void_p(_ptr(send_f)), C.c_void_p(_ptr(send_u))
@@ -457,12 +515,42 @@ class Context:
                                            C.byref(pu), C.byref(bf), C.byref(bu)), "reduce_shards_begin")
         return int(bf.value), int(bu.value)
 
-    def reduce_shards_end(self, recv_f, recv_u, stats=True):
-        """Second half: decode this rank's reduced blocks into the `out` given to begin."""
+    def reduce_shards_end(self, recv_f, recv_u, stats=True, recv_support=None):
+        """Second half: decode this rank's reduced blocks into the `out` given
+        to begin. recv_support (1-bit index): this rank's max-reduced support
+        block (reduce_shards_support), so that stats carry index_lost /
+        index_spurious; without it they read STAT_UNAVAILABLE."""
         st = _lib.PeelStats()
-        check(lib.tagc_reduce_shards_end(self.h, _ptr(recv_f), _ptr(recv_u), C.byref(st) if stats else None),
-              "reduce_shards_end")
+        if recv_support is not None:
+            check(lib.tagc_reduce_shards_end_support(self.h, _ptr(recv_f), _ptr(recv_u), _ptr(recv_support),
+                                                     C.byref(st) if stats else None), "reduce_shards_end")
+        else:
+            check(lib.tagc_reduce_shards_end(self.h, _ptr(recv_f), _ptr(recv_u), C.byref(st) if stats else None),
+                  "reduce_shards_end")
         return PeelStats(**st.as_dict()) if stats else None
+
+    def reduce_shards_support(self, send_support):
+        """1-bit index, after reduce_shards_begin: this rank's support bytes
+        (0/1 per position, owner-major) into send_support (uint8 CUDA tensor
+        of world_size * block_bytes); returns block_bytes (= 32 * block_u32)."""
+        bb = C.c_uint64()
+        p = C.c_void_p(_ptr(send_support))
+        check(lib.tagc_reduce_shards_support(self.h, C.byref(p), C.byref(bb)), "reduce_shards_support")
+        return int(bb.value)
+
+    def tagc_reduce_shards_audit(self, shards: Sequence[ShardSpec], grad, acc, out=None, stats=True):
+        """tagc_reduce_shards with collect_audit (hook.cpp:191-195): returns
+        (out, stats, audit), audit laid out like out (zeros over raw segments)."""
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        out = self._empty(max(owned, 1)) if out is None else out
+        audit = self._empty(max(owned, 1))
+        self._check_exchange(shards, grad, acc, out, owned)
+        scs = [_ShardC(s) for s in shards]
+        arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
+        st = _lib.PeelStats()
+        check(lib.tagc_reduce_shards_audit(self.h, arr, len(scs), _ptr(grad), _ptr(acc), _ptr(out),
+                                           C.byref(st) if stats else None, _ptr(audit)), "tagc_reduce_shards_audit")
+        return out, (PeelStats(**st.as_dict()) if stats else None), audit
 
     def peer_prepare(self, shards: Sequence[ShardSpec]) -> bytes:
         """Allocate this rank's peer-exchange region for the shard layout and
@@ -567,6 +655,11 @@ class Context:
         kinds = {"sgd": 0, "adamw_nm": 1}
         if optimizer not in kinds:
             raise TagcInvalidArgument(2, f"unknown optimizer: {optimizer}")
+        owned = sum(s.size() for s in shards if s.owner == self.rank)
+        self._check_exchange(shards, grad, acc, out, owned)
+        _dev_f32(params, owned, "params", self.device)
+        if adam_v is not None:
+            _dev_f32(adam_v, owned, "adam_v", self.device)
         scs = [_ShardC(s) for s in shards]
         arr = (_lib.Shard * len(scs))(*[s.c for s in scs])
         st = _lib.PeelStats()
@@ -582,6 +675,7 @@ class Context:
         returns out (this rank's decoded shards, complete after finish)."""
         owned = sum(s.size() for s in shards if s.owner == self.rank)
         out = self._empty(max(owned, 1)) if out is None else out
+        self._check_exchange(shards, grad, acc, out, owned)
         scs = [_ShardC(s) for s in shards]
         self._overlap_keep = (scs, grad, acc, out)
         arr = (_lib.Shard * len(scs))(*[s.c for s in scs])

@@ -362,6 +362,50 @@ int tagc_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world
   });
 }
 
+int tagc_reduce_shard_sim_audit(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
+                                const float* const* grads, float* const* accs, float* out,
+                                tagc_peel_stats* stats, float* audit) {
+  return guarded([&] {
+    if (!audit) throw InvalidArgument("null audit buffer");
+    PeelStats st;
+    eng(ctx).reduce_shard_sim(to_shard(shard), world, grads, accs, out, stats ? &st : nullptr, audit);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
+int tagc_reduce_shards_support(tagc_ctx* ctx, uint8_t** send_support, uint64_t* block_bytes) {
+  return guarded([&] { eng(ctx).exchange_support(send_support, block_bytes); });
+}
+
+int tagc_reduce_shards_end_support(tagc_ctx* ctx, const float* recv_f32, const uint32_t* recv_u32,
+                                   const uint8_t* recv_support, tagc_peel_stats* stats) {
+  return guarded([&] {
+    PeelStats st;
+    Engine& e = eng(ctx);
+    e.set_support_recv(recv_support);
+    e.exchange_end(recv_f32, recv_u32, stats ? &st : nullptr);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
+int tagc_reduce_shards_audit(tagc_ctx* ctx, const tagc_shard* shards, uint32_t n_shards, const float* grad,
+                             float* acc, float* out, tagc_peel_stats* stats, float* audit) {
+  return guarded([&] {
+    if (!audit) throw InvalidArgument("null audit buffer");
+    std::vector<ShardSpec> v;
+    for (uint32_t i = 0; i < n_shards; ++i) v.push_back(to_shard(&shards[i]));
+    PeelStats st;
+    eng(ctx).reduce_shards_audit(v, grad, acc, out, stats ? &st : nullptr, audit);
+    if (stats)
+      *stats = tagc_peel_stats{st.presence, st.peeled, st.unresolved, st.index_lost,
+                               st.index_spurious, st.compressed_segments, st.baseline_segments};
+  });
+}
+
 int tagc_baseline_reduce_shard_sim(tagc_ctx* ctx, const tagc_shard* shard, uint32_t world,
                                    const float* const* grads, float* out) {
   return guarded([&] { eng(ctx).baseline_sim(to_shard(shard), world, grads, out); });

@@ -372,12 +372,15 @@ void Engine::sync_check() {
   if (h2d_) cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
   if (d2h_) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
   cuda_check(cudaStreamSynchronize(stream_), "stream sync");
-  uint32_t err = 0;
-  cuda_check(cudaMemcpy(&err, err_flag(), 4, cudaMemcpyDeviceToHost), "D2H err");
-  if (err & 1u) throw InvalidArgument("sparsify: NaN gradient value");
-  uint32_t peer_err = 0;
-  cuda_check(cudaMemcpy(&peer_err, err_flag() + 2, 4, cudaMemcpyDeviceToHost), "D2H err");
-  if (peer_err) throw CudaError("peer exchange: a rank never signalled this step (timeout)");
+  uint32_t err[4] = {0, 0, 0, 0};
+  cuda_check(cudaMemcpy(err, err_flag(), 16, cudaMemcpyDeviceToHost), "D2H err");
+  if (err[0] || err[2]) {  // reported once: clear the sticky flags
+    cuda_check(cudaMemset(err_flag(), 0, 4), "clear err");
+    cuda_check(cudaMemset(err_flag() + 2, 0, 4), "clear err");
+    cuda_check(cudaDeviceSynchronize(), "clear err");
+  }
+  if (err[0] & 1u) throw InvalidArgument("sparsify: NaN gradient value");
+  if (err[2]) throw CudaError("peer exchange: a rank never signalled this step (timeout)");
 }
 
 // ------------------------------------------------------------ select/encode
@@ -441,7 +444,10 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   upload(items.data(), n * sizeof(EncItem), d_items);
   auto* state = static_cast<SelState*>(ws_.get("sel_state", n * sizeof(SelState), true, stream_));
   uint32_t* err = err_flag();
-  zero({{err, 16}});
+  // per-batch words only (err[1] bracket miss, err[3] chunk counter); the
+  // NaN (err[0]) and peer-timeout (err[2]) flags stay sticky until
+  // sync_check reports them, so a later batch or call cannot erase them
+  zero({{err + 1, 4}, {err + 3, 4}});
   if (select) {
     auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleStride * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
@@ -634,7 +640,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
 
 // ------------------------------------------------------------ simulated world
 void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
-                              float* const* accs, float* out, PeelStats* stats) {
+                              float* const* accs, float* out, PeelStats* stats, float* audit) {
   CallScope scope(*this);
   if (world == 0) throw InvalidArgument("world size must be at least 1");
   cfg_.validate_for_world(world);  // hook.cpp:105
@@ -677,6 +683,21 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
   auto* d_ptrs = static_cast<const void**>(ws_.get("sim_ptrs", ptrs.size() * 8, false, stream_));
   upload(ptrs.data(), ptrs.size() * 8, d_ptrs);
   zero({{sk_all, world * SK * 4}});
+  // collect_audit (hook.cpp:115, :191-195): every rank's combined g + acc is
+  // kept before the encode overwrites acc with the residual
+  const uint64_t len = shard.size();
+  float* comb = nullptr;
+  const void** d_audit_ptrs = nullptr;
+  if (audit) {
+    comb = static_cast<float*>(ws_.get("audit_comb", world * len * 4, false, stream_));
+    for (uint32_t r = 0; r < world; ++r) launches_ += launch_add(grads[r], accs[r], comb + r * len, len, stream_);
+    std::vector<const void*> ap;
+    for (uint32_t r = 0; r < world; ++r) ap.push_back(comb + r * len);
+    for (uint32_t r = 0; r < world; ++r) ap.push_back(accs[r]);
+    d_audit_ptrs = static_cast<const void**>(ws_.get("audit_ptrs", ap.size() * 8, false, stream_));
+    upload(ap.data(), ap.size() * 8, d_audit_ptrs);
+    zero({{audit, len * 4}});
+  }
 
   std::vector<EncItem> enc;
   for (uint32_t r = 0; r < world; ++r) {
@@ -696,6 +717,21 @@ void Engine::reduce_shard_sim(const ShardSpec& shard, uint32_t world, const floa
     }
   }
   run_select_encode(enc, w == 4, hp, false, "sim");
+  if (audit) {  // rank-ordered sum of the exchanged sparse vectors, compressed segments only
+    std::vector<AuditItem> ai;
+    uint64_t max_n = 0;
+    for (const SegPlan& p : plan)
+      if (p.compressed) {
+        ai.push_back(AuditItem{audit + p.lo, p.len, p.lo});
+        max_n = std::max(max_n, p.len);
+      }
+    if (!ai.empty()) {
+      auto* d_ai = static_cast<AuditItem*>(ws_.get("audit_items", ai.size() * sizeof(AuditItem), false, stream_));
+      upload(ai.data(), ai.size() * sizeof(AuditItem), d_ai);
+      launches_ += launch_audit(d_ai, uint32_t(ai.size()), max_n, reinterpret_cast<const float* const*>(d_audit_ptrs),
+                                reinterpret_cast<const float* const*>(d_audit_ptrs + world), world, stream_);
+    }
+  }
   // exchange: ascending-rank folds (collectives.cpp:127-166)
   launches_ += launch_rank_sum_u32(reinterpret_cast<const uint32_t* const*>(d_ptrs + world), world,
                                    merged, NW, stream_);
@@ -903,6 +939,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     return;
   }
   capturing_ = &g;
+  const int set0 = peer_.set;  // the captured enqueue flips it; an eager re-run must start from it
   bool ok = true;
   try {
     enqueue_reduce_shards(shards, grad, acc, out, nullptr);
@@ -921,6 +958,7 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
   if (ok && cudaGraphUpload(g.exec, stream_) != cudaSuccess) cudaGetLastError();
   if (graph) cudaGraphDestroy(graph);
   if (!ok) {  // could not capture (e.g. a buffer had to grow): stay eager for this key
+    peer_.set = set0;
     free_graph(g);
     ledger_.wire_bytes = wire0;
     for (const LedgerEntry& l : g.ledger) ledger_.unrecord(l.op, l.tag, l.bits, l.params);
@@ -1095,12 +1133,15 @@ void Engine::finish_exchange(PeelStats* stats) {
     // the signal / wait / pull go in after the decode's allocations: a
     // cudaMalloc behind a wait for peers could stall this rank (and, with all
     // ranks in one process, every rank)
+    // the send set flips as soon as the pull is enqueued: a later throw
+    // (stats sync, NaN, timeout) must not leave this rank on the other set
+    xs_.peer_set = set;
     exchange_end(recv_f, recv_u, stats, [&] {
       launches_ += launch_peer_exchange(di_, peer_.view, set, recv_f, recv_u, err, stream_);
+      peer_.set = set ^ 1;
       ledger_.wire_bytes += uint64_t(world_) * (peer_.Bf + peer_.Bu) * 4;
       ev_record(4);
     });
-    peer_.set ^= 1;
     return;
   }
   const uint64_t Bf = xs_.P.Bf, Bu = xs_.P.Bu;
@@ -1119,6 +1160,14 @@ void Engine::finish_exchange(PeelStats* stats) {
                "ncclReduceScatter u32");
     nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
     ledger_.wire_bytes += W * (Bf + Bu) * 4;
+    if (stats && cfg_.index_width == 1) {  // index_lost / _spurious need the OR of the supports
+      auto* sup_send = static_cast<uint8_t*>(ws_.get("sup_send", W * Bu * 32, false, stream_));
+      auto* sup_recv = static_cast<uint8_t*>(ws_.get("sup_recv", Bu * 32, false, stream_));
+      launches_ += launch_support_bytes(send_u, W * Bu, sup_send, stream_);
+      nccl_check(nccl().ReduceScatter(sup_send, sup_recv, Bu * 32, ncclUint8, ncclMax, comm_, stream_),
+                 "ncclReduceScatter support");
+      xs_.support_recv = sup_recv;
+    }
   }
   ev_record(4);
   exchange_end(recv_f, recv_u, stats);
@@ -1186,6 +1235,38 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     dec.push_back(d);
   }
   run_decode_grouped(dec, hp, w == 1 && W > 1, zero_done, pre_decode);
+  // index_lost / index_spurious (hook.cpp:176-188). A 4-bit index is exact
+  // for W <= 15 (config.cpp:55-58): both are 0. A 1-bit index over several
+  // ranks compares the merged words with the OR of the ranks' supports.
+  unsigned long long* ls = nullptr;
+  bool diag_unavailable = false;
+  if (stats && w == 1 && W > 1 && !dec.empty()) {
+    std::vector<DiagItem> diag;
+    uint32_t max_words = 0;
+    for (const SegPlan& p : plan) {
+      if (!p.compressed || shards[p.shard].owner != rank_) continue;
+      diag.push_back(DiagItem{recv_u + p.word_off, p.word_off, uint32_t(p.len), p.n_words, 1u, 0u});
+      max_words = std::max(max_words, p.n_words);
+    }
+    ls = static_cast<unsigned long long*>(ws_.get("diag_ls", diag.size() * 16, false, stream_));
+    zero({{ls, diag.size() * 16}});
+    auto* d_diag = static_cast<DiagItem*>(ws_.get("diag_items", diag.size() * sizeof(DiagItem), false, stream_));
+    upload(diag.data(), diag.size() * sizeof(DiagItem), d_diag);
+    if (xs_.support_recv) {
+      launches_ += launch_index_diag_support(d_diag, uint32_t(diag.size()), max_words, xs_.support_recv, ls,
+                                             stream_);
+    } else if (peer_.attached && xs_.peer_set >= 0) {
+      // the peers' send blocks of this step still hold their own words: a
+      // peer reuses the set only after this rank signals the next step
+      std::vector<const uint32_t*> rw;
+      for (uint32_t q = 0; q < W; ++q) rw.push_back(peer_.view.send_u[xs_.peer_set][q] + uint64_t(rank_) * P.Bu);
+      auto* d_rw = static_cast<const uint32_t**>(ws_.get("diag_rw", W * 8, false, stream_));
+      upload(rw.data(), W * 8, d_rw);
+      launches_ += launch_index_diag(d_diag, uint32_t(diag.size()), max_words, d_rw, W, ls, stream_);
+    } else {
+      diag_unavailable = true;  // split API without support blocks
+    }
+  }
   if (W > 1 && !unpack.empty()) {
     const uint64_t tt = copy_tiles(unpack.data(), uint32_t(unpack.size()));
     auto* d_un = static_cast<CopyItem*>(desc_buffer("nc_unpack", unpack.size() * sizeof(CopyItem)));
@@ -1206,9 +1287,11 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
   }
   if (stats) {
     dec_stats_.resize(dec.size());
+    std::vector<unsigned long long> lsh(ls ? dec.size() * 2 : 0, 0);
     if (!dec.empty())
       cuda_check(cudaMemcpyAsync(dec_stats_.data(), ws_.get("dec_stats", 16), dec.size() * sizeof(DecStats),
                                  cudaMemcpyDeviceToHost, stream_), "D2H stats");
+    if (ls) cuda_check(cudaMemcpyAsync(lsh.data(), ls, lsh.size() * 8, cudaMemcpyDeviceToHost, stream_), "D2H ls");
     sync_check();
     if (!dec.empty()) fetch_rounds();
     PeelStats st;
@@ -1218,13 +1301,101 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
       st.unresolved += d.unresolved;
     }
     st.peeled = st.presence - st.unresolved;
-    // A 4-bit index is exact for W <= 15 (config.cpp:55-58), so no position is
-    // lost or fabricated; the 1-bit diagnostic needs the per-rank supports and
-    // is only computed in the simulated world.
+    for (size_t i = 0; i + 1 < lsh.size(); i += 2) {
+      st.index_lost += lsh[i];
+      st.index_spurious += lsh[i + 1];
+    }
+    if (diag_unavailable) st.index_lost = st.index_spurious = kStatUnavailable;
     st.compressed_segments = dec.size();
     st.baseline_segments = n_raw_owned;
     *stats = st;
   }
+}
+
+void Engine::exchange_support(uint8_t** send_support, uint64_t* block_bytes) {
+  CallScope scope(*this);
+  if (!xs_.active) throw InvalidArgument("no exchange in progress");
+  if (cfg_.index_width != 1) throw InvalidArgument("support blocks are only needed for a 1-bit index");
+  const uint64_t Bu = xs_.P.Bu;
+  uint8_t* dst = send_support && *send_support
+                     ? *send_support
+                     : static_cast<uint8_t*>(ws_.get("sup_send", world_ * Bu * 32, false, stream_));
+  launches_ += launch_support_bytes(xs_.send_u, world_ * Bu, dst, stream_);
+  cuda_check(cudaGetLastError(), "support launch");
+  if (send_support) *send_support = dst;
+  if (block_bytes) *block_bytes = Bu * 32;
+}
+
+void Engine::reduce_shards_audit(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                                 PeelStats* stats, float* audit) {
+  CallScope scope(*this);
+  if (world_ > 1 && !comm_)
+    throw InvalidArgument("audit_exchanged_sum needs the NCCL exchange (or the simulated world)");
+  cfg_.validate_for_world(world_);
+  uint64_t total = 0;
+  for (const ShardSpec& s : shards) {
+    check_shard(s, world_);
+    total = std::max<uint64_t>(total, s.end);
+  }
+  // combined g + acc before the encode overwrites acc with the residual
+  auto* comb = static_cast<float*>(ws_.get("audit_comb", total * 4, false, stream_));
+  launch_add(grad, acc, comb, total, stream_);
+  enqueue_reduce_shards(shards, grad, acc, out, stats);
+  const ExchangePlan P = plan_exchange(shards, cfg_, world_, rank_);
+  const uint32_t W = world_;
+  std::vector<uint64_t> used(W, 0), aoff(P.segs.size(), 0);
+  for (size_t k = 0; k < P.segs.size(); ++k) {
+    const SegPlan& p = P.segs[k];
+    if (!p.compressed) continue;
+    const uint32_t o = shards[p.shard].owner;
+    aoff[k] = used[o];
+    used[o] += p.len;
+  }
+  uint64_t Ba = 0;
+  for (uint64_t u : used) Ba = std::max(Ba, u);
+  Ba = align_up(std::max<uint64_t>(Ba, 1), 32);
+  auto* send = static_cast<float*>(ws_.get("audit_send", W * Ba * 4, false, stream_));
+  zero({{send, W * Ba * 4}});
+  std::vector<AuditItem> ai;
+  uint64_t max_n = 0;
+  for (size_t k = 0; k < P.segs.size(); ++k) {
+    const SegPlan& p = P.segs[k];
+    if (!p.compressed) continue;
+    ai.push_back(AuditItem{send + shards[p.shard].owner * Ba + aoff[k], p.len, shards[p.shard].begin + p.lo});
+    max_n = std::max(max_n, p.len);
+  }
+  const void* ptrs[2] = {comb, acc};
+  auto* d_ptrs = static_cast<const void**>(ws_.get("audit_ptrs", 16, false, stream_));
+  upload(ptrs, 16, d_ptrs);
+  if (!ai.empty()) {
+    auto* d_ai = static_cast<AuditItem*>(ws_.get("audit_items", ai.size() * sizeof(AuditItem), false, stream_));
+    upload(ai.data(), ai.size() * sizeof(AuditItem), d_ai);
+    launch_audit(d_ai, uint32_t(ai.size()), max_n, reinterpret_cast<const float* const*>(d_ptrs),
+                 reinterpret_cast<const float* const*>(d_ptrs + 1), 1, stream_);
+  }
+  float* recv = send;
+  if (W > 1) {
+    recv = static_cast<float*>(ws_.get("audit_recv", Ba * 4, false, stream_));
+    nccl_check(nccl().ReduceScatter(send, recv, Ba, ncclFloat32, ncclSum, comm_, stream_), "audit reduce-scatter");
+  }
+  uint64_t owned = 0;
+  for (const ShardSpec& s : shards)
+    if (s.owner == rank_) owned += s.size();
+  if (owned) zero({{audit, owned * 4}});
+  std::vector<CopyItem> cp;
+  for (size_t k = 0; k < P.segs.size(); ++k) {
+    const SegPlan& p = P.segs[k];
+    if (!p.compressed || shards[p.shard].owner != rank_) continue;
+    cp.push_back(CopyItem{recv + aoff[k], audit + P.out_off[p.shard] + p.lo, p.len, 0});
+  }
+  if (!cp.empty()) {
+    const uint64_t tt = copy_tiles(cp.data(), uint32_t(cp.size()));
+    auto* d_cp = static_cast<CopyItem*>(ws_.get("audit_copy", cp.size() * sizeof(CopyItem), false, stream_));
+    upload(cp.data(), cp.size() * sizeof(CopyItem), d_cp);
+    launch_copy_items(di_, d_cp, uint32_t(cp.size()), tt, stream_);
+  }
+  cuda_check(cudaGetLastError(), "audit launch");
+  sync_check();
 }
 
 void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* grad, float* out) {

@@ -102,8 +102,11 @@ class Engine {
   void last_peel_rounds(uint32_t out[2]) const { out[0] = rounds_[0]; out[1] = rounds_[1]; }
 
   // hook.cpp:98-200 with `world` logical ranks on this GPU.
+  // audit (optional, dev, shard.size() floats): audit_exchanged_sum
+  // (hook.cpp:191-195), the rank-ordered sum of the sparse vectors exchanged
+  // for compressed segments, zeros elsewhere.
   void reduce_shard_sim(const ShardSpec& shard, uint32_t world, const float* const* grads,
-                        float* const* accs, float* out, PeelStats* stats);
+                        float* const* accs, float* out, PeelStats* stats, float* audit = nullptr);
   // hook.cpp:90-96
   void baseline_sim(const ShardSpec& shard, uint32_t world, const float* const* grads, float* out);
   // One process per GPU, NCCL exchange.
@@ -157,6 +160,18 @@ class Engine {
                     const std::function<void()>& pre_decode = nullptr);
   float* exchange_send_f() const { return xs_.send_f; }
   uint32_t* exchange_send_u() const { return xs_.send_u; }
+  // Split API, 1-bit index: this rank's support (one byte per position,
+  // owner-major blocks of block_bytes = 32 * block_u32) for the caller to
+  // max-reduce-scatter; exchange_end then takes the reduced block as
+  // xs_.support_recv (set_support_recv) and reports index_lost / _spurious.
+  void exchange_support(uint8_t** send_support, uint64_t* block_bytes);
+  void set_support_recv(const uint8_t* recv) { xs_.support_recv = recv; }
+  // reduce_shards plus audit_exchanged_sum (hook.cpp:191-195) for the owned
+  // shards (dev, laid out like out): the sum over ranks of the exchanged
+  // sparse vectors of compressed segments, zeros elsewhere. NCCL world (or
+  // W = 1); diagnostic: an extra uncompressed reduce-scatter.
+  void reduce_shards_audit(const std::vector<ShardSpec>& shards, const float* grad, float* acc, float* out,
+                           PeelStats* stats, float* audit);
   uint64_t exchange_block_f() const { return xs_.P.Bf; }
   uint64_t exchange_block_u() const { return xs_.P.Bu; }
 
@@ -210,6 +225,11 @@ class Engine {
     float* send_f = nullptr;
     uint32_t* send_u = nullptr;
     cudaEvent_t zero_done = nullptr;
+    // index_lost / index_spurious of a 1-bit index over several ranks: the
+    // OR of the ranks' supports, as one byte per position of this rank's
+    // owner block (NCCL / split), or the peer send set holding them
+    const uint8_t* support_recv = nullptr;
+    int peer_set = -1;
   };
   ExchangeState xs_;
   OptEpilogue* opt_dev_ = nullptr;  // device slot of the fused optimizer's scalars

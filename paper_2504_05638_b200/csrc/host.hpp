@@ -87,6 +87,10 @@ SketchGeometry sketch_geometry(uint32_t n, uint32_t ratio, uint32_t rows = 3);
 // reference index.cpp:17-20
 uint32_t words_needed(uint32_t n, uint32_t width);
 
+// index_lost / index_spurious value when the call had no way to see the
+// ranks' supports (split API with a 1-bit index and no support blocks)
+constexpr uint64_t kStatUnavailable = ~0ull;
+
 // reference hook.hpp:45-59
 struct PeelStats {
   uint64_t presence = 0, peeled = 0, unresolved = 0, index_lost = 0, index_spurious = 0,

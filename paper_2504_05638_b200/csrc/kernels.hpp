@@ -120,6 +120,24 @@ int launch_index_diag(const DiagItem* items, uint32_t n_items, uint32_t max_word
                       const uint32_t* const* rank_words, uint32_t world,
                       unsigned long long* lost_spurious /* 2 per item */, cudaStream_t stream);
 
+// Diagnostics outside the simulated world (diag.cu).
+// One byte (0/1) per position from width-1 index words: bytes[32 w + j] = bit j of words[w].
+int launch_support_bytes(const uint32_t* words, uint64_t n_words, uint8_t* bytes, cudaStream_t stream);
+// Width-1 lost/spurious from a support byte map (OR of the ranks' supports;
+// item i's bytes start at support + 32 * items[i].word_off).
+int launch_index_diag_support(const DiagItem* items, uint32_t n_items, uint32_t max_words,
+                              const uint8_t* support, unsigned long long* lost_spurious, cudaStream_t stream);
+// audit_exchanged_sum (hook.cpp:191-195): dst[i] = sum over ranks (ascending)
+// of the exchanged sparse value, recovered from the pre-encode combined value
+// comb[r][src_off + i] and the post-encode residual res[r][src_off + i].
+struct AuditItem {
+  float* dst;
+  uint64_t n;
+  uint64_t src_off;
+};
+int launch_audit(const AuditItem* items, uint32_t n_items, uint64_t max_n, const float* const* comb,
+                 const float* const* res, uint32_t world, cudaStream_t stream);
+
 // ---------------------------------------------------------------- decode
 struct DecodeWork {
   const DecItem* items;

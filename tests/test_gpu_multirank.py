@@ -72,19 +72,24 @@ def test_split_exchange_matches_oracle(orc, world, width, theta, steps):
         send_u = [torch.zeros(world * Bu, dtype=torch.int32, device=DEV) for _ in range(world)]
         outs = [torch.full((max(1, sum(s.size() for s in owned[r])),), float("nan"), device=DEV)
                 for r in range(world)]
+        sup = [torch.zeros(world * Bu * 32, dtype=torch.uint8, device=DEV) for _ in range(world)]
         for r in range(world):
             bf, bu = ctxs[r].reduce_shards_begin(shards, torch.from_numpy(grads[r]).to(DEV), acc[r], outs[r],
                                                  send_f[r], send_u[r])
             assert (bf, bu) == (Bf, Bu)
+            if width == 1:  # index_lost / _spurious need the OR of the ranks' supports
+                assert ctxs[r].reduce_shards_support(sup[r]) == Bu * 32
         stats = []
         for o in range(world):  # the reduce-scatter, ascending rank order
             rf = send_f[0][o * Bf:(o + 1) * Bf].clone()
             ru = send_u[0][o * Bu:(o + 1) * Bu].to(torch.int64)
+            rs = sup[0][o * Bu * 32:(o + 1) * Bu * 32].clone()
             for r in range(1, world):
                 rf += send_f[r][o * Bf:(o + 1) * Bf]
                 ru += send_u[r][o * Bu:(o + 1) * Bu].to(torch.int64)
+                rs = torch.maximum(rs, sup[r][o * Bu * 32:(o + 1) * Bu * 32])
             ru = ((ru & 0xFFFFFFFF) ^ 0x80000000).sub(0x80000000).to(torch.int32)  # wrap to u32 bits
-            stats.append(ctxs[o].reduce_shards_end(rf, ru))
+            stats.append(ctxs[o].reduce_shards_end(rf, ru, recv_support=rs if width == 1 else None))
         torch.cuda.synchronize()
         # oracle, shard by shard (accumulators are updated in place per shard slice)
         refs, rsts = {}, {}
@@ -105,8 +110,31 @@ def test_split_exchange_matches_oracle(orc, world, width, theta, steps):
             for sh in owned[o]:
                 check_close(got[off:off + sh.size()], refs[sh.id])
                 off += sh.size()
-            for k in ("presence", "peeled", "unresolved"):
+            for k in ("presence", "peeled", "unresolved", "index_lost", "index_spurious"):
                 assert getattr(stats[o], k) == sum(rsts[s.id][k] for s in owned[o]), (k, o, stats[o])
+        if width == 1:
+            assert sum(st.index_lost + st.index_spurious for st in stats) > 0  # carries did happen
+
+
+def test_split_exchange_without_support_flags_unavailable():
+    """1-bit index, split API, no support blocks: the diagnostic cannot be
+    computed and says so instead of reporting 0."""
+    world, n = 2, 1 << 16
+    shards = [tagc.ShardSpec(i, i, i * n, (i + 1) * n, [tagc.LayerSegment("b", "feed_forward", i * n, (i + 1) * n)])
+              for i in range(world)]
+    cfg = tagc.CompressionConfig(theta=98.75, ratio=10, index_width=1, policy="all_layers", seed=77)
+    _, Bf, Bu = tagc.plan_exchange(cfg, shards, world, 0)
+    ctxs = [tagc.Context(cfg, world_size=world, rank=r, device=0) for r in range(world)]
+    sf = [torch.zeros(world * Bf, device=DEV) for _ in range(world)]
+    su = [torch.zeros(world * Bu, dtype=torch.int32, device=DEV) for _ in range(world)]
+    outs = [torch.empty(n, device=DEV) for _ in range(world)]
+    for r in range(world):
+        g = torch.from_numpy(lognormal(world * n, r)).to(DEV)
+        ctxs[r].reduce_shards_begin(shards, g, torch.zeros(world * n, device=DEV), outs[r], sf[r], su[r])
+    st = ctxs[0].reduce_shards_end(sf[0][:Bf] + sf[1][:Bf], su[0][:Bu] + su[1][:Bu])
+    assert st.index_lost == tagc.STAT_UNAVAILABLE and st.index_spurious == tagc.STAT_UNAVAILABLE
+    ctxs[1].reduce_shards_end(sf[0][Bf:] + sf[1][Bf:], su[0][Bu:] + su[1][Bu:], stats=False)
+    torch.cuda.synchronize()
 
 
 @pytest.mark.parametrize("world,width,steps", [(2, 4, 5), (4, 4, 2), (2, 1, 2)])
@@ -148,9 +176,12 @@ def test_peer_exchange_matches_oracle(orc, world, width, steps):
         # between generations, which must not stall the other ranks' enqueues
         errs = [None] * world
 
+        want_stats = step == min(1, steps - 1)  # eager; the graph capture / replay steps stay stat-less
+        stats = [None] * world
+
         def run(r):
             try:
-                ctxs[r].tagc_reduce_shards(shards, g_d[r], acc[r], outs[r], stats=False)
+                _, stats[r] = ctxs[r].tagc_reduce_shards(shards, g_d[r], acc[r], outs[r], stats=want_stats)
                 ctxs[r].sync()
             except Exception as e:  # surfaced below
                 errs[r] = e
@@ -163,15 +194,19 @@ def test_peer_exchange_matches_oracle(orc, world, width, steps):
         for e in errs:
             if e is not None:
                 raise e
-        refs = {}
+        refs, rsts = {}, {}
         for sh in shards:
             osh = O.Shard(sh.id, sh.owner, sh.begin, sh.end,
                           [O.Segment(s.kind, s.begin, s.end, s.name) for s in sh.segments])
             a = [oacc[r][sh.begin:sh.end].copy() for r in range(world)]
-            ref, _ = orc.tagc_reduce_shard(osh, [grads[r][sh.begin:sh.end] for r in range(world)], a, ocfg)
+            ref, rst = orc.tagc_reduce_shard(osh, [grads[r][sh.begin:sh.end] for r in range(world)], a, ocfg)
             for r in range(world):
                 oacc[r][sh.begin:sh.end] = a[r]
-            refs[sh.id] = ref.copy()
+            refs[sh.id], rsts[sh.id] = ref.copy(), dict(rst)
+        if want_stats:  # index_lost / _spurious from the peers' send blocks (hook.cpp:176-188)
+            for o in range(world):
+                for k in ("presence", "peeled", "unresolved", "index_lost", "index_spurious"):
+                    assert getattr(stats[o], k) == sum(rsts[s.id][k] for s in owned[o]), (k, o, stats[o])
         for r in range(world):
             assert np.array_equal(bits(acc[r].cpu().numpy()), bits(oacc[r])), (step, r)
         for o in range(world):

@@ -157,7 +157,8 @@ def test_make_shards_matches_reference(orc):
 
 def test_roundtrip_reference_reports_pass():
     # acceptance criterion 1 operating points (reduced trials): the reference
-    # itself passes; the GPU suite reproduces these through the CUDA path.
+    # itself passes. tests/test_gpu_acceptance.py drives the same generator's
+    # trials through the CUDA path at acceptance.cpp's full parameters.
     for r in M["roundtrip"]:
         rep = r["report"]
         assert rep["pass"] == 1 and rep["index_lost"] == 0 and rep["index_spurious"] == 0
@@ -221,3 +222,68 @@ def test_oracle_optimizer(orc):
         _adamw_nm_f32(p_n, dec * np.float32(1.0 / np.float32(world)), v_n, 0.01, 0.1, step)
         assert np.array_equal(bits(v_o), bits(v_n)), step
         assert np.array_equal(bits(p_o), bits(p_n)), step
+
+
+def audit_identity(shard, grads, accs_before, accs_after, cfg_policy="all_layers"):
+    """audit_exchanged_sum restated from what the exchange leaves behind: a
+    rank's exchanged sparse value is its combined g + acc where sparsify left
+    a +0.0 residual (kept, or a +0.0 that was dropped), else +0.0
+    (sparsify.cpp:43, kernels.cpp:95); summed over ranks in ascending order."""
+    n = shard.size
+    out = np.zeros(n, np.float32)
+    for s in shard.segments:
+        lo, hi = s.begin - shard.begin, s.end - shard.begin
+        acc = np.zeros(hi - lo, np.float32)
+        for g, a0, a1 in zip(grads, accs_before, accs_after):
+            comb = (g[lo:hi] + a0[lo:hi]).astype(np.float32)
+            acc = (acc + np.where(bits(a1[lo:hi]) == 0, comb, np.float32(0))).astype(np.float32)
+        out[lo:hi] = acc
+    return out
+
+
+def test_audit_identity_matches_reference(orc, ref):
+    """collect_audit (hook.cpp:191-195): the reference's own
+    audit_exchanged_sum equals the identity the GPU audit kernel computes,
+    bit for bit, over error-feedback steps (ties, zeros, 1- and 4-bit)."""
+    rng = np.random.default_rng(7)
+    for t in range(4):
+        n = int(rng.integers(20000, 80000))
+        world = int(rng.integers(2, 5))
+        width = int(rng.choice([1, 4]))
+        shard = Shard(0, 0, 0, n, [Segment("feed_forward", 0, n)])
+        cfg = Config(99.0, 10, width, "all_layers", True, 77 + t, 3, False, 1)
+        accs = [np.zeros(n, np.float32) for _ in range(world)]
+        for step in range(2):
+            grads = [g.copy() for g in orc.stream(n, 100 * t + step, count=world)]
+            grads[0][:500] = 0.0  # dropped +0.0 elements
+            grads[1][500:900] = np.float32(1.5)  # ties at the threshold
+            before = [a.copy() for a in accs]
+            _, audit = ref.tagc_reduce_shard_audit(shard, grads, accs, cfg)
+            assert np.array_equal(bits(audit), bits(audit_identity(shard, grads, before, accs))), (t, step)
+
+
+def test_roundtrip_generator_pinned_to_reference(orc, ref):
+    """oracle/_ref's ref_roundtrip_trial (roundtrip.cpp:65-95, with the
+    file-static sample_support restated) fed through the reference's own
+    tagc_reduce_shard reproduces roundtrip_experiment's report exactly: the
+    generator the GPU acceptance test uses is the reference's."""
+    from roundtrip_util import roundtrip_report
+
+    n, trials = 10000, 24
+    for theta, ratio, world in ((98.75, 10, 4), (80.0, 2, 2), (90.0, 4, 8)):
+        seed = 20250808 + world + ratio
+        live = ref.roundtrip(n, trials, theta, ratio, 4, world, seed=seed)
+
+        def run(t, grads, tseed):
+            shard = Shard(0, 0, 0, n, [Segment("feed_forward", 0, n)])
+            cfg = Config(theta, ratio, 4, "all_layers", True, tseed, 3, False, 1)
+            accs = [np.zeros(n, np.float32) for _ in range(world)]
+            dec, st, _ = ref.tagc_reduce_shard(shard, list(grads), accs, cfg)
+            return dec, st
+
+        rep = roundtrip_report(ref, n, trials, theta, world, seed, run)
+        for k in ("trials_fully_peeled", "presence_total", "unresolved_total", "index_lost", "index_spurious",
+                  "integer_exact_when_resolved", "pass"):
+            assert rep[k] == live[k], (k, rep[k], live[k])
+        assert rep["mean_peeled_fraction"] == live["mean_peeled_fraction"]
+        assert rep["max_rel_error_resolved"] == live["max_rel_error_resolved"]
