@@ -242,13 +242,16 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
       }
     }
     __syncthreads();  // the tile's entries are visible to the whole CTA
-    // bucket state, one entry per thread (hashing and reductions stay converged)
+    // bucket counts, one entry per thread (hashing and reductions stay
+    // converged): byte counters packed four to a word when the batch has
+    // them (cnt8, L2-resident), else the full (count, index sum) state
     for (uint32_t q = threadIdx.x; q < n_in; q += blockDim.x) {
       const uint32_t i = base + q;
       const uint32_t p = w.plist[i];
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
         const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
-        atomicAdd(w.slot_state + slot, st_add(i));  // result unused: RED.ADD.64
+        if (w.cnt8) red_add_u32(w.cnt8 + (slot >> 2), 1u << (8u * uint32_t(slot & 3u)));
+        else atomicAdd(w.slot_state + slot, st_add(i));  // result unused: RED.ADD.64
       }
     }
     __syncthreads();  // scan storage reuse
@@ -349,7 +352,8 @@ __device__ __forceinline__ uint32_t slot_row(uint64_t local, uint32_t m) {
 // warp's 32 consecutive entries are written as one word (no atomics).
 __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashParams& hp,
                                               uint64_t start, uint64_t stride, uint32_t* s_q = nullptr,
-                                              uint32_t* s_n = nullptr) {
+                                              uint32_t* s_n = nullptr, uint32_t* s_u = nullptr,
+                                              uint32_t* s_un = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t won = 0;
   const uint32_t total = ldcg(&w.qcount[5]);
@@ -365,7 +369,12 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
       for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
         if (r < hp.rows) {  // issue every row's load before inspecting any
           ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
-          st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
+          if (w.cnt8) {
+            const uint64_t sl = e.slot_base + ls[r];
+            st[r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+          } else {
+            st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
+          }
         }
       }
       int best = -1;
@@ -390,6 +399,9 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
           if (r < hp.rows) {
             const uint64_t sl = e.slot_base + ls[r];
             red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
+            // counter mode: only these buckets get a (count, index sum)
+            // state, built by k_r0_subtract from the unresolved entries
+            if (w.cnt8) w.slot_state[sl] = 0ull;
           }
       }
       if (best >= 0) {
@@ -405,25 +417,27 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
     const uint32_t m = __ballot_sync(kFull, peeled);
     if (lane == 0 && base < total) w.bitmap[base >> 5] = m;  // base is a multiple of 32
     if (s_q) stage_push<uint32_t, kR0Stage>(sub, uint32_t(i), s_q, s_n, w.r0_list, &w.qcount[13], lane);
+    if (s_u) stage_push<uint32_t, kR0Stage>(i < total && !peeled, uint32_t(i), s_u, s_un, w.ulist,
+                                            &w.qcount[14], lane);
   }
   won = warp_sum32(won);
   if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
 }
 
 __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
-  __shared__ uint32_t s_q[kR0Stage];
-  __shared__ uint32_t s_n[2], s_base;
+  __shared__ uint32_t s_q[kR0Stage], s_u[kR0Stage];
+  __shared__ uint32_t s_n[2], s_un[2], s_base;
   const bool compact = w.r0_list != nullptr;
-  if (compact) {
-    if (threadIdx.x == 0) {
-      s_n[0] = 0;
-      s_n[1] = kR0Stage;
-    }
-    __syncthreads();
+  const bool ulist = w.cnt8 != nullptr;
+  if (threadIdx.x == 0) {
+    s_n[0] = s_un[0] = 0;
+    s_n[1] = s_un[1] = kR0Stage;
   }
+  __syncthreads();
   round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x,
-                compact ? s_q : nullptr, s_n);
+                compact ? s_q : nullptr, s_n, ulist ? s_u : nullptr, s_un);
   if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
+  if (ulist) stage_flush<uint32_t, kR0Stage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
 }
 
 // Every entry peeled in round 0 leaves the buckets it shares with other
@@ -432,6 +446,43 @@ __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParam
 // entry round 0 left unresolved (slot_mark, set by round0_phase1) are
 // touched: every other bucket would only empty out, and nothing reads an
 // empty bucket again (neither the frontier nor the median estimate).
+// Counter mode (w.cnt8): round 0 kept no index sums, so the state of every
+// bucket holding a round-0 unresolved entry (slot_mark; cleared by
+// k_r0_phase1) is built here from those entries alone - exactly what the
+// full state holds there once the round-0 peeled entries have left - while
+// the peeled entries only take their values out of the marked buckets'
+// residuals. k_peel seeds round 1 from the unresolved entries' buckets.
+__global__ void __launch_bounds__(256) k_r0_subtract_cnt(DecodeWork w, const HashParams hp) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint32_t total = ldcg(&w.qcount[13]);
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < total; base += stride) {
+    const uint64_t j = base + lane;
+    if (j >= total) continue;
+    const uint64_t i = ldcg(w.r0_list + j);
+    const uint2 info = __ldcs(w.pinfo + i);
+    const uint32_t rows = info.y & 0xFFu;
+    const float v = __uint_as_float(info.x);
+    const uint32_t p = __ldcs(w.plist + i);
+    const DecItem* e = w.items + __ldcs(w.pitem + i);
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && ((rows >> r) & 1u)) {
+      const uint64_t loc = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
+      const uint64_t sl = e->slot_base + loc;
+      if ((__ldg(w.slot_mark + (sl >> 5)) >> (sl & 31)) & 1u) red_add_f32(e->sketch + loc, -(dev_sign(hp.row[r], p) * v));
+    }
+  }
+  const uint32_t nu = ldcg(&w.qcount[14]);
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < nu; j += stride) {
+    const uint32_t i = ldcg(w.ulist + j);
+    const uint32_t p = __ldcs(w.plist + i);
+    const DecItem* e = w.items + __ldcs(w.pitem + i);
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+      const uint64_t sl = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
+      atomicAdd(w.slot_state + sl, st_add(i));  // result unused: RED.ADD.64
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashParams hp) {
   __shared__ uint32_t s_q[kPushStage];
   __shared__ uint32_t s_n[2], s_base;
@@ -579,6 +630,31 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
   int mk = 0;
   PEEL_MARK(mk++);
   if (gtid == 0) w.qcount[2] = 1;
+  if (w.cnt8) {  // counter mode: round 1's frontier = the unresolved entries' single-entry buckets
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nu = ldcg(&w.qcount[14]);
+    for (uint64_t base = gtid - lane; base < nu; base += gstride) {
+      const uint64_t j = base + lane;
+      uint32_t p = 0;
+      const DecItem* e = w.items;
+      if (j < nu) {
+        const uint32_t i = ldcg(w.ulist + j);
+        p = __ldcs(w.plist + i);
+        e = w.items + __ldcs(w.pitem + i);
+      }
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+        uint64_t sl = 0;
+        bool push = false;
+        if (j < nu) {
+          sl = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
+          push = st_count(ldcg(w.slot_state + sl)) == 1u;  // one entry: pushed by that entry only
+        }
+        stage_push<uint32_t, kPushStage>(push, uint32_t(sl), s_q, s_nq, qbuf1, &cnt[1], lane);
+      }
+    }
+    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf1, &cnt[1]);
+    grid.sync();
+  }
   uint32_t won = 0, k = 1;
   bool tail = false;
   for (;; ++k) {
@@ -1017,7 +1093,8 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   int per_sm = 0;
   const int g = build_passes(di, w, hp, stream);
   k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
-  k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  if (w.cnt8) k_r0_subtract_cnt<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  else k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_peel, 256, 0);
   const int pg = coop_grid(di, std::max(per_sm, 1));

@@ -134,6 +134,10 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.add.f32 [ga], %1;\n}" ::"l"(p), "f"(v)
                : "memory");
 }
+__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.add.u32 [ga], %1;\n}" ::"l"(p), "r"(v)
+               : "memory");
+}
 __device__ __forceinline__ void red_or_u32(uint32_t* p, uint32_t v) {
   asm volatile("{\n.reg .u64 ga;\ncvta.to.global.u64 ga, %0;\nred.global.or.b32 [ga], %1;\n}" ::"l"(p), "r"(v)
                : "memory");

@@ -593,8 +593,21 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
             stats_base;
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
+  // Counter mode: round 0 needs only "one entry or more" per bucket, so it
+  // counts in bytes (slots bytes instead of 8 * slots: 27 MB at 2^28 / r 10,
+  // L2-resident) and the (count, index sum) state is built later for the few
+  // buckets round 0 leaves unresolved. A byte counter is safe while a bucket
+  // cannot plausibly hold 256 entries: the presence bound over the row
+  // length stays <= 16 (Poisson tail ~1e-200), else the full state is used.
+  bool counters = !ordered && !std::getenv("TAGC_DECODE_FULL_STATE");
+  for (const DecItem& d : items)
+    counters = counters && double(std::min(d.list_cap ? d.list_cap : d.n, d.n)) <= 16.0 * double(d.m);
+  const uint64_t cnt_words = (slots + 3) / 4;
+  w.cnt8 = counters ? static_cast<uint32_t*>(ws_.get("cnt8", cnt_words * 4, false, stream_)) : nullptr;
+  w.ulist = counters ? static_cast<uint32_t*>(ws_.get("ulist", list * 4 + 4, false, stream_)) : nullptr;
   zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)},
-        {w.slot_mark, w.slot_mark ? mark_words * 4 : 0}, {w.slot_state, slots * 8},
+        {w.slot_mark, w.slot_mark ? mark_words * 4 : 0},
+        {counters ? static_cast<void*>(w.cnt8) : static_cast<void*>(w.slot_state), counters ? cnt_words * 4 : slots * 8},
         {w.tile_state, wt * 8}});  // one launch for every decode scratch reset
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {

@@ -145,6 +145,11 @@ struct DecodeWork {
   uint64_t total_word_tiles;
   uint64_t total_slots;
   unsigned long long* slot_state;  // (sum of list indices) << 24 | count, total_slots
+  // Counter mode (non-null): round 0 counts entries per bucket in bytes
+  // packed four to a word (L2-resident), and slot_state is only built for
+  // the buckets of entries round 0 leaves unresolved (ulist, qcount[14]).
+  uint32_t* cnt8;
+  uint32_t* ulist;
   uint32_t* bitmap;                // recovered flag per presence-list entry
   float* val;                      // decoded value per presence-list entry
   uint32_t* slot_mark;             // per bucket: holds an entry round 0 left unresolved (or nullptr)
