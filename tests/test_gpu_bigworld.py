@@ -62,7 +62,9 @@ def int_grad(n, seed, dev=DEV):
     g.manual_seed(seed)
     mag = torch.randn(n, device=dev, generator=g).mul_(1.5).exp_().round_().clamp_(max=4096)
     sign = torch.randint(0, 2, (n,), device=dev, generator=g, dtype=torch.int8)
-    return torch.where(sign.bool(), -mag, mag)
+    # + 0.0: the -0.0 of a zero magnitude becomes +0.0, as g + acc does with
+    # a zero accumulator, so g itself is the first step's combined value
+    return torch.where(sign.bool(), -mag, mag).add_(0.0)
 
 
 def lognormal_np(n, seed):
