@@ -194,6 +194,13 @@ int tagc_ledger_json(tagc_ledger* l, char* buf, size_t len, size_t* needed);
  * (collectives.cpp:60-68); prefix NULL or "" = all rows. */
 int tagc_ledger_bits_per_param(tagc_ledger* l, const char* prefix, double* out);
 int tagc_ledger_clear(tagc_ledger* l);
+/* TrafficLedger::rows() (collectives.hpp:67, ordered by (op, tag)): the row
+ * count, and row i's fields (tag NUL-terminated, truncated to tag_len; any
+ * output pointer may be NULL). A reference-side adapter replays a call's rows
+ * into the reference World's ledger with these. */
+int tagc_ledger_row_count(tagc_ledger* l, uint32_t* out);
+int tagc_ledger_row(tagc_ledger* l, uint32_t i, int32_t* op, char* tag, size_t tag_len, uint64_t* calls,
+                    uint64_t* payload_bits, uint64_t* charged_bits, uint64_t* params);
 tagc_ledger* tagc_ctx_ledger(tagc_ctx* ctx);
 /* Bytes this context actually handed to the transport (NCCL or peer pulls)
  * since creation: measured, beside the ledger's modelled bits. */

@@ -119,6 +119,9 @@ SIGNATURES = {
     "tagc_ledger_json": (C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "tagc_ledger_bits_per_param": (C.c_int, [VP, C.c_char_p, C.POINTER(C.c_double)]),
     "tagc_ledger_clear": (C.c_int, [VP]),
+    "tagc_ledger_row_count": (C.c_int, [VP, C.POINTER(U32)]),
+    "tagc_ledger_row": (C.c_int, [VP, U32, C.POINTER(C.c_int32), C.c_char_p, C.c_size_t, C.POINTER(U64),
+                                  C.POINTER(U64), C.POINTER(U64), C.POINTER(U64)]),
     "tagc_ctx_ledger": (VP, [VP]),
     "tagc_ctx_wire_bytes": (C.c_int, [VP, C.POINTER(U64)]),
     "tagc_wire_bytes_from_device": (C.c_int, [VP, VP, U64, VP]),

@@ -290,6 +290,22 @@ class TrafficLedger:
     def clear(self):
         check(lib.tagc_ledger_clear(self.h))
 
+    def rows(self):
+        """TrafficLedger::rows() (collectives.hpp:67): dicts in (op, tag) order."""
+        n = C.c_uint32()
+        check(lib.tagc_ledger_row_count(self.h, C.byref(n)))
+        names = {v: k for k, v in self.OPS.items()}
+        out = []
+        for i in range(n.value):
+            op = C.c_int32()
+            tag = C.create_string_buffer(512)
+            calls, pb, cb, pr = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+            check(lib.tagc_ledger_row(self.h, i, C.byref(op), tag, len(tag), C.byref(calls), C.byref(pb),
+                                      C.byref(cb), C.byref(pr)))
+            out.append({"op": names[op.value], "tag": tag.value.decode(), "calls": calls.value,
+                        "payload_bits": pb.value, "charged_bits": cb.value, "params": pr.value})
+        return out
+
 
 class Context:
     """Owns a tagc_ctx (one CUDA stream, workspaces, ledger, optional NCCL comm).

@@ -287,6 +287,32 @@ int tagc_ledger_bits_per_param(tagc_ledger* l, const char* prefix, double* out) 
   });
 }
 
+int tagc_ledger_row_count(tagc_ledger* l, uint32_t* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("null output");
+    *out = uint32_t(led(l).rows().size());
+  });
+}
+
+int tagc_ledger_row(tagc_ledger* l, uint32_t i, int32_t* op, char* tag, size_t tag_len, uint64_t* calls,
+                    uint64_t* payload_bits, uint64_t* charged_bits, uint64_t* params) {
+  return guarded([&] {
+    const std::vector<LedgerRow> rows = led(l).rows();
+    if (i >= rows.size()) throw InvalidArgument("ledger row out of range");
+    const LedgerRow& r = rows[i];
+    if (op) *op = int32_t(r.op);
+    if (tag && tag_len) {
+      const size_t k = std::min(tag_len - 1, r.tag.size());
+      std::memcpy(tag, r.tag.data(), k);
+      tag[k] = 0;
+    }
+    if (calls) *calls = r.calls;
+    if (payload_bits) *payload_bits = r.payload_bits;
+    if (charged_bits) *charged_bits = r.charged_bits;
+    if (params) *params = r.params;
+  });
+}
+
 int tagc_ledger_clear(tagc_ledger* l) {
   return guarded([&] { led(l).clear(); });
 }

@@ -368,6 +368,15 @@ void Engine::download(const void* dev, uint64_t bytes, void* host) {
   cuda_check(cudaStreamSynchronize(stream_), "stream sync");
 }
 
+// err[0] doubles as the presence-validation word of the standalone decode
+// entries; once read and reported it must not stay set, or the sticky NaN
+// test of every later encode (k_encode, k_fused_tma) would skip its writes.
+void Engine::clear_err_word(uint32_t seen) {
+  if (!seen) return;
+  cuda_check(cudaMemsetAsync(err_flag(), 0, 4, stream_), "clear err");
+  cuda_check(cudaStreamSynchronize(stream_), "clear err");
+}
+
 void Engine::sync_check() {
   if (h2d_) cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
   if (d2h_) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
@@ -1801,6 +1810,7 @@ void Engine::peeling_decompress(const uint32_t* presence, uint32_t count, uint32
   cuda_check(cudaMemcpyAsync(&ds, ws_.get("dec_stats", 16), sizeof(ds), cudaMemcpyDeviceToHost, stream_), "D2H");
   cuda_check(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, stream_), "D2H err");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
+  clear_err_word(e);
   if (e & 1u) throw InvalidArgument("presence position out of range for sketch geometry");
   if (e & 2u) throw InvalidArgument("presence set contains a duplicate position");
   if (ds.overflow) throw CudaError("decode bucket state overflow");
@@ -1835,6 +1845,7 @@ void Engine::estimation_decompress(const uint32_t* presence, uint32_t count, uin
   uint32_t e = 0;
   cuda_check(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, stream_), "D2H err");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
+  clear_err_word(e);
   if (e & 1u) throw InvalidArgument("presence position out of range for sketch geometry");
   if (e & 4u) throw InvalidArgument("estimation target outside the presence set");
 }

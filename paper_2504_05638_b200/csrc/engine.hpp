@@ -206,6 +206,7 @@ class Engine {
                              const uint32_t* targets, uint32_t n_targets, float* out);
   // Synchronise and surface deferred device errors (NaN input -> invalid).
   void sync_check();
+  void clear_err_word(uint32_t seen);
 
  private:
   struct EncBatch;

@@ -130,6 +130,12 @@ class TrafficLedger {
   std::string to_json() const;
   double bits_per_param_per_rank(const std::string& prefix = "") const;
   void clear() { rows_.clear(); }
+  // rows in (op, tag) order, as TrafficLedger::rows() (collectives.cpp:48-53)
+  std::vector<LedgerRow> rows() const {
+    std::vector<LedgerRow> out;
+    for (const auto& kv : rows_) out.push_back(kv.second);
+    return out;
+  }
   // Bytes actually handed to NCCL (measured, not modelled).
   uint64_t wire_bytes = 0;
 

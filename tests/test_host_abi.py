@@ -170,6 +170,15 @@ def test_ledger_csv_json_match_reference(ref):
         assert led.to_csv() == csv
         assert led.to_json() == js
         assert led.bits_per_param_per_rank(prefix) == bpp
+    rows = led.rows()  # TrafficLedger::rows(): (op, tag) order, one row per distinct key
+    assert [(r["op"], r["tag"]) for r in rows] == sorted({(ops[o], t) for o, t, _, _ in records},
+                                                          key=lambda k: (ops.index(k[0]), k[1]))
+    for r in rows:
+        mine = [(b, p) for o, t, b, p in records if ops[o] == r["op"] and t == r["tag"]]
+        factor = 2 if r["op"] == "all_reduce" else 1
+        assert r["calls"] == len(mine) and r["params"] == sum(p for _, p in mine) % 2**64
+        assert r["payload_bits"] == sum(b for b, _ in mine) % 2**64
+        assert r["charged_bits"] == factor * sum(b for b, _ in mine) % 2**64
     with pytest.raises(tagc.TagcInvalidArgument):
         led.record("broadcast", "x", 1, 1)
     led.clear()
