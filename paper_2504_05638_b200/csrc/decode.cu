@@ -1013,6 +1013,203 @@ __global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const 
   span_end(w.span);
 }
 
+// ------------------------------------------------------------------ round 0 + emit
+// Counter mode without an owner step: round 0 and the dense emit in ONE pass
+// over the word tiles, so round 0's random probes hide under the emit's
+// 4 B/position store stream instead of running as their own latency-bound
+// kernel. Per word tile (all of one item):
+//   (A) every listed entry probes its k byte counters and peels from its
+//       lowest singleton row (the reference's ascending seed order,
+//       decode.cpp:96-99) - value = sign * residual (decode.cpp:110-111),
+//       staged in shared memory; entries sharing a bucket join the compact
+//       subtraction list (pinfo), unresolved ones the ulist (their buckets
+//       marked and their state cleared for k_r0_subtract_cnt);
+//   (B) the tile's chunks are zero-filled (decode.cpp:61-64), take the staged
+//       values and leave by TMA bulk store (the k_emit ring).
+// Entries round 0 leaves unresolved stay zero here: k_final_fix writes them
+// after the frontier rounds and the median estimate.
+constexpr uint32_t kR0EmitCap = 1024;  // staged values per tile (beyond: through val[])
+constexpr uint32_t kR0EStage = 512;    // subtraction / unresolved list staging per CTA (3 CTAs per SM)
+constexpr size_t kR0EmitSmem = 2 * kEmitChunk * sizeof(float) + kR0EmitCap * sizeof(float);
+
+__global__ void __launch_bounds__(256, 3) k_r0_emit(DecodeWork w, const HashParams hp) {
+  extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk] ring, then [kR0EmitCap] staged values
+  float* s_val = ebuf + 2 * kEmitChunk;
+  __shared__ uint32_t s_q[kR0EStage], s_u[kR0EStage];
+  __shared__ uint32_t s_n[2], s_un[2], s_base;
+  if (threadIdx.x == 0) {
+    s_n[0] = s_un[0] = 0;
+    s_n[1] = s_un[1] = kR0EStage;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t total = ldcg(&w.qcount[5]);
+  const uint32_t T = uint32_t(w.total_word_tiles);
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
+  uint32_t n_chunks = 0, won = 0;
+  uint32_t it = t0 < t1 ? find_word_item(w.items, w.n_items, t0) : 0u;
+  for (uint32_t wt = t0; wt < t1; ++wt) {
+    while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
+    const DecItem& e = w.items[it];
+    const uint32_t L0 = min(__ldg(w.tile_base + wt), total);
+    const uint32_t L1 = wt + 1 < T ? min(__ldg(w.tile_base + wt + 1), total) : total;
+    // (A) round 0 over the tile's entries, warps on 32-aligned groups (one
+    // recovered-bit word each; words at tile edges are shared: red.or)
+    for (uint32_t g0 = (L0 & ~31u) + (threadIdx.x & ~31u); g0 < L1; g0 += blockDim.x) {
+      const uint32_t i = g0 + lane;
+      const bool act = i >= L0 && i < L1;
+      bool peeled = false, sub = false, unres = false;
+      if (act) {
+        const uint32_t p = __ldcs(w.plist + i);
+        uint64_t ls[kMaxRows];
+        uint32_t c[kMaxRows];
+#pragma unroll
+        for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r)
+          if (r < hp.rows) {  // every row's probe in flight before any is inspected
+            ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
+            const uint64_t sl = e.slot_base + ls[r];
+            c[r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+          }
+        int best = -1;
+        uint32_t shared = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) {
+          if (r >= hp.rows) continue;
+          shared |= uint32_t(c[r] >= 2u) << r;
+          if (best < 0 && c[r] == 1u) best = int(r);
+        }
+        float v = 0.0f;
+        if (best >= 0) {
+          uint64_t local = 0;
+          float sg = 0.0f;
+#pragma unroll
+          for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r)
+            if (int(r) == best) {
+              local = ls[r];
+              sg = dev_sign(hp.row[r], p);
+            }
+          v = canonical(sg * ldcg(e.sketch + local));
+          peeled = true;
+          sub = shared != 0u;
+          if (sub) w.pinfo[i] = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
+          ++won;
+        } else {  // unresolved after round 0: its buckets get a (count, index sum) state
+          unres = true;
+#pragma unroll
+          for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r)
+            if (r < hp.rows) {
+              const uint64_t sl = e.slot_base + ls[r];
+              red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
+              w.slot_state[sl] = 0ull;
+            }
+        }
+        if (i - L0 < kR0EmitCap) s_val[i - L0] = v;
+        else if (peeled) w.val[i] = v;
+      }
+      const uint32_t m = __ballot_sync(kFull, peeled);
+      if (lane == 0 && m) red_or_u32(w.bitmap + (g0 >> 5), m);
+      stage_push<uint32_t, kR0EStage>(sub, i, s_q, s_n, w.r0_list, &w.qcount[13], lane);
+      stage_push<uint32_t, kR0EStage>(unres, i, s_u, s_un, w.ulist, &w.qcount[14], lane);
+    }
+    __syncthreads();  // staged values visible to the whole CTA
+    // (B) the tile's chunks
+    const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
+    const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
+    const uint64_t p0 = wbase * P;
+    const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
+    uint32_t cur = L0;
+    for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
+      const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
+      float* buf = ebuf + (n_chunks & 1u) * kEmitChunk;
+      if (n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+      }
+      float4* b4 = reinterpret_cast<float4*>(buf);
+      for (uint32_t q = threadIdx.x; q < kEmitChunk / 4; q += blockDim.x) b4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncthreads();
+      for (;;) {
+        const uint32_t i = cur + threadIdx.x;
+        uint32_t p = 0xFFFFFFFFu;
+        if (i < L1) p = __ldcg(w.plist + i);  // just read by (A): an L2 hit
+        const bool in = uint64_t(p) < c0 + clen;
+        if (in) buf[p - c0] = i - L0 < kR0EmitCap ? s_val[i - L0] : __ldcg(w.val + i);
+        const uint32_t cnt = __syncthreads_count(in);
+        cur += cnt;
+        if (cnt < blockDim.x) break;
+      }
+      float* dst = e.out + c0;
+      const uint32_t bytes = (clen * 4u) & ~15u;
+      if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                       "r"(emit_smem_u32(buf)), "r"(bytes)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        for (uint32_t q = bytes / 4u + threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+      } else {  // unaligned output: plain coalesced stores
+        for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the ring count
+      }
+    }
+    __syncthreads();  // (B) is done reading s_val before the next tile's (A)
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  won = warp_sum32(won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  stage_flush<uint32_t, kR0EStage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
+  stage_flush<uint32_t, kR0EStage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
+}
+
+// Counter mode's last step after k_r0_emit: each entry round 0 left
+// unresolved gets its final value into the dense output - the frontier
+// rounds' value, or the median-of-rows estimate (decode.cpp:130-138, :43-47)
+// where the peel stalled.
+__global__ void __launch_bounds__(256) k_final_fix(DecodeWork w, const HashParams hp) {
+  const uint32_t nu = ldcg(&w.qcount[14]);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nu; base += stride) {
+    const uint64_t j = base + lane;
+    uint32_t it = 0xFFFFFFFFu, p = 0;
+    bool todo = false;
+    if (j < nu) {
+      const uint32_t i = ldcg(w.ulist + j);
+      p = __ldg(w.plist + i);
+      it = __ldg(w.pitem + i);
+      const DecItem& e = w.items[it];
+      float v;
+      if ((ldcg(w.bitmap + (i >> 5)) >> (i & 31)) & 1u) {
+        v = ldcg(w.val + i);
+      } else {
+        todo = true;
+        float est[kMaxRows];
+#pragma unroll
+        for (uint32_t r = 0; r < kMaxRows; ++r) {
+          if (r >= hp.rows) break;
+          est[r] = dev_sign(hp.row[r], p) * ldcg(e.sketch + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul));
+        }
+        v = canonical(median_rows(est, hp.rows));
+      }
+      e.out[p] = v;
+    }
+    const uint32_t grp = __match_any_sync(kFull, todo ? it : 0xFFFFFFFFu);
+    if (todo) {
+      const uint32_t leader = __ffs(grp) - 1;
+      uint32_t b0 = 0;
+      if (lane == leader) b0 = atomicAdd(&w.stats[it].unresolved, uint32_t(__popc(grp)));
+      b0 = __shfl_sync(grp, b0, leader);
+      if (w.unresolved) w.unresolved[w.items[it].list_off + b0 + __popc(grp & ((1u << lane) - 1u))] = p;
+    }
+  }
+  span_end(w.span);
+}
+
 // ------------------------------------------------------------------ helpers
 __global__ void k_presence_to_bitmap(const uint32_t* __restrict__ presence, uint32_t count,
                                      uint32_t n, uint32_t* bitmap, uint32_t* err) {
@@ -1088,11 +1285,17 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
 }  // namespace
 
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, bool fused_emit) {
   if (w.n_items == 0) return 0;
   int per_sm = 0;
   const int g = build_passes(di, w, hp, stream);
-  k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  if (fused_emit) {
+    const uint64_t ge = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
+    cudaFuncSetAttribute((const void*)k_r0_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR0EmitSmem));
+    k_r0_emit<<<int(ge), 256, kR0EmitSmem, stream>>>(w, hp);
+  } else {
+    k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  }
   if (w.cnt8) k_r0_subtract_cnt<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   else k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
@@ -1103,6 +1306,10 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   void* args[] = {&wc, &hc};
   cudaLaunchCooperativeKernel((const void*)k_peel, dim3(pg), dim3(256), args, 0, stream);
 
+  if (fused_emit) {  // the dense output is complete after this one
+    k_final_fix<<<di.sms * 4, 256, 0, stream>>>(w, hp);
+    return 5;  // list, round 0 + emit, subtraction, peel, final
+  }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
   return 5;  // list, round 0 (2), peel, final
@@ -1228,6 +1435,14 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
   if (db.Current() != keys)
     cudaMemcpyAsync(keys, db.Current(), size_t(count) * 4, cudaMemcpyDeviceToDevice, stream);
   return 1;
+}
+
+// Loads every kernel of this file now (see preload_all_kernels).
+void preload_decode_kernels() {
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_ord_claim, (const void*)k_ord_keys, (const void*)k_ord_peel, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_push, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  cudaFuncAttributes a;
+  for (const void* f : fns) cudaFuncGetAttributes(&a, f);
+  cudaGetLastError();
 }
 
 }  // namespace tagc_b200

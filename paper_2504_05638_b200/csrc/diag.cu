@@ -118,4 +118,12 @@ int launch_audit(const AuditItem* items, uint32_t n_items, uint64_t max_n, const
   return 1;
 }
 
+// Loads every kernel of this file now (see preload_all_kernels).
+void preload_diag_kernels() {
+  const void* fns[] = {(const void*)k_audit, (const void*)k_index_diag_support, (const void*)k_support_bytes};
+  cudaFuncAttributes a;
+  for (const void* f : fns) cudaFuncGetAttributes(&a, f);
+  cudaGetLastError();
+}
+
 }  // namespace tagc_b200

@@ -123,13 +123,19 @@ ExchangePlan plan_exchange(const std::vector<ShardSpec>& shards, const Compressi
 // ------------------------------------------------------------------ Workspace
 Workspace::~Workspace() {
   for (auto& [k, b] : bufs_) cudaFree(b.ptr);
+  for (void* p : graveyard_) cudaFree(p);
 }
 
 void* Workspace::get(const std::string& name, size_t bytes, bool zero_on_alloc, cudaStream_t s) {
   bytes = std::max<size_t>(bytes, 16);
   Buf& b = bufs_[name];
   if (b.bytes >= bytes) return b.ptr;
-  if (b.ptr) {
+  if (b.ptr && defer_free_) {  // queued work may still use it: keep it, no device sync
+    graveyard_.push_back(b.ptr);
+    total_ -= b.bytes;
+    b.ptr = nullptr;
+    b.bytes = 0;
+  } else if (b.ptr) {
     cuda_check(cudaStreamSynchronize(s), "workspace sync");
     cudaFree(b.ptr);
     total_ -= b.bytes;
@@ -153,6 +159,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
   if (const char* v = std::getenv("TAGC_GRAPHS")) graphs_on_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_SIDE_STREAM")) side_stream_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_DEFER_SCATTER_BYTES")) defer_scatter_bytes_ = std::strtoull(v, nullptr, 10);
+  if (const char* v = std::getenv("TAGC_FUSED_EMIT")) fused_emit_ = std::atoi(v) != 0;
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -174,6 +181,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
   }
   comm_ = static_cast<ncclComm_t>(nccl_comm);
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event create");
+  preload_all_kernels();
 }
 
 Engine::~Engine() {
@@ -190,6 +198,7 @@ Engine::~Engine() {
     if (s.ev) cudaEventDestroy(s.ev);
     if (s.ptr) cudaFreeHost(s.ptr);
   }
+  for (char* p : stage_graveyard_) cudaFreeHost(p);
   for (int i = 0; i < 2; ++i)
     for (cudaEvent_t e : {hev_in_[i], hev_gfree_[i], hev_dec_[i], hev_out_[i]})
       if (e) cudaEventDestroy(e);
@@ -311,25 +320,35 @@ void Engine::upload(const void* host, size_t bytes, void* dev) {
     return;
   }
   Staging& s = stage_[stage_cur_];
-  if (s.off + bytes > s.cap) {
-    // grow: earlier copies of this call may still read the old buffer
-    cuda_check(cudaStreamSynchronize(stream_), "staging grow");
-    if (s.ptr) cudaFreeHost(s.ptr);
-    s.ptr = nullptr;
-    s.cap = std::max<size_t>(std::max<size_t>(2 * s.cap, align_up(bytes, 4096)), 1 << 16);
-    s.off = 0;
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s.ptr), s.cap, cudaHostAllocMapped),
-               "staging alloc");
-    void* dp = nullptr;
-    cuda_check(cudaHostGetDevicePointer(&dp, s.ptr, 0), "staging map");
-    s.dev = static_cast<char*>(dp);
-  }
+  if (s.off + bytes > s.cap) stage_grow(s, bytes);
   std::memcpy(s.ptr + s.off, host, bytes);
   // the SMs pull the descriptors over PCIe (a copy-engine H2D would queue
   // behind the host-buffer path's bulk transfers); workspace destinations
   // have room for the 16-byte round-up
   launches_ += launch_stage_copy(dev, s.dev + s.off, align_up(bytes, 16), stream_);
   s.off = align_up(s.off + bytes, 256);
+}
+
+// A fresh staging buffer for the rest of the call. Earlier copies of this
+// call may still read the old one: with a peer exchange attached it is kept
+// (freed at destruction: cudaFreeHost would synchronise the device), else
+// the stream is drained first.
+void Engine::stage_grow(Staging& s, size_t bytes) {
+  if (s.ptr) {
+    if (peer_.region) {
+      stage_graveyard_.push_back(s.ptr);
+    } else {
+      cuda_check(cudaStreamSynchronize(stream_), "staging grow");
+      cudaFreeHost(s.ptr);
+    }
+  }
+  s.ptr = nullptr;
+  s.cap = std::max<size_t>(std::max<size_t>(2 * s.cap, align_up(bytes, 4096)), 1 << 20);
+  s.off = 0;
+  cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&s.ptr), s.cap, cudaHostAllocMapped), "staging alloc");
+  void* dp = nullptr;
+  cuda_check(cudaHostGetDevicePointer(&dp, s.ptr, 0), "staging map");
+  s.dev = static_cast<char*>(dp);
 }
 
 void Engine::zero(const std::vector<std::pair<void*, uint64_t>>& ranges) {
@@ -371,6 +390,16 @@ void Engine::download(const void* dev, uint64_t bytes, void* host) {
 // err[0] doubles as the presence-validation word of the standalone decode
 // entries; once read and reported it must not stay set, or the sticky NaN
 // test of every later encode (k_encode, k_fused_tma) would skip its writes.
+// TAGC_DEBUG_PEER=1: host-side phase trace of every exchange (rank, phase,
+// wall clock), for diagnosing stalls of ranks sharing one device.
+void Engine::trace(const char* phase) const {
+  static const bool on = std::getenv("TAGC_DEBUG_PEER") != nullptr;
+  if (!on) return;
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  std::fprintf(stderr, "[peer r%u/%u] %.6f %s\n", rank_, world_, double(ts.tv_sec) + ts.tv_nsec * 1e-9, phase);
+}
+
 void Engine::clear_err_word(uint32_t seen) {
   if (!seen) return;
   cuda_check(cudaMemsetAsync(err_flag(), 0, 4, stream_), "clear err");
@@ -378,6 +407,7 @@ void Engine::clear_err_word(uint32_t seen) {
 }
 
 void Engine::sync_check() {
+  trace("sync_check");
   if (h2d_) cuda_check(cudaStreamSynchronize(h2d_), "h2d sync");
   if (d2h_) cuda_check(cudaStreamSynchronize(d2h_), "d2h sync");
   cuda_check(cudaStreamSynchronize(stream_), "stream sync");
@@ -612,6 +642,8 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   for (const DecItem& d : items)
     counters = counters && double(std::min(d.list_cap ? d.list_cap : d.n, d.n)) <= 16.0 * double(d.m);
   const uint64_t cnt_words = (slots + 3) / 4;
+  // round 0 inside the dense emit unless the owner step consumes the values
+  const bool fused = counters && !ordered && !opt_on_ && fused_emit_;
   w.cnt8 = counters ? static_cast<uint32_t*>(ws_.get("cnt8", cnt_words * 4, false, stream_)) : nullptr;
   w.ulist = counters ? static_cast<uint32_t*>(ws_.get("ulist", list * 4 + 4, false, stream_)) : nullptr;
   zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)},
@@ -645,10 +677,10 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     launches_ += launch_decode_ordered(di_, w, hp, ob, stream_, epoch_, &gens);
     ordered_gens_ = gens;
   } else {
-    launches_ += launch_decode(di_, w, hp, stream_);
+    launches_ += launch_decode(di_, w, hp, stream_, fused);
   }
   if (zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait side stream");
-  launches_ += launch_decode_emit(di_, w, stream_, opt_on_ ? opt_dev_ : nullptr);
+  if (!fused) launches_ += launch_decode_emit(di_, w, stream_, opt_on_ ? opt_dev_ : nullptr);
   cuda_check(cudaGetLastError(), "decode launch");
   if (dbg) {
     unsigned long long t[64];
@@ -1123,9 +1155,12 @@ void Engine::exchange_seal() {
 
 void Engine::enqueue_reduce_shards(const std::vector<ShardSpec>& shards, const float* grad, float* acc,
                                    float* out, PeelStats* stats) {
+  trace("enqueue begin");
   open_exchange(shards, grad, acc, out);
   exchange_encode(0, ~0ull);
+  trace("encode enqueued");
   finish_exchange(stats);
+  trace("enqueue end");
 }
 
 // Prologue with this context's transport buffers: the peer region's current
@@ -1159,6 +1194,7 @@ void Engine::finish_exchange(PeelStats* stats) {
     // (stats sync, NaN, timeout) must not leave this rank on the other set
     xs_.peer_set = set;
     exchange_end(recv_f, recv_u, stats, [&] {
+      trace("peer exchange enqueue");
       launches_ += launch_peer_exchange(di_, peer_.view, set, recv_f, recv_u, err, stream_);
       peer_.set = set ^ 1;
       ledger_.wire_bytes += uint64_t(world_) * (peer_.Bf + peer_.Bu) * 4;
@@ -1498,17 +1534,30 @@ void Engine::peer_prepare(const std::vector<ShardSpec>& shards, uint8_t handle[k
   cuda_check(cudaMalloc(&o, std::max<uint64_t>(owned, 1) * 4), "warm-up alloc");
   cuda_check(cudaMemset(g, 0, total * 4), "warm-up zero");
   cuda_check(cudaMemset(a, 0, total * 4), "warm-up zero");
-  for (int rep = 0; rep < 2; ++rep) {
+  // four calls, the later two with statistics: both staging halves and the
+  // statistics path's buffers exist before the first real exchange
+  for (int rep = 0; rep < 4; ++rep) {
     CallScope scope(*this);
     exchange_begin(shards, g, a, o, reinterpret_cast<float*>(ps.region + ps.off_f[0]),
                    reinterpret_cast<uint32_t*>(ps.region + ps.off_u[0]));
     auto* recv_f = static_cast<float*>(ws_.get("nc_recv_f", ps.Bf * 4, false, stream_));
     auto* recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", ps.Bu * 4, false, stream_));
     zero({{recv_f, ps.Bf * 4}, {recv_u, ps.Bu * 4}});
-    exchange_end(recv_f, recv_u, nullptr);
+    PeelStats st{};
+    exchange_end(recv_f, recv_u, rep >= 2 ? &st : nullptr);
   }
+  // staging headroom: a real step's descriptor uploads never regrow a half
+  for (Staging& s : stage_)
+    if (s.cap < (4u << 20)) {
+      cuda_check(cudaStreamSynchronize(stream_), "staging grow");
+      if (s.ptr) cudaFreeHost(s.ptr);
+      s.ptr = nullptr;
+      s.cap = 0;
+      stage_grow(s, 4u << 20);
+    }
+  ws_.set_defer_free(true);
   ensure_aux();
-  peer_preload();
+  preload_all_kernels();
   cuda_check(cudaStreamSynchronize(stream_), "warm-up sync");
   cudaFree(g);
   cudaFree(a);

@@ -34,9 +34,15 @@ class Workspace {
   uint64_t bytes() const { return total_; }
   // bumped on every (re)allocation: captured graphs hold raw pointers
   uint64_t generation() const { return gen_; }
+  // Regrowth keeps the old buffer until destruction instead of syncing and
+  // freeing it: cudaFree synchronises the whole device, which must never
+  // happen while a peer exchange may be spinning on this device.
+  void set_defer_free(bool on) { defer_free_ = on; }
 
  private:
   uint64_t gen_ = 0;
+  bool defer_free_ = false;
+  std::vector<void*> graveyard_;
   struct Buf {
     void* ptr = nullptr;
     size_t bytes = 0;
@@ -207,6 +213,7 @@ class Engine {
   // Synchronise and surface deferred device errors (NaN input -> invalid).
   void sync_check();
   void clear_err_word(uint32_t seen);
+  void trace(const char* phase) const;
 
  private:
   struct EncBatch;
@@ -284,6 +291,8 @@ class Engine {
     size_t cap = 0, off = 0;
     cudaEvent_t ev = nullptr;
   };
+  std::vector<char*> stage_graveyard_;  // outgrown staging buffers (peer mode: freed at destruction)
+  void stage_grow(Staging& s, size_t bytes);
   Staging stage_[2];
   int stage_cur_ = 0, call_depth_ = 0;
   void call_begin();
@@ -319,6 +328,8 @@ class Engine {
   // sketches above this size are scattered by the region-ordered pass
   // (TAGC_DEFER_SCATTER_BYTES; 0 defers every compressed segment's)
   uint64_t defer_scatter_bytes_ = 32ull << 20;
+  // counter-mode decode with round 0 inside the dense emit (TAGC_FUSED_EMIT=1; off: 0.68 vs 0.50 ms on C4)
+  bool fused_emit_ = false;
   bool side_stream_ = true;  // W = 1 raw copies on the low-priority side stream (TAGC_SIDE_STREAM=0: in order)
   bool use_tma_ = true;  // TMA-staged fused pass (TAGC_FUSED_TMA=0 selects the register path)
   uint32_t* err_flag();

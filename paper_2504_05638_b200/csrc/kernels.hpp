@@ -172,8 +172,11 @@ struct DecodeWork {
 // rounds inside one cooperative persistent kernel, estimation of the rest
 // (decode.cpp:53-140 semantics), all into the list-ordered val[]; finish
 // with launch_decode_emit.
+// fused_emit (counter mode, no owner step): round 0 runs inside the dense
+// emit (k_r0_emit) and the final kernel writes the remaining entries, so the
+// output is complete without launch_decode_emit.
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                  cudaStream_t stream);
+                  cudaStream_t stream, bool fused_emit = false);
 
 // Final step of either decode: writes every item's dense output (zeros, and
 // the decoded value of each listed entry).
@@ -240,5 +243,17 @@ struct PeerView {
 int launch_peer_exchange(const DevInfo& di, const PeerView& v, int set, float* recv_f, uint32_t* recv_u,
                          uint32_t* err, cudaStream_t stream);
 void peer_preload();
+void preload_encode_kernels();
+void preload_decode_kernels();
+void preload_diag_kernels();
+// Every kernel of the library loaded up front: with CUDA lazy loading a first
+// launch while another rank of the process spins in k_peer_wait can stall
+// (several ranks on one GPU), and no module load should sit on a timed path.
+inline void preload_all_kernels() {
+  preload_encode_kernels();
+  preload_decode_kernels();
+  preload_diag_kernels();
+  peer_preload();
+}
 
 }  // namespace tagc_b200

@@ -43,5 +43,5 @@ def test_bench_two_ranks_plumbing():
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["peel"]["unresolved"] == 0
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["peel"]["unresolved"] == 0
     assert d["owner_step"]["fused_ms"] > 0 and d["overlap"]["overlapped_ms"] > 0 and d["e2e"]["value"] > 0
