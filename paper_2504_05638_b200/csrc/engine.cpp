@@ -1346,11 +1346,15 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
   if (stats) {
     dec_stats_.resize(dec.size());
     std::vector<unsigned long long> lsh(ls ? dec.size() * 2 : 0, 0);
+    // drain the stream BEFORE the pageable copies: a pageable D2H queued
+    // behind this rank's wait for its peers blocks inside the driver and
+    // stalls every other host thread's CUDA calls (ranks sharing a process)
+    sync_check();
     if (!dec.empty())
       cuda_check(cudaMemcpyAsync(dec_stats_.data(), ws_.get("dec_stats", 16), dec.size() * sizeof(DecStats),
                                  cudaMemcpyDeviceToHost, stream_), "D2H stats");
     if (ls) cuda_check(cudaMemcpyAsync(lsh.data(), ls, lsh.size() * 8, cudaMemcpyDeviceToHost, stream_), "D2H ls");
-    sync_check();
+    cuda_check(cudaStreamSynchronize(stream_), "stats sync");
     if (!dec.empty()) fetch_rounds();
     PeelStats st;
     for (const DecStats& d : dec_stats_) {
