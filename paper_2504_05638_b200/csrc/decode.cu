@@ -258,6 +258,169 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
   }
 }
 
+// Counter mode (byte counters, no list indices in the bucket state): the
+// bucket counts do not depend on the list order, so the build splits into
+// three passes with no look-back chain between word tiles:
+//   k_list_count : per word tile, its present positions' byte-counter REDs
+//                  and its count (tile_base[wt] holds the count), the next
+//                  tile's words already in flight;
+//   k_tile_scan  : one CTA turns the counts into list offsets in place;
+//   k_list_write : per word tile, the list entries at their final index.
+// The merged index is read twice (streamed), against a per-tile look-back
+// whose latency chain grew with the number of CTAs in flight.
+__device__ __forceinline__ void load_tile_raw(const DecItem& e, uint32_t wbase, uint32_t (&raw)[kPerThreadWords]) {
+  const uint32_t w0 = tile_word(wbase, 0);
+  if (w0 + kPerThreadWords <= e.n_words && (reinterpret_cast<uintptr_t>(e.words + w0) & 15u) == 0) {
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; k += 4) {
+      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(e.words + w0 + k));
+      raw[k] = x.x; raw[k + 1] = x.y; raw[k + 2] = x.z; raw[k + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) raw[k] = w0 + k < e.n_words ? __ldcs(e.words + w0 + k) : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
+  using Reduce = cub::BlockReduce<uint32_t, 256>;
+  __shared__ typename Reduce::TempStorage red_tmp;
+  span_begin(w.span);
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
+  if (t0 >= t1) return;
+  uint32_t it = find_word_item(w.items, w.n_items, t0);
+  uint32_t raw[kPerThreadWords];
+  {
+    const DecItem& e = w.items[it];
+    load_tile_raw(e, uint32_t(t0 - e.word_tile_begin) * kWordTile, raw);
+  }
+  for (uint32_t wt = t0; wt < t1; ++wt) {
+    const DecItem& e = w.items[it];
+    const bool w4 = (e.flags & kWidth4) != 0;
+    const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) cnt += __popc(present_bits(raw[k], w4, tile_word(wbase, k), e.n));
+    uint32_t nit = it;  // the next tile's words in flight during the reduction
+    if (wt + 1 < t1) {
+      while (nit + 1 < w.n_items && w.items[nit + 1].word_tile_begin <= wt + 1) ++nit;
+      const DecItem& ne = w.items[nit];
+      load_tile_raw(ne, uint32_t(wt + 1 - ne.word_tile_begin) * kWordTile, raw);
+    }
+    const uint32_t total = Reduce(red_tmp).Sum(cnt);
+    if (threadIdx.x == 0) {
+      w.tile_base[wt] = total;
+      if (total) atomicAdd(&w.stats[it].presence, total);
+    }
+    __syncthreads();  // reduce storage reuse
+    it = nit;
+  }
+}
+
+// In place: tile counts -> exclusive list offsets; the list length (0 when
+// it exceeds the capacity: a corrupt index after a NaN-aborted encode lists
+// nothing) to qcount[5].
+__global__ void __launch_bounds__(1024) k_tile_scan(DecodeWork w) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint64_t s_carry;
+  const uint64_t T = w.total_word_tiles;
+  constexpr uint32_t kPer = 8;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint64_t c0 = 0; c0 < T; c0 += 1024 * kPer) {
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint64_t t = c0 + uint64_t(threadIdx.x) * kPer + k;
+      v[k] = t < T ? w.tile_base[t] : 0u;
+      sum += v[k];
+    }
+    uint32_t off, agg;
+    Scan(tmp).ExclusiveSum(sum, off, agg);
+    const uint64_t carry = s_carry;
+    uint64_t run = carry + off;
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint64_t t = c0 + uint64_t(threadIdx.x) * kPer + k;
+      if (t < T) w.tile_base[t] = uint32_t(run < 0xFFFFFFFFull ? run : 0xFFFFFFFFull);
+      run += v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) w.qcount[5] = s_carry <= w.list_cap ? uint32_t(s_carry) : 0u;
+}
+
+constexpr uint32_t kListStage = 2048;  // staged positions per word tile (beyond: read back)
+
+__global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashParams hp) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_pos[kListStage];
+  const uint32_t total_list = ldcg(&w.qcount[5]);
+  uint32_t t0, t1;
+  cta_tiles(w.total_word_tiles, t0, t1);
+  if (t0 >= t1 || total_list == 0) return;
+  uint32_t it = find_word_item(w.items, w.n_items, t0);
+  uint32_t raw[kPerThreadWords];
+  {
+    const DecItem& e = w.items[it];
+    load_tile_raw(e, uint32_t(t0 - e.word_tile_begin) * kWordTile, raw);
+  }
+  for (uint32_t wt = t0; wt < t1; ++wt) {
+    const DecItem& e = w.items[it];
+    const bool w4 = (e.flags & kWidth4) != 0;
+    const uint32_t P = w4 ? 8u : 32u;
+    const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
+    uint32_t bits[kPerThreadWords], cnt = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) {
+      bits[k] = present_bits(raw[k], w4, tile_word(wbase, k), e.n);
+      cnt += __popc(bits[k]);
+    }
+    uint32_t nit = it;
+    if (wt + 1 < t1) {
+      while (nit + 1 < w.n_items && w.items[nit + 1].word_tile_begin <= wt + 1) ++nit;
+      const DecItem& ne = w.items[nit];
+      load_tile_raw(ne, uint32_t(wt + 1 - ne.word_tile_begin) * kWordTile, raw);
+    }
+    uint32_t off, tile_n;
+    Scan(scan_tmp).ExclusiveSum(cnt, off, tile_n);
+    const uint32_t base = __ldg(w.tile_base + wt);
+    const bool staged = tile_n <= kListStage;
+    uint32_t j = base + off;
+#pragma unroll
+    for (uint32_t k = 0; k < kPerThreadWords; ++k) {
+      const uint32_t wi = tile_word(wbase, k);
+      for (uint32_t x = bits[k]; x; x &= x - 1) {
+        const uint32_t bb = __ffs(x) - 1;
+        const uint32_t p = wi * P + (w4 ? bb / 4 : bb);
+        if (j < total_list) {
+          w.plist[j] = p;
+          w.pitem[j] = it;
+        }
+        if (staged) s_pos[j - base] = p;
+        ++j;
+      }
+    }
+    __syncthreads();  // the tile's positions are visible to the whole CTA
+    // bucket byte counters, one entry per thread (hashing and REDs converged)
+    const uint32_t n_in = base + tile_n <= total_list ? tile_n : (base < total_list ? total_list - base : 0u);
+    for (uint32_t q = threadIdx.x; q < n_in; q += blockDim.x) {
+      const uint32_t p = staged ? s_pos[q] : __ldcg(w.plist + base + q);
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+        const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
+        red_add_u32(w.cnt8 + (slot >> 2), 1u << (8u * uint32_t(slot & 3u)));
+      }
+    }
+    __syncthreads();  // scan storage / stage reuse
+    it = nit;
+  }
+}
+
 // ------------------------------------------------------------------ staging
 // Warp-aggregated appends into a per-CTA shared-memory stage, flushed with one
 // global atomic per CTA; a single list counter hit by every warp serialises at
@@ -436,6 +599,116 @@ __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParam
   __syncthreads();
   round0_phase1(w, hp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x,
                 compact ? s_q : nullptr, s_n, ulist ? s_u : nullptr, s_un);
+  if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
+  if (ulist) stage_flush<uint32_t, kR0Stage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
+}
+
+// Round 0 with the row count fixed at compile time (k = R, the common k = 3)
+// and PER list entries per thread: every entry's bucket probes, then every
+// peeled entry's residual load, are issued before any of them is consumed,
+// so PER x R probes and PER sketch gathers are in flight per thread (the
+// generic kernel has R and 1). Same outputs as round0_phase1; pinfo only
+// where a later pass reads it (compact list: entries with a shared bucket).
+template <int R, int PER>
+__global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashParams hp) {
+  __shared__ uint32_t s_q[kR0Stage], s_u[kR0Stage];
+  __shared__ uint32_t s_n[2], s_un[2], s_base;
+  const bool compact = w.r0_list != nullptr;
+  const bool ulist = w.cnt8 != nullptr;
+  if (threadIdx.x == 0) {
+    s_n[0] = s_un[0] = 0;
+    s_n[1] = s_un[1] = kR0Stage;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t won = 0;
+  const uint32_t total = ldcg(&w.qcount[5]);
+  const uint64_t step = uint64_t(gridDim.x) * blockDim.x * PER;
+  // a warp covers PER consecutive groups of 32 entries (one bitmap word each)
+  const uint64_t wbase0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * PER;
+  for (uint64_t wb = wbase0; wb < total; wb += step) {
+    uint32_t p[PER], it[PER];
+    bool act[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint64_t i = wb + 32u * k + lane;
+      act[k] = i < total;
+      p[k] = act[k] ? __ldcs(w.plist + i) : 0u;
+      it[k] = act[k] ? __ldcs(w.pitem + i) : 0u;
+    }
+    uint64_t ls[PER][R];
+    uint32_t c[PER][R];
+    const float* sk[PER];
+    uint64_t sb[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const DecItem& e = w.items[it[k]];
+      const uint32_t m = e.m;
+      const uint64_t mm = e.mmul;
+      sk[k] = e.sketch;
+      sb[k] = e.slot_base;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ls[k][r] = uint64_t(r) * m + dev_bucket(hp.row[r], p[k], m, mm);
+        const uint64_t sl = sb[k] + ls[k][r];
+        if (!act[k]) c[k][r] = 0u;
+        else if (w.cnt8) c[k][r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+        else c[k][r] = st_count(ldcg(w.slot_state + sl));
+      }
+    }
+    int best[PER];
+    uint32_t shared[PER];
+    float resid[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      best[k] = -1;
+      shared[k] = 0u;
+      uint64_t local = 0;
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {  // lowest singleton row wins
+        shared[k] |= uint32_t(c[k][r] >= 2u) << r;
+        if (c[k][r] == 1u) {
+          best[k] = r;
+          local = ls[k][r];
+        }
+      }
+      resid[k] = best[k] >= 0 ? ldcg(sk[k] + local) : 0.0f;  // every gather in flight together
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint64_t i = wb + 32u * k + lane;
+      const bool peeled = act[k] && best[k] >= 0;
+      const bool sub = peeled && shared[k] != 0u;
+      if (act[k]) {
+        uint2 info = make_uint2(0u, 0u);
+        if (peeled) {
+          float sg = 0.0f;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r == best[k]) sg = dev_sign(hp.row[r], p[k]);
+          const float v = canonical(sg * resid[k]);
+          w.val[i] = v;
+          info = make_uint2(__float_as_uint(v), shared[k] | 0x100u | (uint32_t(best[k]) << 12));
+          ++won;
+        } else if (w.slot_mark) {  // unresolved after round 0: its buckets still matter
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint64_t sl = sb[k] + ls[k][r];
+            red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
+            if (w.cnt8) w.slot_state[sl] = 0ull;  // built by k_r0_subtract_cnt
+          }
+        }
+        if (!compact || sub) w.pinfo[i] = info;
+      }
+      const uint32_t bm = __ballot_sync(kFull, peeled);
+      if (lane == 0 && wb + 32u * k < total) w.bitmap[(wb >> 5) + k] = bm;
+      if (compact) stage_push<uint32_t, kR0Stage>(sub, uint32_t(i), s_q, s_n, w.r0_list, &w.qcount[13], lane);
+      if (ulist) stage_push<uint32_t, kR0Stage>(act[k] && !peeled, uint32_t(i), s_u, s_un, w.ulist,
+                                                &w.qcount[14], lane);
+    }
+  }
+  won = warp_sum32(won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
   if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
   if (ulist) stage_flush<uint32_t, kR0Stage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
 }
@@ -1276,6 +1549,14 @@ int grid_for(uint64_t n, int threads) {
 // count -> scan -> list + bucket state (bucket state zeroed in between: it is
 // first touched by k_list). Returns the grid used for the word-tile passes.
 int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, cudaStream_t stream) {
+  if (w.cnt8) {  // counter mode: count, scan, write (no look-back)
+    const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
+    const uint64_t gn = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 8);
+    k_list_count<<<int(gn), 256, 0, stream>>>(w);
+    k_tile_scan<<<1, 1024, 0, stream>>>(w);
+    k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // byte counters were zeroed by the caller
+    return int(gc);
+  }
   const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
   const int g = int(g64);
   k_list<<<g, 256, 0, stream>>>(w, hp);  // bucket and tile state were zeroed by the caller
@@ -1288,11 +1569,14 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
                   cudaStream_t stream, bool fused_emit) {
   if (w.n_items == 0) return 0;
   int per_sm = 0;
-  const int g = build_passes(di, w, hp, stream);
+  build_passes(di, w, hp, stream);
+  const int list_launches = w.cnt8 ? 3 : 1;
   if (fused_emit) {
     const uint64_t ge = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
     cudaFuncSetAttribute((const void*)k_r0_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR0EmitSmem));
     k_r0_emit<<<int(ge), 256, kR0EmitSmem, stream>>>(w, hp);
+  } else if (hp.rows == 3) {
+    k_r0_phase1_k<3, 2><<<di.sms * 8, 256, 0, stream>>>(w, hp);
   } else {
     k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   }
@@ -1308,11 +1592,11 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
 
   if (fused_emit) {  // the dense output is complete after this one
     k_final_fix<<<di.sms * 4, 256, 0, stream>>>(w, hp);
-    return 5;  // list, round 0 + emit, subtraction, peel, final
+    return list_launches + 4;  // list, round 0 + emit, subtraction, peel, final
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return 5;  // list, round 0 (2), peel, final
+  return list_launches + 4;  // list, round 0 (2), peel, final
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
@@ -1323,7 +1607,8 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   int per_sm = 0;
   const int g = build_passes(di, w, hp, stream);
   const int grid = di.sms * 4;
-  k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
+  if (hp.rows == 3) k_r0_phase1_k<3, 2><<<grid, 256, 0, stream>>>(w, hp);
+  else k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
   ++epoch;
   OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
   cudaMemsetAsync(ob.count, 0, 4, stream);
@@ -1439,7 +1724,7 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_decode_kernels() {
-  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_ord_claim, (const void*)k_ord_keys, (const void*)k_ord_peel, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_push, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_claim, (const void*)k_ord_keys, (const void*)k_ord_peel, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_push, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

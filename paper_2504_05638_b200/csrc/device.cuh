@@ -23,6 +23,11 @@ constexpr uint32_t kSampleStride = 3 * kSampleBins;  // per item: coarse, fine (
 // Large segments sample 1024 elements of every kSampleMaxStride-th tile
 // (1/32 of the data); the window's rank margin scales with 1/sqrt(sample).
 constexpr uint64_t kSampleMaxStride = 8;
+// ... and at most kSampleMaxTiles chunks (2M samples) per segment: past that
+// the stride grows (a 2^28-element bucket samples every 32nd tile, 1/128).
+// sigma of the sampled rank then is ~140 at theta = 99, a window of ~0.1 %
+// of the segment, still tiny against the fused pass's streaming.
+constexpr uint64_t kSampleMaxTiles = 2048;
 constexpr uint32_t kRadixBins = 2048;   // 11/10/10-bit digits of the key
 constexpr uint32_t kDecWordTile = 4096; // merged-index words per decode word tile (16 per thread)
 constexpr uint32_t kMaxFlatItems = 4096; // items per call (flattened iteration bound)

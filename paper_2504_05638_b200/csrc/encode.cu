@@ -1024,26 +1024,35 @@ __host__ __device__ constexpr int digit_bits(int pass) { return pass == 0 ? 11 :
 constexpr uint32_t kFinalKeys = 8192;  // per-item capacity of the target sub-bin list
 
 // --------------------------------------------------------------- finalize
-// k_finish_select, one CTA per item:
-// (1) checks that tau (the c-th smallest key, sparsify.cpp:33-37) falls
-//     inside the window, so every speculative decision outside it was right,
-//     and names the fine sub-bin holding it;
-// (2) gathers that sub-bin's keys from the item's candidates into shared
-//     memory;
-// (3) radix-selects tau exactly among them.
+// k_finish_select, a grid of kFinishCtas CTAs per item (blockIdx.y = item):
+// (1) every CTA checks that tau (the c-th smallest key, sparsify.cpp:33-37)
+//     falls inside the window, so every speculative decision outside it was
+//     right, and names the fine sub-bin holding it (the same answer in every
+//     CTA: the item's fine histogram is read-only here);
+// (2) the CTAs gather that sub-bin's keys from their slice of the item's
+//     candidates into the item's key list (sel_list, kFinalKeys per item);
+// (3) the last CTA of the item to finish radix-selects tau exactly among
+//     them (streaming all candidates again if the sub-bin overflowed the
+//     list: massive ties) and leaves the fine histogram and the counters
+//     zeroed for the next call.
 // Bit-identical to nth_element (sparsify.cpp:35-36).
-__global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restrict__ items,
-                                                        SelState* __restrict__ state,
-                                                        uint32_t* __restrict__ fine_hist,
-                                                        const uint2* __restrict__ cand,
-                                                        uint32_t* __restrict__ err) {
+constexpr uint32_t kFinishCtas = 16;
+constexpr uint32_t kFinishThreads = 256;
+
+__global__ void __launch_bounds__(kFinishThreads) k_finish_select(const EncItem* __restrict__ items,
+                                                                  SelState* __restrict__ state,
+                                                                  uint32_t* __restrict__ fine_hist,
+                                                                  const uint2* __restrict__ cand,
+                                                                  uint32_t* __restrict__ sel_list,
+                                                                  uint32_t* __restrict__ err) {
   __shared__ uint32_t keys[kFinalKeys];
   __shared__ uint32_t hist[kRadixBins];
-  __shared__ uint32_t s_digit, s_below, s_n;
-  const uint32_t item = blockIdx.x;
+  __shared__ uint32_t s_digit, s_below, s_last;
+  const uint32_t item = blockIdx.y;
   const EncItem e = items[item];
   const SelState s = state[item];
   uint32_t* fh = fine_hist + uint64_t(item) * kRadixBins;
+  uint32_t* list = sel_list + uint64_t(item) * kFinalKeys;
   const bool overflow = s.cnt_in > e.cand_cap || s.cnt_hi > e.hi_cap;
   const uint32_t Z = s.cnt_zero, L = s.cnt_lo, I = s.cnt_in;
   int action = 0;  // 0 none (NaN), 1 tau = 0, 2 select among candidates, 3 fallback
@@ -1052,49 +1061,68 @@ __global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restric
     else if (!overflow && Z + L < e.c && e.c <= Z + L + I) action = 2;
     else action = 3;
   }
-  if (threadIdx.x == 0) s_n = 0;
   uint32_t rank = 0, sub = 0;
   if (action == 2) {
-    find_digit<1024>(fh, kRadixBins, e.c - Z - L - 1, &s_digit, &s_below);
+    find_digit<kFinishThreads>(fh, kRadixBins, e.c - Z - L - 1, &s_digit, &s_below);
     sub = s_digit;  // target sub-bin
     rank = e.c - Z - L - 1 - s_below;
-  } else if (threadIdx.x == 0) {
-    if (action == 1) {
-      state[item].tau_key = 0;
-      state[item].status = kStatusReady;
-    } else if (action == 3) {  // bracket missed: restore + full radix select
-      state[item].status = kStatusFallback;
-      state[item].prefix = 0;
-      state[item].rank = e.c - 1;
-      atomicOr(err + 1, 1u);
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) fh[i] = 0;  // left zero for the next call
-  if (action != 2) return;
-  // (2) the target sub-bin's keys
-  const uint2* ck = cand + e.cand_off;
-  const uint32_t nc = min(s.cnt_in, e.cand_cap);
-  constexpr uint32_t kB = 8;  // candidate loads in flight per thread
-  for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += kB * blockDim.x) {
-    uint32_t kk[kB];
+    // (2) this CTA's slice of the candidates
+    const uint2* ck = cand + e.cand_off;
+    const uint32_t nc = min(s.cnt_in, e.cand_cap);
+    const uint32_t per = (nc + gridDim.x - 1) / gridDim.x;
+    const uint32_t c0 = min(nc, blockIdx.x * per), c1 = min(nc, c0 + per);
+    constexpr uint32_t kB = 4;  // candidate loads in flight per thread
+    const uint32_t lane = threadIdx.x & 31;
+    // warp-uniform trip count (the ballots below need every lane)
+    for (uint32_t w0 = c0 + (threadIdx.x & ~31u); w0 < c1; w0 += kB * blockDim.x) {
+      uint32_t kk[kB];
 #pragma unroll
-    for (uint32_t b = 0; b < kB; ++b) {
-      const uint32_t i = i0 + b * blockDim.x;
-      kk[b] = i < nc ? (__ldcs(&ck[i].y) & 0x7FFFFFFFu) : 0xFFFFFFFFu;
-    }
+      for (uint32_t b = 0; b < kB; ++b) {
+        const uint32_t i = w0 + lane + b * blockDim.x;
+        kk[b] = i < c1 ? (__ldcs(&ck[i].y) & 0x7FFFFFFFu) : 0xFFFFFFFFu;
+      }
 #pragma unroll
-    for (uint32_t b = 0; b < kB; ++b) {
-      if (kk[b] != 0xFFFFFFFFu && ((kk[b] - s.klo) >> s.fshift) == sub) {
-        const uint32_t idx = atomicAdd(&s_n, 1u);
-        if (idx < kFinalKeys) keys[idx] = kk[b];
+      for (uint32_t b = 0; b < kB; ++b) {
+        const bool hit = kk[b] != 0xFFFFFFFFu && ((kk[b] - s.klo) >> s.fshift) == sub;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, hit);
+        if (!m) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&state[item].n_sel, uint32_t(__popc(m)));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + __popc(m & ((1u << lane) - 1u));
+        if (hit && base < kFinalKeys) list[base] = kk[b];
       }
     }
   }
+  // (3) the last CTA of the item finishes it
+  __threadfence();
   __syncthreads();
-  const uint32_t nk = s_n;
+  if (threadIdx.x == 0) s_last = atomicAdd(&state[item].pad, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (uint32_t i = threadIdx.x; i < kRadixBins; i += blockDim.x) fh[i] = 0;  // left zero for the next call
+  if (action != 2) {
+    if (threadIdx.x == 0) {
+      if (action == 1) {
+        state[item].tau_key = 0;
+        state[item].status = kStatusReady;
+      } else if (action == 3) {  // bracket missed: restore + full radix select
+        state[item].status = kStatusFallback;
+        state[item].prefix = 0;
+        state[item].rank = e.c - 1;
+        atomicOr(err + 1, 1u);
+      }
+      state[item].n_sel = 0;
+      state[item].pad = 0;
+    }
+    return;
+  }
+  const uint32_t nk = __ldcg(&state[item].n_sel);
   const bool in_smem = nk <= kFinalKeys;
-  // (3) exact radix select
+  if (in_smem)
+    for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) keys[i] = __ldcg(list + i);
+  const uint2* ck = cand + e.cand_off;
+  const uint32_t nc = min(s.cnt_in, e.cand_cap);
   uint32_t prefix = 0;
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
@@ -1114,7 +1142,7 @@ __global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restric
       }
     }
     __syncthreads();
-    find_digit<1024>(hist, 1u << bits, rank, &s_digit, &s_below);
+    find_digit<kFinishThreads>(hist, 1u << bits, rank, &s_digit, &s_below);
     rank -= s_below;
     prefix |= s_digit << shift;
     __syncthreads();
@@ -1122,40 +1150,76 @@ __global__ void __launch_bounds__(1024) k_finish_select(const EncItem* __restric
   if (threadIdx.x == 0) {
     state[item].tau_key = prefix;
     state[item].status = kStatusReady;
+    state[item].n_sel = 0;
+    state[item].pad = 0;
   }
 }
 
 // --------------------------------------------------------------- fixup
 // Window candidates with key > tau were written as dropped: make them kept
-// (residual 0, index field set, sketch scatter).
+// (residual 0, index field set, sketch scatter). Each CTA walks a contiguous
+// range of the flattened candidates in 256-wide chunks; a chunk inside one
+// item (the common case) takes its kept count and its deferred-scatter log
+// slots with ONE atomic per chunk (block count / scan), a mixed chunk per
+// warp and item - per-warp atomics on one item's counters serialised at a
+// single L2 address once an item had 10^5 candidates.
 template <bool kW4>
 __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items,
                                                SelState* __restrict__ state, uint32_t n_items,
                                                const uint2* __restrict__ cand, const HashParams hp,
                                                const uint32_t* __restrict__ err, uint2* __restrict__ hi_pool) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t pref[kMaxFlatItems + 1];
   __shared__ uint32_t s_tau[kMaxFlatItems];
+  __shared__ uint32_t s_base;
   if (err[0]) return;
   for (uint32_t i = threadIdx.x; i < n_items; i += blockDim.x) s_tau[i] = state[i].tau_key;
   const uint32_t total = flat_prefix(n_items, [&](uint32_t i) {
     return state[i].status == kStatusReady ? min(state[i].cnt_in, items[i].cand_cap) : 0u;
   }, pref);
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < total;
-       base += gridDim.x * blockDim.x) {
-    const uint32_t j = base + lane;
+  const uint32_t per = ((total + gridDim.x - 1) / gridDim.x + 255u) & ~255u;
+  const uint32_t j0 = min(total, blockIdx.x * per), j1 = min(total, j0 + per);
+  for (uint32_t c = j0; c < j1; c += blockDim.x) {
+    const uint32_t j = c + threadIdx.x;
+    const bool valid = j < j1;
     uint32_t it = 0xFFFFFFFFu;
     bool keep = false;
     uint2 kv = make_uint2(0u, 0u);
-    if (j < total) {
+    if (valid) {
       it = flat_item(pref, n_items, j);
       kv = cand[items[it].cand_off + (j - pref[it])];
       keep = (kv.y & 0x7FFFFFFFu) > s_tau[it];
     }
-    // kept counts, aggregated over the lanes of the same item
-    const uint32_t grp = __match_any_sync(kFull, it);
-    const uint32_t km = __ballot_sync(kFull, keep) & grp;
-    if (keep && lane == __ffs(km) - 1) atomicAdd(&state[it].kept, __popc(km));
+    const uint32_t it0 = flat_item(pref, n_items, c);
+    const bool uni = __syncthreads_and(!valid || it == it0) != 0;  // block-uniform
+    const EncItem& e0 = items[it0];
+    const bool log0 = (e0.flags & kWriteSketch) && (e0.flags & kDeferScatter);
+    uint32_t slot = 0;
+    if (uni) {
+      uint32_t off, nk;
+      Scan(scan_tmp).ExclusiveSum(keep ? 1u : 0u, off, nk);
+      if (threadIdx.x == 0) {
+        if (nk) atomicAdd(&state[it0].kept, nk);
+        s_base = (log0 && nk) ? atomicAdd(&state[it0].cnt_hi, nk) : 0u;
+      }
+      __syncthreads();
+      slot = s_base + off;
+      __syncthreads();  // s_base / scan storage reuse
+    } else {
+      // kept counts, aggregated over the lanes of the same item
+      const uint32_t grp = __match_any_sync(kFull, it);
+      const uint32_t km = __ballot_sync(kFull, keep) & grp;
+      if (keep && lane == __ffs(km) - 1) atomicAdd(&state[it].kept, __popc(km));
+      if (keep && (items[it].flags & kWriteSketch) && (items[it].flags & kDeferScatter)) {
+        const uint32_t leader = __ffs(km) - 1;
+        uint32_t b0 = 0;
+        if (lane == leader) b0 = atomicAdd(&state[it].cnt_hi, __popc(km));
+        b0 = __shfl_sync(km, b0, leader);
+        slot = b0 + __popc(km & ((1u << lane) - 1u));
+      }
+    }
     if (!keep) continue;
     const EncItem& e = items[it];
     const uint32_t p = kv.x;
@@ -1170,12 +1234,6 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
     if ((e.flags & kWriteSketch) && !(e.flags & kDeferScatter)) {
       scatter_sketch(e, hp, p, v);
     } else if (e.flags & kWriteSketch) {  // log it with the speculatively kept: the deferred scatter takes both
-      const uint32_t dm = km;  // the kept lanes of this item, all on this branch
-      const uint32_t leader = __ffs(dm) - 1;
-      uint32_t b0 = 0;
-      if (lane == leader) b0 = atomicAdd(&state[it].cnt_hi, __popc(dm));
-      b0 = __shfl_sync(dm, b0, leader);
-      const uint32_t slot = b0 + __popc(dm & ((1u << lane) - 1u));
       if (slot < e.hi_cap) hi_pool[e.hi_off + slot] = kv;  // kept <= n - c < hi_cap
     }
   }
@@ -1279,6 +1337,30 @@ __global__ void __launch_bounds__(256) k_ds_place(const EncItem* __restrict__ it
     const uint32_t slot = atomicAdd(&hist[off >> kRegionShift], 1u);
     records[slot] = make_uint2(uint32_t(off), __float_as_uint(x));
   });
+}
+
+// The deferred sketches start at zero: written here, right before the apply
+// (full-sector stores allocate their lines in L2 without a DRAM read), for
+// the items whose select is final (a fallen-back item was re-encoded exactly
+// and scattered directly into its freshly cleared sketch).
+__global__ void __launch_bounds__(256) k_ds_zero(const EncItem* __restrict__ items,
+                                                 const SelState* __restrict__ state, uint32_t n_items,
+                                                 uint32_t rows) {
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint32_t it = 0; it < n_items; ++it) {
+    const EncItem& e = items[it];
+    if (!(e.flags & kDeferScatter) || !(e.flags & kWriteSketch) || state[it].status != kStatusReady) continue;
+    const uint64_t n = uint64_t(rows) * e.m;
+    float* p = e.sketch;
+    const uint64_t mis = ((16u - (reinterpret_cast<uintptr_t>(p) & 15u)) & 15u) / 4u;
+    const uint64_t head = n < mis ? n : mis;
+    for (uint64_t i = tid; i < head; i += stride) p[i] = 0.0f;
+    float4* p4 = reinterpret_cast<float4*>(p + head);
+    const uint64_t n4 = (n - head) / 4;
+    for (uint64_t i = tid; i < n4; i += stride) p4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint64_t i = head + 4 * n4 + tid; i < n; i += stride) p[i] = 0.0f;
+  }
 }
 
 // Records in region order, grid-stride: all CTAs sweep the regions together.
@@ -1741,8 +1823,8 @@ int launch_select_finish(const DevInfo& di, const EncItem* items, SelState* stat
                          uint32_t* fb_hist, uint2* cand, uint2* hi_pool, uint32_t* sel_list,
                          uint32_t* err, cudaStream_t stream) {
   if (n_items == 0) return 0;
-  k_finish_select<<<n_items, 1024, 0, stream>>>(items, state, fine_hist, cand, err);
-  (void)sel_list;
+  k_finish_select<<<dim3(kFinishCtas, n_items), kFinishThreads, 0, stream>>>(items, state, fine_hist, cand,
+                                                                           sel_list, err);
   if (w4) k_fixup<true><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err, hi_pool);
   else k_fixup<false><<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, cand, hp, err, hi_pool);
   // bracket-miss repair: one cooperative launch that exits at once unless some item fell back
@@ -1832,8 +1914,9 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
   k_ds_count<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, region_count);
   k_ds_scan<<<1, 1024, 0, stream>>>(region_count, cursor, n_records);
   k_ds_place<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, cursor, records);
+  k_ds_zero<<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, hp.rows);
   k_ds_apply<<<di.sms * 8, 256, 0, stream>>>(records, n_records, base);
-  return 4;
+  return 5;
 }
 
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream) {
@@ -1890,7 +1973,7 @@ int launch_index_diag(const DiagItem* items, uint32_t n_items, uint32_t max_word
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_encode_kernels() {
-  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_count, (const void*)k_ds_place, (const void*)k_ds_scan, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
+  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_zero, (const void*)k_ds_count, (const void*)k_ds_place, (const void*)k_ds_scan, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

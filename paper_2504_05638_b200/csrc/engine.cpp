@@ -439,7 +439,10 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     e.sample_stride = 0;
     e.sample_tiles = 0;
     if (select && e.n > kSmallSegment) {
-      const uint64_t stride = std::max<uint64_t>(1, std::min<uint64_t>(kSampleMaxStride, t / 16));
+      // at most kSampleMaxTiles chunks per segment (2M samples): beyond that the
+      // sample passes only widen nothing but their own HBM read
+      const uint64_t stride = std::max<uint64_t>(std::max<uint64_t>(1, std::min<uint64_t>(kSampleMaxStride, t / 16)),
+                                                 (t + kSampleMaxTiles - 1) / kSampleMaxTiles);
       e.sample_stride = uint32_t(stride);
       e.sample_tiles = uint32_t((t + stride - 1) / stride);
       samples += e.sample_tiles;
@@ -461,8 +464,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     const float* lo = nullptr;
     const float* hi_end = nullptr;
     auto big = [&](const EncItem& e) {
-      return select && (e.flags & kHasAcc) && (e.flags & kWriteSketch) &&
-             uint64_t(hp.rows) * e.m * 4 > defer_scatter_bytes_;
+      return select && (e.flags & kHasAcc) && (e.flags & kWriteSketch) && big_sketch(uint64_t(hp.rows) * e.m);
     };
     for (const EncItem& e : items)
       if (big(e)) {
@@ -478,6 +480,13 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
           ds_cap += uint64_t(hp.rows) * e.hi_cap;
         }
     }
+    // The exchange prologue leaves big sketches unzeroed (big_sketch): the
+    // deferred ones are zeroed by the deferred scatter right before their
+    // REDs, any others (span too large to defer) now, before the scatter.
+    std::vector<std::pair<void*, uint64_t>> now;
+    for (const EncItem& e : items)
+      if (big(e) && !(e.flags & kDeferScatter)) now.push_back({e.sketch, uint64_t(hp.rows) * e.m * 4});
+    if (!now.empty()) zero(now);
   }
   auto* d_items = static_cast<EncItem*>(desc_buffer("enc_items", n * sizeof(EncItem)));
   upload(items.data(), n * sizeof(EncItem), d_items);
@@ -1058,8 +1067,24 @@ void Engine::exchange_prologue(const std::vector<ShardSpec>& shards, const float
   auto* send_u = user_send_u ? user_send_u : static_cast<uint32_t*>(ws_.get("nc_send_u", W * Bu * 4, false, stream_));
   xs_.send_f = send_f;
   xs_.send_u = send_u;
+  // every owner block's sketches start at zero; big ones (deferred scatter)
+  // are zeroed by the encode itself, just before their REDs
   std::vector<std::pair<void*, uint64_t>> zr;
-  for (uint32_t o = 0; o < W; ++o) zr.push_back({send_f + o * Bf, P.skc[o] * 4});
+  const uint32_t rows = cfg_.sketch_rows;
+  for (uint32_t o = 0; o < W; ++o) {
+    uint64_t run = 0, end = 0;  // current run of small sketches [run, end)
+    for (const SegPlan& p : P.segs) {
+      if (!p.compressed || shards[p.shard].owner != o) continue;
+      const uint64_t sk = uint64_t(rows) * p.m;
+      if (big_sketch(sk)) {
+        if (end > run) zr.push_back({send_f + o * Bf + run, (end - run) * 4});
+        run = end = p.sk_off + align_up(sk, 4);
+      } else {
+        end = p.sk_off + align_up(sk, 4);
+      }
+    }
+    if (end > run) zr.push_back({send_f + o * Bf + run, (end - run) * 4});
+  }
   zero(zr);
   xs_.begun = true;
 }

@@ -328,6 +328,8 @@ class Engine {
   // sketches above this size are scattered by the region-ordered pass
   // (TAGC_DEFER_SCATTER_BYTES; 0 defers every compressed segment's)
   uint64_t defer_scatter_bytes_ = 32ull << 20;
+  // sketches whose scatter is deferred to the region-ordered pass (> 32 MB)
+  bool big_sketch(uint64_t floats) const { return floats * 4 > defer_scatter_bytes_; }
   // counter-mode decode with round 0 inside the dense emit (TAGC_FUSED_EMIT=1; off: 0.68 vs 0.50 ms on C4)
   bool fused_emit_ = false;
   bool side_stream_ = true;  // W = 1 raw copies on the low-priority side stream (TAGC_SIDE_STREAM=0: in order)

@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include <cstdint>
 
 #include "device.cuh"
@@ -73,7 +75,11 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
 // 16 MB region of [base, base + span_floats) (after launch_select_finish).
 // region_count: kMaxRegions (4096) u32, zero on entry (left zero); cursor:
 // 4096 u32; records: 3 x (sum of the items' hi_cap) uint2. Returns -1 when
-// the span is too large (then nothing was launched).
+// the span is too large (then nothing was launched). The deferred sketches
+// (of items whose select did not fall back: the exact re-encode scatters
+// directly) are zeroed here, between the record placement and the apply, so
+// their lines are freshly allocated in L2 when the REDs arrive instead of
+// being read back from DRAM; callers leave them unzeroed.
 int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
                             const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
                             uint32_t* region_count, uint32_t* cursor, uint32_t* n_records, uint2* records,
