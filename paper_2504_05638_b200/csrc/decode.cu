@@ -976,85 +976,190 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
 // entry-centric round above: every entry peels from its lowest singleton
 // slot, exactly the reference's ascending seed order. Generation g+1 is the
 // queue of slots whose count dropped to one while generation g was processed,
-// ordered as the reference's deque orders it: by the processing order of the
-// peeled entry, then by row. Pushes carry that key, the host sorts each
-// generation (cub radix sort), and an entry that is a singleton in several
-// queued slots is peeled from the first of them (epoch-tagged atomicMax
-// claims).
-struct OrdPush {
-  unsigned long long* keys;
-  uint32_t* slots;
-  uint32_t* count;
-  unsigned long long* slot_key;  // per slot: (epoch << 36) | max FIFO key of this generation
-  unsigned long long tag;        // epoch << 36 of the generation doing the subtractions
-};
-constexpr unsigned long long kKeyMask = (1ull << 36) - 1ull;
+// ordered as the reference's deque orders it: by the FIFO position j of the
+// peeled entry, then by row. A slot is queued when the LAST subtraction of
+// the generation (in FIFO order) leaves one entry, so every subtraction
+// atomicMax-es its key j * rows + r into the slot; keys are unique per slot
+// and dense in [0, qlen * rows), so the order is a placement into a dense
+// key array plus an order-preserving compaction — no sort. An entry that is a
+// singleton in several queued slots is peeled from the first of them
+// (epoch-tagged atomicMax claims on ~j).
+//
+// Everything runs in ONE cooperative kernel (k_ord_loop): generation 0's
+// subtraction, then per generation place | count | write + claim | peel,
+// separated by grid barriers; once a generation holds <= kOrdTail slots, CTA
+// 0 finishes alone with block barriers. No host round trip, so the call is
+// graph-capturable like the unordered decode.
+constexpr uint32_t kOrdTail = 2048;
+constexpr uint32_t kOrdWrap = 0xF0000000u;
 
-constexpr uint32_t kOrdStage = 2048;
+__device__ __forceinline__ unsigned long long ord_tag(uint32_t ep, uint64_t key) {
+  return (uint64_t(ep) << 32) | key;
+}
 
-__device__ __forceinline__ void ord_push(bool push, uint32_t slot, unsigned long long* s_k, uint32_t* s_s,
-                                         uint32_t* s_n, const OrdPush& o) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t mask = __ballot_sync(kFull, push);
-  if (!mask) return;
-  const uint32_t leader = __ffs(mask) - 1, cnt = __popc(mask);
-  uint32_t b = 0, direct = 0;
-  if (lane == leader) {
-    b = atomicAdd(s_n, cnt);
-    if (b + cnt > kOrdStage) {
-      if (b < kOrdStage) atomicMin(s_n + 1, b);  // [b, stage) stays unwritten
-      direct = 1;
-      b = atomicAdd(o.count, cnt);
-    }
+template <typename Sync>
+__device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const HashParams& hp, const OrdState& o,
+                                                   uint32_t g, uint32_t n, uint64_t dom, uint32_t ep, uint32_t part,
+                                                   uint32_t nparts, uint32_t* cnt, uint32_t* s_q, uint32_t* s_nq,
+                                                   uint32_t* s_base, uint32_t* s_warp, Sync sync) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t rows = hp.rows;
+  const uint32_t* u = (g & 1) ? o.u1 : o.u0;
+  // A: place every pushed slot at its FIFO key
+  for (uint32_t t = part * blockDim.x + tid; t < n; t += nparts * blockDim.x) {
+    const uint32_t s = ldcg(u + t);
+    o.dense[uint32_t(ldcg(o.slot_key + s))] = s + 1u;
   }
-  b = __shfl_sync(kFull, b, leader);
-  direct = __shfl_sync(kFull, direct, leader);
-  if (push) {
-    const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
-    if (direct) {
-      o.keys[idx] = 0ull;
-      o.slots[idx] = slot;
+  sync();
+  // B: non-empty keys per part (contiguous chunks of 1024-key tiles)
+  const uint64_t tiles = (dom + 1023) / 1024;
+  const uint64_t per = (tiles + nparts - 1) / nparts;
+  const uint64_t lo = min(dom, uint64_t(part) * per * 1024), hi = min(dom, lo + per * 1024);
+  uint32_t c = 0;
+  for (uint64_t k = lo + tid * 4; k < hi; k += blockDim.x * 4) {
+    if (k + 4 <= hi) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(o.dense + k));
+      c += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
     } else {
-      s_k[idx] = 0ull;
-      s_s[idx] = slot;
+      for (uint64_t x = k; x < hi; ++x) c += ldcg(o.dense + x) != 0;
     }
   }
+  c = warp_sum32(c);
+  if (lane == 0) s_warp[wid] = c;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += s_warp[i];
+    o.cta[part] = t;
+  }
+  sync();
+  // C: ordered write of the queue (+ reset of the dense keys, + claims)
+  uint32_t off = 0;
+  for (uint32_t i = tid; i < part; i += blockDim.x) off += ldcg(o.cta + i);
+  off = warp_sum32(off);
+  __syncthreads();
+  if (lane == 0) s_warp[wid] = off;
+  __syncthreads();
+  off = 0;
+  for (uint32_t i = 0; i < blockDim.x / 32; ++i) off += s_warp[i];
+  __syncthreads();
+  for (uint64_t base = lo; base < hi; base += blockDim.x * 4) {
+    const uint64_t k = base + tid * 4;
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (k + 4 <= hi) {
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(o.dense + k));
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      for (uint32_t x = 0; x < 4; ++x) if (k + x < hi) v[x] = ldcg(o.dense + k + x);
+    }
+    const uint32_t mine = (v[0] != 0) + (v[1] != 0) + (v[2] != 0) + (v[3] != 0);
+    // block exclusive scan of mine (thread order = key order)
+    uint32_t incl = mine;
+    _Pragma("unroll") for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, d);
+      if (lane >= uint32_t(d)) incl += y;
+    }
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, total = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+      const uint32_t x = s_warp[i];
+      wbase += i < wid ? x : 0u;
+      total += x;
+    }
+    uint32_t pos = off + wbase + incl - mine;
+    if (mine) {
+      if (k + 4 <= hi) *reinterpret_cast<uint4*>(o.dense + k) = make_uint4(0, 0, 0, 0);
+      else for (uint32_t x = 0; x < 4; ++x) if (k + x < hi) o.dense[k + x] = 0;
+      for (uint32_t x = 0; x < 4; ++x) if (v[x]) {
+        const uint32_t s = v[x] - 1u;
+        o.q[pos] = s;
+        const unsigned long long st = ldcg(w.slot_state + s);
+        if (st_count(st) == 1u) atomicMax(o.claim + st_entry(st), ord_tag(ep, ~pos));
+        ++pos;
+      }
+    }
+    off += total;
+    __syncthreads();
+  }
+  sync();
+  // D: peel the queue; subtractions are tagged with the next epoch
+  uint32_t won = 0;
+  uint32_t* un = (g & 1) ? o.u0 : o.u1;
+  uint32_t* cn = cnt + (g + 1) % 3;
+  for (uint32_t base = part * blockDim.x; base < n; base += nparts * blockDim.x) {
+    const uint32_t j = base + tid;
+    bool win = false;
+    uint32_t slot = 0, i = 0, p = 0;
+    const DecItem* e = w.items;
+    float v = 0.0f;
+    if (j < n) {
+      slot = ldcg(o.q + j);
+      const unsigned long long st = ldcg(w.slot_state + slot);
+      if (st_count(st) == 1u) {
+        i = st_entry(st);
+        win = ldcg(o.claim + i) == ord_tag(ep, ~j);
+        if (win) {
+          p = w.plist[i];
+          e = w.items + w.pitem[i];
+          const uint64_t local = slot - e->slot_base;
+          const uint32_t row = uint32_t(local / e->m);
+          v = canonical(dev_sign(row_coef(hp, row), p) * ldcg(e->sketch + local));  // decode.cpp:110-111
+          w.val[i] = v;
+          red_or_u32(w.bitmap + (i >> 5), 1u << (i & 31));
+          ++won;
+        }
+      }
+    }
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < rows) {
+      bool push = false;
+      uint64_t s = 0;
+      if (win) {
+        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
+        s = e->slot_base + local;
+        if (s != slot) {
+          red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
+          atomicMax(o.slot_key + s, ord_tag(ep + 1, uint64_t(j) * rows + r));
+          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
+          push = st_count(old) == 2u;
+        }
+      }
+      stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, un, cn, lane);
+    }
+  }
+  stage_flush<uint32_t, kPushStage>(s_q, s_nq, s_base, un, cn);
+  return won;
 }
 
-__device__ __forceinline__ void ord_flush(unsigned long long* s_k, uint32_t* s_s, uint32_t* s_n,
-                                          uint32_t* s_b, const OrdPush& o) {
-  __syncthreads();
+__global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams hp, OrdState o) {
+  __shared__ uint32_t s_q[kPushStage];
+  __shared__ uint32_t s_nq[2], s_base, s_warp[8];
   if (threadIdx.x == 0) {
-    const uint32_t n = min(min(s_n[0], kOrdStage), s_n[1]);
-    *s_b = n ? atomicAdd(o.count, n) : 0u;
-    s_n[0] = n;
+    s_nq[0] = 0;
+    s_nq[1] = kPushStage;
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < *s_n; i += blockDim.x) {
-    o.keys[*s_b + i] = s_k[i];
-    o.slots[*s_b + i] = s_s[i];
-  }
-}
-
-// Generation-0 subtraction; pushes are keyed (winner slot, row).
-__global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams hp, OrdPush o) {
-  __shared__ unsigned long long s_k[kOrdStage];
-  __shared__ uint32_t s_s[kOrdStage];
-  __shared__ uint32_t s_n[2], s_b;  // [0] reserved, [1] end of the contiguous written prefix
-  if (threadIdx.x == 0) {
-    s_n[0] = 0;
-    s_n[1] = kOrdStage;
-  }
-  __syncthreads();
+  cg::grid_group grid = cg::this_grid();
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t* cnt = w.qcount + 8;
+  uint32_t ep = ldcg(o.epoch);
+  if (ep >= kOrdWrap) {  // once per 2^32 generations: restart the tags from zero
+    for (uint64_t x = gtid; x < o.slot_key_cap; x += gstride) o.slot_key[x] = 0ull;
+    for (uint64_t x = gtid; x < o.claim_cap; x += gstride) o.claim[x] = 0ull;
+    ep = 0;
+    grid.sync();
+  }
+  ++ep;  // generation 0's subtractions
+  // ---- generation 0: round-0 peeled entries leave every bucket they share;
+  // pushes keyed (winner slot, row) — the reference's ascending seed order
   const uint32_t total = w.qcount[5];
-  for (uint64_t base = start - lane; base < total; base += stride) {
+  for (uint64_t base = gtid - lane; base < total; base += gstride) {
     const uint64_t i = base + lane;
     uint32_t p = 0, rows = 0;
     float v = 0.0f;
-    unsigned long long wkey = 0;
+    uint64_t wkey = 0;
     const DecItem* e = w.items;
     if (i < total) {
       const uint2 info = w.pinfo[i];
@@ -1075,92 +1180,57 @@ __global__ void __launch_bounds__(256) k_r0_push(DecodeWork w, const HashParams 
         const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
         s = e->slot_base + local;
         red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
-        // the reference queues a slot when its LAST subtraction of the
-        // generation (in FIFO order) leaves one position: keep the max key
-        atomicMax(o.slot_key + s, o.tag | (wkey + r));
+        atomicMax(o.slot_key + s, ord_tag(ep, wkey + r));
         const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(uint32_t(i)));
         push = st_count(old) == 2u;
       }
-      ord_push(push, uint32_t(s), s_k, s_s, s_n, o);
+      stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, o.u0, cnt, lane);
     }
   }
-  ord_flush(s_k, s_s, s_n, &s_b, o);
-}
-
-__global__ void __launch_bounds__(256) k_ord_keys(unsigned long long* keys, const uint32_t* slots,
-                                                  uint32_t n, const unsigned long long* slot_key) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    keys[j] = slot_key[slots[j]] & kKeyMask;
-}
-
-__global__ void __launch_bounds__(256) k_ord_claim(DecodeWork w, const uint32_t* __restrict__ q,
-                                                   uint32_t qlen, unsigned long long* claim,
-                                                   uint32_t epoch) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < qlen; j += gridDim.x * blockDim.x) {
-    const unsigned long long st = w.slot_state[q[j]];
-    if (st_count(st) != 1u) continue;
-    atomicMax(claim + st_entry(st), (uint64_t(epoch) << 32) | uint64_t(~j));
-  }
-}
-
-__global__ void __launch_bounds__(256) k_ord_peel(DecodeWork w, const HashParams hp,
-                                                  const uint32_t* __restrict__ q, uint32_t qlen,
-                                                  const unsigned long long* __restrict__ claim,
-                                                  uint32_t epoch, OrdPush o) {
-  __shared__ unsigned long long s_k[kOrdStage];
-  __shared__ uint32_t s_s[kOrdStage];
-  __shared__ uint32_t s_n[2], s_b;  // [0] reserved, [1] end of the contiguous written prefix
-  if (threadIdx.x == 0) {
-    s_n[0] = 0;
-    s_n[1] = kOrdStage;
-  }
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  uint32_t won = 0;
-  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < qlen; base += stride) {
-    const uint32_t j = base + lane;
-    bool win = false;
-    uint32_t slot = 0, i = 0, p = 0;
-    const DecItem* e = w.items;
-    float v = 0.0f;
-    if (j < qlen) {
-      slot = q[j];
-      const unsigned long long st = w.slot_state[slot];
-      if (st_count(st) == 1u) {
-        i = st_entry(st);
-        win = claim[i] == ((uint64_t(epoch) << 32) | uint64_t(~j));
-        if (win) {
-          p = w.plist[i];
-          e = w.items + w.pitem[i];
-          const uint64_t local = slot - e->slot_base;
-          const uint32_t row = uint32_t(local / e->m);
-          v = canonical(dev_sign(row_coef(hp, row), p) * e->sketch[local]);  // decode.cpp:110-111
-          w.val[i] = v;
-          red_or_u32(w.bitmap + (i >> 5), 1u << (i & 31));
-          ++won;
-        }
-      }
+  stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, o.u0, cnt);
+  // ---- generations >= 1
+  uint64_t dom = w.total_slots * hp.rows;
+  uint32_t won = 0, g = 0;
+  bool tail = false;
+  for (;; ++g) {
+    grid.sync();
+    const uint32_t n = ldcg(cnt + g % 3);
+    if (n == 0) break;
+    if (n <= kOrdTail) {  // every CTA sees the same n
+      tail = true;
+      break;
     }
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      bool push = false;
-      uint64_t s = 0;
-      if (win) {
-        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
-        s = e->slot_base + local;
-        if (s != slot) {
-          red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
-          atomicMax(o.slot_key + s, o.tag | (uint64_t(j) * hp.rows + r));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
-          push = st_count(old) == 2u;
-        }
-      }
-      ord_push(push, uint32_t(s), s_k, s_s, s_n, o);
+    if (gtid == 0) {
+      cnt[(g + 2) % 3] = 0;
+      w.qcount[2] += 1;
     }
+    won += ord_generation(w, hp, o, g, n, dom, ep, blockIdx.x, gridDim.x, cnt, s_q, s_nq, &s_base, s_warp,
+                          [&] { grid.sync(); });
+    dom = uint64_t(n) * hp.rows;
+    ++ep;
   }
   won = warp_sum32(won);
   if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
-  ord_flush(s_k, s_s, s_n, &s_b, o);
+  if (blockIdx.x != 0) return;
+  if (tail) {  // ---- one CTA finishes with block barriers
+    won = 0;
+    for (;; ++g) {
+      __syncthreads();
+      const uint32_t n = ldcg(cnt + g % 3);
+      if (n == 0) break;
+      if (threadIdx.x == 0) {
+        cnt[(g + 2) % 3] = 0;
+        w.qcount[3] += 1;
+      }
+      won += ord_generation(w, hp, o, g, n, dom, ep, 0, 1, cnt, s_q, s_nq, &s_base, s_warp,
+                            [] { __syncthreads(); });
+      dom = uint64_t(n) * hp.rows;
+      ++ep;
+    }
+    won = warp_sum32(won);
+    if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  }
+  if (threadIdx.x == 0) *o.epoch = ep;
 }
 
 // ------------------------------------------------------------------ estimate
@@ -1599,50 +1669,28 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   return list_launches + 4;  // list, round 0 (2), peel, final
 }
 
-int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                          const OrderedBuffers& ob, cudaStream_t stream, uint32_t& epoch,
-                          uint32_t* rounds) {
-  if (w.n_items == 0) return 0;
-  int launches = 0;
+int ordered_loop_grid(const DevInfo& di) {
   int per_sm = 0;
-  const int g = build_passes(di, w, hp, stream);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ord_loop, 256, 0);
+  return std::max(per_sm, 1) * di.sms;
+}
+
+int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp, const OrdState& o,
+                          cudaStream_t stream) {
+  if (w.n_items == 0) return 0;
+  build_passes(di, w, hp, stream);
   const int grid = di.sms * 4;
   if (hp.rows == 3) k_r0_phase1_k<3, 2><<<grid, 256, 0, stream>>>(w, hp);
   else k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);
-  ++epoch;
-  OrdPush o{ob.keys[0], ob.slots[0], ob.count, ob.slot_key, uint64_t(epoch) << 36};
-  cudaMemsetAsync(ob.count, 0, 4, stream);
-  k_r0_push<<<grid, 256, 0, stream>>>(w, hp, o);
-  launches += 3;  // list, round 0, push
-  uint32_t gen = 1;
-  unsigned long long* cur_keys = ob.keys[0];
-  uint32_t* cur_slots = ob.slots[0];
-  for (;;) {
-    cudaMemcpyAsync(ob.host_count, ob.count, 4, cudaMemcpyDeviceToHost, stream);
-    cudaStreamSynchronize(stream);
-    const uint32_t cnt = *ob.host_count;
-    if (cnt == 0) break;
-    k_ord_keys<<<grid, 256, 0, stream>>>(cur_keys, cur_slots, cnt, ob.slot_key);
-    cub::DoubleBuffer<unsigned long long> dk(cur_keys, cur_keys == ob.keys[0] ? ob.keys[1] : ob.keys[0]);
-    cub::DoubleBuffer<uint32_t> dv(cur_slots, cur_slots == ob.slots[0] ? ob.slots[1] : ob.slots[0]);
-    size_t tb = ob.scratch_bytes;
-    cub::DeviceRadixSort::SortPairs(ob.scratch, tb, dk, dv, int(cnt), 0, 36, stream);
-    const uint32_t* q = dv.Current();
-    // the next generation's pushes go to the buffers the sort left free
-    ++epoch;
-    OrdPush no{dk.Alternate(), dv.Alternate(), ob.count, ob.slot_key, uint64_t(epoch) << 36};
-    k_ord_claim<<<grid, 256, 0, stream>>>(w, q, cnt, ob.claim, epoch);
-    cudaMemsetAsync(ob.count, 0, 4, stream);
-    k_ord_peel<<<grid, 256, 0, stream>>>(w, hp, q, cnt, ob.claim, epoch, no);
-    cur_keys = dk.Alternate();
-    cur_slots = dv.Alternate();
-    launches += 4;
-    ++gen;
-  }
-  if (rounds) *rounds = gen;
+  DecodeWork wa = w;
+  HashParams ha = hp;
+  OrdState oa = o;
+  void* args[] = {&wa, &ha, &oa};
+  cudaLaunchCooperativeKernel((const void*)k_ord_loop, dim3(ordered_loop_grid(di)), dim3(256), args, 0, stream);
+  int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return launches + 2;
+  return (w.cnt8 ? 3 : 1) + 3;  // build, round 0, loop, estimate
 }
 
 int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream, const OptEpilogue* dev_opt) {
@@ -1656,14 +1704,6 @@ int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stre
     k_emit<false><<<int(g), 256, kEmitSmem, stream>>>(w, nullptr);
   }
   return 1;
-}
-
-size_t ordered_sort_scratch_bytes(uint32_t count) {
-  size_t temp = 0;
-  cub::DoubleBuffer<unsigned long long> dk(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> dv(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, int(count), 0, 64);
-  return temp;
 }
 
 int launch_presence_to_bitmap(const uint32_t* presence, uint32_t count, uint32_t n,
@@ -1724,7 +1764,7 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_decode_kernels() {
-  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_claim, (const void*)k_ord_keys, (const void*)k_ord_peel, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_push, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

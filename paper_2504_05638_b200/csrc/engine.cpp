@@ -203,7 +203,6 @@ Engine::~Engine() {
     for (cudaEvent_t e : {hev_in_[i], hev_gfree_[i], hev_dec_[i], hev_out_[i]})
       if (e) cudaEventDestroy(e);
   if (hev_join_) cudaEventDestroy(hev_join_);
-  if (ord_host_count_) cudaFreeHost(ord_host_count_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
   if (aux_) {
@@ -374,8 +373,8 @@ void Engine::fetch_rounds() {
   uint32_t q[4] = {0, 0, 0, 0};
   cuda_check(cudaMemcpyAsync(q, ws_.get("qcount", 16), 16, cudaMemcpyDeviceToHost, stream_), "D2H q");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
-  rounds_[0] = last_ordered_ ? ordered_gens_ : q[2];
-  rounds_[1] = last_ordered_ ? 0 : q[3];
+  rounds_[0] = q[2];
+  rounds_[1] = q[3];
 }
 
 // Index::to_bytes / CountSketch::to_bytes (index.cpp:59-69, sketch.cpp:77-89)
@@ -669,22 +668,19 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   if (ordered) {
     // 1-bit merged index over several ranks: carries can hide positions whose
     // mass stays in the sketch, so values follow the reference's FIFO order
-    OrderedBuffers ob{};
-    ob.keys[0] = static_cast<unsigned long long*>(ws_.get("ord_k0", slots * 8, false, stream_));
-    ob.keys[1] = static_cast<unsigned long long*>(ws_.get("ord_k1", slots * 8, false, stream_));
-    ob.slots[0] = static_cast<uint32_t*>(ws_.get("ord_s0", slots * 4, false, stream_));
-    ob.slots[1] = static_cast<uint32_t*>(ws_.get("ord_s1", slots * 4, false, stream_));
-    ob.count = static_cast<uint32_t*>(ws_.get("ord_count", 16, false, stream_));
-    if (!ord_host_count_)
-      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ord_host_count_), 64, cudaHostAllocDefault), "pinned");
-    ob.host_count = ord_host_count_;
-    ob.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", list * 8, true, stream_));
-    ob.slot_key = static_cast<unsigned long long*>(ws_.get("ord_slot_key", slots * 8, true, stream_));
-    ob.scratch_bytes = ordered_sort_scratch_bytes(uint32_t(std::min<uint64_t>(slots, 0x7FFFFFFF)));
-    ob.scratch = ws_.get("ord_scratch", ob.scratch_bytes, false, stream_);
-    uint32_t gens = 0;
-    launches_ += launch_decode_ordered(di_, w, hp, ob, stream_, epoch_, &gens);
-    ordered_gens_ = gens;
+    if (slots * hp.rows >= (1ull << 32)) throw CudaError("ordered decode batch exceeds 2^32 FIFO keys");
+    OrdState o{};
+    o.slot_key_cap = slots;
+    o.claim_cap = list;
+    o.slot_key = static_cast<unsigned long long*>(ws_.get("ord_slot_key", slots * 8, true, stream_));
+    o.claim = static_cast<unsigned long long*>(ws_.get("ord_claim", list * 8, true, stream_));
+    o.dense = static_cast<uint32_t*>(ws_.get("ord_dense", (slots * hp.rows + 4) * 4, true, stream_));
+    o.q = static_cast<uint32_t*>(ws_.get("ord_q", slots * 4, false, stream_));
+    o.u0 = static_cast<uint32_t*>(ws_.get("ord_u0", slots * 4, false, stream_));
+    o.u1 = static_cast<uint32_t*>(ws_.get("ord_u1", slots * 4, false, stream_));
+    o.cta = static_cast<uint32_t*>(ws_.get("ord_cta", size_t(ordered_loop_grid(di_)) * 4, false, stream_));
+    o.epoch = static_cast<uint32_t*>(ws_.get("ord_epoch", 16, true, stream_));  // fixed size: never regrown
+    launches_ += launch_decode_ordered(di_, w, hp, o, stream_);
   } else {
     launches_ += launch_decode(di_, w, hp, stream_, fused);
   }
@@ -937,8 +933,8 @@ void Engine::reduce_shards(const std::vector<ShardSpec>& shards, const float* gr
     throw InvalidArgument("multi-rank context has no NCCL communicator or peer exchange");
   static const bool peel_dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   const bool legacy = stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread;
-  const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy &&  // default streams cannot be captured
-                        !(cfg_.index_width == 1 && world_ > 1);  // the ordered peel loops on the host
+  // default streams cannot be captured
+  const bool eligible = graphs_on_ && !stats && !timing_ && !peel_dbg && !legacy;
   if (!eligible) {
     enqueue_reduce_shards(shards, grad, acc, out, stats);
     return;

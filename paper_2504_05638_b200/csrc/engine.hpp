@@ -255,7 +255,6 @@ class Engine {
     std::vector<void*> opened;
   };
   PeerState peer_;
-  uint32_t* ord_host_count_ = nullptr;  // pinned read-back of the ordered peel's generation size
   void peer_release();
   void peer_fill(const std::vector<char*>& bases);
   struct LedgerEntry {
@@ -352,8 +351,6 @@ class Engine {
   // host mirrors of the last decode's per-item stats (device -> host)
   std::vector<DecStats> dec_stats_;
   uint32_t rounds_[2] = {0, 0};
-  uint32_t epoch_ = 0;         // ordered-peel claim epochs (monotonic per context)
-  uint32_t ordered_gens_ = 0;  // generations of the last ordered peel
   bool last_ordered_ = false;
   void fetch_rounds();
 };

@@ -194,23 +194,26 @@ int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stre
 // Writes the step's OptEpilogue into its device slot (stream-ordered before
 // the kernels that read it; launched outside any graph).
 int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream);
-// FIFO-order peel (see decode.cu): host-driven generations, one sort each.
-// claim: u64 per presence-list entry, zero-initialised once;
-// epoch is advanced per generation and persists across calls.
-struct OrderedBuffers {
-  unsigned long long* keys[2];
-  uint32_t* slots[2];  // capacity total_slots each
-  uint32_t* count;
-  uint32_t* host_count;       // page-locked read-back slot (a pageable read-back blocks other threads)
-  unsigned long long* claim;  // per presence-list entry
-  unsigned long long* slot_key;  // u64 per slot, zero-initialised once
-  void* scratch;
-  size_t scratch_bytes;
+// FIFO-order peel (see decode.cu): every generation on the device, inside
+// one cooperative persistent kernel (no host round trip, graph-capturable).
+// slot_key / claim are epoch-tagged, zero-initialised once; epoch is a
+// persistent device word (never reallocated) advanced per generation;
+// dense holds one u32 per FIFO key (total_slots * rows, zero-initialised
+// once, restored to zero by every compaction).
+struct OrdState {
+  unsigned long long* slot_key;  // per slot: (epoch << 32) | FIFO key of its last subtraction
+  unsigned long long* claim;     // per presence-list entry: (epoch << 32) | ~queue position
+  uint32_t* dense;               // per FIFO key: slot + 1, 0 = empty
+  uint32_t* q;                   // the generation's queue in FIFO order
+  uint32_t* u0;                  // unordered pushes, even generations
+  uint32_t* u1;                  // unordered pushes, odd generations
+  uint32_t* cta;                 // per-CTA counts of the compaction
+  uint32_t* epoch;               // persistent device epoch
+  uint64_t slot_key_cap, claim_cap;  // allocated elements (cleared on epoch wrap)
 };
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                          const OrderedBuffers& ob, cudaStream_t stream, uint32_t& epoch,
-                          uint32_t* rounds);
-size_t ordered_sort_scratch_bytes(uint32_t count);
+                          const OrdState& o, cudaStream_t stream);
+int ordered_loop_grid(const DevInfo& di);
 
 // Presence list -> bitmap (width-1 index) with bounds/duplicate checks for the
 // standalone peeling API (decode.cpp:15-20, :89-94). err bit 1 = OOB, 2 = dup.
