@@ -807,86 +807,127 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
 }
 
 // ------------------------------------------------------------------ frontier
-// Rounds >= 1, single-phase over the frontier: a slot holding exactly one
-// entry i (decode.cpp:104-106) claims i (an entry reachable through several
-// singleton slots is claimed once), reads value = sign * residual into val[i]
-// and removes i from its other buckets, pushing buckets whose count drops to
-// one onto the next frontier. Claims, reads and subtractions of one round run
-// concurrently: a remover updates the residual before it decrements the
-// count (fence in between) and a reader acquires the count before it reads
-// the residual, so a bucket seen holding one entry shows exactly that entry's
-// residual. The peeled set is the complement of the 2-core either way
+// Rounds >= 1 in ONE cooperative persistent kernel. A slot holding exactly
+// one entry i (decode.cpp:104-106) claims i (an entry reachable through
+// several singleton slots is claimed once: atomicOr on its recovered bit),
+// reads value = sign * residual into val[i] and removes i from its other
+// buckets; a bucket whose count drops to one is pushed for the next round
+// together with its remaining entry, which the decrement's returned state
+// names exactly (count 1: the low bits of the index sum).
+//
+// Per round the dependent chain is two L2 round trips: {claim, position,
+// residual} then {residual REDs, count decrements}. No state re-read: a
+// pushed (slot, entry) pair is stale only if entry was peeled elsewhere,
+// which the claim detects. No fence between a removal's residual update and
+// its count decrement: within a round a claimed slot's residual can only be
+// changed by the removal of its own single entry, and rounds are separated
+// by a barrier. The next frontier stays in the pushing CTA's shared memory
+// (global overflow beyond kLocalQ); the grid barrier is one atomic per CTA
+// that also sums the CTAs' push counts, so no CTA reads a global counter.
+// Once a round's frontier is small, CTA 0 finishes alone with block
+// barriers. The peeled set is the complement of the 2-core either way
 // (order-independent); values match the reference's FIFO peel within fp32
 // reassociation.
-__device__ __forceinline__ uint32_t frontier_pass(const DecodeWork& w, const HashParams& hp,
-                                                  const SlotItems& si, const uint32_t* q, uint32_t total,
-                                                  uint64_t start, uint64_t stride, uint32_t* s_q,
-                                                  uint32_t* s_nq, uint32_t* nq, uint32_t* ncount) {
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t won = 0;
-  for (uint64_t base = start - lane; base < total; base += stride) {
-    const uint64_t j = base + lane;
-    bool win = false;
-    uint32_t i = 0, p = 0, row = 0;
-    float v = 0.0f;
-    const DecItem* e = w.items;
-    if (j < total) {
-      const uint32_t slot = ldcg(q + j);
-      const unsigned long long st = ld_acquire(w.slot_state + slot);
-      if (st_count(st) == 1u) {
-        i = st_entry(st);
-        // the entry's position and the bucket's residual are read before the
-        // claim resolves (the count was acquired: the residual is the single
-        // entry's); a lost claim just discards them - one L2 round trip less
-        // on the round's dependency chain
-        e = w.items + si.find(slot);
-        const uint64_t local = slot - e->slot_base;
-        const uint32_t pp = __ldg(w.plist + i);
-        const float resid = ldcg(e->sketch + local);
-        const uint32_t bit = 1u << (i & 31);
-        if (!(atomicOr(w.bitmap + (i >> 5), bit) & bit)) {
-          win = true;
-          p = pp;
-          row = slot_row(local, e->m);
-          float sg = 0.0f;
-          _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
-          v = canonical(sg * resid);
-          w.val[i] = v;
-        }
-      }
-    }
-    if (win) {
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && r != row)
-        red_add_f32(e->sketch + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul), -(dev_sign(hp.row[r], p) * v));
-      __threadfence();  // residual updates before the count decrements
-      ++won;
-    }
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      bool push = false;
-      uint64_t s = 0;
-      if (win && r != row) {
-        s = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
-        const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
-        push = st_count(old) == 2u;
-      }
-      stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, nq, ncount, lane);
-    }
+constexpr uint32_t kLocalQ = 2048;  // (slot, entry) pairs per CTA and round
+
+__device__ __forceinline__ void local_push(bool push, uint32_t slot, uint32_t entry, uint2* s_next,
+                                           uint32_t* s_nn, uint32_t* gq, uint32_t* gcount, uint32_t lane) {
+  const uint32_t mask = __ballot_sync(kFull, push);
+  if (!mask) return;
+  const uint32_t leader = __ffs(mask) - 1;
+  uint32_t b = 0;
+  if (lane == leader) b = atomicAdd(s_nn, uint32_t(__popc(mask)));
+  b = __shfl_sync(kFull, b, leader);
+  if (push) {
+    const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
+    if (idx < kLocalQ) s_next[idx] = make_uint2(slot, entry);
+    else gq[atomicAdd(gcount, 1u)] = slot;  // overflow: re-read its state next round
   }
-  return won;
 }
 
-// Frontier counters rotate over three words (qcount[8..10]): round k reads
-// counter k%3, pushes into (k+1)%3, and thread 0 clears (k+2)%3, which no
-// thread touches during round k. Queue buffers alternate. Round 0 (k = 0)
-// was k_r0_phase1 / k_r0_subtract, which left round 1's frontier in queue 1
-// / qcount[9].
-__global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams hp) {
-  __shared__ uint32_t s_q[kPushStage];
-  __shared__ unsigned long long s_sbase[kPeelItemsSmem];
-  __shared__ uint32_t s_nq[2], s_base;
+// One frontier element per lane. kPair: (slot, entry) from a local queue;
+// otherwise a slot from a global queue (its state names the entry).
+template <bool kPair>
+__device__ __forceinline__ uint32_t peel_one(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
+                                             bool have, uint32_t slot, uint32_t i, uint2* s_next, uint32_t* s_nn,
+                                             uint32_t* gq, uint32_t* gcount, uint32_t lane) {
+  if (!kPair && have) {
+    const unsigned long long st = ldcg(w.slot_state + slot);
+    have = st_count(st) == 1u;
+    i = st_entry(st);
+  }
+  bool win = false;
+  uint32_t p = 0, row = 0;
+  float v = 0.0f;
+  const DecItem* e = w.items;
+  if (have) {
+    e = w.items + si.find(slot);
+    const uint64_t local = slot - e->slot_base;
+    const uint32_t pp = __ldg(w.plist + i);
+    const float resid = ldcg(e->sketch + local);
+    const uint32_t bit = 1u << (i & 31);
+    if (!(atomicOr(w.bitmap + (i >> 5), bit) & bit)) {
+      win = true;
+      p = pp;
+      row = slot_row(local, e->m);
+      float sg = 0.0f;
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
+      v = canonical(sg * resid);
+      w.val[i] = v;
+    }
+  }
+  unsigned long long old[kMaxRows];
+  uint32_t sl[kMaxRows];
+  _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+    old[r] = 0ull;
+    sl[r] = 0u;
+    if (win && r != row) {
+      const uint64_t loc = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
+      sl[r] = uint32_t(e->slot_base + loc);
+      red_add_f32(e->sketch + loc, -(dev_sign(hp.row[r], p) * v));
+      old[r] = atomicAdd(w.slot_state + e->slot_base + loc, st_sub(i));
+    }
+  }
+  _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
+    const bool push = win && r != row && st_count(old[r]) == 2u;
+    local_push(push, sl[r], st_entry(old[r] + st_sub(i)), s_next, s_nn, gq, gcount, lane);
+  }
+  return win ? 1u : 0u;
+}
+
+// Grid barrier that also sums a per-CTA value: barrier k adds
+// (1 << 40 | add) into word k % 3 and waits for every CTA's arrival; the
+// word of barrier k - 1 is free again once barrier k has passed (each CTA
+// read it before arriving at k), so CTA 0 clears it for barrier k + 2.
+__device__ __forceinline__ uint32_t grid_barrier_sum(unsigned long long* bar, uint32_t k, uint32_t add,
+                                                     uint32_t* s_out) {
+  __syncthreads();
   if (threadIdx.x == 0) {
+    unsigned long long* word = bar + k % 3;
+    __threadfence();
+    atomicAdd(word, (1ull << 40) | uint64_t(add));
+    const unsigned long long target = uint64_t(gridDim.x) << 40;
+    unsigned long long v;
+    do {
+      v = ld_acquire(word);
+    } while (v < target);
+    __threadfence();
+    *s_out = uint32_t(v & ((1ull << 40) - 1ull));
+    if (blockIdx.x == 0) bar[(k + 2) % 3] = 0ull;
+  }
+  __syncthreads();
+  return *s_out;
+}
+
+__global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams hp) {
+  __shared__ uint2 s_lq[2][kLocalQ];
+  __shared__ uint32_t s_q[kPushStage / 4];
+  __shared__ unsigned long long s_sbase[kPeelItemsSmem];
+  __shared__ uint32_t s_ln[2], s_nq[2], s_base, s_total;
+  if (threadIdx.x == 0) {
+    s_ln[0] = s_ln[1] = 0;
     s_nq[0] = 0;
-    s_nq[1] = kPushStage;
+    s_nq[1] = kPushStage / 4;
   }
   const bool cache = w.n_items <= kPeelItemsSmem;
   if (cache)
@@ -894,6 +935,7 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
   __syncthreads();
   const SlotItems si{cache ? s_sbase : nullptr, w.items, w.n_items};
   cg::grid_group grid = cg::this_grid();
+  const uint32_t lane = threadIdx.x & 31;
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
   uint32_t* cnt = w.qcount + 8;
@@ -904,7 +946,6 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
   PEEL_MARK(mk++);
   if (gtid == 0) w.qcount[2] = 1;
   if (w.cnt8) {  // counter mode: round 1's frontier = the unresolved entries' single-entry buckets
-    const uint32_t lane = threadIdx.x & 31;
     const uint32_t nu = ldcg(&w.qcount[14]);
     for (uint64_t base = gtid - lane; base < nu; base += gstride) {
       const uint64_t j = base + lane;
@@ -922,48 +963,85 @@ __global__ void __launch_bounds__(256, 3) k_peel(DecodeWork w, const HashParams 
           sl = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
           push = st_count(ldcg(w.slot_state + sl)) == 1u;  // one entry: pushed by that entry only
         }
-        stage_push<uint32_t, kPushStage>(push, uint32_t(sl), s_q, s_nq, qbuf1, &cnt[1], lane);
+        stage_push<uint32_t, kPushStage / 4>(push, uint32_t(sl), s_q, s_nq, qbuf1, &cnt[1], lane);
       }
     }
-    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf1, &cnt[1]);
+    stage_flush<uint32_t, kPushStage / 4>(s_q, s_nq, &s_base, qbuf1, &cnt[1]);
     grid.sync();
   }
+  // round k reads the local queue s_lq[k & 1] and the global overflow
+  // qbuf(k) / cnt[k % 3]; it pushes into s_lq[(k + 1) & 1] / qbuf(k + 1)
   uint32_t won = 0, k = 1;
-  bool tail = false;
-  for (;; ++k) {
-    if (k > 1) grid.sync();
-    PEEL_MARK(mk++);
-    const uint32_t qlen = ldcg(&cnt[k % 3]);
-    if (qlen == 0) break;
-    if (qlen <= kTail) {  // every CTA sees the same qlen
-      tail = true;
-      break;
+  bool tail = ldcg(&cnt[1]) <= kTail;
+  if (!tail) {
+    for (;; ++k) {
+      if (gtid == 0) cnt[(k + 2) % 3] = 0;
+      const uint32_t nl = min(s_ln[k & 1], kLocalQ);
+      const uint32_t ng = ldcg(&cnt[k % 3]);
+      uint2* nxt = s_lq[(k + 1) & 1];
+      uint32_t* nn = &s_ln[(k + 1) & 1];
+      for (uint32_t b = 0; b < nl; b += blockDim.x) {
+        const uint32_t j = b + threadIdx.x;
+        const uint2 e = j < nl ? s_lq[k & 1][j] : make_uint2(0, 0);
+        won += peel_one<true>(w, hp, si, j < nl, e.x, e.y, nxt, nn, qbuf(k + 1), &cnt[(k + 1) % 3], lane);
+      }
+      for (uint64_t b = gtid - lane; b < ng; b += gstride) {
+        const uint64_t j = b + lane;
+        won += peel_one<false>(w, hp, si, j < ng, j < ng ? ldcg(qbuf(k) + j) : 0u, 0u, nxt, nn, qbuf(k + 1),
+                               &cnt[(k + 1) % 3], lane);
+      }
+      __syncthreads();
+      const uint32_t total = grid_barrier_sum(w.bar, k, *nn, &s_total);
+      PEEL_MARK(mk++);
+      if (threadIdx.x == 0) s_ln[k & 1] = 0;  // read by every thread before the barrier
+      if (gtid == 0) w.qcount[2] += 1;
+      if (total == 0) break;
+      if (total <= kTail) {  // hand the frontier to CTA 0: local queues join the global overflow
+        const uint32_t n = min(*nn, kLocalQ);
+        if (threadIdx.x == 0) s_base = n ? atomicAdd(&cnt[(k + 1) % 3], n) : 0u;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) qbuf(k + 1)[s_base + j] = nxt[j].x;
+        if (threadIdx.x == 0) *nn = 0;
+        grid_barrier_sum(w.bar, k + 1, 0, &s_total);
+        ++k;
+        tail = true;
+        break;
+      }
+      __syncthreads();
     }
-    if (gtid == 0) {
-      cnt[(k + 2) % 3] = 0;
-      w.qcount[2] += 1;
-    }
-    won += frontier_pass(w, hp, si, qbuf(k), qlen, gtid, gstride, s_q, s_nq, qbuf(k + 1), &cnt[(k + 1) % 3]);
-    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf(k + 1), &cnt[(k + 1) % 3]);
+  } else {
+    k = 1;
   }
   won = warp_sum32(won);
-  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
   if (!tail || blockIdx.x != 0) return;
-  // ---- tail: one CTA finishes with block barriers
+  // ---- tail: one CTA finishes with block barriers; round k's global part
+  // is qbuf(k) / cnt[k % 3] (the handed-over frontier), later rounds local
   won = 0;
   for (;; ++k) {
+    if (threadIdx.x == 0) cnt[(k + 2) % 3] = 0;
+    const uint32_t nl = min(s_ln[k & 1], kLocalQ);
+    const uint32_t ng = ldcg(&cnt[k % 3]);
+    uint2* nxt = s_lq[(k + 1) & 1];
+    uint32_t* nn = &s_ln[(k + 1) & 1];
+    if (nl == 0 && ng == 0) break;
+    for (uint32_t b = 0; b < nl; b += blockDim.x) {
+      const uint32_t j = b + threadIdx.x;
+      const uint2 e = j < nl ? s_lq[k & 1][j] : make_uint2(0, 0);
+      won += peel_one<true>(w, hp, si, j < nl, e.x, e.y, nxt, nn, qbuf(k + 1), &cnt[(k + 1) % 3], lane);
+    }
+    for (uint32_t b = threadIdx.x - lane; b < ng; b += blockDim.x) {
+      const uint32_t j = b + lane;
+      won += peel_one<false>(w, hp, si, j < ng, j < ng ? ldcg(qbuf(k) + j) : 0u, 0u, nxt, nn, qbuf(k + 1),
+                             &cnt[(k + 1) % 3], lane);
+    }
     __syncthreads();
-    const uint32_t qlen = ldcg(&cnt[k % 3]);
-    if (qlen == 0) break;
     if (threadIdx.x == 0) {
-      cnt[(k + 2) % 3] = 0;
+      s_ln[k & 1] = 0;
       w.qcount[3] += 1;
     }
-    won += frontier_pass(w, hp, si, qbuf(k), qlen, threadIdx.x, blockDim.x, s_q, s_nq, qbuf(k + 1),
-                         &cnt[(k + 1) % 3]);
-    stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, qbuf(k + 1), &cnt[(k + 1) % 3]);
-    __threadfence();
     PEEL_MARK(mk++);
+    __syncthreads();
   }
   won = warp_sum32(won);
   if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);

@@ -636,6 +636,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
   w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 64, false, stream_));
+  w.bar = static_cast<unsigned long long*>(ws_.get("peel_bar", 32, false, stream_));
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", (stats_base + n) * sizeof(DecStats), false, stream_)) +
             stats_base;
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
@@ -654,7 +655,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   const bool fused = counters && !ordered && !opt_on_ && fused_emit_;
   w.cnt8 = counters ? static_cast<uint32_t*>(ws_.get("cnt8", cnt_words * 4, false, stream_)) : nullptr;
   w.ulist = counters ? static_cast<uint32_t*>(ws_.get("ulist", list * 4 + 4, false, stream_)) : nullptr;
-  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.stats, n * sizeof(DecStats)},
+  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
         {w.slot_mark, w.slot_mark ? mark_words * 4 : 0},
         {counters ? static_cast<void*>(w.cnt8) : static_cast<void*>(w.slot_state), counters ? cnt_words * 4 : slots * 8},
         {w.tile_state, wt * 8}});  // one launch for every decode scratch reset

@@ -172,6 +172,7 @@ struct DecodeWork {
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
+  unsigned long long* bar;         // k_peel's grid barrier words [3] (zeroed per call)
   unsigned long long* span;        // optional: execution span of build .. final (timing mode)
 };
 // Presence list + bucket state from the merged index, round-0 peel, frontier
