@@ -18,6 +18,7 @@
 // runs instead (kernels launched unconditionally, early-exiting per item).
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -1243,103 +1244,171 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 // Items whose sketch is far bigger than L2 (kDeferScatter) skip the sketch
 // REDs in the fused pass and in k_fixup: every kept entry (pos, v) is logged
 // in the item's hi_pool instead. Once tau is final, the (entry, row) updates
-// are bucketed by 16 MB region of the sketch address space (a counting sort)
-// and applied region by region, so the REDs hit L2 instead of
-// read-modify-writing random DRAM sectors. Same sums as the direct scatter;
-// only the float summation order differs, as it does between any two runs
-// of the direct scatter.
-constexpr uint32_t kRegionShift = 22;  // 4M floats = 16 MB per region
-constexpr uint32_t kMaxRegions = 4096;
+// are binned by region of the sketch address space and applied region by
+// region.
+//  * k_ds_place: each CTA stages a batch of updates in shared memory, sorts
+//    it by bin there (counting sort) and writes every bin's run contiguously
+//    into that bin's fixed-capacity slice (bins are hash-uniform: capacity =
+//    mean * 17/16 + 1024, the excess goes to an overflow list). No count
+//    pass, no global scan, coalesced runs instead of 8-byte scatters.
+//  * spans up to 2^26 floats (256 MB): k_ds_apply_smem sums each 32K-float
+//    region in shared memory (the CTAs of a bin read the bin's run, L2
+//    resident, and keep their region's updates) and stores it with plain
+//    coalesced stores over the deferred sketches' part of the region — no
+//    zeroing pass, no L2 atomics. Larger spans: zeroing pass + L2 REDs bin by
+//    bin (k_ds_apply).
+//  * k_ds_overflow adds the overflow list with REDs, after the apply.
+// Same sums as the direct scatter; only the float summation order differs,
+// as it does between any two runs of the direct scatter.
+constexpr uint32_t kApplyShift = 15;  // 32K floats = 128 KB per shared-memory region
+constexpr uint32_t kApplyRegion = 1u << kApplyShift;
+constexpr uint32_t kDsBatch = 8192;   // staged updates per place batch
+constexpr uint32_t kDsThreads = 512;
+using BlockScanDs = cub::BlockScan<uint32_t, kDsThreads>;
 
 __device__ __forceinline__ uint32_t ds_entries(const EncItem& e, const SelState& st) {
   return (st.status == kStatusReady && (e.flags & kDeferScatter) && (e.flags & kWriteSketch))
              ? min(st.cnt_hi, e.hi_cap) : 0u;
 }
 
-// Per-CTA contiguous range of the flattened entries; every CTA reserves
-// its region slices with one atomic per region, then places its records.
-__global__ void __launch_bounds__(256) k_ds_count(const EncItem* __restrict__ items,
-                                                  const SelState* __restrict__ state, uint32_t n_items,
-                                                  const uint2* __restrict__ hi_pool, const HashParams hp,
-                                                  const float* base, uint32_t* __restrict__ region_count) {
-  __shared__ uint32_t pref[kMaxFlatItems + 1];
-  __shared__ uint32_t hist[kMaxRegions];
-  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x) hist[i] = 0;
-  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i]); }, pref);
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
-    const uint32_t it = flat_item(pref, n_items, j);
-    const EncItem& e = items[it];
-    const uint32_t p = hi_pool[e.hi_off + (j - pref[it])].x;
-    const uint64_t sk = uint64_t(e.sketch - base);
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-      const uint64_t off = sk + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
-      atomicAdd(&hist[off >> kRegionShift], 1u);
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x)
-    if (hist[i]) atomicAdd(region_count + i, hist[i]);
+__device__ __forceinline__ uint32_t ds_cap(uint32_t total_updates, uint32_t n_bins) {
+  const uint64_t mean = (uint64_t(total_updates) + n_bins - 1) / n_bins;
+  return uint32_t(mean + mean / 16 + 1024);
 }
 
-// Exclusive scan of the region counts into cursors (one CTA); counts are
-// left zeroed for the next call.
-__global__ void __launch_bounds__(1024) k_ds_scan(uint32_t* __restrict__ region_count,
-                                                  uint32_t* __restrict__ cursor, uint32_t* __restrict__ n_records) {
-  using Scan = cub::BlockScan<uint32_t, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  constexpr int kPer = kMaxRegions / 1024;
-  uint32_t v[kPer], sum = 0;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    v[k] = region_count[threadIdx.x * kPer + k];
-    region_count[threadIdx.x * kPer + k] = 0;
-    sum += v[k];
-  }
-  uint32_t off, total;
-  Scan(tmp).ExclusiveSum(sum, off, total);
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    cursor[threadIdx.x * kPer + k] = off;
-    off += v[k];
-  }
-  if (threadIdx.x == 0) *n_records = total;
-}
-
-__global__ void __launch_bounds__(256) k_ds_place(const EncItem* __restrict__ items,
-                                                  const SelState* __restrict__ state, uint32_t n_items,
-                                                  const uint2* __restrict__ hi_pool, const HashParams hp,
-                                                  const float* base, uint32_t* __restrict__ cursor,
-                                                  uint2* __restrict__ records) {
+// fill[n_bins] (zero on entry) counts each bin's updates; records hold bin b
+// at [b * cap, b * cap + min(fill[b], cap)); ctl[0] = overflow count,
+// ctl[1] = cap.
+__global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restrict__ items,
+                                                         const SelState* __restrict__ state, uint32_t n_items,
+                                                         const uint2* __restrict__ hi_pool, const HashParams hp,
+                                                         const float* base, uint32_t shift, uint32_t n_bins,
+                                                         uint32_t* __restrict__ fill, uint32_t* __restrict__ ctl,
+                                                         uint2* __restrict__ records, uint2* __restrict__ ovf) {
   __shared__ uint32_t pref[kMaxFlatItems + 1];
-  __shared__ uint32_t hist[kMaxRegions];
-  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x) hist[i] = 0;
+  __shared__ typename BlockScanDs::TempStorage s_scan;
+  extern __shared__ uint2 s_dyn[];
+  uint2* s_u = s_dyn;               // unsorted batch
+  uint2* s_s = s_dyn + kDsBatch;    // sorted batch
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn + 2 * kDsBatch);  // [n_bins]: count, then cursor
+  uint32_t* s_loff = s_hist + n_bins;                                     // [n_bins]: local offset
+  uint32_t* s_gb = s_loff + n_bins;                                       // [n_bins]: global base
+  const uint32_t rows = hp.rows;
   const uint32_t total = flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i]); }, pref);
-  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint32_t j0 = min(total, blockIdx.x * per), j1 = min(total, j0 + per);
-  auto each = [&](auto&& f) {
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-      const uint32_t it = flat_item(pref, n_items, j);
-      const EncItem& e = items[it];
-      const uint2 kv = hi_pool[e.hi_off + (j - pref[it])];
-      const uint64_t sk = uint64_t(e.sketch - base);
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-        const uint64_t off = sk + uint64_t(r) * e.m + dev_bucket(hp.row[r], kv.x, e.m, e.mmul);
-        f(off, dev_sign(hp.row[r], kv.x) * __uint_as_float(kv.y));
+  const uint32_t cap = ds_cap(total * rows, n_bins);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl[1] = cap;
+  const uint32_t per_batch = kDsBatch / rows;
+  const uint32_t per_cta = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t j0 = min(total, blockIdx.x * per_cta), j1 = min(total, j0 + per_cta);
+  for (uint32_t b0 = j0; b0 < j1; b0 += per_batch) {
+    const uint32_t b1 = min(j1, b0 + per_batch);
+    const uint32_t nrec = (b1 - b0) * rows;
+    for (uint32_t i = threadIdx.x; i < n_bins; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    // every thread's entries loaded before any is hashed (memory-level parallelism)
+    constexpr uint32_t kPer = (kDsBatch + kDsThreads - 1) / kDsThreads;
+    uint2 kv[kPer];
+    uint32_t kit[kPer];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t j = b0 + q * blockDim.x + threadIdx.x;
+      kit[q] = 0;
+      kv[q] = make_uint2(0, 0);
+      if (j < b1) {
+        kit[q] = flat_item(pref, n_items, j);
+        kv[q] = __ldcs(hi_pool + items[kit[q]].hi_off + (j - pref[kit[q]]));
       }
     }
-  };
-  each([&](uint64_t off, float) { atomicAdd(&hist[off >> kRegionShift], 1u); });
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kMaxRegions; i += blockDim.x)
-    if (hist[i]) hist[i] = atomicAdd(cursor + i, hist[i]);  // this CTA's slice of region i
-  __syncthreads();
-  each([&](uint64_t off, float x) {
-    const uint32_t slot = atomicAdd(&hist[off >> kRegionShift], 1u);
-    records[slot] = make_uint2(uint32_t(off), __float_as_uint(x));
-  });
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t j = b0 + q * blockDim.x + threadIdx.x;
+      if (j >= b1) continue;
+      const EncItem& e = items[kit[q]];
+      const uint64_t sk = uint64_t(e.sketch - base);
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < rows) {
+        const uint32_t off = uint32_t(sk + uint64_t(r) * e.m + dev_bucket(hp.row[r], kv[q].x, e.m, e.mmul));
+        s_u[(j - b0) * rows + r] =
+            make_uint2(off, __float_as_uint(dev_sign(hp.row[r], kv[q].x) * __uint_as_float(kv[q].y)));
+        atomicAdd(&s_hist[off >> shift], 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of the bin counts (each thread a run of bins); global slices reserved in parallel
+      const uint32_t per = (n_bins + blockDim.x - 1) / blockDim.x;
+      const uint32_t c0 = min(n_bins, threadIdx.x * per), c1 = min(n_bins, c0 + per);
+      uint32_t sum = 0;
+      for (uint32_t b = c0; b < c1; ++b) sum += s_hist[b];
+      uint32_t off;
+      BlockScanDs(s_scan).ExclusiveSum(sum, off);
+      for (uint32_t b = c0; b < c1; ++b) {
+        const uint32_t h = s_hist[b];
+        s_gb[b] = h ? atomicAdd(fill + b, h) : 0u;
+        s_loff[b] = off;
+        s_hist[b] = off;  // becomes the placement cursor
+        off += h;
+      }
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nrec; k += blockDim.x) {
+      const uint2 rec = s_u[k];
+      s_s[atomicAdd(&s_hist[rec.x >> shift], 1u)] = rec;
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nrec; k += blockDim.x) {
+      const uint2 rec = s_s[k];
+      const uint32_t b = rec.x >> shift;
+      const uint32_t g = s_gb[b] + (k - s_loff[b]);
+      if (g < cap) records[uint64_t(b) * cap + g] = rec;
+      else ovf[atomicAdd(ctl, 1u)] = rec;
+    }
+    __syncthreads();
+  }
 }
 
-// The deferred sketches start at zero: written here, right before the apply
+// One CTA per 32K-float region (2^(shift - 15) CTAs per bin): the bin's run
+// is read by each of its CTAs (L2 resident), each keeps its region's updates
+// in shared memory, then stores the region over the part that belongs to
+// deferred, finally-selected sketches (gaps and fallen-back items are left
+// alone).
+__global__ void __launch_bounds__(kDsThreads) k_ds_apply_smem(const EncItem* __restrict__ items,
+                                                              const SelState* __restrict__ state, uint32_t n_items,
+                                                              uint32_t rows, uint32_t shift,
+                                                              const uint2* __restrict__ records,
+                                                              const uint32_t* __restrict__ fill,
+                                                              const uint32_t* __restrict__ ctl, float* base) {
+  extern __shared__ float4 s_acc4[];
+  float* s_acc = reinterpret_cast<float*>(s_acc4);
+  const uint32_t reg = blockIdx.x;
+  const uint32_t b = reg >> (shift - kApplyShift);
+  for (uint32_t i = threadIdx.x; i < kApplyRegion / 4; i += blockDim.x) s_acc4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  const uint32_t cap = ctl[1];
+  const uint32_t n = min(fill[b], cap);
+  const uint2* run = records + uint64_t(b) * cap;
+  constexpr uint32_t kDepth = 8;  // loads in flight per thread
+  for (uint32_t i0 = 0; i0 < n; i0 += blockDim.x * kDepth) {
+    uint2 r[kDepth];
+#pragma unroll
+    for (uint32_t q = 0; q < kDepth; ++q) {
+      const uint32_t i = i0 + q * blockDim.x + threadIdx.x;
+      r[q] = i < n ? __ldcg(run + i) : make_uint2(0xFFFFFFFFu, 0u);
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < kDepth; ++q)
+      if ((r[q].x >> kApplyShift) == reg) atomicAdd(s_acc + (r[q].x & (kApplyRegion - 1u)), __uint_as_float(r[q].y));
+  }
+  __syncthreads();
+  const uint64_t g0 = uint64_t(reg) << kApplyShift, g1 = g0 + kApplyRegion;
+  for (uint32_t it = 0; it < n_items; ++it) {
+    const EncItem& e = items[it];
+    if (!(e.flags & kDeferScatter) || !(e.flags & kWriteSketch) || state[it].status != kStatusReady) continue;
+    const uint64_t a = uint64_t(e.sketch - base), z = a + uint64_t(rows) * e.m;
+    const uint64_t lo = a > g0 ? a : g0, hi = z < g1 ? z : g1;
+    for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) __stcs(base + x, s_acc[x - g0]);
+  }
+}
+
+// The RED path's sketches start at zero: written right before the apply
 // (full-sector stores allocate their lines in L2 without a DRAM read), for
 // the items whose select is final (a fallen-back item was re-encoded exactly
 // and scattered directly into its freshly cleared sketch).
@@ -1363,12 +1432,28 @@ __global__ void __launch_bounds__(256) k_ds_zero(const EncItem* __restrict__ ite
   }
 }
 
-// Records in region order, grid-stride: all CTAs sweep the regions together.
-__global__ void __launch_bounds__(256) k_ds_apply(const uint2* __restrict__ records,
-                                                  const uint32_t* __restrict__ n_records, float* base) {
-  const uint32_t total = *n_records;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint2 r = __ldcs(records + i);
+// RED path: bins in order (CTA-strided over bins, grid-stride inside), so all
+// CTAs sweep the address space together and the REDs hit L2.
+__global__ void __launch_bounds__(256) k_ds_apply(const uint2* __restrict__ records, const uint32_t* __restrict__ fill,
+                                                  const uint32_t* __restrict__ ctl, uint32_t n_bins, float* base) {
+  const uint32_t cap = ctl[1];
+  for (uint32_t b = 0; b < n_bins; ++b) {
+    const uint32_t n = min(fill[b], cap);
+    const uint2* run = records + uint64_t(b) * cap;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint2 r = __ldcs(run + i);
+      red_add_f32(base + r.x, __uint_as_float(r.y));
+    }
+  }
+}
+
+// Updates beyond their bin's capacity (never, for hash-uniform bins), after
+// the apply.
+__global__ void __launch_bounds__(256) k_ds_overflow(const uint2* __restrict__ ovf, const uint32_t* __restrict__ ctl,
+                                                     float* base) {
+  const uint32_t n = ctl[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint2 r = ovf[i];
     red_add_f32(base + r.x, __uint_as_float(r.y));
   }
 }
@@ -1905,18 +1990,35 @@ int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stre
 
 int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
                             const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
-                            uint32_t* region_count, uint32_t* cursor, uint32_t* n_records, uint2* records,
-                            cudaStream_t stream) {
+                            uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf, cudaStream_t stream) {
   if (!n_items) return 0;
-  if (span_floats > (uint64_t(kMaxRegions) << kRegionShift) || span_floats > 0xFFFFFFFFull)
-    return -1;  // caller scatters directly
-  const int g = di.sms * 4;
-  k_ds_count<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, region_count);
-  k_ds_scan<<<1, 1024, 0, stream>>>(region_count, cursor, n_records);
-  k_ds_place<<<g, 256, 0, stream>>>(items, state, n_items, hi_pool, hp, base, cursor, records);
-  k_ds_zero<<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, hp.rows);
-  k_ds_apply<<<di.sms * 8, 256, 0, stream>>>(records, n_records, base);
-  return 5;
+  if (span_floats > 0xFFFFFFFFull || span_floats == 0) return -1;  // caller scatters directly
+  uint32_t lg = 0;
+  while ((1ull << lg) < span_floats) ++lg;
+  const bool smem = lg <= 27;  // one shared-memory region per bin, <= 4096 bins
+  static const uint32_t extra = std::getenv("TAGC_DS_BIN_SHIFT") ? uint32_t(std::atoi(std::getenv("TAGC_DS_BIN_SHIFT"))) : 0u;
+  const uint32_t shift = smem ? std::max<uint32_t>(kApplyShift + extra, lg > 12 ? lg - 12 : 0)
+                              : std::max<uint32_t>(22, lg - 12);
+  const uint32_t n_bins = uint32_t((span_floats + (1ull << shift) - 1) >> shift);
+  const int smem_place = int(2 * kDsBatch * sizeof(uint2) + 3 * n_bins * sizeof(uint32_t));
+  cudaFuncSetAttribute((const void*)k_ds_place, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_place);
+  k_ds_place<<<di.sms, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, shift, n_bins,
+                                                         fill, ctl, records, ovf);
+  int l = 1;
+  if (smem) {
+    const uint32_t regions = uint32_t((span_floats + kApplyRegion - 1) >> kApplyShift);
+    cudaFuncSetAttribute((const void*)k_ds_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kApplyRegion * 4));
+    k_ds_apply_smem<<<regions, kDsThreads, kApplyRegion * 4, stream>>>(items, state, n_items, hp.rows, shift,
+                                                                       records, fill, ctl, base);
+    ++l;
+  } else {
+    k_ds_zero<<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, hp.rows);
+    k_ds_apply<<<di.sms * 8, 256, 0, stream>>>(records, fill, ctl, n_bins, base);
+    l += 2;
+  }
+  k_ds_overflow<<<di.sms, 256, 0, stream>>>(ovf, ctl, base);
+  return l + 1;
 }
 
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream) {
@@ -1973,7 +2075,7 @@ int launch_index_diag(const DiagItem* items, uint32_t n_items, uint32_t max_word
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_encode_kernels() {
-  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_zero, (const void*)k_ds_count, (const void*)k_ds_place, (const void*)k_ds_scan, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
+  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_apply_smem, (const void*)k_ds_zero, (const void*)k_ds_overflow, (const void*)k_ds_place, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

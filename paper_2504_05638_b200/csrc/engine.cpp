@@ -470,7 +470,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
         if (!lo || e.sketch < lo) lo = e.sketch;
         if (!hi_end || e.sketch + uint64_t(hp.rows) * e.m > hi_end) hi_end = e.sketch + uint64_t(hp.rows) * e.m;
       }
-    if (lo && uint64_t(hi_end - lo) < (uint64_t(4096) << 22) && uint64_t(hi_end - lo) <= 0xFFFFFFFFull) {
+    if (lo && uint64_t(hi_end - lo) <= 0xFFFFFFFFull) {
       ds_base = const_cast<float*>(lo);
       ds_span = uint64_t(hi_end - lo);
       for (EncItem& e : items)
@@ -494,7 +494,9 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   // per-batch words only (err[1] bracket miss, err[3] chunk counter); the
   // NaN (err[0]) and peer-timeout (err[2]) flags stay sticky until
   // sync_check reports them, so a later batch or call cannot erase them
-  zero({{err + 1, 4}, {err + 3, 4}});
+  uint32_t* ds_fill = ds_base ? static_cast<uint32_t*>(ws_.get("ds_fill", (kDsMaxBins + 4) * 4, false, stream_))
+                              : nullptr;
+  zero({{err + 1, 4}, {err + 3, 4}, {ds_fill, ds_fill ? (kDsMaxBins + 4) * 4 : 0}});
   if (select) {
     auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleStride * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
@@ -520,11 +522,11 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
     if (ds_base) {
-      auto* rc = static_cast<uint32_t*>(ws_.get("ds_count", 4096 * 4, true, stream_));
-      auto* cur = static_cast<uint32_t*>(ws_.get("ds_cursor", 4096 * 4 + 16, false, stream_));
-      auto* rec = static_cast<uint2*>(ws_.get("ds_records", ds_cap * 8, false, stream_));
-      const int l = launch_deferred_scatter(di_, d_items, state, n, hp_pool, hp, ds_base, ds_span, rc, cur,
-                                            cur + 4096, rec, stream_);
+      auto* rec = static_cast<uint2*>(ws_.get("ds_records", (ds_cap + ds_cap / 16 + uint64_t(kDsMaxBins) * 1024) * 8,
+                                              false, stream_));
+      auto* ovf = static_cast<uint2*>(ws_.get("ds_overflow", ds_cap * 8, false, stream_));
+      const int l = launch_deferred_scatter(di_, d_items, state, n, hp_pool, hp, ds_base, ds_span, ds_fill,
+                                            ds_fill + kDsMaxBins, rec, ovf, stream_);
       if (l < 0) throw CudaError("deferred sketch scatter: span too large");
       launches_ += l;
     }

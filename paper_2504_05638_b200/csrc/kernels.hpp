@@ -71,19 +71,20 @@ int launch_rank_sum_f32(const float* const* in_ptrs, uint32_t world, float* out,
 // Wrapping u32 word sum (kernels.cpp:65-84).
 int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t* out, uint64_t n,
                         cudaStream_t stream);
-// Sketch scatter of the kDeferScatter items' logged kept entries, bucketed by
-// 16 MB region of [base, base + span_floats) (after launch_select_finish).
-// region_count: kMaxRegions (4096) u32, zero on entry (left zero); cursor:
-// 4096 u32; records: 3 x (sum of the items' hi_cap) uint2. Returns -1 when
-// the span is too large (then nothing was launched). The deferred sketches
-// (of items whose select did not fall back: the exact re-encode scatters
-// directly) are zeroed here, between the record placement and the apply, so
-// their lines are freshly allocated in L2 when the REDs arrive instead of
-// being read back from DRAM; callers leave them unzeroed.
+// Sketch scatter of the kDeferScatter items' logged kept entries, binned by
+// region of [base, base + span_floats) (after launch_select_finish).
+// fill: kDsMaxBins u32 and ctl: 4 u32, both zero on entry (the caller zeroes
+// them per batch); records: rows x (sum of the items' hi_cap) x 17/16 +
+// kDsMaxBins x 1024 uint2; ovf: rows x (sum of hi_cap) uint2. Returns -1
+// when the span exceeds 2^32 floats (nothing launched). Spans up to 2^26
+// floats are summed per region in shared memory and stored over the
+// deferred sketches of items whose select did not fall back (the exact
+// re-encode scatters directly), so callers leave those sketches unzeroed;
+// larger spans are zeroed here and applied with L2 REDs bin by bin.
+constexpr uint32_t kDsMaxBins = 4096;
 int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
                             const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
-                            uint32_t* region_count, uint32_t* cursor, uint32_t* n_records, uint2* records,
-                            cudaStream_t stream);
+                            uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf, cudaStream_t stream);
 // Owner-side optimizer step on the decoded shard (train.cpp:202-220, 355-359):
 // kind 0 SGD, 1 momentum-free AdamW (adam_v in/out).
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream);
