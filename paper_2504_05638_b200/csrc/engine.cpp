@@ -11,6 +11,8 @@
 // plain fp32 sums (hook.cpp:125-135) and leave the accumulator untouched.
 #include "engine.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "nccl_dl.hpp"
 
 #include <algorithm>
@@ -254,7 +256,14 @@ void Engine::last_kernel_spans(float out_ms[2]) {
     if (t[2 * i + 1] > t[2 * i] && t[2 * i] != ~0ull) out_ms[i] = float(double(t[2 * i + 1] - t[2 * i]) * 1e-6);
 }
 
+// Stage boundaries: CUDA events in timing mode, and always an NVTX range per
+// stage (host-side enqueue spans for nsys / ncu --nvtx; no-ops without a tool).
 void Engine::ev_record(int i) {
+  static const char* const kStage[] = {"tagc:prep", "tagc:select_fused", "tagc:select_finish", "tagc:exchange",
+                                       "tagc:decode"};
+  if (nvtx_open_) nvtxRangeEnd(nvtx_range_);
+  nvtx_open_ = i >= 0 && i < 5;
+  if (nvtx_open_) nvtx_range_ = nvtxRangeStartA(kStage[i]);
   if (timing_) cuda_check(cudaEventRecord(ev_[i], stream_), "event record");
   static const bool probe = std::getenv("TAGC_TIMING_PROBE") != nullptr;
   if (timing_ && probe) {

@@ -1,6 +1,6 @@
 """Debug: W contexts on one GPU with the peer exchange; per-call host timing."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2504_05638_b200 as tagc
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 2

@@ -1,6 +1,6 @@
 """Small multi-segment 1-bit exchange (ordered peel) for compute-sanitizer."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 import oracle as O
