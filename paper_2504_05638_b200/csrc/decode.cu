@@ -1714,10 +1714,14 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
 }  // namespace
 
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                  cudaStream_t stream, bool fused_emit) {
-  if (w.n_items == 0) return 0;
+                  cudaStream_t stream, bool fused_emit, cudaEvent_t sketch_ready) {
+  if (w.n_items == 0) {
+    if (sketch_ready) cudaStreamWaitEvent(stream, sketch_ready, 0);
+    return 0;
+  }
   int per_sm = 0;
   build_passes(di, w, hp, stream);
+  if (sketch_ready) cudaStreamWaitEvent(stream, sketch_ready, 0);
   const int list_launches = w.cnt8 ? 3 : 1;
   if (fused_emit) {
     const uint64_t ge = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
@@ -1754,9 +1758,13 @@ int ordered_loop_grid(const DevInfo& di) {
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp, const OrdState& o,
-                          cudaStream_t stream) {
-  if (w.n_items == 0) return 0;
+                          cudaStream_t stream, cudaEvent_t sketch_ready) {
+  if (w.n_items == 0) {
+    if (sketch_ready) cudaStreamWaitEvent(stream, sketch_ready, 0);
+    return 0;
+  }
   build_passes(di, w, hp, stream);
+  if (sketch_ready) cudaStreamWaitEvent(stream, sketch_ready, 0);
   const int grid = di.sms * 4;
   if (hp.rows == 3) k_r0_phase1_k<3, 2><<<grid, 256, 0, stream>>>(w, hp);
   else k_r0_phase1<<<grid, 256, 0, stream>>>(w, hp);

@@ -207,6 +207,12 @@ Engine::~Engine() {
   if (hev_join_) cudaEventDestroy(hev_join_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
+  if (ds_stream_) {
+    cudaStreamSynchronize(ds_stream_);
+    cudaEventDestroy(ds_fork_);
+    cudaEventDestroy(ds_done_);
+    cudaStreamDestroy(ds_stream_);
+  }
   if (aux_) {
     cudaStreamSynchronize(aux_);
     cudaEventDestroy(aux_fork_);
@@ -534,8 +540,23 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
       auto* rec = static_cast<uint2*>(ws_.get("ds_records", (ds_cap + ds_cap / 16 + uint64_t(kDsMaxBins) * 1024) * 8,
                                               false, stream_));
       auto* ovf = static_cast<uint2*>(ws_.get("ds_overflow", ds_cap * 8, false, stream_));
+      cudaStream_t ds_s = stream_;
+      if (ds_side_ok_) {  // overlaps the decode's list build (W == 1: the index is final here)
+        if (!ds_stream_) {
+          cuda_check(cudaStreamCreateWithFlags(&ds_stream_, cudaStreamNonBlocking), "ds stream");
+          cuda_check(cudaEventCreateWithFlags(&ds_fork_, cudaEventDisableTiming), "ds event");
+          cuda_check(cudaEventCreateWithFlags(&ds_done_, cudaEventDisableTiming), "ds event");
+        }
+        cuda_check(cudaEventRecord(ds_fork_, stream_), "ds fork");
+        cuda_check(cudaStreamWaitEvent(ds_stream_, ds_fork_, 0), "ds fork wait");
+        ds_s = ds_stream_;
+      }
       const int l = launch_deferred_scatter(di_, d_items, state, n, hp_pool, hp, ds_base, ds_span, ds_fill,
-                                            ds_fill + kDsMaxBins, rec, ovf, stream_);
+                                            ds_fill + kDsMaxBins, rec, ovf, ds_s);
+      if (ds_side_ok_) {
+        cuda_check(cudaEventRecord(ds_done_, ds_stream_), "ds done");
+        sketch_pending_ = true;
+      }
       if (l < 0) throw CudaError("deferred sketch scatter: span too large");
       launches_ += l;
     }
@@ -563,6 +584,16 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
 }
 
 // ------------------------------------------------------------------ decode
+cudaEvent_t Engine::take_sketch_event() {
+  if (!sketch_pending_) return nullptr;
+  sketch_pending_ = false;
+  return ds_done_;
+}
+
+void Engine::join_sketch() {
+  if (cudaEvent_t e = take_sketch_event()) cuda_check(cudaStreamWaitEvent(stream_, e, 0), "ds join");
+}
+
 void Engine::ensure_aux() {
   if (aux_) return;
   int lo = 0, hi = 0;  // lowest priority: decode kernels take SMs first as side CTAs retire
@@ -692,9 +723,9 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     o.u1 = static_cast<uint32_t*>(ws_.get("ord_u1", slots * 4, false, stream_));
     o.cta = static_cast<uint32_t*>(ws_.get("ord_cta", size_t(ordered_loop_grid(di_)) * 4, false, stream_));
     o.epoch = static_cast<uint32_t*>(ws_.get("ord_epoch", 16, true, stream_));  // fixed size: never regrown
-    launches_ += launch_decode_ordered(di_, w, hp, o, stream_);
+    launches_ += launch_decode_ordered(di_, w, hp, o, stream_, take_sketch_event());
   } else {
-    launches_ += launch_decode(di_, w, hp, stream_, fused);
+    launches_ += launch_decode(di_, w, hp, stream_, fused, take_sketch_event());
   }
   if (zero_done) cuda_check(cudaStreamWaitEvent(stream_, zero_done, 0), "wait side stream");
   if (!fused) launches_ += launch_decode_emit(di_, w, stream_, opt_on_ ? opt_dev_ : nullptr);
@@ -1138,7 +1169,9 @@ void Engine::exchange_encode(uint64_t lo, uint64_t hi) {
       pack.push_back(CopyItem{grad + b, send_f + o * Bf + p.raw_off, p.len, 0});
     }
   }
+  ds_side_ok_ = W == 1;
   run_select_encode(enc, w == 4, hp, false, "nccl");
+  ds_side_ok_ = false;
   // raw segments (W > 1): packed into the send blocks before the exchange
   if (!pack.empty()) {
     const uint64_t tt = copy_tiles(pack.data(), uint32_t(pack.size()));
@@ -1326,6 +1359,7 @@ void Engine::exchange_end(const float* recv_f_in, const uint32_t* recv_u_in, Pee
     dec.push_back(d);
   }
   run_decode_grouped(dec, hp, w == 1 && W > 1, zero_done, pre_decode);
+  join_sketch();  // no owned compressed segment decoded: the side scatter still joins here
   // index_lost / index_spurious (hook.cpp:176-188). A 4-bit index is exact
   // for W <= 15 (config.cpp:55-58): both are 0. A 1-bit index over several
   // ranks compares the merged words with the OR of the ranks' supports.

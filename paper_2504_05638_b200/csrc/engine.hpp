@@ -318,6 +318,15 @@ class Engine {
   cudaStream_t aux_ = nullptr;
   cudaEvent_t aux_fork_ = nullptr, aux_join_ = nullptr;
   void ensure_aux();
+  // W == 1 exchange: the deferred sketch scatter runs on ds_stream_ while the
+  // decode builds its presence list from the (already final) index; round 0
+  // waits on ds_done_ (sketch_pending_) before it reads the sketch.
+  cudaStream_t ds_stream_ = nullptr;
+  cudaEvent_t ds_fork_ = nullptr, ds_done_ = nullptr;
+  bool ds_side_ok_ = false;       // set by the W == 1 exchange encode
+  bool sketch_pending_ = false;   // ds_done_ recorded, not yet waited on by stream_
+  cudaEvent_t take_sketch_event();  // the event to wait on before reading sketches (or nullptr)
+  void join_sketch();             // stream_ waits on a pending sketch scatter
   void upload(const void* host, size_t bytes, void* dev);
   // zero byte ranges with one kernel launch (no copy-engine memset)
   void zero(const std::vector<std::pair<void*, uint64_t>>& ranges);

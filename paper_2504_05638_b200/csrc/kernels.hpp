@@ -183,8 +183,10 @@ struct DecodeWork {
 // fused_emit (counter mode, no owner step): round 0 runs inside the dense
 // emit (k_r0_emit) and the final kernel writes the remaining entries, so the
 // output is complete without launch_decode_emit.
+// sketch_ready (if set): waited on after the list build, before the first
+// kernel that reads the sketches (the deferred scatter may still run).
 int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                  cudaStream_t stream, bool fused_emit = false);
+                  cudaStream_t stream, bool fused_emit = false, cudaEvent_t sketch_ready = nullptr);
 
 // Final step of either decode: writes every item's dense output (zeros, and
 // the decoded value of each listed entry).
@@ -214,7 +216,7 @@ struct OrdState {
   uint64_t slot_key_cap, claim_cap;  // allocated elements (cleared on epoch wrap)
 };
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
-                          const OrdState& o, cudaStream_t stream);
+                          const OrdState& o, cudaStream_t stream, cudaEvent_t sketch_ready = nullptr);
 int ordered_loop_grid(const DevInfo& di);
 
 // Presence list -> bitmap (width-1 index) with bounds/duplicate checks for the
