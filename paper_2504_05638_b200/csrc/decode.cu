@@ -81,6 +81,15 @@ __device__ __forceinline__ uint32_t present_bits(uint32_t x, bool w4, uint32_t w
   return x;
 }
 
+// Same without the item-end mask: for words wholly inside the item.
+__device__ __forceinline__ uint32_t present_bits_full(uint32_t x, bool w4) {
+  return w4 ? ((x | x >> 1 | x >> 2 | x >> 3) & 0x11111111u) : x;
+}
+// Thread-owned words [w0, w0 + kPerThreadWords) all inside the item's n positions.
+__device__ __forceinline__ bool words_full(uint32_t w0, uint32_t nwords, bool w4, uint32_t n) {
+  return uint64_t(w0 + nwords) * (w4 ? 8u : 32u) <= uint64_t(n);
+}
+
 __device__ __forceinline__ float canonical(float v) { return v == 0.0f ? 0.0f : v; }
 
 __device__ __forceinline__ uint32_t warp_sum32(uint32_t x) {
@@ -300,8 +309,13 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
     uint32_t cnt = 0;
+    if (words_full(tile_word(wbase, 0), kPerThreadWords, w4, e.n)) {
 #pragma unroll
-    for (uint32_t k = 0; k < kPerThreadWords; ++k) cnt += __popc(present_bits(raw[k], w4, tile_word(wbase, k), e.n));
+      for (uint32_t k = 0; k < kPerThreadWords; ++k) cnt += __popc(present_bits_full(raw[k], w4));
+    } else {
+#pragma unroll
+      for (uint32_t k = 0; k < kPerThreadWords; ++k) cnt += __popc(present_bits(raw[k], w4, tile_word(wbase, k), e.n));
+    }
     uint32_t nit = it;  // the next tile's words in flight during the reduction
     if (wt + 1 < t1) {
       while (nit + 1 < w.n_items && w.items[nit + 1].word_tile_begin <= wt + 1) ++nit;
@@ -376,9 +390,10 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
     const uint32_t P = w4 ? 8u : 32u;
     const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
     uint32_t bits[kPerThreadWords], cnt = 0;
+    const bool full = words_full(tile_word(wbase, 0), kPerThreadWords, w4, e.n);
 #pragma unroll
     for (uint32_t k = 0; k < kPerThreadWords; ++k) {
-      bits[k] = present_bits(raw[k], w4, tile_word(wbase, k), e.n);
+      bits[k] = full ? present_bits_full(raw[k], w4) : present_bits(raw[k], w4, tile_word(wbase, k), e.n);
       cnt += __popc(bits[k]);
     }
     uint32_t nit = it;
@@ -1374,6 +1389,28 @@ __global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const 
   uint32_t n_chunks = 0;  // chunks stored by this CTA (ring position)
   if (t0 < t1) {
     uint32_t it = find_word_item(w.items, w.n_items, t0);
+    // Entry windows: thread t holds list entry wb + t (position, value) of
+    // the current window and, one window ahead, of the next, so the loads
+    // of the entries a chunk needs were issued a window earlier (the list
+    // range of this CTA's tiles is contiguous and ascending).
+    const uint32_t lbeg = __ldg(w.tile_base + t0);
+    uint32_t lend = t1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + t1) : total;
+    lend = lend < total ? lend : total;
+    uint32_t wb = lbeg;  // first entry of the current window
+    uint32_t cons = 0;   // entries of the current window already placed
+    auto load_win = [&](uint32_t base, uint32_t& p, float& v) {
+      const uint32_t i = base + threadIdx.x;
+      p = 0xFFFFFFFFu;
+      v = 0.0f;
+      if (i < lend) {
+        p = __ldcs(w.plist + i);
+        v = __ldcs(w.val + i);
+      }
+    };
+    uint32_t wp, np;
+    float wv, nv;
+    load_win(wb, wp, wv);
+    load_win(wb + blockDim.x, np, nv);
     for (uint32_t wt = t0; wt < t1; ++wt) {
       while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
       const DecItem& e = w.items[it];
@@ -1381,7 +1418,7 @@ __global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const 
       const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
       const uint64_t p0 = wbase * P;
       const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
-      uint32_t cur = __ldg(w.tile_base + wt);
+      // the tile's entries end at le (positions restart at the next item)
       uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
       le = le < total ? le : total;
       for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
@@ -1395,16 +1432,21 @@ __global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const 
         float4* b4 = reinterpret_cast<float4*>(buf);
         for (uint32_t q = threadIdx.x; q < kEmitChunk / 4; q += blockDim.x) b4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
-        // this chunk's entries: positions below c0 + clen, from `cur` on
+        // this chunk's entries: the window's unplaced entries below c0 + clen
+        // that belong to this tile (list index < le)
         for (;;) {
-          const uint32_t i = cur + threadIdx.x;
-          uint32_t p = 0xFFFFFFFFu;
-          if (i < le) p = __ldcs(w.plist + i);
-          const bool in = uint64_t(p) < c0 + clen;
-          if (in) buf[p - c0] = __ldcs(w.val + i);
-          const uint32_t cnt = __syncthreads_count(in);
-          cur += cnt;
-          if (cnt < blockDim.x) break;
+          const uint32_t i = wb + threadIdx.x;
+          const bool in = threadIdx.x >= cons && i < le && uint64_t(wp) < c0 + clen;
+          if (in) buf[wp - c0] = wv;
+          cons += __syncthreads_count(in);
+          const uint32_t rest = min(wb + blockDim.x, le);
+          if (wb + cons < rest) break;          // stopped inside the window: chunk done
+          if (wb + blockDim.x > le) break;      // the tile's entries end inside the window
+          wb += blockDim.x;                      // window used up: advance, prefetch the next
+          cons = 0;
+          wp = np;
+          wv = nv;
+          load_win(wb + blockDim.x, np, nv);
         }
         float* dst = e.out + c0;
         const uint32_t bytes = (clen * 4u) & ~15u;
