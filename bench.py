@@ -279,14 +279,34 @@ def compressed_elems(tagc, shards, cfg):
     return n
 
 
-def fused_bytes_per_elem(cfg):
+DEFER_SCATTER_BYTES = 32 << 20  # engine default (TAGC_DEFER_SCATTER_BYTES): larger sketches are deferred
+
+
+def fused_bytes_per_elem(cfg, deferred=False):
     """SURVEY.md §8(d) bytes per compressed element of the dominant kernel, the
     fused select + split + encode pass (k_fused_tma): read g and acc (8 B),
     write the residual (4 B) and the packed index (w/8 B), plus a 24*d sketch
-    read-modify-write (d = 1 - theta/100). The separate select pass of the
-    survey's model (8 B) is gone: selection rides on the same pass, bracketed
-    by two small passes over a 1/32 sample (separate kernels, not counted)."""
-    return 12.0 + cfg.index_width / 8.0 + 24.0 * (1.0 - cfg.theta / 100.0)
+    read-modify-write (d = 1 - theta/100), or, for a segment whose sketch is
+    deferred to the region-sorted scatter (> 32 MB), an 8*d (pos, v) log
+    write instead. The separate select pass of the survey's model (8 B) is
+    gone: selection rides on the same pass, bracketed by two small passes over
+    a 1/32 sample (separate kernels, not counted)."""
+    d = 1.0 - cfg.theta / 100.0
+    return 12.0 + cfg.index_width / 8.0 + (8.0 if deferred else 24.0) * d
+
+
+def fused_bytes(tagc, shards, cfg):
+    """Algorithmic bytes of one k_fused_tma launch over every compressed
+    segment of this rank (every shard is encoded by every rank)."""
+    total = 0.0
+    for sh in shards:
+        for s in sh.segments:
+            if tagc.kind_compressible(s.kind, cfg.policy, cfg.include_out_proj) and \
+                    s.size() >= cfg.min_compress_segment and cfg.ratio > 1:
+                g = tagc.sketch_geometry(s.size(), cfg.ratio, cfg.sketch_rows)
+                sketch = 4 * g["rows"] * g["buckets_per_row"]
+                total += s.size() * fused_bytes_per_elem(cfg, sketch > DEFER_SCATTER_BYTES)
+    return total
 
 
 def decode_bytes_per_elem(cfg):
@@ -355,6 +375,7 @@ def measure_exchange(rig, tagc, name, args, full=True):
     }
     state = dict(specs=specs, cfg=cfg, shards=shards, total=total, n_params=n_params, ctx=ctx, grad=grad,
                  acc=acc, out=out, owned=owned, comp=comp, owned_comp=owned_comp, ms=ms, span_ms=span_ms,
+                 fused_bytes=fused_bytes(tagc, shards, cfg),
                  clk=clk, step=step)
     return res, state
 
@@ -531,7 +552,7 @@ def run_b200(args):
     cfg, world = S["cfg"], rig.world
     hbm, peak_kind = peaks()
     fused_ms = S["span_ms"][0]
-    fused_bytes = S["comp"] * fused_bytes_per_elem(cfg)
+    fused_bytes = S["fused_bytes"]
     achieved = fused_bytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else 0.0
     dec_bytes = S["owned_comp"] * decode_bytes_per_elem(cfg)
     dec_ms = S["span_ms"][1]
@@ -574,7 +595,7 @@ def run_b200(args):
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(fused_bytes),
-                     "bytes_per_elem": round(fused_bytes_per_elem(cfg), 4),
+                     "bytes_per_elem": round(fused_bytes / max(S["comp"], 1), 4),
                      "kernel_ms": round(fused_ms, 4),
                      "timed": "k_fused_tma launches: device span from %globaltimer stamps written by the "
                               "kernel (first CTA start to last CTA end), mean of the timed launches, max "
