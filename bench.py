@@ -553,6 +553,7 @@ def run_b200(args):
     hbm, peak_kind = peaks()
     fused_ms = S["span_ms"][0]
     fused_bytes = S["fused_bytes"]
+    fused_bpe = fused_bytes / max(S["comp"], 1)
     achieved = fused_bytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else 0.0
     dec_bytes = S["owned_comp"] * decode_bytes_per_elem(cfg)
     dec_ms = S["span_ms"][1]
@@ -595,7 +596,7 @@ def run_b200(args):
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(fused_bytes),
-                     "bytes_per_elem": round(fused_bytes / max(S["comp"], 1), 4),
+                     "bytes_per_elem": round(fused_bpe, 4),
                      "kernel_ms": round(fused_ms, 4),
                      "timed": "k_fused_tma launches: device span from %globaltimer stamps written by the "
                               "kernel (first CTA start to last CTA end), mean of the timed launches, max "

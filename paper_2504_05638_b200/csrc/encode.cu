@@ -1262,8 +1262,9 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 // as it does between any two runs of the direct scatter.
 constexpr uint32_t kApplyShift = 15;  // 32K floats = 128 KB per shared-memory region
 constexpr uint32_t kApplyRegion = 1u << kApplyShift;
-constexpr uint32_t kDsBatch = 8192;   // staged updates per place batch
-constexpr uint32_t kDsThreads = 512;
+constexpr uint32_t kDsBatch = 4096;   // staged updates per place batch
+constexpr uint32_t kDsThreads = 256;  // place: 2 CTAs per SM
+constexpr uint32_t kApplyThreads = 512;
 using BlockScanDs = cub::BlockScan<uint32_t, kDsThreads>;
 
 __device__ __forceinline__ uint32_t ds_entries(const EncItem& e, const SelState& st) {
@@ -1279,7 +1280,7 @@ __device__ __forceinline__ uint32_t ds_cap(uint32_t total_updates, uint32_t n_bi
 // fill[n_bins] (zero on entry) counts each bin's updates; records hold bin b
 // at [b * cap, b * cap + min(fill[b], cap)); ctl[0] = overflow count,
 // ctl[1] = cap.
-__global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restrict__ items,
+__global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __restrict__ items,
                                                          const SelState* __restrict__ state, uint32_t n_items,
                                                          const uint2* __restrict__ hi_pool, const HashParams hp,
                                                          const float* base, uint32_t shift, uint32_t n_bins,
@@ -1305,13 +1306,14 @@ __global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restri
     const uint32_t nrec = (b1 - b0) * rows;
     for (uint32_t i = threadIdx.x; i < n_bins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
-    // every thread's entries loaded before any is hashed (memory-level parallelism)
-    constexpr uint32_t kPer = (kDsBatch + kDsThreads - 1) / kDsThreads;
+    // kPer entries per thread loaded before any is hashed (memory-level parallelism)
+    constexpr uint32_t kPer = 8;
+    for (uint32_t q0 = b0; q0 < b1; q0 += kPer * blockDim.x) {
     uint2 kv[kPer];
     uint32_t kit[kPer];
 #pragma unroll
     for (uint32_t q = 0; q < kPer; ++q) {
-      const uint32_t j = b0 + q * blockDim.x + threadIdx.x;
+      const uint32_t j = q0 + q * blockDim.x + threadIdx.x;
       kit[q] = 0;
       kv[q] = make_uint2(0, 0);
       if (j < b1) {
@@ -1321,7 +1323,7 @@ __global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restri
     }
 #pragma unroll
     for (uint32_t q = 0; q < kPer; ++q) {
-      const uint32_t j = b0 + q * blockDim.x + threadIdx.x;
+      const uint32_t j = q0 + q * blockDim.x + threadIdx.x;
       if (j >= b1) continue;
       const EncItem& e = items[kit[q]];
       const uint64_t sk = uint64_t(e.sketch - base);
@@ -1331,6 +1333,7 @@ __global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restri
             make_uint2(off, __float_as_uint(dev_sign(hp.row[r], kv[q].x) * __uint_as_float(kv[q].y)));
         atomicAdd(&s_hist[off >> shift], 1u);
       }
+    }
     }
     __syncthreads();
     {  // exclusive scan of the bin counts (each thread a run of bins); global slices reserved in parallel
@@ -1370,7 +1373,7 @@ __global__ void __launch_bounds__(kDsThreads) k_ds_place(const EncItem* __restri
 // in shared memory, then stores the region over the part that belongs to
 // deferred, finally-selected sketches (gaps and fallen-back items are left
 // alone).
-__global__ void __launch_bounds__(kDsThreads) k_ds_apply_smem(const EncItem* __restrict__ items,
+__global__ void __launch_bounds__(kApplyThreads) k_ds_apply_smem(const EncItem* __restrict__ items,
                                                               const SelState* __restrict__ state, uint32_t n_items,
                                                               uint32_t rows, uint32_t shift,
                                                               const uint2* __restrict__ records,
@@ -2002,14 +2005,14 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
   const uint32_t n_bins = uint32_t((span_floats + (1ull << shift) - 1) >> shift);
   const int smem_place = int(2 * kDsBatch * sizeof(uint2) + 3 * n_bins * sizeof(uint32_t));
   cudaFuncSetAttribute((const void*)k_ds_place, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_place);
-  k_ds_place<<<di.sms, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, shift, n_bins,
+  k_ds_place<<<di.sms * 2, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, shift, n_bins,
                                                          fill, ctl, records, ovf);
   int l = 1;
   if (smem) {
     const uint32_t regions = uint32_t((span_floats + kApplyRegion - 1) >> kApplyShift);
     cudaFuncSetAttribute((const void*)k_ds_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kApplyRegion * 4));
-    k_ds_apply_smem<<<regions, kDsThreads, kApplyRegion * 4, stream>>>(items, state, n_items, hp.rows, shift,
+    k_ds_apply_smem<<<regions, kApplyThreads, kApplyRegion * 4, stream>>>(items, state, n_items, hp.rows, shift,
                                                                        records, fill, ctl, base);
     ++l;
   } else {
