@@ -860,54 +860,128 @@ __device__ __forceinline__ void local_push(bool push, uint32_t slot, uint32_t en
   }
 }
 
-// One frontier element per lane. kPair: (slot, entry) from a local queue;
-// otherwise a slot from a global queue (its state names the entry).
-template <bool kPair>
-__device__ __forceinline__ uint32_t peel_one(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
-                                             bool have, uint32_t slot, uint32_t i, uint2* s_next, uint32_t* s_nn,
-                                             uint32_t* gq, uint32_t* gcount, uint32_t lane) {
-  if (!kPair && have) {
-    const unsigned long long st = ldcg(w.slot_state + slot);
-    have = st_count(st) == 1u;
-    i = st_entry(st);
+// kN frontier elements per lane, processed together (their L2 trips
+// overlap). kPair: (slot, entry) from a local queue; otherwise a slot from a
+// global queue (its state names the entry).
+template <bool kPair, int kN, int R>
+__device__ __forceinline__ uint32_t peel_n(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
+                                           const bool (&have_in)[kN], const uint32_t (&slot)[kN],
+                                           const uint32_t (&i_in)[kN], uint2* s_next, uint32_t* s_nn, uint32_t* gq,
+                                           uint32_t* gcount, uint32_t lane) {
+  bool have[kN];
+  uint32_t i[kN];
+#pragma unroll
+  for (int k = 0; k < kN; ++k) {
+    have[k] = have_in[k];
+    i[k] = i_in[k];
   }
-  bool win = false;
-  uint32_t p = 0, row = 0;
-  float v = 0.0f;
-  const DecItem* e = w.items;
-  if (have) {
-    e = w.items + si.find(slot);
-    const uint64_t local = slot - e->slot_base;
-    const uint32_t pp = __ldg(w.plist + i);
-    const float resid = ldcg(e->sketch + local);
-    const uint32_t bit = 1u << (i & 31);
-    if (!(atomicOr(w.bitmap + (i >> 5), bit) & bit)) {
-      win = true;
-      p = pp;
-      row = slot_row(local, e->m);
+  if (!kPair) {
+    unsigned long long st[kN];
+#pragma unroll
+    for (int k = 0; k < kN; ++k) st[k] = have[k] ? ldcg(w.slot_state + slot[k]) : 0ull;
+#pragma unroll
+    for (int k = 0; k < kN; ++k) {
+      have[k] = have[k] && st_count(st[k]) == 1u;
+      i[k] = st_entry(st[k]);
+    }
+  }
+  bool win[kN];
+  uint32_t p[kN], row[kN], pp[kN], old_bits[kN];
+  float v[kN], resid[kN];
+  const DecItem* e[kN];
+  uint64_t local[kN];
+#pragma unroll
+  for (int k = 0; k < kN; ++k) {  // claims, positions and residuals of every element in flight together
+    e[k] = w.items;
+    local[k] = 0;
+    pp[k] = 0;
+    resid[k] = 0.0f;
+    old_bits[k] = ~0u;
+    if (have[k]) {
+      e[k] = w.items + si.find(slot[k]);
+      local[k] = slot[k] - e[k]->slot_base;
+      pp[k] = __ldg(w.plist + i[k]);
+      resid[k] = ldcg(e[k]->sketch + local[k]);
+      old_bits[k] = atomicOr(w.bitmap + (i[k] >> 5), 1u << (i[k] & 31));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kN; ++k) {
+    win[k] = have[k] && !((old_bits[k] >> (i[k] & 31)) & 1u);
+    p[k] = 0;
+    row[k] = 0;
+    v[k] = 0.0f;
+    if (win[k]) {
+      p[k] = pp[k];
+      row[k] = slot_row(local[k], e[k]->m);
       float sg = 0.0f;
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r == row) sg = dev_sign(hp.row[r], p);
-      v = canonical(sg * resid);
-      w.val[i] = v;
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r == row[k]) sg = dev_sign(hp.row[r], p[k]);
+      v[k] = canonical(sg * resid[k]);
+      w.val[i[k]] = v[k];
     }
   }
-  unsigned long long old[kMaxRows];
-  uint32_t sl[kMaxRows];
-  _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-    old[r] = 0ull;
-    sl[r] = 0u;
-    if (win && r != row) {
-      const uint64_t loc = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
-      sl[r] = uint32_t(e->slot_base + loc);
-      red_add_f32(e->sketch + loc, -(dev_sign(hp.row[r], p) * v));
-      old[r] = atomicAdd(w.slot_state + e->slot_base + loc, st_sub(i));
+  unsigned long long old[kN][R];
+  uint32_t sl[kN][R];
+#pragma unroll
+  for (int k = 0; k < kN; ++k) {
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows) {
+      old[k][r] = 0ull;
+      sl[k][r] = 0u;
+      if (win[k] && r != row[k]) {
+        const uint64_t loc = uint64_t(r) * e[k]->m + dev_bucket(hp.row[r], p[k], e[k]->m, e[k]->mmul);
+        sl[k][r] = uint32_t(e[k]->slot_base + loc);
+        red_add_f32(e[k]->sketch + loc, -(dev_sign(hp.row[r], p[k]) * v[k]));
+        old[k][r] = atomicAdd(w.slot_state + e[k]->slot_base + loc, st_sub(i[k]));
+      }
     }
   }
-  _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-    const bool push = win && r != row && st_count(old[r]) == 2u;
-    local_push(push, sl[r], st_entry(old[r] + st_sub(i)), s_next, s_nn, gq, gcount, lane);
+  uint32_t won = 0;
+#pragma unroll
+  for (int k = 0; k < kN; ++k) {
+    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows) {
+      const bool push = win[k] && r != row[k] && st_count(old[k][r]) == 2u;
+      local_push(push, sl[k][r], st_entry(old[k][r] + st_sub(i[k])), s_next, s_nn, gq, gcount, lane);
+    }
+    won += win[k] ? 1u : 0u;
   }
-  return win ? 1u : 0u;
+  return won;
+}
+
+// One round's share of a CTA: the local pairs [0, nl) and the global slots
+// [g0, ng) strided by gstride, kPeelN per lane.
+constexpr int kPeelN = 2;
+template <int R>
+__device__ __forceinline__ uint32_t peel_round(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
+                                               const uint2* cur, uint32_t nl, const uint32_t* gsrc, uint32_t ng,
+                                               uint64_t g0, uint64_t gstride, uint2* s_next, uint32_t* s_nn,
+                                               uint32_t* gq, uint32_t* gcount, uint32_t lane) {
+  uint32_t won = 0;
+  for (uint32_t b = 0; b < nl; b += blockDim.x * kPeelN) {
+    bool have[kPeelN];
+    uint32_t sl[kPeelN], en[kPeelN];
+#pragma unroll
+    for (int k = 0; k < kPeelN; ++k) {
+      const uint32_t j = b + k * blockDim.x + threadIdx.x;
+      have[k] = j < nl;
+      const uint2 x = have[k] ? cur[j] : make_uint2(0, 0);
+      sl[k] = x.x;
+      en[k] = x.y;
+    }
+    won += peel_n<true, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, gq, gcount, lane);
+  }
+  for (uint64_t b = g0 - lane; b < ng; b += gstride * kPeelN) {
+    bool have[kPeelN];
+    uint32_t sl[kPeelN], en[kPeelN];
+#pragma unroll
+    for (int k = 0; k < kPeelN; ++k) {
+      const uint64_t j = b + k * gstride + lane;
+      have[k] = j < ng;
+      sl[k] = have[k] ? ldcg(gsrc + j) : 0u;
+      en[k] = 0u;
+    }
+    won += peel_n<false, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, gq, gcount, lane);
+  }
+  return won;
 }
 
 // Grid barrier that also sums a per-CTA value: barrier k adds
@@ -934,22 +1008,18 @@ __device__ __forceinline__ uint32_t grid_barrier_sum(unsigned long long* bar, ui
   return *s_out;
 }
 
+// R: rows compiled in (3, the common k, or kMaxRows for any k <= 8).
+template <int R>
 __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams hp) {
   __shared__ uint2 s_lq[2][kLocalQ];
-  __shared__ uint32_t s_q[kPushStage / 4];
   __shared__ unsigned long long s_sbase[kPeelItemsSmem];
-  __shared__ uint32_t s_ln[2], s_nq[2], s_base, s_total;
-  if (threadIdx.x == 0) {
-    s_ln[0] = s_ln[1] = 0;
-    s_nq[0] = 0;
-    s_nq[1] = kPushStage / 4;
-  }
+  __shared__ uint32_t s_ln[2], s_base, s_total;
+  if (threadIdx.x == 0) s_ln[0] = s_ln[1] = 0;
   const bool cache = w.n_items <= kPeelItemsSmem;
   if (cache)
     for (uint32_t i = threadIdx.x; i < w.n_items; i += blockDim.x) s_sbase[i] = w.items[i].slot_base;
   __syncthreads();
   const SlotItems si{cache ? s_sbase : nullptr, w.items, w.n_items};
-  cg::grid_group grid = cg::this_grid();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
@@ -960,72 +1030,79 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
   int mk = 0;
   PEEL_MARK(mk++);
   if (gtid == 0) w.qcount[2] = 1;
-  if (w.cnt8) {  // counter mode: round 1's frontier = the unresolved entries' single-entry buckets
-    const uint32_t nu = ldcg(&w.qcount[14]);
-    for (uint64_t base = gtid - lane; base < nu; base += gstride) {
-      const uint64_t j = base + lane;
-      uint32_t p = 0;
-      const DecItem* e = w.items;
-      if (j < nu) {
-        const uint32_t i = ldcg(w.ulist + j);
-        p = __ldcs(w.plist + i);
-        e = w.items + __ldcs(w.pitem + i);
-      }
-      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
-        uint64_t sl = 0;
-        bool push = false;
-        if (j < nu) {
-          sl = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
-          push = st_count(ldcg(w.slot_state + sl)) == 1u;  // one entry: pushed by that entry only
-        }
-        stage_push<uint32_t, kPushStage / 4>(push, uint32_t(sl), s_q, s_nq, qbuf1, &cnt[1], lane);
-      }
-    }
-    stage_flush<uint32_t, kPushStage / 4>(s_q, s_nq, &s_base, qbuf1, &cnt[1]);
-    grid.sync();
-  }
   // round k reads the local queue s_lq[k & 1] and the global overflow
-  // qbuf(k) / cnt[k % 3]; it pushes into s_lq[(k + 1) & 1] / qbuf(k + 1)
-  uint32_t won = 0, k = 1;
-  bool tail = ldcg(&cnt[1]) <= kTail;
-  if (!tail) {
-    for (;; ++k) {
-      if (gtid == 0) cnt[(k + 2) % 3] = 0;
-      const uint32_t nl = min(s_ln[k & 1], kLocalQ);
-      const uint32_t ng = ldcg(&cnt[k % 3]);
-      uint2* nxt = s_lq[(k + 1) & 1];
-      uint32_t* nn = &s_ln[(k + 1) & 1];
-      for (uint32_t b = 0; b < nl; b += blockDim.x) {
-        const uint32_t j = b + threadIdx.x;
-        const uint2 e = j < nl ? s_lq[k & 1][j] : make_uint2(0, 0);
-        won += peel_one<true>(w, hp, si, j < nl, e.x, e.y, nxt, nn, qbuf(k + 1), &cnt[(k + 1) % 3], lane);
+  // qbuf(k) / cnt[k % 3]; it pushes into s_lq[(k + 1) & 1] / qbuf(k + 1).
+  // Grid barriers are numbered 0 (round 1's frontier), 1, 2, ...
+  uint32_t total;
+  if (w.cnt8) {
+    // counter mode: round 1's frontier = the unresolved entries' single-
+    // entry buckets, each pushed by its only entry as a local (slot, entry)
+    // pair; two entries per lane in flight
+    const uint32_t nu = ldcg(&w.qcount[14]);
+    for (uint64_t base = gtid - lane; base < nu; base += 2 * gstride) {
+      uint32_t ii[2], p[2];
+      const DecItem* e[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t j = base + h * gstride + lane;
+        ii[h] = j < nu ? ldcg(w.ulist + j) : 0u;
       }
-      for (uint64_t b = gtid - lane; b < ng; b += gstride) {
-        const uint64_t j = b + lane;
-        won += peel_one<false>(w, hp, si, j < ng, j < ng ? ldcg(qbuf(k) + j) : 0u, 0u, nxt, nn, qbuf(k + 1),
-                               &cnt[(k + 1) % 3], lane);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool ok = base + h * gstride + lane < nu;
+        p[h] = ok ? __ldcs(w.plist + ii[h]) : 0u;
+        e[h] = w.items + (ok ? __ldcs(w.pitem + ii[h]) : 0u);
       }
-      __syncthreads();
-      const uint32_t total = grid_barrier_sum(w.bar, k, *nn, &s_total);
-      PEEL_MARK(mk++);
-      if (threadIdx.x == 0) s_ln[k & 1] = 0;  // read by every thread before the barrier
-      if (gtid == 0) w.qcount[2] += 1;
-      if (total == 0) break;
-      if (total <= kTail) {  // hand the frontier to CTA 0: local queues join the global overflow
-        const uint32_t n = min(*nn, kLocalQ);
-        if (threadIdx.x == 0) s_base = n ? atomicAdd(&cnt[(k + 1) % 3], n) : 0u;
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) qbuf(k + 1)[s_base + j] = nxt[j].x;
-        if (threadIdx.x == 0) *nn = 0;
-        grid_barrier_sum(w.bar, k + 1, 0, &s_total);
-        ++k;
-        tail = true;
-        break;
+      uint32_t sl[2][R];
+      uint32_t one[2] = {0u, 0u};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool ok = base + h * gstride + lane < nu;
+        _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows) {
+          sl[h][r] = uint32_t(e[h]->slot_base + uint64_t(r) * e[h]->m + dev_bucket(hp.row[r], p[h], e[h]->m, e[h]->mmul));
+          if (ok && st_count(ldcg(w.slot_state + sl[h][r])) == 1u) one[h] |= 1u << r;
+        }
       }
-      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows)
+          local_push((one[h] >> r) & 1u, sl[h][r], ii[h], s_lq[1], &s_ln[1], qbuf1, &cnt[1], lane);
+      }
     }
+    __syncthreads();
+    total = grid_barrier_sum(w.bar, 0, s_ln[1], &s_total);
   } else {
-    k = 1;
+    total = ldcg(&cnt[1]);  // k_r0_subtract's global pushes
+  }
+  uint32_t won = 0, k = 1;
+  bool tail = false;
+  for (;; ++k) {
+    if (total == 0) break;
+    if (total <= kTail) {  // hand the frontier to CTA 0: local queues join the global part of round k
+      const uint32_t n = min(s_ln[k & 1], kLocalQ);
+      if (threadIdx.x == 0) s_base = n ? atomicAdd(&cnt[k % 3], n) : 0u;
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) qbuf(k)[s_base + j] = s_lq[k & 1][j].x;
+      if (threadIdx.x == 0) s_ln[k & 1] = 0;
+      grid_barrier_sum(w.bar, k, 0, &s_total);
+      tail = true;
+      break;
+    }
+    if (gtid == 0) {
+      cnt[(k + 2) % 3] = 0;
+      w.qcount[2] += 1;
+    }
+    const uint32_t nl = min(s_ln[k & 1], kLocalQ);
+    const uint32_t ng = ldcg(&cnt[k % 3]);
+    uint2* nxt = s_lq[(k + 1) & 1];
+    uint32_t* nn = &s_ln[(k + 1) & 1];
+    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, gtid, gstride, nxt, nn, qbuf(k + 1),
+                         &cnt[(k + 1) % 3], lane);
+    __syncthreads();
+    total = grid_barrier_sum(w.bar, k, *nn, &s_total);
+    PEEL_MARK(mk++);
+    if (threadIdx.x == 0) s_ln[k & 1] = 0;  // read by every thread before the barrier
+    __syncthreads();
   }
   won = warp_sum32(won);
   if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
@@ -1040,16 +1117,8 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     uint2* nxt = s_lq[(k + 1) & 1];
     uint32_t* nn = &s_ln[(k + 1) & 1];
     if (nl == 0 && ng == 0) break;
-    for (uint32_t b = 0; b < nl; b += blockDim.x) {
-      const uint32_t j = b + threadIdx.x;
-      const uint2 e = j < nl ? s_lq[k & 1][j] : make_uint2(0, 0);
-      won += peel_one<true>(w, hp, si, j < nl, e.x, e.y, nxt, nn, qbuf(k + 1), &cnt[(k + 1) % 3], lane);
-    }
-    for (uint32_t b = threadIdx.x - lane; b < ng; b += blockDim.x) {
-      const uint32_t j = b + lane;
-      won += peel_one<false>(w, hp, si, j < ng, j < ng ? ldcg(qbuf(k) + j) : 0u, 0u, nxt, nn, qbuf(k + 1),
-                             &cnt[(k + 1) % 3], lane);
-    }
+    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, threadIdx.x, blockDim.x, nxt, nn, qbuf(k + 1),
+                      &cnt[(k + 1) % 3], lane);
     __syncthreads();
     if (threadIdx.x == 0) {
       s_ln[k & 1] = 0;
@@ -1777,12 +1846,13 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   if (w.cnt8) k_r0_subtract_cnt<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   else k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_peel, 256, 0);
+  const void* peel = hp.rows == 3 ? (const void*)k_peel<3> : (const void*)k_peel<kMaxRows>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel, 256, 0);
   const int pg = coop_grid(di, std::max(per_sm, 1));
   DecodeWork wc = w;
   HashParams hc = hp;
   void* args[] = {&wc, &hc};
-  cudaLaunchCooperativeKernel((const void*)k_peel, dim3(pg), dim3(256), args, 0, stream);
+  cudaLaunchCooperativeKernel(peel, dim3(pg), dim3(256), args, 0, stream);
 
   if (fused_emit) {  // the dense output is complete after this one
     k_final_fix<<<di.sms * 4, 256, 0, stream>>>(w, hp);
@@ -1892,7 +1962,7 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_decode_kernels() {
-  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel<3>, (const void*)k_peel<kMaxRows>, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();
