@@ -50,7 +50,7 @@ __device__ __forceinline__ unsigned long long st_sub(uint32_t i) { return ~st_ad
 __device__ __forceinline__ uint32_t st_count(unsigned long long s) { return uint32_t(s & kCountMask); }
 __device__ __forceinline__ uint32_t st_entry(unsigned long long s) { return uint32_t(s >> 24); }
 constexpr uint32_t kWordTile = kDecWordTile;
-constexpr uint32_t kTail = 512;  // frontier size at which one CTA finishes
+constexpr uint32_t kTail = 512;  // frontier size at which one CTA finishes (<= kLocalQ, kPeelHandoff)
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned long long ldcg(const unsigned long long* p) { return __ldcg(p); }
@@ -1078,13 +1078,19 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
   bool tail = false;
   for (;; ++k) {
     if (total == 0) break;
-    if (total <= kTail) {  // hand the frontier to CTA 0: local queues join the global part of round k
+    if (total <= kTail) {  // hand the local pairs to CTA 0 (w.handoff, count qcount[15])
       const uint32_t n = min(s_ln[k & 1], kLocalQ);
-      if (threadIdx.x == 0) s_base = n ? atomicAdd(&cnt[k % 3], n) : 0u;
+      if (threadIdx.x == 0) s_base = n ? atomicAdd(&w.qcount[15], n) : 0u;
       __syncthreads();
-      for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) qbuf(k)[s_base + j] = s_lq[k & 1][j].x;
+      for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) w.handoff[s_base + j] = s_lq[k & 1][j];
       if (threadIdx.x == 0) s_ln[k & 1] = 0;
       grid_barrier_sum(w.bar, k, 0, &s_total);
+      if (blockIdx.x == 0) {
+        const uint32_t nh = ldcg(&w.qcount[15]);  // <= total <= kTail <= kLocalQ
+        for (uint32_t j = threadIdx.x; j < nh; j += blockDim.x) s_lq[k & 1][j] = __ldcg(w.handoff + j);
+        if (threadIdx.x == 0) s_ln[k & 1] = nh;
+        __syncthreads();
+      }
       tail = true;
       break;
     }

@@ -679,6 +679,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
   w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 64, false, stream_));
   w.bar = static_cast<unsigned long long*>(ws_.get("peel_bar", 32, false, stream_));
+  w.handoff = static_cast<uint2*>(ws_.get("peel_handoff", kPeelHandoff * sizeof(uint2), false, stream_));
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", (stats_base + n) * sizeof(DecStats), false, stream_)) +
             stats_base;
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))

@@ -146,6 +146,7 @@ int launch_audit(const AuditItem* items, uint32_t n_items, uint64_t max_n, const
                  const float* const* res, uint32_t world, cudaStream_t stream);
 
 // ---------------------------------------------------------------- decode
+constexpr uint32_t kPeelHandoff = 512;
 struct DecodeWork {
   const DecItem* items;
   uint32_t n_items;
@@ -168,12 +169,13 @@ struct DecodeWork {
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
   uint32_t* queue[2];              // capacity total_slots each
   uint64_t list_cap;               // presence-list capacity (sum of the items' bounds)
-  uint32_t* qcount;                // [2] rounds, [3] tail rounds, [4] peeled, [8..10] frontier sizes,
+  uint32_t* qcount;                // [2] rounds, [3] tail rounds, [4] peeled, [8..10] frontier sizes, [15] handoff,
                                    // [5] presence total
   DecStats* stats;                 // n_items
   uint32_t* unresolved;            // optional: per item region at list_off
   unsigned long long* dbg;         // optional: globaltimer marks of the peel phases
   unsigned long long* bar;         // k_peel's grid barrier words [3] (zeroed per call)
+  uint2* handoff;                  // k_peel's frontier handed to its single-CTA tail (kPeelHandoff pairs)
   unsigned long long* span;        // optional: execution span of build .. final (timing mode)
 };
 // Presence list + bucket state from the merged index, round-0 peel, frontier
