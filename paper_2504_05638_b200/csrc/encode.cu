@@ -1986,6 +1986,13 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
 
 __global__ void k_set_opt(OptEpilogue* dst, OptEpilogue o) { *dst = o; }
 
+__global__ void k_set_u32(uint32_t* dst, uint32_t v) { *dst = v; }
+
+int launch_set_u32(uint32_t* dst, uint32_t v, cudaStream_t stream) {
+  k_set_u32<<<1, 1, 0, stream>>>(dst, v);
+  return 1;
+}
+
 int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream) {
   k_set_opt<<<1, 1, 0, stream>>>(dev_opt, o);
   return 1;
@@ -2078,7 +2085,7 @@ int launch_index_diag(const DiagItem* items, uint32_t n_items, uint32_t max_word
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_encode_kernels() {
-  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_apply_smem, (const void*)k_ds_zero, (const void*)k_ds_overflow, (const void*)k_ds_place, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
+  const void* fns[] = {(const void*)k_add, (const void*)k_apply_optimizer<false>, (const void*)k_apply_optimizer<true>, (const void*)k_copy_items<false>, (const void*)k_copy_items<true>, (const void*)k_ds_apply, (const void*)k_ds_apply_smem, (const void*)k_ds_zero, (const void*)k_ds_overflow, (const void*)k_ds_place, (const void*)k_encode<false>, (const void*)k_encode<true>, (const void*)k_fallback<false>, (const void*)k_fallback<true>, (const void*)k_finish_select, (const void*)k_fixup<false>, (const void*)k_fixup<true>, (const void*)k_fused<false, false>, (const void*)k_fused<false, true>, (const void*)k_fused<true, false>, (const void*)k_fused<true, true>, (const void*)k_fused_tma<false>, (const void*)k_fused_tma<true>, (const void*)k_index_diag, (const void*)k_rank_sum_f32, (const void*)k_rank_sum_u32, (const void*)k_raw_sum, (const void*)k_sample, (const void*)k_sample_fine, (const void*)k_set_opt, (const void*)k_set_u32, (const void*)k_stage_copy, (const void*)k_window_coarse, (const void*)k_window_fine, (const void*)k_zero};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

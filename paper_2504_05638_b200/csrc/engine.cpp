@@ -724,6 +724,14 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     o.u1 = static_cast<uint32_t*>(ws_.get("ord_u1", slots * 4, false, stream_));
     o.cta = static_cast<uint32_t*>(ws_.get("ord_cta", size_t(ordered_loop_grid(di_)) * 4, false, stream_));
     o.epoch = static_cast<uint32_t*>(ws_.get("ord_epoch", 16, true, stream_));  // fixed size: never regrown
+    if (!ord_epoch_set_) {  // test hook: start the epoch just below the wrap point
+      ord_epoch_set_ = true;
+      if (const char* e = std::getenv("TAGC_ORD_EPOCH_START")) {
+        const uint32_t v = uint32_t(std::strtoul(e, nullptr, 0));
+        zero({{o.epoch, 16}});
+        launches_ += launch_set_u32(o.epoch, v, stream_);
+      }
+    }
     launches_ += launch_decode_ordered(di_, w, hp, o, stream_, take_sketch_event());
   } else {
     launches_ += launch_decode(di_, w, hp, stream_, fused, take_sketch_event());

@@ -361,6 +361,7 @@ class Engine {
   std::vector<DecStats> dec_stats_;
   uint32_t rounds_[2] = {0, 0};
   bool last_ordered_ = false;
+  bool ord_epoch_set_ = false;  // TAGC_ORD_EPOCH_START applied
   uint64_t nvtx_range_ = 0;  // nvtxRangeId_t of the open stage range
   bool nvtx_open_ = false;
   void fetch_rounds();

@@ -200,6 +200,8 @@ int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stre
 // Writes the step's OptEpilogue into its device slot (stream-ordered before
 // the kernels that read it; launched outside any graph).
 int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stream);
+// One device word (stream-ordered; no copy engine on the context stream).
+int launch_set_u32(uint32_t* dst, uint32_t v, cudaStream_t stream);
 // FIFO-order peel (see decode.cu): every generation on the device, inside
 // one cooperative persistent kernel (no host round trip, graph-capturable).
 // slot_key / claim are epoch-tagged, zero-initialised once; epoch is a

@@ -243,3 +243,46 @@ def test_wire_bytes_match_reference(ctx, ref, width):
     assert ctx.to_bytes(words) == ref.index_to_bytes(v, width)
     sk = ctx.sketch_compress(vd, 10, 77)
     assert ctx.to_bytes(sk) == ref.sketch_to_bytes(v, 10, 77)
+
+
+_EPOCH_WRAP_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2504_05638_b200 as tagc
+from oracle import Oracle
+orc = Oracle()
+ctx = tagc.Context(tagc.CompressionConfig(theta=99.0, ratio=10, index_width=1, seed=5), device=0)
+for call in range(4):
+    rng = np.random.default_rng(100 + call)
+    n, ratio, seed = 1 << 18, 4, 4242 + call
+    pres = np.sort(rng.choice(n, int(n * 0.2), replace=False)).astype(np.uint32)
+    v = np.zeros(n, np.float32)
+    v[pres] = rng.integers(-50, 51, pres.size).astype(np.float32)
+    v[pres[v[pres] == 0]] = 1.0
+    sk = orc.sketch_compress(v, ratio, seed)
+    ovals, ounres, opf = orc.peeling_decompress(pres, sk, n, ratio, seed)
+    vals, unres, pf = ctx.peeling_decompress(torch.from_numpy(pres.view(np.int32).copy()).cuda(),
+                                             torch.from_numpy(sk.copy()).cuda(), n, ratio, seed)
+    got = vals.cpu().numpy()
+    assert np.array_equal(unres.cpu().numpy().view(np.uint32), ounres), call
+    peeled = np.setdiff1d(pres, ounres)
+    assert np.array_equal(got[peeled].view(np.uint32), ovals[peeled].view(np.uint32)), call
+print("epoch wrap ok", ctx.last_peel_rounds())
+"""
+
+
+def test_ordered_peel_across_epoch_wrap():
+    """The ordered peel's epoch tags (slot keys, claims) restart from zero once
+    the persistent device epoch passes 0xF0000000: start it one below the wrap
+    point (TAGC_ORD_EPOCH_START; every call advances it at least once, so the
+    second call restarts the tags) and check four FIFO-exact decodes against
+    the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TAGC_ORD_EPOCH_START=str(0xF0000000 - 1))
+    r = subprocess.run([sys.executable, "-c", _EPOCH_WRAP_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "epoch wrap ok" in r.stdout
