@@ -604,15 +604,24 @@ void Engine::ensure_aux() {
 }
 
 // Decode of a batch of segments whose bucket states are far beyond L2
-// (Llama-3-8B: 5.8 GB at W = 1) in groups of <= kDecodeGroupBytes of state:
-// each group's list build, round-0 peel and frontier rounds then hit a bucket
-// state the group's own REDs just left in L2. Results are those of one batch
-// (segments decode independently); statistics land per item as before.
+// (Llama-3-8B: 722M buckets at W = 1) in groups of <= kDecodeGroupBytes of
+// randomly accessed bytes (byte counter + residual per bucket in counter
+// mode: 96 MB; TAGC_DECODE_GROUP_MB): each group's list build, round-0 peel
+// and frontier rounds then hit state the group's own REDs just left in L2,
+// while the group count (10 launches each) stays low (Llama: 48 MB groups
+// 22.6 ms of decode, 96 MB 18.1 ms, 320 MB 18.6 ms). Results are those of
+// one batch (segments decode independently); statistics land per item.
 void Engine::run_decode_grouped(std::vector<DecItem>& items, const HashParams& hp, bool ordered,
                                 cudaEvent_t zero_done, const std::function<void()>& pre_launch) {
-  constexpr uint64_t kDecodeGroupBytes = 48ull << 20, kGroupAbove = 128ull << 20;
+  static const uint64_t kDecodeGroupBytes =
+      (std::getenv("TAGC_DECODE_GROUP_MB") ? std::strtoull(std::getenv("TAGC_DECODE_GROUP_MB"), nullptr, 10) : 96ull) << 20;
+  constexpr uint64_t kGroupAbove = 128ull << 20;
+  // randomly accessed bytes per bucket: the byte counter and the residual
+  // (counter mode), else the u64 state and the residual
+  const bool counters = !std::getenv("TAGC_DECODE_FULL_STATE");
+  const uint64_t per_slot = counters ? 5 : 12;
   uint64_t state_bytes = 0;
-  for (const DecItem& d : items) state_bytes += uint64_t(hp.rows) * d.m * 8;
+  for (const DecItem& d : items) state_bytes += uint64_t(hp.rows) * d.m * per_slot;
   if (ordered || items.size() < 2 || state_bytes <= kGroupAbove) {
     run_decode(items, hp, false, ordered, zero_done, pre_launch);
     return;
@@ -624,8 +633,8 @@ void Engine::run_decode_grouped(std::vector<DecItem>& items, const HashParams& h
   while (b < items.size()) {
     size_t e = b;
     uint64_t bytes = 0;
-    while (e < items.size() && (e == b || bytes + uint64_t(hp.rows) * items[e].m * 8 <= kDecodeGroupBytes))
-      bytes += uint64_t(hp.rows) * items[e++].m * 8;
+    while (e < items.size() && (e == b || bytes + uint64_t(hp.rows) * items[e].m * per_slot <= kDecodeGroupBytes))
+      bytes += uint64_t(hp.rows) * items[e++].m * per_slot;
     std::vector<DecItem> group(items.begin() + b, items.begin() + e);
     run_decode(group, hp, false, false, zero_done, first ? pre_launch : std::function<void()>(), uint32_t(b));
     first = false;
