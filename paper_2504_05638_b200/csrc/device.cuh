@@ -69,6 +69,8 @@ struct EncItem {
   uint32_t n, m, c, flags;
   uint32_t cand_cap, sample_stride, sample_tiles, hi_cap;
   uint64_t mmul;  // fastmod multiplier for m (fastmod_magic), set by the engine
+  uint32_t ds_group;  // deferred-scatter group (kDeferScatter items; groups span <= 2^27 floats)
+  uint32_t ds_pad;
 };
 
 // Select state per item (device; reset by the window kernel every call).

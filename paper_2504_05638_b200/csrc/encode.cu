@@ -1267,9 +1267,11 @@ constexpr uint32_t kDsThreads = 256;  // place: 2 CTAs per SM
 constexpr uint32_t kApplyThreads = 512;
 using BlockScanDs = cub::BlockScan<uint32_t, kDsThreads>;
 
-__device__ __forceinline__ uint32_t ds_entries(const EncItem& e, const SelState& st) {
-  return (st.status == kStatusReady && (e.flags & kDeferScatter) && (e.flags & kWriteSketch))
-             ? min(st.cnt_hi, e.hi_cap) : 0u;
+__device__ __forceinline__ bool ds_member(const EncItem& e, const SelState& st, uint32_t group) {
+  return st.status == kStatusReady && (e.flags & kDeferScatter) && (e.flags & kWriteSketch) && e.ds_group == group;
+}
+__device__ __forceinline__ uint32_t ds_entries(const EncItem& e, const SelState& st, uint32_t group) {
+  return ds_member(e, st, group) ? min(st.cnt_hi, e.hi_cap) : 0u;
 }
 
 __device__ __forceinline__ uint32_t ds_cap(uint32_t total_updates, uint32_t n_bins) {
@@ -1283,8 +1285,9 @@ __device__ __forceinline__ uint32_t ds_cap(uint32_t total_updates, uint32_t n_bi
 __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __restrict__ items,
                                                          const SelState* __restrict__ state, uint32_t n_items,
                                                          const uint2* __restrict__ hi_pool, const HashParams hp,
-                                                         const float* base, uint32_t shift, uint32_t n_bins,
-                                                         uint32_t* __restrict__ fill, uint32_t* __restrict__ ctl,
+                                                         const float* base, uint32_t group, uint32_t shift,
+                                                         uint32_t n_bins, uint32_t* __restrict__ fill,
+                                                         uint32_t* __restrict__ ctl,
                                                          uint2* __restrict__ records, uint2* __restrict__ ovf) {
   __shared__ uint32_t pref[kMaxFlatItems + 1];
   __shared__ typename BlockScanDs::TempStorage s_scan;
@@ -1295,7 +1298,8 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
   uint32_t* s_loff = s_hist + n_bins;                                     // [n_bins]: local offset
   uint32_t* s_gb = s_loff + n_bins;                                       // [n_bins]: global base
   const uint32_t rows = hp.rows;
-  const uint32_t total = flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i]); }, pref);
+  const uint32_t total =
+      flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i], group); }, pref);
   const uint32_t cap = ds_cap(total * rows, n_bins);
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl[1] = cap;
   const uint32_t per_batch = kDsBatch / rows;
@@ -1375,7 +1379,7 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
 // alone).
 __global__ void __launch_bounds__(kApplyThreads) k_ds_apply_smem(const EncItem* __restrict__ items,
                                                               const SelState* __restrict__ state, uint32_t n_items,
-                                                              uint32_t rows, uint32_t shift,
+                                                              uint32_t group, uint32_t rows, uint32_t shift,
                                                               const uint2* __restrict__ records,
                                                               const uint32_t* __restrict__ fill,
                                                               const uint32_t* __restrict__ ctl, float* base) {
@@ -1404,7 +1408,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_ds_apply_smem(const EncItem* 
   const uint64_t g0 = uint64_t(reg) << kApplyShift, g1 = g0 + kApplyRegion;
   for (uint32_t it = 0; it < n_items; ++it) {
     const EncItem& e = items[it];
-    if (!(e.flags & kDeferScatter) || !(e.flags & kWriteSketch) || state[it].status != kStatusReady) continue;
+    if (!ds_member(e, state[it], group)) continue;
     const uint64_t a = uint64_t(e.sketch - base), z = a + uint64_t(rows) * e.m;
     const uint64_t lo = a > g0 ? a : g0, hi = z < g1 ? z : g1;
     for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) __stcs(base + x, s_acc[x - g0]);
@@ -1417,12 +1421,12 @@ __global__ void __launch_bounds__(kApplyThreads) k_ds_apply_smem(const EncItem* 
 // and scattered directly into its freshly cleared sketch).
 __global__ void __launch_bounds__(256) k_ds_zero(const EncItem* __restrict__ items,
                                                  const SelState* __restrict__ state, uint32_t n_items,
-                                                 uint32_t rows) {
+                                                 uint32_t group, uint32_t rows) {
   const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint32_t it = 0; it < n_items; ++it) {
     const EncItem& e = items[it];
-    if (!(e.flags & kDeferScatter) || !(e.flags & kWriteSketch) || state[it].status != kStatusReady) continue;
+    if (!ds_member(e, state[it], group)) continue;
     const uint64_t n = uint64_t(rows) * e.m;
     float* p = e.sketch;
     const uint64_t mis = ((16u - (reinterpret_cast<uintptr_t>(p) & 15u)) & 15u) / 4u;
@@ -1999,8 +2003,9 @@ int launch_set_opt(OptEpilogue* dev_opt, const OptEpilogue& o, cudaStream_t stre
 }
 
 int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
-                            const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
-                            uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf, cudaStream_t stream) {
+                            uint32_t group, const uint2* hi_pool, const HashParams& hp, float* base,
+                            uint64_t span_floats, uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf,
+                            cudaStream_t stream) {
   if (!n_items) return 0;
   if (span_floats > 0xFFFFFFFFull || span_floats == 0) return -1;  // caller scatters directly
   uint32_t lg = 0;
@@ -2012,18 +2017,18 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
   const uint32_t n_bins = uint32_t((span_floats + (1ull << shift) - 1) >> shift);
   const int smem_place = int(2 * kDsBatch * sizeof(uint2) + 3 * n_bins * sizeof(uint32_t));
   cudaFuncSetAttribute((const void*)k_ds_place, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_place);
-  k_ds_place<<<di.sms * 2, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, shift, n_bins,
-                                                         fill, ctl, records, ovf);
+  k_ds_place<<<di.sms * 2, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, group, shift,
+                                                         n_bins, fill, ctl, records, ovf);
   int l = 1;
   if (smem) {
     const uint32_t regions = uint32_t((span_floats + kApplyRegion - 1) >> kApplyShift);
     cudaFuncSetAttribute((const void*)k_ds_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kApplyRegion * 4));
-    k_ds_apply_smem<<<regions, kApplyThreads, kApplyRegion * 4, stream>>>(items, state, n_items, hp.rows, shift,
-                                                                       records, fill, ctl, base);
+    k_ds_apply_smem<<<regions, kApplyThreads, kApplyRegion * 4, stream>>>(items, state, n_items, group, hp.rows,
+                                                                           shift, records, fill, ctl, base);
     ++l;
   } else {
-    k_ds_zero<<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, hp.rows);
+    k_ds_zero<<<di.sms * 4, 256, 0, stream>>>(items, state, n_items, group, hp.rows);
     k_ds_apply<<<di.sms * 8, 256, 0, stream>>>(records, fill, ctl, n_bins, base);
     l += 2;
   }

@@ -472,31 +472,40 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   for (EncItem& e : items) e.mmul = fastmod_magic(e.m);
   // Sketches far beyond L2: defer their scatter to the region-ordered pass
   // (exchange path only, with selection; one span of < 2^32 floats).
-  float* ds_base = nullptr;
-  uint64_t ds_span = 0, ds_cap = 0;
+  // Deferred items are grouped in sketch-address order into spans of at most
+  // 2^27 floats (the deferred scatter's shared-memory path); a group is one
+  // launch_deferred_scatter call.
+  struct DsGroup {
+    float* base;
+    uint64_t span, cap;
+  };
+  std::vector<DsGroup> ds_groups;
+  uint64_t ds_cap = 0;
   {
-    const float* lo = nullptr;
-    const float* hi_end = nullptr;
     auto big = [&](const EncItem& e) {
       return select && (e.flags & kHasAcc) && (e.flags & kWriteSketch) && big_sketch(uint64_t(hp.rows) * e.m);
     };
-    for (const EncItem& e : items)
-      if (big(e)) {
-        if (!lo || e.sketch < lo) lo = e.sketch;
-        if (!hi_end || e.sketch + uint64_t(hp.rows) * e.m > hi_end) hi_end = e.sketch + uint64_t(hp.rows) * e.m;
-      }
-    if (lo && uint64_t(hi_end - lo) <= 0xFFFFFFFFull) {
-      ds_base = const_cast<float*>(lo);
-      ds_span = uint64_t(hi_end - lo);
-      for (EncItem& e : items)
-        if (big(e)) {
-          e.flags |= kDeferScatter;
-          ds_cap += uint64_t(hp.rows) * e.hi_cap;
-        }
+    std::vector<uint32_t> order;
+    for (uint32_t i = 0; i < items.size(); ++i)
+      if (big(items[i])) order.push_back(i);
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return items[a].sketch < items[b].sketch; });
+    constexpr uint64_t kGroupSpan = 1ull << 27;
+    for (uint32_t i : order) {
+      EncItem& e = items[i];
+      const uint64_t len = uint64_t(hp.rows) * e.m;
+      if (len > 0xFFFFFFFFull) continue;  // scattered directly (zeroed below)
+      if (ds_groups.empty() || uint64_t(e.sketch + len - ds_groups.back().base) > kGroupSpan)
+        ds_groups.push_back(DsGroup{e.sketch, 0, 0});
+      DsGroup& g = ds_groups.back();
+      g.span = std::max<uint64_t>(g.span, uint64_t(e.sketch + len - g.base));
+      g.cap += uint64_t(hp.rows) * e.hi_cap;
+      e.flags |= kDeferScatter;
+      e.ds_group = uint32_t(ds_groups.size() - 1);
     }
+    for (const DsGroup& g : ds_groups) ds_cap = std::max(ds_cap, g.cap);
     // The exchange prologue leaves big sketches unzeroed (big_sketch): the
-    // deferred ones are zeroed by the deferred scatter right before their
-    // REDs, any others (span too large to defer) now, before the scatter.
+    // deferred ones are written (or zeroed) by the deferred scatter, any
+    // others now, before the scatter.
     std::vector<std::pair<void*, uint64_t>> now;
     for (const EncItem& e : items)
       if (big(e) && !(e.flags & kDeferScatter)) now.push_back({e.sketch, uint64_t(hp.rows) * e.m * 4});
@@ -509,9 +518,10 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
   // per-batch words only (err[1] bracket miss, err[3] chunk counter); the
   // NaN (err[0]) and peer-timeout (err[2]) flags stay sticky until
   // sync_check reports them, so a later batch or call cannot erase them
-  uint32_t* ds_fill = ds_base ? static_cast<uint32_t*>(ws_.get("ds_fill", (kDsMaxBins + 4) * 4, false, stream_))
-                              : nullptr;
-  zero({{err + 1, 4}, {err + 3, 4}, {ds_fill, ds_fill ? (kDsMaxBins + 4) * 4 : 0}});
+  const uint64_t ds_words = ds_groups.size() * uint64_t(kDsMaxBins + 4);  // fill + ctl per group
+  uint32_t* ds_fill = ds_groups.empty() ? nullptr
+                                        : static_cast<uint32_t*>(ws_.get("ds_fill", ds_words * 4, false, stream_));
+  zero({{err + 1, 4}, {err + 3, 4}, {ds_fill, ds_fill ? ds_words * 4 : 0}});
   if (select) {
     auto* sh = static_cast<uint32_t*>(ws_.get("sample_hist", size_t(n) * kSampleStride * 4, true, stream_));
     auto* fh = static_cast<uint32_t*>(ws_.get("fb_hist", size_t(n) * kRadixBins * 4, true, stream_));
@@ -536,7 +546,7 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     ev_record(2);
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
-    if (ds_base) {
+    if (!ds_groups.empty()) {
       auto* rec = static_cast<uint2*>(ws_.get("ds_records", (ds_cap + ds_cap / 16 + uint64_t(kDsMaxBins) * 1024) * 8,
                                               false, stream_));
       auto* ovf = static_cast<uint2*>(ws_.get("ds_overflow", ds_cap * 8, false, stream_));
@@ -551,14 +561,17 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
         cuda_check(cudaStreamWaitEvent(ds_stream_, ds_fork_, 0), "ds fork wait");
         ds_s = ds_stream_;
       }
-      const int l = launch_deferred_scatter(di_, d_items, state, n, hp_pool, hp, ds_base, ds_span, ds_fill,
-                                            ds_fill + kDsMaxBins, rec, ovf, ds_s);
+      for (uint32_t g = 0; g < ds_groups.size(); ++g) {  // groups share the record buffers: in stream order
+        uint32_t* fill = ds_fill + uint64_t(g) * (kDsMaxBins + 4);
+        const int l = launch_deferred_scatter(di_, d_items, state, n, g, hp_pool, hp, ds_groups[g].base,
+                                              ds_groups[g].span, fill, fill + kDsMaxBins, rec, ovf, ds_s);
+        if (l < 0) throw CudaError("deferred sketch scatter: span too large");
+        launches_ += l;
+      }
       if (ds_side_ok_) {
         cuda_check(cudaEventRecord(ds_done_, ds_stream_), "ds done");
         sketch_pending_ = true;
       }
-      if (l < 0) throw CudaError("deferred sketch scatter: span too large");
-      launches_ += l;
     }
     ev_record(3);
     static const bool sel_dbg = std::getenv("TAGC_DEBUG_SELECT") != nullptr;

@@ -82,9 +82,12 @@ int launch_rank_sum_u32(const uint32_t* const* in_ptrs, uint32_t world, uint32_t
 // re-encode scatters directly), so callers leave those sketches unzeroed;
 // larger spans are zeroed here and applied with L2 REDs bin by bin.
 constexpr uint32_t kDsMaxBins = 4096;
+// One call per deferred-scatter group: the items with ds_group == group,
+// whose sketches lie in [base, base + span_floats).
 int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelState* state, uint32_t n_items,
-                            const uint2* hi_pool, const HashParams& hp, float* base, uint64_t span_floats,
-                            uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf, cudaStream_t stream);
+                            uint32_t group, const uint2* hi_pool, const HashParams& hp, float* base,
+                            uint64_t span_floats, uint32_t* fill, uint32_t* ctl, uint2* records, uint2* ovf,
+                            cudaStream_t stream);
 // Owner-side optimizer step on the decoded shard (train.cpp:202-220, 355-359):
 // kind 0 SGD, 1 momentum-free AdamW (adam_v in/out).
 int launch_apply_optimizer(const OptEpilogue& o, uint64_t n, cudaStream_t stream);
