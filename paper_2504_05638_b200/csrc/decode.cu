@@ -92,6 +92,17 @@ __device__ __forceinline__ bool words_full(uint32_t w0, uint32_t nwords, bool w4
 
 __device__ __forceinline__ float canonical(float v) { return v == 0.0f ? 0.0f : v; }
 
+// Counter mode: one counter of 2^cnt_shift bits (8 or 4) per bucket, packed
+// into u32 words (w.cnt8).
+__device__ __forceinline__ void cnt_add(const DecodeWork& w, uint64_t slot) {
+  const uint32_t cs = w.cnt_shift, per = 5u - cs;
+  red_add_u32(w.cnt8 + (slot >> per), 1u << (uint32_t(slot & ((1u << per) - 1u)) << cs));
+}
+__device__ __forceinline__ uint32_t cnt_get(const DecodeWork& w, uint64_t slot) {
+  const uint32_t cs = w.cnt_shift, per = 5u - cs;
+  return (ldcg(w.cnt8 + (slot >> per)) >> (uint32_t(slot & ((1u << per) - 1u)) << cs)) & ((1u << (1u << cs)) - 1u);
+}
+
 __device__ __forceinline__ uint32_t warp_sum32(uint32_t x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
       const uint32_t p = w.plist[i];
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
         const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
-        if (w.cnt8) red_add_u32(w.cnt8 + (slot >> 2), 1u << (8u * uint32_t(slot & 3u)));
+        if (w.cnt8) cnt_add(w, slot);
         else atomicAdd(w.slot_state + slot, st_add(i));  // result unused: RED.ADD.64
       }
     }
@@ -428,7 +439,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
       const uint32_t p = staged ? s_pos[q] : __ldcg(w.plist + base + q);
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
         const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
-        red_add_u32(w.cnt8 + (slot >> 2), 1u << (8u * uint32_t(slot & 3u)));
+        cnt_add(w, slot);
       }
     }
     __syncthreads();  // scan storage / stage reuse
@@ -549,7 +560,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
           ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
           if (w.cnt8) {
             const uint64_t sl = e.slot_base + ls[r];
-            st[r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+            st[r] = cnt_get(w, sl);
           } else {
             st[r] = ldcg(w.slot_state + e.slot_base + ls[r]);
           }
@@ -667,7 +678,7 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
         ls[k][r] = uint64_t(r) * m + dev_bucket(hp.row[r], p[k], m, mm);
         const uint64_t sl = sb[k] + ls[k][r];
         if (!act[k]) c[k][r] = 0u;
-        else if (w.cnt8) c[k][r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+        else if (w.cnt8) c[k][r] = cnt_get(w, sl);
         else c[k][r] = st_count(ldcg(w.slot_state + sl));
       }
     }
@@ -1607,7 +1618,7 @@ __global__ void __launch_bounds__(256, 3) k_r0_emit(DecodeWork w, const HashPara
           if (r < hp.rows) {  // every row's probe in flight before any is inspected
             ls[r] = uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
             const uint64_t sl = e.slot_base + ls[r];
-            c[r] = (ldcg(w.cnt8 + (sl >> 2)) >> (8u * uint32_t(sl & 3u))) & 0xFFu;
+            c[r] = cnt_get(w, sl);
           }
         int best = -1;
         uint32_t shared = 0;

@@ -707,15 +707,23 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.unresolved = want_unresolved ? static_cast<uint32_t*>(ws_.get("unresolved", list * 4, false, stream_))
                                  : nullptr;
   // Counter mode: round 0 needs only "one entry or more" per bucket, so it
-  // counts in bytes (slots bytes instead of 8 * slots: 27 MB at 2^28 / r 10,
+  // counts in bytes or nibbles (slots bytes instead of 8 * slots: 27 MB at 2^28 / r 10,
   // L2-resident) and the (count, index sum) state is built later for the few
   // buckets round 0 leaves unresolved. A byte counter is safe while a bucket
   // cannot plausibly hold 256 entries: the presence bound over the row
   // length stays <= 16 (Poisson tail ~1e-200), else the full state is used.
+  // Nibble counters (half the footprint, so they stay in L2 under the list
+  // build's streams) while the bound stays <= m / 2: P(Poisson(0.5) >= 16)
+  // ~ 1e-18 per bucket.
   bool counters = !ordered && !std::getenv("TAGC_DECODE_FULL_STATE");
-  for (const DecItem& d : items)
-    counters = counters && double(std::min(d.list_cap ? d.list_cap : d.n, d.n)) <= 16.0 * double(d.m);
-  const uint64_t cnt_words = (slots + 3) / 4;
+  bool nibbles = counters && !std::getenv("TAGC_DECODE_BYTE_COUNTERS");
+  for (const DecItem& d : items) {
+    const double bound = double(std::min(d.list_cap ? d.list_cap : d.n, d.n));
+    counters = counters && bound <= 16.0 * double(d.m);
+    nibbles = nibbles && bound <= 0.5 * double(d.m);
+  }
+  w.cnt_shift = nibbles ? 2u : 3u;
+  const uint64_t cnt_words = nibbles ? (slots + 7) / 8 : (slots + 3) / 4;
   // round 0 inside the dense emit unless the owner step consumes the values
   const bool fused = counters && !ordered && !opt_on_ && fused_emit_;
   w.cnt8 = counters ? static_cast<uint32_t*>(ws_.get("cnt8", cnt_words * 4, false, stream_)) : nullptr;

@@ -160,6 +160,7 @@ struct DecodeWork {
   // packed four to a word (L2-resident), and slot_state is only built for
   // the buckets of entries round 0 leaves unresolved (ulist, qcount[14]).
   uint32_t* cnt8;
+  uint32_t cnt_shift;              // log2 of the counter width: 3 (bytes) or 2 (nibbles)
   uint32_t* ulist;
   uint32_t* bitmap;                // recovered flag per presence-list entry
   float* val;                      // decoded value per presence-list entry
