@@ -189,6 +189,10 @@ std::vector<float> baseline_reduce_shard(const ShardSpec& shard, std::span<const
   CShard cs(shard);
   check(tagc_ctx_ledger_reset(ctx));
   check(tagc_baseline_reduce_shard_sim(ctx, &cs.s, w, dg.data(), d + w * n));
+  // the context works on its own non-blocking stream and this call returns
+  // no statistics (so it does not synchronise): wait before the legacy-stream
+  // copy reads the result, and before the next call overwrites the inputs
+  check(tagc_ctx_sync(ctx));
   std::vector<float> out(n);
   cuda(cudaMemcpy(out.data(), d + w * n, n * 4, cudaMemcpyDeviceToHost), "D2H");
   replay_ledger(ctx, world);
@@ -227,6 +231,7 @@ ShardReduceResult tagc_reduce_shard(const ShardSpec& shard, std::span<const std:
     check(tagc_reduce_shard_sim_audit(ctx, &cs.s, w, dg.data(), da.data(), d_out, &st, d_audit));
   else
     check(tagc_reduce_shard_sim(ctx, &cs.s, w, dg.data(), da.data(), d_out, &st));
+  check(tagc_ctx_sync(ctx));  // (a call with statistics has synchronised already; kept explicit)
   ShardReduceResult res;
   res.decoded.emplace(n);
   cuda(cudaMemcpy(res.decoded->data(), d_out, n * 4, cudaMemcpyDeviceToHost), "D2H out");
