@@ -162,6 +162,7 @@ Engine::Engine(const CompressionConfig& cfg, uint32_t world, uint32_t rank, int 
   if (const char* v = std::getenv("TAGC_SIDE_STREAM")) side_stream_ = std::atoi(v) != 0;
   if (const char* v = std::getenv("TAGC_DEFER_SCATTER_BYTES")) defer_scatter_bytes_ = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("TAGC_FUSED_EMIT")) fused_emit_ = std::atoi(v) != 0;
+  if (const char* v = std::getenv("TAGC_FORCE_COLLECTIVE")) force_collective_ = std::atoi(v) != 0;
   if (world == 0 || rank >= world) throw InvalidArgument("rank must be below the world size");
   cfg_.validate_for_world(world);
   int ndev = 0;
@@ -1312,8 +1313,9 @@ void Engine::finish_exchange(PeelStats* stats) {
   uint32_t* send_u = xs_.send_u;
   float* recv_f = send_f;
   uint32_t* recv_u = send_u;
-  if (W > 1) {
+  if (W > 1 || (force_collective_ && comm_)) {
     if (!comm_) throw InvalidArgument("multi-rank context has no NCCL communicator or peer exchange");
+    join_sketch();  // W == 1 side-stream scatter: the sketches are final before they are sent
     recv_f = static_cast<float*>(ws_.get("nc_recv_f", Bf * 4, false, stream_));
     recv_u = static_cast<uint32_t*>(ws_.get("nc_recv_u", Bu * 4, false, stream_));
     nccl_check(nccl().GroupStart(), "ncclGroupStart");
@@ -1576,7 +1578,7 @@ void Engine::baseline_shards(const std::vector<ShardSpec>& shards, const float* 
   }
   launches_ = 0;
   const float* base = grad + shards[0].begin;
-  if (world_ == 1) {
+  if (world_ == 1 && !(force_collective_ && comm_)) {
     cuda_check(cudaMemcpyAsync(out, base, L * 4, cudaMemcpyDeviceToDevice, stream_), "D2D");
   } else {
     if (!comm_) throw InvalidArgument("multi-rank context has no NCCL communicator");

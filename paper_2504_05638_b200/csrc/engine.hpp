@@ -340,6 +340,9 @@ class Engine {
   bool big_sketch(uint64_t floats) const { return floats * 4 > defer_scatter_bytes_; }
   // counter-mode decode with round 0 inside the dense emit (TAGC_FUSED_EMIT=1; off: 0.68 vs 0.50 ms on C4)
   bool fused_emit_ = false;
+  // TAGC_FORCE_COLLECTIVE=1: a one-rank NCCL context runs the grouped
+  // reduce-scatters anyway (exercises the NCCL data path on one GPU)
+  bool force_collective_ = false;
   bool side_stream_ = true;  // W = 1 raw copies on the low-priority side stream (TAGC_SIDE_STREAM=0: in order)
   bool use_tma_ = true;  // TMA-staged fused pass (TAGC_FUSED_TMA=0 selects the register path)
   uint32_t* err_flag();

@@ -124,3 +124,48 @@ def test_graph_replay_matches_oracle(world1):
         assert np.array_equal(bits(acc.cpu().numpy()), bits(oacc))
         check_close(out.cpu().numpy(), ref)
     assert ctx.last_launches() > 10
+
+
+@pytest.mark.parametrize("width", [4, 1])
+def test_nccl_collective_one_rank_matches_oracle(world1, monkeypatch, width):
+    """The NCCL data path on one GPU: a one-rank communicator
+    (tagc_nccl_unique_id + tagc_ctx_init_nccl) with TAGC_FORCE_COLLECTIVE=1
+    runs the grouped ncclReduceScatter of the f32 and u32 owner blocks (and,
+    for a 1-bit index with stats, the ncclMax support reduce-scatter), and the
+    owner decodes the RECEIVED blocks. Against the oracle over three
+    error-feedback steps, and the uncompressed comparator through
+    ncclReduceScatter equal to the gradient bit for bit."""
+    shards, grads, refs = world1
+    monkeypatch.setenv("TAGC_FORCE_COLLECTIVE", "1")
+    cfg = dict(CFG, index_width=width)
+    ctx = tagc.Context(tagc.CompressionConfig(**cfg), device=0)
+    ctx.init_nccl(tagc.Context.nccl_unique_id())
+    n = shards[0].size()
+    acc = torch.zeros(n, device=DEV)
+    out = torch.empty(n, device=DEV)
+    if width == 4:
+        for g, (ref, rst, oacc) in zip(grads, refs):
+            _, st = ctx.tagc_reduce_shards(shards, torch.from_numpy(g).to(DEV), acc, out, stats=True)
+            assert np.array_equal(bits(acc.cpu().numpy()), bits(oacc))
+            for k in ("presence", "peeled", "unresolved", "compressed_segments", "baseline_segments"):
+                assert getattr(st, k) == rst[k], (k, st, rst)
+            check_close(out.cpu().numpy(), ref)
+    else:  # 1-bit: the in-place W=1 path of a context without the collective as the reference
+        ref_ctx = tagc.Context(tagc.CompressionConfig(**cfg), device=0)
+        ref_acc = torch.zeros(n, device=DEV)
+        ref_out = torch.empty(n, device=DEV)
+        for g in grads:
+            gd = torch.from_numpy(g).to(DEV)
+            _, st = ctx.tagc_reduce_shards(shards, gd, acc, out, stats=True)
+            _, rst = ref_ctx.tagc_reduce_shards(shards, gd, ref_acc, ref_out, stats=True)
+            assert np.array_equal(bits(acc.cpu().numpy()), bits(ref_acc.cpu().numpy()))
+            # values: the same tolerance as against the oracle (peel rounds
+            # subtract with float REDs, whose order differs run to run)
+            check_close(out.cpu().numpy(), ref_out.cpu().numpy().astype(np.float64))
+            assert (st.presence, st.peeled, st.unresolved, st.index_lost, st.index_spurious) == \
+                (rst.presence, rst.peeled, rst.unresolved, rst.index_lost, rst.index_spurious)
+    g = torch.from_numpy(grads[0]).to(DEV)
+    base = torch.empty(n, device=DEV)
+    ctx.baseline_reduce_shards(shards, g, base)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(base.cpu().numpy()), bits(grads[0]))
