@@ -1263,7 +1263,7 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 constexpr uint32_t kApplyShift = 15;  // 32K floats = 128 KB per shared-memory region
 constexpr uint32_t kApplyRegion = 1u << kApplyShift;
 constexpr uint32_t kDsBatch = 4096;   // staged updates per place batch
-constexpr uint32_t kDsThreads = 256;  // place: 2 CTAs per SM
+constexpr uint32_t kDsThreads = 512;  // place: 2 CTAs per SM
 constexpr uint32_t kApplyThreads = 512;
 using BlockScanDs = cub::BlockScan<uint32_t, kDsThreads>;
 
@@ -1311,7 +1311,7 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
     for (uint32_t i = threadIdx.x; i < n_bins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     // kPer entries per thread loaded before any is hashed (memory-level parallelism)
-    constexpr uint32_t kPer = 8;
+    constexpr uint32_t kPer = 4;
     for (uint32_t q0 = b0; q0 < b1; q0 += kPer * blockDim.x) {
     uint2 kv[kPer];
     uint32_t kit[kPer];
