@@ -1260,7 +1260,7 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 //  * k_ds_overflow adds the overflow list with REDs, after the apply.
 // Same sums as the direct scatter; only the float summation order differs,
 // as it does between any two runs of the direct scatter.
-constexpr uint32_t kApplyShift = 15;  // 32K floats = 128 KB per shared-memory region
+constexpr uint32_t kApplyShift = 14;  // 16K floats = 64 KB per shared-memory region (2 per 32K-float bin)
 constexpr uint32_t kApplyRegion = 1u << kApplyShift;
 constexpr uint32_t kDsBatch = 4096;   // staged updates per place batch
 constexpr uint32_t kDsThreads = 512;  // place: 2 CTAs per SM
@@ -2010,8 +2010,8 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
   if (span_floats > 0xFFFFFFFFull || span_floats == 0) return -1;  // caller scatters directly
   uint32_t lg = 0;
   while ((1ull << lg) < span_floats) ++lg;
-  const bool smem = lg <= 27;  // one shared-memory region per bin, <= 4096 bins
-  static const uint32_t extra = std::getenv("TAGC_DS_BIN_SHIFT") ? uint32_t(std::atoi(std::getenv("TAGC_DS_BIN_SHIFT"))) : 0u;
+  const bool smem = lg <= 27;  // bins of 2 shared-memory regions, <= 4096 bins
+  static const uint32_t extra = std::getenv("TAGC_DS_BIN_SHIFT") ? uint32_t(std::atoi(std::getenv("TAGC_DS_BIN_SHIFT"))) : 1u;
   const uint32_t shift = smem ? std::max<uint32_t>(kApplyShift + extra, lg > 12 ? lg - 12 : 0)
                               : std::max<uint32_t>(22, lg - 12);
   const uint32_t n_bins = uint32_t((span_floats + (1ull << shift) - 1) >> shift);
