@@ -1251,9 +1251,11 @@ __global__ void __launch_bounds__(256) k_fixup(const EncItem* __restrict__ items
 //    into that bin's fixed-capacity slice (bins are hash-uniform: capacity =
 //    mean * 17/16 + 1024, the excess goes to an overflow list). No count
 //    pass, no global scan, coalesced runs instead of 8-byte scatters.
-//  * spans up to 2^26 floats (256 MB): k_ds_apply_smem sums each 32K-float
-//    region in shared memory (the CTAs of a bin read the bin's run, L2
-//    resident, and keep their region's updates) and stores it with plain
+//  * groups spanning up to 2^27 floats (512 MB; the engine splits larger
+//    sets of deferred sketches into such groups): bins of 32K floats, and
+//    k_ds_apply_smem sums each 16K-float region in shared memory (the two
+//    CTAs of a bin read the bin's run, L2 resident, and keep their region's
+//    updates) and stores it with plain
 //    coalesced stores over the deferred sketches' part of the region — no
 //    zeroing pass, no L2 atomics. Larger spans: zeroing pass + L2 REDs bin by
 //    bin (k_ds_apply).
@@ -1372,7 +1374,7 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
   }
 }
 
-// One CTA per 32K-float region (2^(shift - 15) CTAs per bin): the bin's run
+// One CTA per 16K-float region (2^(shift - kApplyShift) CTAs per bin): the bin's run
 // is read by each of its CTAs (L2 resident), each keeps its region's updates
 // in shared memory, then stores the region over the part that belongs to
 // deferred, finally-selected sketches (gaps and fallen-back items are left
