@@ -1180,16 +1180,26 @@ template <typename Sync>
 __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const HashParams& hp, const OrdState& o,
                                                    uint32_t g, uint32_t n, uint64_t dom, uint32_t ep, uint32_t part,
                                                    uint32_t nparts, uint32_t* cnt, uint32_t* s_q, uint32_t* s_nq,
-                                                   uint32_t* s_base, uint32_t* s_warp, Sync sync) {
+                                                   uint32_t* s_base, uint32_t* s_warp, Sync sync, int& mk) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t rows = hp.rows;
   const uint32_t* u = (g & 1) ? o.u1 : o.u0;
   // A: place every pushed slot at its FIFO key
-  for (uint32_t t = part * blockDim.x + tid; t < n; t += nparts * blockDim.x) {
-    const uint32_t s = ldcg(u + t);
-    o.dense[uint32_t(ldcg(o.slot_key + s))] = s + 1u;
+  for (uint32_t t0 = part * blockDim.x + tid; t0 < n; t0 += 4 * nparts * blockDim.x) {
+    uint32_t sl[4], key[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // four slots' key loads in flight per thread
+      const uint32_t t = t0 + q * nparts * blockDim.x;
+      sl[q] = t < n ? ldcg(u + t) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) key[q] = sl[q] != 0xFFFFFFFFu ? uint32_t(ldcg(o.slot_key + sl[q])) : 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (sl[q] != 0xFFFFFFFFu) o.dense[key[q]] = sl[q] + 1u;
   }
   sync();
+  PEEL_MARK(mk++);
   // B: non-empty keys per part (contiguous chunks of 1024-key tiles)
   const uint64_t tiles = (dom + 1023) / 1024;
   const uint64_t per = (tiles + nparts - 1) / nparts;
@@ -1212,6 +1222,7 @@ __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const Ha
     o.cta[part] = t;
   }
   sync();
+  PEEL_MARK(mk++);
   // C: ordered write of the queue (+ reset of the dense keys, + claims)
   uint32_t off = 0;
   for (uint32_t i = tid; i < part; i += blockDim.x) off += ldcg(o.cta + i);
@@ -1250,11 +1261,13 @@ __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const Ha
     if (mine) {
       if (k + 4 <= hi) *reinterpret_cast<uint4*>(o.dense + k) = make_uint4(0, 0, 0, 0);
       else for (uint32_t x = 0; x < 4; ++x) if (k + x < hi) o.dense[k + x] = 0;
+      unsigned long long st[4];
+#pragma unroll
+      for (uint32_t x = 0; x < 4; ++x) st[x] = v[x] ? ldcg(w.slot_state + (v[x] - 1u)) : 0ull;  // in flight together
+#pragma unroll
       for (uint32_t x = 0; x < 4; ++x) if (v[x]) {
-        const uint32_t s = v[x] - 1u;
-        o.q[pos] = s;
-        const unsigned long long st = ldcg(w.slot_state + s);
-        if (st_count(st) == 1u) atomicMax(o.claim + st_entry(st), ord_tag(ep, ~pos));
+        o.q[pos] = v[x] - 1u;
+        if (st_count(st[x]) == 1u) atomicMax(o.claim + st_entry(st[x]), ord_tag(ep, ~pos));
         ++pos;
       }
     }
@@ -1262,6 +1275,7 @@ __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const Ha
     __syncthreads();
   }
   sync();
+  PEEL_MARK(mk++);
   // D: peel the queue; subtractions are tagged with the next epoch
   uint32_t won = 0;
   uint32_t* un = (g & 1) ? o.u0 : o.u1;
@@ -1323,6 +1337,8 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gstride = uint64_t(gridDim.x) * blockDim.x;
   uint32_t* cnt = w.qcount + 8;
+  int mk = 0;
+  PEEL_MARK(mk++);
   uint32_t ep = ldcg(o.epoch);
   if (ep >= kOrdWrap) {  // once per 2^32 generations: restart the tags from zero
     for (uint64_t x = gtid; x < o.slot_key_cap; x += gstride) o.slot_key[x] = 0ull;
@@ -1367,6 +1383,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
     }
   }
   stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, o.u0, cnt);
+  PEEL_MARK(mk++);
   // ---- generations >= 1
   uint64_t dom = w.total_slots * hp.rows;
   uint32_t won = 0, g = 0;
@@ -1384,7 +1401,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
       w.qcount[2] += 1;
     }
     won += ord_generation(w, hp, o, g, n, dom, ep, blockIdx.x, gridDim.x, cnt, s_q, s_nq, &s_base, s_warp,
-                          [&] { grid.sync(); });
+                          [&] { grid.sync(); }, mk);
     dom = uint64_t(n) * hp.rows;
     ++ep;
   }
@@ -1402,7 +1419,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
         w.qcount[3] += 1;
       }
       won += ord_generation(w, hp, o, g, n, dom, ep, 0, 1, cnt, s_q, s_nq, &s_base, s_warp,
-                            [] { __syncthreads(); });
+                            [] { __syncthreads(); }, mk);
       dom = uint64_t(n) * hp.rows;
       ++ep;
     }
