@@ -597,6 +597,10 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
         const float v = canonical(sg * ldcg(e.sketch + local));
         w.val[i] = v;
         info = make_uint2(__float_as_uint(v), shared | 0x100u | (uint32_t(best) << 12));
+        if (w.wmask && shared) {  // ordered peel: winner slot of an entry that pushes
+          const uint64_t ws = e.slot_base + local;
+          red_or_u32(w.wmask + (ws >> 5), 1u << (ws & 31));
+        }
         peeled = true;
         sub = shared != 0u;
         ++won;
@@ -716,6 +720,14 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
           w.val[i] = v;
           info = make_uint2(__float_as_uint(v), shared[k] | 0x100u | (uint32_t(best[k]) << 12));
           ++won;
+          if (w.wmask && shared[k]) {  // ordered peel: winner slot of an entry that pushes
+            uint64_t lb = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (r == best[k]) lb = ls[k][r];
+            const uint64_t ws = sb[k] + lb;
+            red_or_u32(w.wmask + (ws >> 5), 1u << (ws & 31));
+          }
         } else if (w.slot_mark) {  // unresolved after round 0: its buckets still matter
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -1347,6 +1359,66 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
     grid.sync();
   }
   ++ep;  // generation 0's subtractions
+  // Generation 0's FIFO keys are (winner slot, row); only winners of entries
+  // with a shared bucket push, so the keys are made dense over those: rank of
+  // the winner slot among them (popcount prefix of wmask), times rows.
+  const uint64_t nwords = o.wwords;
+  uint32_t n_win;
+  {
+    const uint64_t per = (nwords + gridDim.x - 1) / gridDim.x;
+    const uint64_t w0 = min(nwords, uint64_t(blockIdx.x) * per), w1 = min(nwords, w0 + per);
+    uint32_t c = 0;
+    for (uint64_t x = w0 + threadIdx.x; x < w1; x += blockDim.x) c += __popc(ldcg(o.wmask + x));
+    c = warp_sum32(c);
+    if (lane == 0) s_warp[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += s_warp[i];
+      o.cta[blockIdx.x] = t;
+    }
+    grid.sync();
+    uint32_t off = 0, all = 0;
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      const uint32_t x = ldcg(o.cta + i);
+      all += x;
+      off += i < blockIdx.x ? x : 0u;
+    }
+    off = warp_sum32(off);
+    all = warp_sum32(all);
+    __syncthreads();
+    if (lane == 0) s_warp[threadIdx.x >> 5] = off;
+    __syncthreads();
+    off = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) off += s_warp[i];
+    __syncthreads();
+    if (lane == 0) s_warp[threadIdx.x >> 5] = all;
+    __syncthreads();
+    n_win = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) n_win += s_warp[i];
+    __syncthreads();
+    // exclusive prefix per word of this CTA's range, 256 words at a time
+    for (uint64_t b = w0; b < w1; b += blockDim.x) {
+      const uint64_t x = b + threadIdx.x;
+      const uint32_t pc = x < w1 ? __popc(ldcg(o.wmask + x)) : 0u;
+      uint32_t incl = pc;
+      _Pragma("unroll") for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= uint32_t(d)) incl += y;
+      }
+      if (lane == 31) s_warp[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      uint32_t wbase = 0, tot = 0;
+      for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+        wbase += i < (threadIdx.x >> 5) ? s_warp[i] : 0u;
+        tot += s_warp[i];
+      }
+      if (x < w1) o.wrank[x] = off + wbase + incl - pc;
+      off += tot;
+      __syncthreads();
+    }
+    grid.sync();
+  }
   // ---- generation 0: round-0 peeled entries leave every bucket they share;
   // pushes keyed (winner slot, row) — the reference's ascending seed order
   const uint32_t total = w.qcount[5];
@@ -1365,7 +1437,10 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
         e = w.items + w.pitem[i];
         const uint32_t best = (info.y >> 12) & 0xFu;
         const uint64_t ws = e->slot_base + uint64_t(best) * e->m + dev_bucket(row_coef(hp, best), p, e->m, e->mmul);
-        wkey = ws * hp.rows;
+        if (rows) {  // rank of the winner slot among the pushing entries' winners
+          const uint32_t wm = ldcg(o.wmask + (ws >> 5));
+          wkey = uint64_t(ldcg(o.wrank + (ws >> 5)) + __popc(wm & ((1u << (ws & 31)) - 1u))) * hp.rows;
+        }
       }
     }
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
@@ -1385,7 +1460,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
   stage_flush<uint32_t, kPushStage>(s_q, s_nq, &s_base, o.u0, cnt);
   PEEL_MARK(mk++);
   // ---- generations >= 1
-  uint64_t dom = w.total_slots * hp.rows;
+  uint64_t dom = uint64_t(n_win) * hp.rows;
   uint32_t won = 0, g = 0;
   bool tail = false;
   for (;; ++g) {

@@ -729,7 +729,10 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   const bool fused = counters && !ordered && !opt_on_ && fused_emit_;
   w.cnt8 = counters ? static_cast<uint32_t*>(ws_.get("cnt8", cnt_words * 4, false, stream_)) : nullptr;
   w.ulist = counters ? static_cast<uint32_t*>(ws_.get("ulist", list * 4 + 4, false, stream_)) : nullptr;
-  zero({{w.bitmap, bm * 4}, {w.qcount, 64}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
+  const uint64_t wwords = mark_words + 1;
+  w.wmask = ordered ? static_cast<uint32_t*>(ws_.get("ord_wmask", wwords * 4, false, stream_)) : nullptr;
+  zero({{w.wmask, w.wmask ? wwords * 4 : 0},
+        {w.bitmap, bm * 4}, {w.qcount, 64}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
         {w.slot_mark, w.slot_mark ? mark_words * 4 : 0},
         {counters ? static_cast<void*>(w.cnt8) : static_cast<void*>(w.slot_state), counters ? cnt_words * 4 : slots * 8},
         {w.tile_state, wt * 8}});  // one launch for every decode scratch reset
@@ -754,6 +757,9 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     o.u0 = static_cast<uint32_t*>(ws_.get("ord_u0", slots * 4, false, stream_));
     o.u1 = static_cast<uint32_t*>(ws_.get("ord_u1", slots * 4, false, stream_));
     o.cta = static_cast<uint32_t*>(ws_.get("ord_cta", size_t(ordered_loop_grid(di_)) * 4, false, stream_));
+    o.wmask = w.wmask;
+    o.wrank = static_cast<uint32_t*>(ws_.get("ord_wrank", wwords * 4, false, stream_));
+    o.wwords = wwords;
     o.epoch = static_cast<uint32_t*>(ws_.get("ord_epoch", 16, true, stream_));  // fixed size: never regrown
     if (!ord_epoch_set_) {  // test hook: start the epoch just below the wrap point
       ord_epoch_set_ = true;

@@ -162,6 +162,7 @@ struct DecodeWork {
   uint32_t* cnt8;
   uint32_t cnt_shift;              // log2 of the counter width: 3 (bytes) or 2 (nibbles)
   uint32_t* ulist;
+  uint32_t* wmask;                 // ordered peel: winner-slot bits set by round 0 (or nullptr)
   uint32_t* bitmap;                // recovered flag per presence-list entry
   float* val;                      // decoded value per presence-list entry
   uint32_t* slot_mark;             // per bucket: holds an entry round 0 left unresolved (or nullptr)
@@ -220,6 +221,9 @@ struct OrdState {
   uint32_t* u0;                  // unordered pushes, even generations
   uint32_t* u1;                  // unordered pushes, odd generations
   uint32_t* cta;                 // per-CTA counts of the compaction
+  uint32_t* wmask;               // per slot bit: winner slot of a round-0 entry with a shared bucket (zeroed per call)
+  uint32_t* wrank;               // per wmask word: exclusive popcount prefix
+  uint64_t wwords;               // wmask words
   uint32_t* epoch;               // persistent device epoch
   uint64_t slot_key_cap, claim_cap;  // allocated elements (cleared on epoch wrap)
 };
