@@ -1421,14 +1421,17 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
   }
   // ---- generation 0: round-0 peeled entries leave every bucket they share;
   // pushes keyed (winner slot, row) — the reference's ascending seed order
-  const uint32_t total = w.qcount[5];
+  // only round 0's compact list (entries peeled with a shared bucket) pushes
+  const uint32_t total = ldcg(&w.qcount[13]);
   for (uint64_t base = gtid - lane; base < total; base += gstride) {
-    const uint64_t i = base + lane;
+    const uint64_t j = base + lane;
+    uint64_t i = 0;
     uint32_t p = 0, rows = 0;
     float v = 0.0f;
     uint64_t wkey = 0;
     const DecItem* e = w.items;
-    if (i < total) {
+    if (j < total) {
+      i = ldcg(w.r0_list + j);
       const uint2 info = w.pinfo[i];
       if (info.y & 0x100u) {
         rows = info.y & 0xFFu;

@@ -693,7 +693,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   const uint64_t mark_words = (slots + 31) / 32;
   w.slot_mark = ordered ? nullptr : static_cast<uint32_t*>(ws_.get("slot_mark", mark_words * 4, false, stream_));
   w.tile_base = static_cast<uint32_t*>(ws_.get("tile_base", wt * 4, false, stream_));
-  w.r0_list = ordered ? nullptr : static_cast<uint32_t*>(ws_.get("r0_list", list * 4 + 4, false, stream_));
+  w.r0_list = static_cast<uint32_t*>(ws_.get("r0_list", list * 4 + 4, false, stream_));
   w.tile_state = static_cast<unsigned long long*>(ws_.get("tile_state", wt * 8 + 8, false, stream_));
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
   w.pitem = static_cast<uint32_t*>(ws_.get("pitem", list * 4, false, stream_));
