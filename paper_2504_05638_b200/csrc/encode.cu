@@ -1413,7 +1413,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_ds_apply_smem(const EncItem* 
     if (!ds_member(e, state[it], group)) continue;
     const uint64_t a = uint64_t(e.sketch - base), z = a + uint64_t(rows) * e.m;
     const uint64_t lo = a > g0 ? a : g0, hi = z < g1 ? z : g1;
-    for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) __stcs(base + x, s_acc[x - g0]);
+    for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) base[x] = s_acc[x - g0];
   }
 }
 
