@@ -1896,10 +1896,13 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
       const uint64_t g = std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
       // one contiguous range per CTA while every sketch fits in L2 together;
-      // beyond that, 64-tile chunks dealt round-robin keep the active window
-      // (G x 64 tiles = 77M elements, ~31 MB of sketch) L2-resident
+      // beyond that, small chunks claimed from a counter keep every CTA in
+      // one narrow window of the shard, whose sketch rows stay L2-resident
+      // (Llama-3-8B fused pass: 64-tile chunks 19.1 ms, 8: 18.6, 2: 18.35,
+      // 1: 18.9 — the counter atomics start to cost; TAGC_FUSED_CHUNK)
       const uint64_t contiguous = (total_tiles + (g ? g : 1) - 1) / (g ? g : 1);
-      const uint32_t chunk = uint32_t(sketch_bytes <= (48ull << 20) ? 0 : std::min<uint64_t>(64, contiguous));
+      static const uint64_t chunk_tiles = std::getenv("TAGC_FUSED_CHUNK") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK"), nullptr, 10) : 2;
+      const uint32_t chunk = uint32_t(sketch_bytes <= (48ull << 20) ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
       kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
                                                                  hi_pool, fine_hist, err, span, chunk);
     };
