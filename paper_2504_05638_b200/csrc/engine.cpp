@@ -490,7 +490,10 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     for (uint32_t i = 0; i < items.size(); ++i)
       if (big(items[i])) order.push_back(i);
     std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return items[a].sketch < items[b].sketch; });
-    constexpr uint64_t kGroupSpan = 1ull << 27;
+    // TAGC_DS_GROUP_SPAN (floats): a smaller span for tests (several groups)
+    const uint64_t kGroupSpan = std::getenv("TAGC_DS_GROUP_SPAN")
+                                           ? std::max<uint64_t>(1, std::strtoull(std::getenv("TAGC_DS_GROUP_SPAN"), nullptr, 10))
+                                           : (1ull << 27);
     for (uint32_t i : order) {
       EncItem& e = items[i];
       const uint64_t len = uint64_t(hp.rows) * e.m;

@@ -223,3 +223,14 @@ def test_split_exchange_deferred_scatter(orc, monkeypatch, world, width, theta, 
     beyond L2) forced on every segment: same parity bar against the oracle."""
     monkeypatch.setenv("TAGC_DEFER_SCATTER_BYTES", "0")
     test_split_exchange_matches_oracle(orc, world, width, theta, steps)
+
+
+@pytest.mark.parametrize("world,width,theta,steps", [(2, 4, 99.0, 2), (3, 1, 98.75, 1)])
+def test_split_exchange_deferred_scatter_groups(orc, monkeypatch, world, width, theta, steps):
+    """The deferred scatter in several groups (every segment deferred, groups
+    capped at 2^14 floats of sketch span: one launch_deferred_scatter call per
+    group, each with its own bins and fill counters over the shared record
+    buffers): same parity bar against the oracle."""
+    monkeypatch.setenv("TAGC_DEFER_SCATTER_BYTES", "0")
+    monkeypatch.setenv("TAGC_DS_GROUP_SPAN", str(1 << 14))
+    test_split_exchange_matches_oracle(orc, world, width, theta, steps)
