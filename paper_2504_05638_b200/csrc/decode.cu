@@ -278,14 +278,16 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
   }
 }
 
-// Counter mode (byte counters, no list indices in the bucket state): the
+// Counter mode (bucket counters, no list indices in the bucket state): the
 // bucket counts do not depend on the list order, so the build splits into
-// three passes with no look-back chain between word tiles:
-//   k_list_count : per word tile, its present positions' byte-counter REDs
-//                  and its count (tile_base[wt] holds the count), the next
-//                  tile's words already in flight;
-//   k_tile_scan  : one CTA turns the counts into list offsets in place;
-//   k_list_write : per word tile, the list entries at their final index.
+// two passes over the same per-CTA tile ranges, with no look-back chain
+// between word tiles:
+//   k_list_count : per word tile its present count (into the tile_state
+//                  words, free in counter mode) and per CTA their sum, the
+//                  next tile's words already in flight;
+//   k_list_write : the CTA's list offset from the per-CTA sums, its tiles'
+//                  offsets (tile_base) by a block scan, then per word tile the
+//                  list entries at their final index and the counter REDs.
 // The merged index is read twice (streamed), against a per-tile look-back
 // whose latency chain grew with the number of CTAs in flight.
 __device__ __forceinline__ void load_tile_raw(const DecItem& e, uint32_t wbase, uint32_t (&raw)[kPerThreadWords]) {
@@ -308,7 +310,12 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
   span_begin(w.span);
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
-  if (t0 >= t1) return;
+  uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(w.tile_state);  // counter mode: tile_state is free
+  uint32_t cta_sum = 0;
+  if (t0 >= t1) {
+    if (threadIdx.x == 0) w.cta_cnt[blockIdx.x] = 0;
+    return;
+  }
   uint32_t it = find_word_item(w.items, w.n_items, t0);
   uint32_t raw[kPerThreadWords];
   {
@@ -335,48 +342,14 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
     }
     const uint32_t total = Reduce(red_tmp).Sum(cnt);
     if (threadIdx.x == 0) {
-      w.tile_base[wt] = total;
+      tile_cnt[wt] = total;
+      cta_sum += total;
       if (total) atomicAdd(&w.stats[it].presence, total);
     }
     __syncthreads();  // reduce storage reuse
     it = nit;
   }
-}
-
-// In place: tile counts -> exclusive list offsets; the list length (0 when
-// it exceeds the capacity: a corrupt index after a NaN-aborted encode lists
-// nothing) to qcount[5].
-__global__ void __launch_bounds__(1024) k_tile_scan(DecodeWork w) {
-  using Scan = cub::BlockScan<uint32_t, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint64_t s_carry;
-  const uint64_t T = w.total_word_tiles;
-  constexpr uint32_t kPer = 8;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint64_t c0 = 0; c0 < T; c0 += 1024 * kPer) {
-    uint32_t v[kPer], sum = 0;
-#pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint64_t t = c0 + uint64_t(threadIdx.x) * kPer + k;
-      v[k] = t < T ? w.tile_base[t] : 0u;
-      sum += v[k];
-    }
-    uint32_t off, agg;
-    Scan(tmp).ExclusiveSum(sum, off, agg);
-    const uint64_t carry = s_carry;
-    uint64_t run = carry + off;
-#pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint64_t t = c0 + uint64_t(threadIdx.x) * kPer + k;
-      if (t < T) w.tile_base[t] = uint32_t(run < 0xFFFFFFFFull ? run : 0xFFFFFFFFull);
-      run += v[k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = carry + agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) w.qcount[5] = s_carry <= w.list_cap ? uint32_t(s_carry) : 0u;
+  if (threadIdx.x == 0) w.cta_cnt[blockIdx.x] = cta_sum;
 }
 
 constexpr uint32_t kListStage = 2048;  // staged positions per word tile (beyond: read back)
@@ -385,10 +358,59 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
   using Scan = cub::BlockScan<uint32_t, 256>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_pos[kListStage];
-  const uint32_t total_list = ldcg(&w.qcount[5]);
+  // this CTA's list offset and the list length from the per-CTA counts of
+  // k_list_count (same grid, same tile ranges): no separate scan kernel
+  __shared__ uint32_t s_pre[8], s_all[8];
+  uint32_t pre = 0, all = 0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    const uint32_t c = ldcg(w.cta_cnt + b);
+    all += c;
+    pre += b < blockIdx.x ? c : 0u;
+  }
+  pre = warp_sum32(pre);
+  all = warp_sum32(all);
+  if ((threadIdx.x & 31) == 0) {
+    s_pre[threadIdx.x >> 5] = pre;
+    s_all[threadIdx.x >> 5] = all;
+  }
+  __syncthreads();
+  uint64_t run = 0, tot = 0;
+  for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+    run += s_pre[i];
+    tot += s_all[i];
+  }
+  // the list length, or 0 when it exceeds the capacity (a corrupt index
+  // after a NaN-aborted encode lists nothing)
+  const uint32_t total_list = tot <= w.list_cap ? uint32_t(tot) : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.qcount[5] = total_list;
+  const uint32_t* tile_cnt = reinterpret_cast<const uint32_t*>(w.tile_state);
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
+  // list offset of every tile of this CTA (k_emit, this pass): a block scan
+  // of the tiles' counts, 256 tiles at a time
+  for (uint32_t b0 = t0; b0 < t1; b0 += blockDim.x) {
+    const uint32_t wt = b0 + threadIdx.x;
+    const uint32_t c = wt < t1 ? ldcg(tile_cnt + wt) : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, d);
+      if ((threadIdx.x & 31) >= uint32_t(d)) incl += y;
+    }
+    __syncthreads();  // s_pre reuse
+    if ((threadIdx.x & 31) == 31) s_pre[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    uint64_t wbase = 0, btot = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+      wbase += i < (threadIdx.x >> 5) ? s_pre[i] : 0u;
+      btot += s_pre[i];
+    }
+    const uint64_t off = run + wbase + incl - c;
+    if (wt < t1) w.tile_base[wt] = uint32_t(off < 0xFFFFFFFFull ? off : 0xFFFFFFFFull);
+    run += btot;
+  }
   if (t0 >= t1 || total_list == 0) return;
+  __syncthreads();
   uint32_t it = find_word_item(w.items, w.n_items, t0);
   uint32_t raw[kPerThreadWords];
   {
@@ -415,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
     }
     uint32_t off, tile_n;
     Scan(scan_tmp).ExclusiveSum(cnt, off, tile_n);
-    const uint32_t base = __ldg(w.tile_base + wt);
+    const uint32_t base = ldcg(w.tile_base + wt);
     const bool staged = tile_n <= kListStage;
     uint32_t j = base + off;
 #pragma unroll
@@ -1920,11 +1942,12 @@ int grid_for(uint64_t n, int threads) {
 // first touched by k_list). Returns the grid used for the word-tile passes.
 int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, cudaStream_t stream) {
   if (w.cnt8) {  // counter mode: count, scan, write (no look-back)
-    const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
-    const uint64_t gn = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 8);
-    k_list_count<<<int(gn), 256, 0, stream>>>(w);
-    k_tile_scan<<<1, 1024, 0, stream>>>(w);
-    k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // byte counters were zeroed by the caller
+    // count and write on the same grid (the same tile range per CTA): the
+    // write pass turns the per-CTA counts into list offsets itself
+    const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1),
+                                           std::min<uint64_t>(uint64_t(di.sms) * 4, kListMaxCtas));
+    k_list_count<<<int(gc), 256, 0, stream>>>(w);
+    k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // counters were zeroed by the caller
     return int(gc);
   }
   const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
@@ -1944,7 +1967,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   int per_sm = 0;
   build_passes(di, w, hp, stream);
   if (sketch_ready) cudaStreamWaitEvent(stream, sketch_ready, 0);
-  const int list_launches = w.cnt8 ? 3 : 1;
+  const int list_launches = w.cnt8 ? 2 : 1;
   if (fused_emit) {
     const uint64_t ge = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 3);
     cudaFuncSetAttribute((const void*)k_r0_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR0EmitSmem));
@@ -1999,7 +2022,7 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
-  return (w.cnt8 ? 3 : 1) + 3;  // build, round 0, loop, estimate
+  return (w.cnt8 ? 2 : 1) + 3;  // build, round 0, loop, estimate
 }
 
 int launch_decode_emit(const DevInfo& di, const DecodeWork& w, cudaStream_t stream, const OptEpilogue* dev_opt) {
@@ -2073,7 +2096,7 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_decode_kernels() {
-  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_tile_scan, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel<3>, (const void*)k_peel<kMaxRows>, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel<3>, (const void*)k_peel<kMaxRows>, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();

@@ -150,6 +150,7 @@ int launch_audit(const AuditItem* items, uint32_t n_items, uint64_t max_n, const
 
 // ---------------------------------------------------------------- decode
 constexpr uint32_t kPeelHandoff = 512;
+constexpr uint32_t kListMaxCtas = 1024;
 struct DecodeWork {
   const DecItem* items;
   uint32_t n_items;
@@ -169,6 +170,7 @@ struct DecodeWork {
   uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
   uint32_t* r0_list;               // round-0 peeled entries sharing a bucket (count qcount[13]), or nullptr
   unsigned long long* tile_state;  // single-pass scan: per word tile, flag << 32 | count (zeroed per call)
+  uint32_t* cta_cnt;               // counter mode: per list-build CTA, its tiles' present count (kListMaxCtas)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
