@@ -92,6 +92,12 @@ __device__ __forceinline__ bool words_full(uint32_t w0, uint32_t nwords, bool w4
 
 __device__ __forceinline__ float canonical(float v) { return v == 0.0f ? 0.0f : v; }
 
+// Item of presence-list entry i: a one-item decode (one huge segment) keeps
+// no per-entry item array (pitem is neither written nor read).
+__device__ __forceinline__ uint32_t item_of(const DecodeWork& w, uint64_t i) {
+  return w.n_items == 1 ? 0u : __ldcs(w.pitem + i);
+}
+
 // Counter mode: one counter of 2^cnt_shift bits (8 or 4) per bucket, packed
 // into u32 words (w.cnt8).
 __device__ __forceinline__ void cnt_add(const DecodeWork& w, uint64_t slot) {
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(256) k_list(DecodeWork w, const HashParams hp)
         const uint32_t bb = __ffs(x) - 1;
         if (j < cap) {
           w.plist[j] = wi * P + (w4 ? bb / 4 : bb);
-          w.pitem[j] = it;
+          if (w.n_items > 1) w.pitem[j] = it;
         }
         ++j;
       }
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
         const uint32_t p = wi * P + (w4 ? bb / 4 : bb);
         if (j < total_list) {
           w.plist[j] = p;
-          w.pitem[j] = it;
+          if (w.n_items > 1) w.pitem[j] = it;
         }
         if (staged) s_pos[j - base] = p;
         ++j;
@@ -573,7 +579,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
     bool peeled = false, sub = false;  // sub: peeled with a shared bucket (k_r0_subtract's work)
     if (i < total) {
       const uint32_t p = __ldcs(w.plist + i);
-      const DecItem& e = w.items[__ldcs(w.pitem + i)];
+      const DecItem& e = w.items[item_of(w, i)];
       uint64_t ls[kMaxRows];
       unsigned long long st[kMaxRows];
 #pragma unroll
@@ -686,7 +692,7 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
       const uint64_t i = wb + 32u * k + lane;
       act[k] = i < total;
       p[k] = act[k] ? __ldcs(w.plist + i) : 0u;
-      it[k] = act[k] ? __ldcs(w.pitem + i) : 0u;
+      it[k] = act[k] ? item_of(w, i) : 0u;
     }
     uint64_t ls[PER][R];
     uint32_t c[PER][R];
@@ -797,7 +803,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract_cnt(DecodeWork w, const Has
     const uint32_t rows = info.y & 0xFFu;
     const float v = __uint_as_float(info.x);
     const uint32_t p = __ldcs(w.plist + i);
-    const DecItem* e = w.items + __ldcs(w.pitem + i);
+    const DecItem* e = w.items + item_of(w, i);
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows && ((rows >> r) & 1u)) {
       const uint64_t loc = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
       const uint64_t sl = e->slot_base + loc;
@@ -808,7 +814,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract_cnt(DecodeWork w, const Has
   for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < nu; j += stride) {
     const uint32_t i = ldcg(w.ulist + j);
     const uint32_t p = __ldcs(w.plist + i);
-    const DecItem* e = w.items + __ldcs(w.pitem + i);
+    const DecItem* e = w.items + item_of(w, i);
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
       const uint64_t sl = e->slot_base + uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
       atomicAdd(w.slot_state + sl, st_add(i));  // result unused: RED.ADD.64
@@ -844,7 +850,7 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
         rows = info.y & 0xFFu;
         v = __uint_as_float(info.x);
         p = __ldcs(w.plist + i);
-        e = w.items + __ldcs(w.pitem + i);
+        e = w.items + item_of(w, i);
       }
     }
     unsigned long long old[kMaxRows];
@@ -1095,7 +1101,7 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
       for (int h = 0; h < 2; ++h) {
         const bool ok = base + h * gstride + lane < nu;
         p[h] = ok ? __ldcs(w.plist + ii[h]) : 0u;
-        e[h] = w.items + (ok ? __ldcs(w.pitem + ii[h]) : 0u);
+        e[h] = w.items + (ok ? item_of(w, ii[h]) : 0u);
       }
       uint32_t sl[2][R];
       uint32_t one[2] = {0u, 0u};
@@ -1327,7 +1333,7 @@ __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const Ha
         win = ldcg(o.claim + i) == ord_tag(ep, ~j);
         if (win) {
           p = w.plist[i];
-          e = w.items + w.pitem[i];
+          e = w.items + item_of(w, i);
           const uint64_t local = slot - e->slot_base;
           const uint32_t row = uint32_t(local / e->m);
           v = canonical(dev_sign(row_coef(hp, row), p) * ldcg(e->sketch + local));  // decode.cpp:110-111
@@ -1458,7 +1464,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
         rows = info.y & 0xFFu;
         v = __uint_as_float(info.x);
         p = w.plist[i];
-        e = w.items + w.pitem[i];
+        e = w.items + item_of(w, i);
         const uint32_t best = (info.y >> 12) & 0xFu;
         const uint64_t ws = e->slot_base + uint64_t(best) * e->m + dev_bucket(row_coef(hp, best), p, e->m, e->mmul);
         if (rows) {  // rank of the winner slot among the pushing entries' winners
@@ -1544,7 +1550,7 @@ __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp
     uint32_t it = 0xFFFFFFFFu, p = 0;
     if (todo) {
       p = w.plist[i];
-      it = w.pitem[i];
+      it = item_of(w, i);
       const DecItem& e = w.items[it];
       float est[kMaxRows];
 #pragma unroll
@@ -1846,7 +1852,7 @@ __global__ void __launch_bounds__(256) k_final_fix(DecodeWork w, const HashParam
     if (j < nu) {
       const uint32_t i = ldcg(w.ulist + j);
       p = __ldg(w.plist + i);
-      it = __ldg(w.pitem + i);
+      it = item_of(w, i);
       const DecItem& e = w.items[it];
       float v;
       if ((ldcg(w.bitmap + (i >> 5)) >> (i & 31)) & 1u) {
