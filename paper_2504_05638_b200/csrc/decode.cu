@@ -314,8 +314,18 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
   using Reduce = cub::BlockReduce<uint32_t, 256>;
   __shared__ typename Reduce::TempStorage red_tmp;
   span_begin(w.span);
+  // two count CTAs per write CTA (k_list_write runs gridDim.x / 2 CTAs):
+  // CTA c counts one half of write CTA c / 2's tile range
   uint32_t t0, t1;
-  cta_tiles(w.total_word_tiles, t0, t1);
+  {
+    const uint32_t sp = w.list_split;  // count CTAs per write CTA: 1 or 2
+    const uint32_t T = uint32_t(w.total_word_tiles), G = gridDim.x / sp, b = blockIdx.x / sp;
+    const uint32_t chunk = T / G, extra = T % G;
+    const uint32_t b0 = b * chunk + min(b, extra), b1 = b0 + chunk + (b < extra ? 1u : 0u);
+    const uint32_t mid = b0 + (b1 - b0) / 2;
+    t0 = sp == 1 ? b0 : ((blockIdx.x & 1) ? mid : b0);
+    t1 = sp == 1 ? b1 : ((blockIdx.x & 1) ? b1 : mid);
+  }
   uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(w.tile_state);  // counter mode: tile_state is free
   uint32_t cta_sum = 0;
   if (t0 >= t1) {
@@ -368,10 +378,10 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
   // k_list_count (same grid, same tile ranges): no separate scan kernel
   __shared__ uint32_t s_pre[8], s_all[8];
   uint32_t pre = 0, all = 0;
-  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+  for (uint32_t b = threadIdx.x; b < w.list_split * gridDim.x; b += blockDim.x) {  // count CTAs of this pass
     const uint32_t c = ldcg(w.cta_cnt + b);
     all += c;
-    pre += b < blockIdx.x ? c : 0u;
+    pre += b < w.list_split * blockIdx.x ? c : 0u;
   }
   pre = warp_sum32(pre);
   all = warp_sum32(all);
@@ -1952,7 +1962,7 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
     // write pass turns the per-CTA counts into list offsets itself
     const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1),
                                            std::min<uint64_t>(uint64_t(di.sms) * 4, kListMaxCtas));
-    k_list_count<<<int(gc), 256, 0, stream>>>(w);
+    k_list_count<<<int(w.list_split * gc), 256, 0, stream>>>(w);
     k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // counters were zeroed by the caller
     return int(gc);
   }

@@ -698,7 +698,9 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.tile_base = static_cast<uint32_t*>(ws_.get("tile_base", wt * 4, false, stream_));
   w.r0_list = static_cast<uint32_t*>(ws_.get("r0_list", list * 4 + 4, false, stream_));
   w.tile_state = static_cast<unsigned long long*>(ws_.get("tile_state", wt * 8 + 8, false, stream_));
-  w.cta_cnt = static_cast<uint32_t*>(ws_.get("list_cta_cnt", kListMaxCtas * 4, false, stream_));
+  w.cta_cnt = static_cast<uint32_t*>(ws_.get("list_cta_cnt", 2 * kListMaxCtas * 4, false, stream_));
+  static const uint32_t list_split = std::getenv("TAGC_LIST_SPLIT") ? std::max(1, std::min(2, std::atoi(std::getenv("TAGC_LIST_SPLIT")))) : 2u;
+  w.list_split = list_split;
   w.plist = static_cast<uint32_t*>(ws_.get("plist", list * 4, false, stream_));
   w.pitem = static_cast<uint32_t*>(ws_.get("pitem", list * 4, false, stream_));
   w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));

@@ -170,7 +170,8 @@ struct DecodeWork {
   uint32_t* tile_base;             // presence-list offset of every word tile (build -> emit)
   uint32_t* r0_list;               // round-0 peeled entries sharing a bucket (count qcount[13]), or nullptr
   unsigned long long* tile_state;  // single-pass scan: per word tile, flag << 32 | count (zeroed per call)
-  uint32_t* cta_cnt;               // counter mode: per list-build CTA, its tiles' present count (kListMaxCtas)
+  uint32_t* cta_cnt;               // counter mode: per list-count CTA, its tiles' present count (2 x kListMaxCtas)
+  uint32_t list_split;             // list-count CTAs per list-write CTA (1 or 2)
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask
