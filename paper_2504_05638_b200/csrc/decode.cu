@@ -1225,7 +1225,7 @@ __device__ __forceinline__ unsigned long long ord_tag(uint32_t ep, uint64_t key)
   return (uint64_t(ep) << 32) | key;
 }
 
-template <typename Sync>
+template <int R, typename Sync>
 __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const HashParams& hp, const OrdState& o,
                                                    uint32_t g, uint32_t n, uint64_t dom, uint32_t ep, uint32_t part,
                                                    uint32_t nparts, uint32_t* cnt, uint32_t* s_q, uint32_t* s_nq,
@@ -1329,50 +1329,87 @@ __device__ __forceinline__ uint32_t ord_generation(const DecodeWork& w, const Ha
   uint32_t won = 0;
   uint32_t* un = (g & 1) ? o.u0 : o.u1;
   uint32_t* cn = cnt + (g + 1) % 3;
-  for (uint32_t base = part * blockDim.x; base < n; base += nparts * blockDim.x) {
-    const uint32_t j = base + tid;
-    bool win = false;
-    uint32_t slot = 0, i = 0, p = 0;
-    const DecItem* e = w.items;
-    float v = 0.0f;
-    if (j < n) {
-      slot = ldcg(o.q + j);
-      const unsigned long long st = ldcg(w.slot_state + slot);
-      if (st_count(st) == 1u) {
-        i = st_entry(st);
-        win = ldcg(o.claim + i) == ord_tag(ep, ~j);
-        if (win) {
-          p = w.plist[i];
-          e = w.items + item_of(w, i);
-          const uint64_t local = slot - e->slot_base;
-          const uint32_t row = uint32_t(local / e->m);
-          v = canonical(dev_sign(row_coef(hp, row), p) * ldcg(e->sketch + local));  // decode.cpp:110-111
-          w.val[i] = v;
-          red_or_u32(w.bitmap + (i >> 5), 1u << (i & 31));
-          ++won;
+  // two queue entries per thread in flight; an entry's position, item and
+  // residual are read together with its claim (one dependent trip less)
+  constexpr int kD = 2;
+  for (uint32_t base = part * blockDim.x * kD; base < n; base += nparts * blockDim.x * kD) {
+    uint32_t jj[kD], slot[kD], i[kD], pp[kD], p[kD];
+    bool live[kD], win[kD];
+    unsigned long long st[kD], cl[kD];
+    const DecItem* e[kD];
+    float resid[kD], v[kD];
+#pragma unroll
+    for (int h = 0; h < kD; ++h) {
+      jj[h] = base + h * blockDim.x + tid;
+      live[h] = jj[h] < n;
+      slot[h] = live[h] ? ldcg(o.q + jj[h]) : 0u;
+    }
+#pragma unroll
+    for (int h = 0; h < kD; ++h) st[h] = live[h] ? ldcg(w.slot_state + slot[h]) : 0ull;
+#pragma unroll
+    for (int h = 0; h < kD; ++h) {
+      live[h] = live[h] && st_count(st[h]) == 1u;
+      i[h] = st_entry(st[h]);
+      e[h] = w.items;
+      cl[h] = 0ull;
+      pp[h] = 0u;
+      resid[h] = 0.0f;
+      if (live[h]) {
+        cl[h] = ldcg(o.claim + i[h]);
+        pp[h] = w.plist[i[h]];
+        e[h] = w.items + item_of(w, i[h]);
+        resid[h] = ldcg(e[h]->sketch + (slot[h] - e[h]->slot_base));
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < kD; ++h) {
+      win[h] = live[h] && cl[h] == ord_tag(ep, ~jj[h]);
+      p[h] = 0u;
+      v[h] = 0.0f;
+      if (win[h]) {
+        p[h] = pp[h];
+        const uint32_t row = uint32_t((slot[h] - e[h]->slot_base) / e[h]->m);
+        v[h] = canonical(dev_sign(row_coef(hp, row), p[h]) * resid[h]);  // decode.cpp:110-111
+        w.val[i[h]] = v[h];
+        red_or_u32(w.bitmap + (i[h] >> 5), 1u << (i[h] & 31));
+        ++won;
+      }
+    }
+    unsigned long long old[kD][R];
+    uint32_t ss[kD][R], sub[kD];
+#pragma unroll
+    for (int h = 0; h < kD; ++h) {
+      sub[h] = 0u;
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < rows) {
+        old[h][r] = 0ull;
+        ss[h][r] = 0u;
+        if (win[h]) {
+          const uint64_t local = uint64_t(r) * e[h]->m + dev_bucket(hp.row[r], p[h], e[h]->m, e[h]->mmul);
+          const uint64_t sl = e[h]->slot_base + local;
+          if (sl != slot[h]) {
+            sub[h] |= 1u << r;
+            ss[h][r] = uint32_t(sl);
+            red_add_f32(e[h]->sketch + local, -(dev_sign(hp.row[r], p[h]) * v[h]));
+            atomicMax(o.slot_key + sl, ord_tag(ep + 1, uint64_t(jj[h]) * rows + r));
+            old[h][r] = atomicAdd(w.slot_state + sl, st_sub(i[h]));
+          }
         }
       }
     }
-    _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < rows) {
-      bool push = false;
-      uint64_t s = 0;
-      if (win) {
-        const uint64_t local = uint64_t(r) * e->m + dev_bucket(hp.row[r], p, e->m, e->mmul);
-        s = e->slot_base + local;
-        if (s != slot) {
-          red_add_f32(e->sketch + local, -(dev_sign(hp.row[r], p) * v));
-          atomicMax(o.slot_key + s, ord_tag(ep + 1, uint64_t(j) * rows + r));
-          const unsigned long long old = atomicAdd(w.slot_state + s, st_sub(i));
-          push = st_count(old) == 2u;
-        }
+#pragma unroll
+    for (int h = 0; h < kD; ++h) {
+      _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < rows) {
+        const bool push = ((sub[h] >> r) & 1u) && st_count(old[h][r]) == 2u;
+        stage_push<uint32_t, kPushStage>(push, ss[h][r], s_q, s_nq, un, cn, lane);
       }
-      stage_push<uint32_t, kPushStage>(push, uint32_t(s), s_q, s_nq, un, cn, lane);
     }
   }
   stage_flush<uint32_t, kPushStage>(s_q, s_nq, s_base, un, cn);
   return won;
 }
 
+// R: rows compiled in (3, or kMaxRows for any k <= 8).
+template <int R>
 __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams hp, OrdState o) {
   __shared__ uint32_t s_q[kPushStage];
   __shared__ uint32_t s_nq[2], s_base, s_warp[8];
@@ -1515,7 +1552,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
       cnt[(g + 2) % 3] = 0;
       w.qcount[2] += 1;
     }
-    won += ord_generation(w, hp, o, g, n, dom, ep, blockIdx.x, gridDim.x, cnt, s_q, s_nq, &s_base, s_warp,
+    won += ord_generation<R>(w, hp, o, g, n, dom, ep, blockIdx.x, gridDim.x, cnt, s_q, s_nq, &s_base, s_warp,
                           [&] { grid.sync(); }, mk);
     dom = uint64_t(n) * hp.rows;
     ++ep;
@@ -1533,7 +1570,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
         cnt[(g + 2) % 3] = 0;
         w.qcount[3] += 1;
       }
-      won += ord_generation(w, hp, o, g, n, dom, ep, 0, 1, cnt, s_q, s_nq, &s_base, s_warp,
+      won += ord_generation<R>(w, hp, o, g, n, dom, ep, 0, 1, cnt, s_q, s_nq, &s_base, s_warp,
                             [] { __syncthreads(); }, mk);
       dom = uint64_t(n) * hp.rows;
       ++ep;
@@ -2013,10 +2050,11 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   return list_launches + 4;  // list, round 0 (2), peel, final
 }
 
-int ordered_loop_grid(const DevInfo& di) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ord_loop, 256, 0);
-  return std::max(per_sm, 1) * di.sms;
+int ordered_loop_grid(const DevInfo& di) {  // the larger of the two instantiations' grids (per-CTA scratch)
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, (const void*)k_ord_loop<3>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, (const void*)k_ord_loop<kMaxRows>, 256, 0);
+  return std::max(std::max(a, b), 1) * di.sms;
 }
 
 int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashParams& hp, const OrdState& o,
@@ -2034,8 +2072,10 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   HashParams ha = hp;
   OrdState oa = o;
   void* args[] = {&wa, &ha, &oa};
-  cudaLaunchCooperativeKernel((const void*)k_ord_loop, dim3(ordered_loop_grid(di)), dim3(256), args, 0, stream);
+  const void* loop = hp.rows == 3 ? (const void*)k_ord_loop<3> : (const void*)k_ord_loop<kMaxRows>;
   int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loop, 256, 0);
+  cudaLaunchCooperativeKernel(loop, dim3(std::max(per_sm, 1) * di.sms), dim3(256), args, 0, stream);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
   k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
   return (w.cnt8 ? 2 : 1) + 3;  // build, round 0, loop, estimate
@@ -2112,7 +2152,7 @@ int launch_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t count, void* sc
 
 // Loads every kernel of this file now (see preload_all_kernels).
 void preload_decode_kernels() {
-  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_list_write, (const void*)k_ord_loop, (const void*)k_peel<3>, (const void*)k_peel<kMaxRows>, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
+  const void* fns[] = {(const void*)k_r0_emit, (const void*)k_final_fix, (const void*)k_emit<false>, (const void*)k_emit<true>, (const void*)k_estimate_targets, (const void*)k_final, (const void*)k_list, (const void*)k_list_count, (const void*)k_list_write, (const void*)k_ord_loop<3>, (const void*)k_ord_loop<kMaxRows>, (const void*)k_peel<3>, (const void*)k_peel<kMaxRows>, (const void*)k_presence_to_bitmap, (const void*)k_r0_phase1, (const void*)k_r0_phase1_k<3, 2>, (const void*)k_r0_subtract, (const void*)k_r0_subtract_cnt, (const void*)k_word_counts, (const void*)k_word_positions};
   cudaFuncAttributes a;
   for (const void* f : fns) cudaFuncGetAttributes(&a, f);
   cudaGetLastError();
