@@ -535,6 +535,54 @@ def owner_step_and_overlap(rig, tagc, S, args):
     return owner, overlap
 
 
+def paper_w2_simulated(rig, tagc, args):
+    """The paper setting (GPT-2, theta 98.75, r 10, 1-bit index) at W = 2 with
+    both ranks simulated on this one GPU (tagc_reduce_shard_sim per shard:
+    both ranks' encode, the rank-ordered sums, and the 1-bit merged index's
+    FIFO-ordered peel, k_ord_loop). Not a multi-GPU number: the two ranks'
+    work runs back to back on one device, so value = 2 x params x 4 B / t is
+    a lower bound for two GPUs."""
+    torch = rig.torch
+    W = 2
+    specs, cfg, shards = make_workload(tagc, "gpt2-paper", W)
+    total = shards[-1].end
+    n_params = sum(sp.param_count for sp in specs)
+    grads = [synthetic_grad(torch, total, n_params, rig.dev, 2000 + r) for r in range(W)]
+    accs = [torch.zeros(total, device=rig.dev) for _ in range(W)]
+    ctx = tagc.Context(cfg, device=rig.local, stream=rig.stream.cuda_stream)
+
+    def step():
+        st = None
+        for sh in shards:
+            _, st = ctx.tagc_reduce_shard_sim(sh, [g[sh.begin:sh.end] for g in grads],
+                                              [a[sh.begin:sh.end] for a in accs])
+        return st
+
+    for _ in range(max(args.warmup, 3)):
+        st = step()
+    rig.torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    n = max(args.steps, 5)
+    ev[0].record(rig.stream)
+    for _ in range(n):
+        st = step()
+    ev[1].record(rig.stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / n
+    res = {"workload": WORKLOADS["gpt2-paper"][0] + ", W=2 simulated on one GPU (tagc_reduce_shard_sim)",
+           "value": round(W * total * 4.0 / (ms * 1e-3) / 1e9, 3), "ms_per_step": round(ms, 4),
+           "last_shard_peel": {"presence": st.presence, "unresolved": st.unresolved,
+                               "index_lost": st.index_lost, "index_spurious": st.index_spurious,
+                               "ordered_generations": ctx.last_peel_rounds()},
+           "note": "both ranks on one device back to back (not a scaling point); the FIFO-ordered 1-bit peel "
+                   "runs on the device (k_ord_loop)"}
+    ctx.close()
+    del grads, accs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
 def free_state(rig, S):
     S["ctx"].sync()
     S["ctx"].close()
@@ -583,6 +631,8 @@ def run_b200(args):
                 r["owner_step"], r["overlap"] = owner_step_and_overlap(rig, tagc, S2, args)
             free_state(rig, S2)
             extras[name] = r
+        if world == 1:
+            extras["gpt2-paper-w2-simulated"] = paper_w2_simulated(rig, tagc, args)
 
     result = {
         "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": world,
