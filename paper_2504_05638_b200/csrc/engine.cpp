@@ -551,7 +551,9 @@ void Engine::run_select_encode(std::vector<EncItem>& items, bool w4, const HashP
     launches_ += launch_select_finish(di_, d_items, state, n, tiles, hp, w4, fine, fh, cd, hp_pool, sl,
                                       err, stream_);
     if (!ds_groups.empty()) {
-      auto* rec = static_cast<uint2*>(ws_.get("ds_records", (ds_cap + ds_cap / 16 + uint64_t(kDsMaxBins) * 1024) * 8,
+      // bins x capacity, capacity = ceil(total / bins) * 17/16 + 1024 per bin
+      // (k_ds_place): at most total * 17/16 + bins * 1026 records
+      auto* rec = static_cast<uint2*>(ws_.get("ds_records", (ds_cap + ds_cap / 16 + 16 + uint64_t(kDsMaxBins) * 1026) * 8,
                                               false, stream_));
       auto* ovf = static_cast<uint2*>(ws_.get("ds_overflow", ds_cap * 8, false, stream_));
       cudaStream_t ds_s = stream_;
