@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
                                                          const SelState* __restrict__ state, uint32_t n_items,
                                                          const uint2* __restrict__ hi_pool, const HashParams hp,
                                                          const float* base, uint32_t group, uint32_t shift,
-                                                         uint32_t n_bins, uint32_t* __restrict__ fill,
+                                                         uint32_t n_bins, uint32_t tight, uint32_t* __restrict__ fill,
                                                          uint32_t* __restrict__ ctl,
                                                          uint2* __restrict__ records, uint2* __restrict__ ovf) {
   __shared__ uint32_t pref[kMaxFlatItems + 1];
@@ -1302,7 +1302,9 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_ds_place(const EncItem* __res
   const uint32_t rows = hp.rows;
   const uint32_t total =
       flat_prefix(n_items, [&](uint32_t i) { return ds_entries(items[i], state[i], group); }, pref);
-  const uint32_t cap = ds_cap(total * rows, n_bins);
+  // tight (test hook TAGC_DS_TIGHT): a quarter of the mean per bin, so most
+  // updates take the overflow path
+  const uint32_t cap = tight ? max(1u, (total * rows / n_bins) / 4u) : ds_cap(total * rows, n_bins);
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl[1] = cap;
   const uint32_t per_batch = kDsBatch / rows;
   const uint32_t per_cta = (total + gridDim.x - 1) / gridDim.x;
@@ -2021,9 +2023,10 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
                               : std::max<uint32_t>(22, lg - 12);
   const uint32_t n_bins = uint32_t((span_floats + (1ull << shift) - 1) >> shift);
   const int smem_place = int(2 * kDsBatch * sizeof(uint2) + 3 * n_bins * sizeof(uint32_t));
+  const uint32_t tight = std::getenv("TAGC_DS_TIGHT") && std::atoi(std::getenv("TAGC_DS_TIGHT")) != 0 ? 1u : 0u;
   cudaFuncSetAttribute((const void*)k_ds_place, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_place);
   k_ds_place<<<di.sms * 2, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, group, shift,
-                                                         n_bins, fill, ctl, records, ovf);
+                                                         n_bins, tight, fill, ctl, records, ovf);
   int l = 1;
   if (smem) {
     const uint32_t regions = uint32_t((span_floats + kApplyRegion - 1) >> kApplyShift);

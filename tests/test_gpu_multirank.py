@@ -234,3 +234,13 @@ def test_split_exchange_deferred_scatter_groups(orc, monkeypatch, world, width, 
     monkeypatch.setenv("TAGC_DEFER_SCATTER_BYTES", "0")
     monkeypatch.setenv("TAGC_DS_GROUP_SPAN", str(1 << 14))
     test_split_exchange_matches_oracle(orc, world, width, theta, steps)
+
+
+@pytest.mark.parametrize("world,width,theta,steps", [(2, 4, 99.0, 2)])
+def test_split_exchange_deferred_scatter_overflow(orc, monkeypatch, world, width, theta, steps):
+    """The deferred scatter's overflow path: bins capped at a quarter of their
+    mean load (TAGC_DS_TIGHT), so most updates go to the overflow list and
+    are added with REDs after the shared-memory apply: same parity bar."""
+    monkeypatch.setenv("TAGC_DEFER_SCATTER_BYTES", "0")
+    monkeypatch.setenv("TAGC_DS_TIGHT", "1")
+    test_split_exchange_matches_oracle(orc, world, width, theta, steps)
