@@ -490,11 +490,14 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
 // global atomic per CTA; a single list counter hit by every warp serialises at
 // one L2 slice otherwise. s_n[0] = reserved entries, s_n[1] = end of the
 // contiguous written prefix (an overflowing warp goes straight to the list).
+// Returns (warp-uniform) whether the stage now holds more than flush_at
+// entries: a caller whose loop is CTA-uniform flushes mid-loop when any warp
+// saw that (__syncthreads_or), so the direct path stays a rare fallback.
 template <typename T, uint32_t kCap>
-__device__ __forceinline__ void stage_push(bool push, T val, T* s_buf, uint32_t* s_n, T* g_buf,
-                                           uint32_t* g_count, uint32_t lane) {
+__device__ __forceinline__ bool stage_push(bool push, T val, T* s_buf, uint32_t* s_n, T* g_buf,
+                                           uint32_t* g_count, uint32_t lane, uint32_t flush_at = kCap) {
   const uint32_t mask = __ballot_sync(kFull, push);
-  if (!mask) return;
+  if (!mask) return false;
   const uint32_t leader = __ffs(mask) - 1, cnt = __popc(mask);
   uint32_t b = 0, direct = 0;
   if (lane == leader) {
@@ -512,6 +515,7 @@ __device__ __forceinline__ void stage_push(bool push, T val, T* s_buf, uint32_t*
     if (direct) g_buf[idx] = val;
     else s_buf[idx] = val;
   }
+  return direct || b + cnt > flush_at;
 }
 
 template <typename T, uint32_t kCap>
@@ -534,7 +538,7 @@ __device__ __forceinline__ void stage_flush(T* s_buf, uint32_t* s_n, uint32_t* s
 }
 
 constexpr uint32_t kPushStage = 8192;  // next-frontier slots per CTA
-constexpr uint32_t kR0Stage = 1024;    // round-0 subtraction entries per phase-1 CTA
+constexpr uint32_t kR0Stage = 2048;    // round-0 subtraction entries per phase-1 CTA
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -628,7 +632,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
             red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
             // counter mode: only these buckets get a (count, index sum)
             // state, built by k_r0_subtract from the unresolved entries
-            if (w.cnt8) w.slot_state[sl] = 0ull;
+            if (w.cnt8 && !w.state_zeroed) w.slot_state[sl] = 0ull;
           }
       }
       if (best >= 0) {
@@ -692,9 +696,11 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
   uint32_t won = 0;
   const uint32_t total = ldcg(&w.qcount[5]);
   const uint64_t step = uint64_t(gridDim.x) * blockDim.x * PER;
-  // a warp covers PER consecutive groups of 32 entries (one bitmap word each)
-  const uint64_t wbase0 = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * PER;
-  for (uint64_t wb = wbase0; wb < total; wb += step) {
+  // a warp covers PER consecutive groups of 32 entries (one bitmap word each);
+  // the loop bound is CTA-uniform (stage flushes need every thread)
+  for (uint64_t cb = uint64_t(blockIdx.x) * blockDim.x * PER; cb < total; cb += step) {
+    const uint64_t wb = cb + uint64_t(threadIdx.x & ~31u) * PER;
+    bool full = false;
     uint32_t p[PER], it[PER];
     bool act[PER];
 #pragma unroll
@@ -771,16 +777,24 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
           for (int r = 0; r < R; ++r) {
             const uint64_t sl = sb[k] + ls[k][r];
             red_or_u32(w.slot_mark + (sl >> 5), 1u << (sl & 31));
-            if (w.cnt8) w.slot_state[sl] = 0ull;  // built by k_r0_subtract_cnt
+            if (w.cnt8 && !w.state_zeroed) w.slot_state[sl] = 0ull;  // built by k_r0_subtract_cnt
           }
         }
         if (!compact || sub) w.pinfo[i] = info;
       }
       const uint32_t bm = __ballot_sync(kFull, peeled);
       if (lane == 0 && wb + 32u * k < total) w.bitmap[(wb >> 5) + k] = bm;
-      if (compact) stage_push<uint32_t, kR0Stage>(sub, uint32_t(i), s_q, s_n, w.r0_list, &w.qcount[13], lane);
-      if (ulist) stage_push<uint32_t, kR0Stage>(act[k] && !peeled, uint32_t(i), s_u, s_un, w.ulist,
-                                                &w.qcount[14], lane);
+      // flush once a stage could not take another iteration's entries
+      constexpr uint32_t kAt = kR0Stage - 256u * PER;
+      if (compact) full |= stage_push<uint32_t, kR0Stage>(sub, uint32_t(i), s_q, s_n, w.r0_list, &w.qcount[13], lane, kAt);
+      if (ulist) full |= stage_push<uint32_t, kR0Stage>(act[k] && !peeled, uint32_t(i), s_u, s_un, w.ulist,
+                                                        &w.qcount[14], lane, kAt);
+    }
+    // a single list counter hit by every overflowing warp serialised round 0
+    // at high load (theta = 90: ~2M same-address atomics)
+    if (__syncthreads_or(full)) {
+      if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
+      if (ulist) stage_flush<uint32_t, kR0Stage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
     }
   }
   won = warp_sum32(won);
@@ -904,21 +918,37 @@ __global__ void __launch_bounds__(256) k_r0_subtract(DecodeWork w, const HashPar
 // barriers. The peeled set is the complement of the 2-core either way
 // (order-independent); values match the reference's FIFO peel within fp32
 // reassociation.
-constexpr uint32_t kLocalQ = 2048;  // (slot, entry) pairs per CTA and round
+constexpr uint32_t kLocalQ = 2048;   // (slot, entry) pairs per CTA and round
+constexpr uint32_t kOvfStage = 2048; // overflow slots staged per CTA before one global append
 
-__device__ __forceinline__ void local_push(bool push, uint32_t slot, uint32_t entry, uint2* s_next,
-                                           uint32_t* s_nn, uint32_t* gq, uint32_t* gcount, uint32_t lane) {
+// Overflow beyond the local queue: the slot alone (its state names the entry
+// next round), staged in shared memory and appended to the round's global
+// queue with one atomic per flush (stage_push / stage_flush). A per-warp
+// append on the one queue counter serialised millions of pushes at high load
+// (theta = 90: 6 ms of k_peel).
+struct PeelOvf {
+  uint32_t* s_buf;   // kOvfStage slots
+  uint32_t* s_n;     // stage_push's two words
+  uint32_t* s_base;
+  uint32_t* gq;      // the next round's global queue and its counter
+  uint32_t* gcount;
+};
+
+// Returns (warp-uniform) whether the overflow stage should be flushed.
+template <uint32_t kFlushAt>
+__device__ __forceinline__ bool local_push(bool push, uint32_t slot, uint32_t entry, uint2* s_next,
+                                           uint32_t* s_nn, const PeelOvf& ov, uint32_t lane) {
   const uint32_t mask = __ballot_sync(kFull, push);
-  if (!mask) return;
+  if (!mask) return false;
   const uint32_t leader = __ffs(mask) - 1;
   uint32_t b = 0;
   if (lane == leader) b = atomicAdd(s_nn, uint32_t(__popc(mask)));
   b = __shfl_sync(kFull, b, leader);
-  if (push) {
-    const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
-    if (idx < kLocalQ) s_next[idx] = make_uint2(slot, entry);
-    else gq[atomicAdd(gcount, 1u)] = slot;  // overflow: re-read its state next round
-  }
+  const uint32_t idx = b + __popc(mask & ((1u << lane) - 1u));
+  if (push && idx < kLocalQ) s_next[idx] = make_uint2(slot, entry);
+  if (b + __popc(mask) <= kLocalQ) return false;
+  return stage_push<uint32_t, kOvfStage>(push && idx >= kLocalQ, slot, ov.s_buf, ov.s_n, ov.gq, ov.gcount, lane,
+                                         kFlushAt);
 }
 
 // kN frontier elements per lane, processed together (their L2 trips
@@ -927,8 +957,8 @@ __device__ __forceinline__ void local_push(bool push, uint32_t slot, uint32_t en
 template <bool kPair, int kN, int R>
 __device__ __forceinline__ uint32_t peel_n(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
                                            const bool (&have_in)[kN], const uint32_t (&slot)[kN],
-                                           const uint32_t (&i_in)[kN], uint2* s_next, uint32_t* s_nn, uint32_t* gq,
-                                           uint32_t* gcount, uint32_t lane) {
+                                           const uint32_t (&i_in)[kN], uint2* s_next, uint32_t* s_nn,
+                                           const PeelOvf& ov, bool& full, uint32_t lane) {
   bool have[kN];
   uint32_t i[kN];
 #pragma unroll
@@ -997,25 +1027,33 @@ __device__ __forceinline__ uint32_t peel_n(const DecodeWork& w, const HashParams
     }
   }
   uint32_t won = 0;
+  // an iteration pushes at most blockDim * kN * (R - 1) slots
+  constexpr uint32_t kAt = kOvfStage > 256u * kN * (R - 1) ? kOvfStage - 256u * kN * (R - 1) : 0u;
 #pragma unroll
   for (int k = 0; k < kN; ++k) {
     _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows) {
       const bool push = win[k] && r != row[k] && st_count(old[k][r]) == 2u;
-      local_push(push, sl[k][r], st_entry(old[k][r] + st_sub(i[k])), s_next, s_nn, gq, gcount, lane);
+      full |= local_push<kAt>(push, sl[k][r], st_entry(old[k][r] + st_sub(i[k])), s_next, s_nn, ov, lane);
     }
     won += win[k] ? 1u : 0u;
   }
   return won;
 }
 
+__device__ __forceinline__ void ovf_flush(const PeelOvf& ov) {
+  stage_flush<uint32_t, kOvfStage>(ov.s_buf, ov.s_n, ov.s_base, ov.gq, ov.gcount);
+}
+
 // One round's share of a CTA: the local pairs [0, nl) and the global slots
-// [g0, ng) strided by gstride, kPeelN per lane.
+// [0, ng) strided by gstride from cta0 (CTA-uniform loop bounds: the
+// overflow stage is flushed mid-round when a warp finds it nearly full),
+// kPeelN per lane. The stage is flushed at the end.
 constexpr int kPeelN = 2;
 template <int R>
 __device__ __forceinline__ uint32_t peel_round(const DecodeWork& w, const HashParams& hp, const SlotItems& si,
                                                const uint2* cur, uint32_t nl, const uint32_t* gsrc, uint32_t ng,
-                                               uint64_t g0, uint64_t gstride, uint2* s_next, uint32_t* s_nn,
-                                               uint32_t* gq, uint32_t* gcount, uint32_t lane) {
+                                               uint64_t cta0, uint64_t gstride, uint2* s_next, uint32_t* s_nn,
+                                               const PeelOvf& ov, uint32_t lane) {
   uint32_t won = 0;
   for (uint32_t b = 0; b < nl; b += blockDim.x * kPeelN) {
     bool have[kPeelN];
@@ -1028,20 +1066,25 @@ __device__ __forceinline__ uint32_t peel_round(const DecodeWork& w, const HashPa
       sl[k] = x.x;
       en[k] = x.y;
     }
-    won += peel_n<true, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, gq, gcount, lane);
+    bool full = false;
+    won += peel_n<true, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, ov, full, lane);
+    if (__syncthreads_or(full)) ovf_flush(ov);
   }
-  for (uint64_t b = g0 - lane; b < ng; b += gstride * kPeelN) {
+  for (uint64_t b = cta0; b < ng; b += gstride * kPeelN) {
     bool have[kPeelN];
     uint32_t sl[kPeelN], en[kPeelN];
 #pragma unroll
     for (int k = 0; k < kPeelN; ++k) {
-      const uint64_t j = b + k * gstride + lane;
+      const uint64_t j = b + k * gstride + threadIdx.x;
       have[k] = j < ng;
       sl[k] = have[k] ? ldcg(gsrc + j) : 0u;
       en[k] = 0u;
     }
-    won += peel_n<false, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, gq, gcount, lane);
+    bool full = false;
+    won += peel_n<false, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, ov, full, lane);
+    if (__syncthreads_or(full)) ovf_flush(ov);
   }
+  ovf_flush(ov);
   return won;
 }
 
@@ -1073,8 +1116,13 @@ template <int R>
 __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams hp) {
   __shared__ uint2 s_lq[2][kLocalQ];
   __shared__ unsigned long long s_sbase[kPeelItemsSmem];
-  __shared__ uint32_t s_ln[2], s_base, s_total;
-  if (threadIdx.x == 0) s_ln[0] = s_ln[1] = 0;
+  __shared__ uint32_t s_ovf[kOvfStage];
+  __shared__ uint32_t s_ln[2], s_on[2], s_obase, s_base, s_total;
+  if (threadIdx.x == 0) {
+    s_ln[0] = s_ln[1] = 0;
+    s_on[0] = 0;
+    s_on[1] = kOvfStage;
+  }
   const bool cache = w.n_items <= kPeelItemsSmem;
   if (cache)
     for (uint32_t i = threadIdx.x; i < w.n_items; i += blockDim.x) s_sbase[i] = w.items[i].slot_base;
@@ -1099,17 +1147,19 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     // entry buckets, each pushed by its only entry as a local (slot, entry)
     // pair; two entries per lane in flight
     const uint32_t nu = ldcg(&w.qcount[14]);
-    for (uint64_t base = gtid - lane; base < nu; base += 2 * gstride) {
+    const PeelOvf ov{s_ovf, s_on, &s_obase, qbuf1, &cnt[1]};
+    constexpr uint32_t kAt = kOvfStage > 256u * 2u * R ? kOvfStage - 256u * 2u * R : 0u;
+    for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < nu; base += 2 * gstride) {  // CTA-uniform
       uint32_t ii[2], p[2];
       const DecItem* e[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint64_t j = base + h * gstride + lane;
+        const uint64_t j = base + h * gstride + threadIdx.x;
         ii[h] = j < nu ? ldcg(w.ulist + j) : 0u;
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const bool ok = base + h * gstride + lane < nu;
+        const bool ok = base + h * gstride + threadIdx.x < nu;
         p[h] = ok ? __ldcs(w.plist + ii[h]) : 0u;
         e[h] = w.items + (ok ? item_of(w, ii[h]) : 0u);
       }
@@ -1117,19 +1167,21 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
       uint32_t one[2] = {0u, 0u};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const bool ok = base + h * gstride + lane < nu;
+        const bool ok = base + h * gstride + threadIdx.x < nu;
         _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows) {
           sl[h][r] = uint32_t(e[h]->slot_base + uint64_t(r) * e[h]->m + dev_bucket(hp.row[r], p[h], e[h]->m, e[h]->mmul));
           if (ok && st_count(ldcg(w.slot_state + sl[h][r])) == 1u) one[h] |= 1u << r;
         }
       }
+      bool full = false;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows)
-          local_push((one[h] >> r) & 1u, sl[h][r], ii[h], s_lq[1], &s_ln[1], qbuf1, &cnt[1], lane);
+          full |= local_push<kAt>((one[h] >> r) & 1u, sl[h][r], ii[h], s_lq[1], &s_ln[1], ov, lane);
       }
+      if (__syncthreads_or(full)) ovf_flush(ov);
     }
-    __syncthreads();
+    ovf_flush(ov);
     total = grid_barrier_sum(w.bar, 0, s_ln[1], &s_total);
   } else {
     total = ldcg(&cnt[1]);  // k_r0_subtract's global pushes
@@ -1162,8 +1214,9 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     const uint32_t ng = ldcg(&cnt[k % 3]);
     uint2* nxt = s_lq[(k + 1) & 1];
     uint32_t* nn = &s_ln[(k + 1) & 1];
-    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, gtid, gstride, nxt, nn, qbuf(k + 1),
-                         &cnt[(k + 1) % 3], lane);
+    const PeelOvf ov{s_ovf, s_on, &s_obase, qbuf(k + 1), &cnt[(k + 1) % 3]};
+    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, uint64_t(blockIdx.x) * blockDim.x, gstride, nxt,
+                         nn, ov, lane);
     __syncthreads();
     total = grid_barrier_sum(w.bar, k, *nn, &s_total);
     PEEL_MARK(mk++);
@@ -1183,8 +1236,8 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     uint2* nxt = s_lq[(k + 1) & 1];
     uint32_t* nn = &s_ln[(k + 1) & 1];
     if (nl == 0 && ng == 0) break;
-    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, threadIdx.x, blockDim.x, nxt, nn, qbuf(k + 1),
-                      &cnt[(k + 1) % 3], lane);
+    const PeelOvf ov{s_ovf, s_on, &s_obase, qbuf(k + 1), &cnt[(k + 1) % 3]};
+    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, 0, blockDim.x, nxt, nn, ov, lane);
     __syncthreads();
     if (threadIdx.x == 0) {
       s_ln[k & 1] = 0;

@@ -732,6 +732,25 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
     nibbles = nibbles && bound <= 0.5 * double(d.m);
   }
   w.cnt_shift = nibbles ? 2u : 3u;
+  // High load: round 0 leaves a large share of the entries unresolved, and
+  // clearing their rows' states one random 8-byte store at a time costs more
+  // than one streaming clear of the whole state. Expected unresolved entries
+  // per item: bound * (1 - e^-lambda)^rows, lambda = bound / m (Poisson row
+  // loads); each random store is charged 256 bytes against 8 per slot (the
+  // measured break-even: C4 theta 95 clears up front, theta 98 does not).
+  // TAGC_DECODE_ZERO_STATE=0/1 forces either way.
+  bool zero_state = false;
+  if (counters) {
+    double unres = 0.0;
+    for (const DecItem& d : items) {
+      const double bound = double(std::min(d.list_cap ? d.list_cap : d.n, d.n));
+      const double lam = bound / double(d.m);
+      unres += bound * std::pow(1.0 - std::exp(-lam), double(hp.rows));
+    }
+    zero_state = unres * hp.rows * 256.0 > double(slots) * 8.0;
+    if (const char* z = std::getenv("TAGC_DECODE_ZERO_STATE")) zero_state = std::atoi(z) != 0;
+  }
+  w.state_zeroed = zero_state ? 1u : 0u;
   const uint64_t cnt_words = nibbles ? (slots + 7) / 8 : (slots + 3) / 4;
   // round 0 inside the dense emit unless the owner step consumes the values
   const bool fused = counters && !ordered && !opt_on_ && fused_emit_;
@@ -743,6 +762,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
         {w.bitmap, bm * 4}, {w.qcount, 64}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
         {w.slot_mark, w.slot_mark ? mark_words * 4 : 0},
         {counters ? static_cast<void*>(w.cnt8) : static_cast<void*>(w.slot_state), counters ? cnt_words * 4 : slots * 8},
+        {zero_state ? static_cast<void*>(w.slot_state) : nullptr, zero_state ? slots * 8 : 0},
         {w.tile_state, wt * 8}});  // one launch for every decode scratch reset
   static const bool dbg = std::getenv("TAGC_DEBUG_PEEL") != nullptr;
   if (dbg) {

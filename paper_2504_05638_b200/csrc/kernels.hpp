@@ -172,6 +172,8 @@ struct DecodeWork {
   unsigned long long* tile_state;  // single-pass scan: per word tile, flag << 32 | count (zeroed per call)
   uint32_t* cta_cnt;               // counter mode: per list-count CTA, its tiles' present count (2 x kListMaxCtas)
   uint32_t list_split;             // list-count CTAs per list-write CTA (1 or 2)
+  uint32_t state_zeroed;           // counter mode: slot_state cleared up front (high load), so round 0
+                                   // does not clear the unresolved entries' buckets one by one
   uint32_t* plist;                 // flat presence list (all items), count in qcount[5]
   uint32_t* pitem;                 // item of each flat presence entry
   uint2* pinfo;                    // per presence entry: round-0 value, shared-row mask

@@ -57,7 +57,7 @@ def main():
         rows.append({"theta": theta, "ratio": ratio, "ms_per_step": round(ms, 3),
                      "gbs": round(n * 4 / (ms * 1e-3) / 1e9, 1), "k_fused_ms": round(spans[0], 3),
                      "decode_ms": round(spans[1], 3), "presence": st.presence, "peeled": st.peeled,
-                     "unresolved": st.unresolved})
+                     "unresolved": st.unresolved, "rounds": list(ctx.last_peel_rounds())})
         print(json.dumps(rows[-1]), flush=True)
         del ctx, acc
         torch.cuda.empty_cache()
