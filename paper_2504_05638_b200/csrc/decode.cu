@@ -456,12 +456,36 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
     const uint32_t base = ldcg(w.tile_base + wt);
     const bool staged = tile_n <= kListStage;
     uint32_t j = base + off;
+    // a thread's words cover consecutive positions: pack their presence into
+    // 32-position masks (w = 4: four words of 8 positions per mask, the
+    // nibble-any bits compressed to one bit each), so position = pos0 + 32 g
+    // + bit and the extraction loop runs over 4 masks instead of 16 words
+    uint32_t msk[kPerThreadWords];
+    if (w4) {
 #pragma unroll
-    for (uint32_t k = 0; k < kPerThreadWords; ++k) {
-      const uint32_t wi = tile_word(wbase, k);
-      for (uint32_t x = bits[k]; x; x &= x - 1) {
-        const uint32_t bb = __ffs(x) - 1;
-        const uint32_t p = wi * P + (w4 ? bb / 4 : bb);
+      for (uint32_t g = 0; g < kPerThreadWords / 4; ++g) {
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          uint32_t x = bits[4 * g + q];  // bits 0, 4, ..., 28
+          x = (x | x >> 3) & 0x03030303u;
+          x = (x | x >> 6) & 0x000F000Fu;
+          x = (x | x >> 12) & 0xFFu;
+          c |= x << (8 * q);
+        }
+        msk[g] = c;
+      }
+    } else {
+#pragma unroll
+      for (uint32_t k = 0; k < kPerThreadWords; ++k) msk[k] = bits[k];
+    }
+    const uint32_t groups = w4 ? kPerThreadWords / 4 : kPerThreadWords;
+    const uint32_t pos0 = tile_word(wbase, 0) * P;
+#pragma unroll
+    for (uint32_t g = 0; g < kPerThreadWords; ++g) {
+      if (g >= groups) break;
+      for (uint32_t x = msk[g]; x; x &= x - 1) {
+        const uint32_t p = pos0 + 32u * g + uint32_t(__ffs(x) - 1);
         if (j < total_list) {
           w.plist[j] = p;
           if (w.n_items > 1) w.pitem[j] = it;
@@ -1043,6 +1067,12 @@ __device__ __forceinline__ uint32_t peel_n(const DecodeWork& w, const HashParams
 __device__ __forceinline__ void ovf_flush(const PeelOvf& ov) {
   stage_flush<uint32_t, kOvfStage>(ov.s_buf, ov.s_n, ov.s_base, ov.gq, ov.gcount);
 }
+// end of a loop: flush only a non-empty stage (no pushes until the next
+// round's barrier, so every thread reads the same count)
+__device__ __forceinline__ void ovf_flush_end(const PeelOvf& ov) {
+  __syncthreads();
+  if (ov.s_n[0] != 0u) ovf_flush(ov);
+}
 
 // One round's share of a CTA: the local pairs [0, nl) and the global slots
 // [0, ng) strided by gstride from cta0 (CTA-uniform loop bounds: the
@@ -1068,7 +1098,7 @@ __device__ __forceinline__ uint32_t peel_round(const DecodeWork& w, const HashPa
     }
     bool full = false;
     won += peel_n<true, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, ov, full, lane);
-    if (__syncthreads_or(full)) ovf_flush(ov);
+    if (b + blockDim.x * kPeelN < nl && __syncthreads_or(full)) ovf_flush(ov);  // (CTA-uniform)
   }
   for (uint64_t b = cta0; b < ng; b += gstride * kPeelN) {
     bool have[kPeelN];
@@ -1082,9 +1112,9 @@ __device__ __forceinline__ uint32_t peel_round(const DecodeWork& w, const HashPa
     }
     bool full = false;
     won += peel_n<false, kPeelN, R>(w, hp, si, have, sl, en, s_next, s_nn, ov, full, lane);
-    if (__syncthreads_or(full)) ovf_flush(ov);
+    if (b + gstride * kPeelN < ng && __syncthreads_or(full)) ovf_flush(ov);
   }
-  ovf_flush(ov);
+  ovf_flush_end(ov);
   return won;
 }
 
@@ -1179,9 +1209,9 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
         _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(R); ++r) if (r < hp.rows)
           full |= local_push<kAt>((one[h] >> r) & 1u, sl[h][r], ii[h], s_lq[1], &s_ln[1], ov, lane);
       }
-      if (__syncthreads_or(full)) ovf_flush(ov);
+      if (base + 2 * gstride < nu && __syncthreads_or(full)) ovf_flush(ov);
     }
-    ovf_flush(ov);
+    ovf_flush_end(ov);
     total = grid_barrier_sum(w.bar, 0, s_ln[1], &s_total);
   } else {
     total = ldcg(&cnt[1]);  // k_r0_subtract's global pushes

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+T=r02bn
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "codec or golden or multirank or bigworld" 2>&1 | tail -2
+TAGC_GRAPHS=0 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --no-e2e --no-owner-step > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/${T}_launches.csv 2>&1 | grep -E "list_write|r0_phase1|k_peel|emit"
+for i in 1 2; do timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-owner-step 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['stages_ms'], d['extras']['gpt2']['ms_per_step'])"; done
+for t in 90 95; do timeout 300 python tools/density_sweep.py --steps 3 --theta $t 2>&1 | tail -1; done
