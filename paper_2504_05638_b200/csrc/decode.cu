@@ -1718,99 +1718,140 @@ __device__ __forceinline__ uint32_t emit_smem_u32(const void* p) {
 
 // kOpt (the owner's optimizer step instead of the bulk store): one buffer,
 // 4 CTAs per SM, so more parameter / state loads are in flight.
+// Word tiles are claimed one at a time from a counter (qcount[6]) instead
+// of a static per-CTA range: a persistent store stream with a fixed share per
+// CTA ends with the slowest SM (1 GB: 6.3 TB/s static vs 7.4 TB/s claimed,
+// tools/micro/write_pattern.cu). The next tile is claimed while the current
+// one is stored, and its bounds and first two entry windows are loaded one
+// chunk later, so a tile switch exposes no load latency.
 template <bool kOpt>
 __global__ void __launch_bounds__(256, kOpt ? 4 : 1) k_emit(DecodeWork w, const OptEpilogue* __restrict__ opt) {
   extern __shared__ __align__(128) float ebuf[];  // [2][kEmitChunk] ([1] with kOpt)
-  uint32_t t0, t1;
-  cta_tiles(w.total_word_tiles, t0, t1);
+  __shared__ uint32_t s_claim;
+  const uint32_t T = uint32_t(w.total_word_tiles);
   const uint32_t total = w.qcount[5];
   uint32_t n_chunks = 0;  // chunks stored by this CTA (ring position)
-  if (t0 < t1) {
-    uint32_t it = find_word_item(w.items, w.n_items, t0);
-    // Entry windows: thread t holds list entry wb + t (position, value) of
-    // the current window and, one window ahead, of the next, so the loads
-    // of the entries a chunk needs were issued a window earlier (the list
-    // range of this CTA's tiles is contiguous and ascending).
-    const uint32_t lbeg = __ldg(w.tile_base + t0);
-    uint32_t lend = t1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + t1) : total;
-    lend = lend < total ? lend : total;
+  auto tile_end = [&](uint32_t t) {
+    uint32_t le = t + 1 < T ? __ldg(w.tile_base + t + 1) : total;
+    return le < total ? le : total;
+  };
+  // entry window at list index base (thread t: entry base + t), bounded by lend
+  auto load_win = [&](uint32_t base, uint32_t lend, uint32_t& p, float& v) {
+    const uint32_t i = base + threadIdx.x;
+    p = 0xFFFFFFFFu;
+    v = 0.0f;
+    if (i < lend) {
+      p = __ldcs(w.plist + i);
+      v = __ldcs(w.val + i);
+    }
+  };
+  if (threadIdx.x == 0) s_claim = atomicAdd(&w.qcount[6], 1u);
+  __syncthreads();
+  uint32_t wt = s_claim;
+  uint32_t lbeg = 0, le = 0, wp = 0, np = 0;
+  float wv = 0.0f, nv = 0.0f;
+  if (wt < T) {
+    lbeg = __ldg(w.tile_base + wt);
+    le = tile_end(wt);
+    load_win(lbeg, le, wp, wv);
+    load_win(lbeg + blockDim.x, le, np, nv);
+  }
+  while (wt < T) {
+    __syncthreads();  // every thread has read s_claim
+    if (threadIdx.x == 0) s_claim = atomicAdd(&w.qcount[6], 1u);  // the next tile, read after the first chunk's barrier
+    const DecItem& e = w.items[find_word_item(w.items, w.n_items, wt)];
+    const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
+    const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
+    const uint64_t p0 = wbase * P;
+    const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
     uint32_t wb = lbeg;  // first entry of the current window
     uint32_t cons = 0;   // entries of the current window already placed
-    auto load_win = [&](uint32_t base, uint32_t& p, float& v) {
-      const uint32_t i = base + threadIdx.x;
-      p = 0xFFFFFFFFu;
-      v = 0.0f;
-      if (i < lend) {
-        p = __ldcs(w.plist + i);
-        v = __ldcs(w.val + i);
-      }
-    };
-    uint32_t wp, np;
-    float wv, nv;
-    load_win(wb, wp, wv);
-    load_win(wb + blockDim.x, np, nv);
-    for (uint32_t wt = t0; wt < t1; ++wt) {
-      while (it + 1 < w.n_items && w.items[it + 1].word_tile_begin <= wt) ++it;
-      const DecItem& e = w.items[it];
-      const uint64_t P = (e.flags & kWidth4) ? 8u : 32u;
-      const uint64_t wbase = uint64_t(wt - e.word_tile_begin) * kWordTile;
-      const uint64_t p0 = wbase * P;
-      const uint64_t p1 = min(uint64_t(e.n), (wbase + kWordTile) * P);
-      // the tile's entries end at le (positions restart at the next item)
-      uint32_t le = wt + 1 < uint32_t(w.total_word_tiles) ? __ldg(w.tile_base + wt + 1) : total;
-      le = le < total ? le : total;
-      for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks) {
-        const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
-        float* buf = kOpt ? ebuf : ebuf + (n_chunks & 1u) * kEmitChunk;
-        if (kOpt && n_chunks) __syncthreads();  // every thread is done reading the previous chunk
-        if (!kOpt && n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
-          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncthreads();
-        }
-        float4* b4 = reinterpret_cast<float4*>(buf);
-        for (uint32_t q = threadIdx.x; q < kEmitChunk / 4; q += blockDim.x) b4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t nt = T, nlb = 0, nle = 0;  // the next tile and its list range
+    uint32_t fp = 0xFFFFFFFFu, gp = 0xFFFFFFFFu;  // its first two windows
+    float fv = 0.0f, gv = 0.0f;
+    bool next_loaded = false;
+    uint32_t k = 0;  // chunk of this tile
+    for (uint64_t c0 = p0; c0 < p1; c0 += kEmitChunk, ++n_chunks, ++k) {
+      const uint32_t clen = uint32_t(p1 - c0 < kEmitChunk ? p1 - c0 : kEmitChunk);
+      float* buf = kOpt ? ebuf : ebuf + (n_chunks & 1u) * kEmitChunk;
+      if (kOpt && n_chunks) __syncthreads();  // every thread is done reading the previous chunk
+      if (!kOpt && n_chunks >= 2) {  // the store issued from this buffer two chunks ago has read it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncthreads();
-        // this chunk's entries: the window's unplaced entries below c0 + clen
-        // that belong to this tile (list index < le)
-        for (;;) {
-          const uint32_t i = wb + threadIdx.x;
-          const bool in = threadIdx.x >= cons && i < le && uint64_t(wp) < c0 + clen;
-          if (in) buf[wp - c0] = wv;
-          cons += __syncthreads_count(in);
-          const uint32_t rest = min(wb + blockDim.x, le);
-          if (wb + cons < rest) break;          // stopped inside the window: chunk done
-          if (wb + blockDim.x > le) break;      // the tile's entries end inside the window
-          wb += blockDim.x;                      // window used up: advance, prefetch the next
-          cons = 0;
-          wp = np;
-          wv = nv;
-          load_win(wb + blockDim.x, np, nv);
+      }
+      float4* b4 = reinterpret_cast<float4*>(buf);
+      for (uint32_t q = threadIdx.x; q < kEmitChunk / 4; q += blockDim.x) b4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncthreads();
+      if (k == 0) {  // the claim is visible: its list range in flight during this chunk
+        nt = s_claim;
+        if (nt < T) {
+          nlb = __ldg(w.tile_base + nt);
+          nle = tile_end(nt);
         }
-        float* dst = e.out + c0;
-        const uint32_t bytes = (clen * 4u) & ~15u;
-        if (kOpt) {  // owner-side optimizer step on the chunk (no bulk store)
-          const OptEpilogue o = *opt;
-          if (o.kind == 1) opt_range<true, false>(o, dst, buf, clen);
-          else opt_range<false, false>(o, dst, buf, clen);
-        } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                         "r"(emit_smem_u32(buf)), "r"(bytes)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
-          for (uint32_t q = bytes / 4u + threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
-        } else {  // unaligned output: plain coalesced stores
-          for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
-          __syncthreads();
-          if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the ring count
+      } else if (!next_loaded && nt < T) {  // bounds arrived: the next tile's first windows
+        load_win(nlb, nle, fp, fv);
+        load_win(nlb + blockDim.x, nle, gp, gv);
+        next_loaded = true;
+      }
+      // this chunk's entries: the window's unplaced entries below c0 + clen
+      // (list index < le: the tile's own entries)
+      for (;;) {
+        const uint32_t i = wb + threadIdx.x;
+        const bool in = threadIdx.x >= cons && i < le && uint64_t(wp) < c0 + clen;
+        if (in) buf[wp - c0] = wv;
+        cons += __syncthreads_count(in);
+        const uint32_t rest = min(wb + blockDim.x, le);
+        if (wb + cons < rest) break;          // stopped inside the window: chunk done
+        if (wb + blockDim.x > le) break;      // the tile's entries end inside the window
+        wb += blockDim.x;                      // window used up: advance, prefetch the next
+        cons = 0;
+        wp = np;
+        wv = nv;
+        load_win(wb + blockDim.x, le, np, nv);
+      }
+      float* dst = e.out + c0;
+      const uint32_t bytes = (clen * 4u) & ~15u;
+      if (kOpt) {  // owner-side optimizer step on the chunk (no bulk store)
+        const OptEpilogue o = *opt;
+        if (o.kind == 1) opt_range<true, false>(o, dst, buf, clen);
+        else opt_range<false, false>(o, dst, buf, clen);
+      } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && bytes) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                       "r"(emit_smem_u32(buf)), "r"(bytes)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        for (uint32_t q = bytes / 4u + threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+      } else {  // unaligned output: plain coalesced stores
+        for (uint32_t q = threadIdx.x; q < clen; q += blockDim.x) dst[q] = buf[q];
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the ring count
       }
     }
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (k == 0) {  // no chunk (cannot happen for a listed tile): take the claim anyway
+      __syncthreads();
+      nt = s_claim;
+      if (nt < T) {
+        nlb = __ldg(w.tile_base + nt);
+        nle = tile_end(nt);
+      }
+    }
+    if (nt < T && !next_loaded) {  // a one-chunk tile: load now
+      load_win(nlb, nle, fp, fv);
+      load_win(nlb + blockDim.x, nle, gp, gv);
+    }
+    wt = nt;
+    lbeg = nlb;
+    le = nle;
+    wp = fp;
+    wv = fv;
+    np = gp;
+    nv = gv;
   }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   span_end(w.span);
 }
 
