@@ -1904,7 +1904,8 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       // 1: 18.9 — the counter atomics start to cost; TAGC_FUSED_CHUNK)
       const uint64_t contiguous = (total_tiles + (g ? g : 1) - 1) / (g ? g : 1);
       static const uint64_t chunk_tiles = std::getenv("TAGC_FUSED_CHUNK") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK"), nullptr, 10) : 2;
-      const uint32_t chunk = uint32_t(sketch_bytes <= (48ull << 20) ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
+      static const uint64_t chunk_above = (std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB"), nullptr, 10) : 48ull) << 20;
+      const uint32_t chunk = uint32_t(sketch_bytes <= chunk_above ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
       kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
                                                                  hi_pool, fine_hist, err, span, chunk);
     };
