@@ -750,11 +750,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
         pit = find_tile_item(items, n_items, t0);
         for (uint64_t tile = t0; tile < t1; ++tile) push(tile);
       } else {
-        for (;;) {
-          const uint64_t c0 = uint64_t(atomicAdd(err + 3, 1u)) * chunk;
-          if (c0 >= total_tiles) break;
+        // the next claim is issued before the current chunk's tiles are
+        // pushed, so its round trip overlaps the waits for free stages
+        uint64_t c0 = uint64_t(atomicAdd(err + 3, 1u)) * chunk;
+        while (c0 < total_tiles) {
+          const uint64_t cn = uint64_t(atomicAdd(err + 3, 1u)) * chunk;
           const uint64_t c1 = min(total_tiles, c0 + chunk);
           for (uint64_t tile = c0; tile < c1; ++tile) push(tile);
+          c0 = cn;
         }
       }
       push(kNoTile);
@@ -1896,7 +1899,18 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
     auto launch_tma = [&](auto kern) {
       // opt-in to > 48 KB of dynamic shared memory (cheap; per launch keeps it per device)
       cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
-      const uint64_t g = std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
+      // A batch that scatters into no sketch (every sketch deferred: C4) is a
+      // pure stream: non-persistent, ceil(tiles / 8) CTAs of 8 contiguous
+      // tiles each, a retiring CTA's slot refilled, so no SM waits on the
+      // slowest share (C4: 0.580 -> 0.525 ms; the bare ring of
+      // tools/micro/tma_ring.cu: 6.2 -> 6.6 TB/s). Batches with direct
+      // scatters stay persistent (GPT-2 0.25 -> 0.30 ms, Llama-3-8B 18.4 ->
+      // 23.2 ms non-persistent). TAGC_FUSED_TILES_PER_CTA overrides (0:
+      // persistent).
+      static const char* per_env = std::getenv("TAGC_FUSED_TILES_PER_CTA");
+      const uint64_t per_cta = per_env ? std::strtoull(per_env, nullptr, 10) : (sketch_bytes == 0 ? 8 : 0);
+      const uint64_t g = per_cta ? (total_tiles + per_cta - 1) / per_cta
+                                 : std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
       // one contiguous range per CTA while every sketch fits in L2 together;
       // beyond that, small chunks claimed from a counter keep every CTA in
       // one narrow window of the shard, whose sketch rows stay L2-resident
@@ -1905,7 +1919,7 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       const uint64_t contiguous = (total_tiles + (g ? g : 1) - 1) / (g ? g : 1);
       static const uint64_t chunk_tiles = std::getenv("TAGC_FUSED_CHUNK") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK"), nullptr, 10) : 2;
       static const uint64_t chunk_above = (std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB"), nullptr, 10) : 48ull) << 20;
-      const uint32_t chunk = uint32_t(sketch_bytes <= chunk_above ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
+      const uint32_t chunk = uint32_t(per_cta || sketch_bytes <= chunk_above ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
       kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
                                                                  hi_pool, fine_hist, err, span, chunk);
     };
