@@ -2121,8 +2121,9 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
   if (w.cnt8) {  // counter mode: count, scan, write (no look-back)
     // count and write on the same grid (the same tile range per CTA): the
     // write pass turns the per-CTA counts into list offsets itself
+    static const uint64_t list_ctas = std::getenv("TAGC_LIST_CTAS") ? std::strtoull(std::getenv("TAGC_LIST_CTAS"), nullptr, 10) : 0;
     const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1),
-                                           std::min<uint64_t>(uint64_t(di.sms) * 4, kListMaxCtas));
+                                           std::min<uint64_t>(list_ctas ? list_ctas : uint64_t(di.sms) * 4, kListMaxCtas));
     k_list_count<<<int(w.list_split * gc), 256, 0, stream>>>(w);
     k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // counters were zeroed by the caller
     return int(gc);
@@ -2150,7 +2151,11 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
     cudaFuncSetAttribute((const void*)k_r0_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR0EmitSmem));
     k_r0_emit<<<int(ge), 256, kR0EmitSmem, stream>>>(w, hp);
   } else if (hp.rows == 3) {
-    k_r0_phase1_k<3, 2><<<di.sms * 8, 256, 0, stream>>>(w, hp);
+    // TAGC_R0_GRID=0: one pass (ceil(list bound / 512) CTAs), else CTAs per SM
+    static const int r0_grid = std::getenv("TAGC_R0_GRID") ? std::atoi(std::getenv("TAGC_R0_GRID")) : 8;
+    const uint64_t g0 = r0_grid > 0 ? uint64_t(di.sms) * r0_grid
+                                    : std::max<uint64_t>(1, (w.list_cap + 511) / 512);
+    k_r0_phase1_k<3, 2><<<int(std::min<uint64_t>(g0, 1u << 20)), 256, 0, stream>>>(w, hp);
   } else {
     k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   }
