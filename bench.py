@@ -410,7 +410,7 @@ def end_to_end(rig, S, args):
     host_grad = torch.empty(S["total"], dtype=torch.float32, pin_memory=True)
     host_grad.copy_(S["grad"].cpu())
     host_out = torch.empty(max(S["owned"], 1), dtype=torch.float32, pin_memory=True)
-    steps = max(args.steps, 30)  # the pipeline's fill and drain (about one step) are paid once
+    steps = max(args.steps, 60)  # the pipeline's fill and drain (about one step) are paid once
     for _ in range(2):
         ctx.tagc_reduce_shards_host(shards, host_grad, S["acc"], host_out)
     ctx.host_join()
