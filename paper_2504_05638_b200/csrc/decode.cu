@@ -372,8 +372,11 @@ constexpr uint32_t kListStage = 2048;  // staged positions per word tile (beyond
 
 __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashParams hp) {
   using Scan = cub::BlockScan<uint32_t, 256>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_pos[kListStage];
+  // double-buffered per tile (scan storage, staged positions), so a tile
+  // needs no trailing barrier: tile i + 2 reuses tile i's buffers only after
+  // every thread has passed tile i + 1's scan
+  __shared__ typename Scan::TempStorage scan_tmp[2];
+  __shared__ uint32_t s_pos[2][kListStage];
   // this CTA's list offset and the list length from the per-CTA counts of
   // k_list_count (same grid, same tile ranges): no separate scan kernel
   __shared__ uint32_t s_pre[8], s_all[8];
@@ -402,6 +405,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
   const uint32_t* tile_cnt = reinterpret_cast<const uint32_t*>(w.tile_state);
   uint32_t t0, t1;
   cta_tiles(w.total_word_tiles, t0, t1);
+  uint64_t tile_base = run;  // list offset of the current tile (the tiles' counts run on from here)
   // list offset of every tile of this CTA (k_emit, this pass): a block scan
   // of the tiles' counts, 256 tiles at a time
   for (uint32_t b0 = t0; b0 < t1; b0 += blockDim.x) {
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
     const DecItem& e = w.items[it];
     load_tile_raw(e, uint32_t(t0 - e.word_tile_begin) * kWordTile, raw);
   }
-  for (uint32_t wt = t0; wt < t1; ++wt) {
+  for (uint32_t wt = t0, buf = 0; wt < t1; ++wt, buf ^= 1u) {
     const DecItem& e = w.items[it];
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t P = w4 ? 8u : 32u;
@@ -452,8 +456,10 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
       load_tile_raw(ne, uint32_t(wt + 1 - ne.word_tile_begin) * kWordTile, raw);
     }
     uint32_t off, tile_n;
-    Scan(scan_tmp).ExclusiveSum(cnt, off, tile_n);
-    const uint32_t base = ldcg(w.tile_base + wt);
+    Scan(scan_tmp[buf]).ExclusiveSum(cnt, off, tile_n);
+    // = tile_base[wt] (same counts as k_list_count), no load
+    const uint32_t base = uint32_t(tile_base < 0xFFFFFFFFull ? tile_base : 0xFFFFFFFFull);
+    tile_base += tile_n;
     const bool staged = tile_n <= kListStage;
     uint32_t j = base + off;
     // a thread's words cover consecutive positions: pack their presence into
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
           w.plist[j] = p;
           if (w.n_items > 1) w.pitem[j] = it;
         }
-        if (staged) s_pos[j - base] = p;
+        if (staged) s_pos[buf][j - base] = p;
         ++j;
       }
     }
@@ -498,13 +504,12 @@ __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashP
     // bucket byte counters, one entry per thread (hashing and REDs converged)
     const uint32_t n_in = base + tile_n <= total_list ? tile_n : (base < total_list ? total_list - base : 0u);
     for (uint32_t q = threadIdx.x; q < n_in; q += blockDim.x) {
-      const uint32_t p = staged ? s_pos[q] : __ldcg(w.plist + base + q);
+      const uint32_t p = staged ? s_pos[buf][q] : __ldcg(w.plist + base + q);
       _Pragma("unroll") for (uint32_t r = 0; r < uint32_t(kMaxRows); ++r) if (r < hp.rows) {
         const uint64_t slot = e.slot_base + uint64_t(r) * e.m + dev_bucket(hp.row[r], p, e.m, e.mmul);
         cnt_add(w, slot);
       }
     }
-    __syncthreads();  // scan storage / stage reuse
     it = nit;
   }
 }
