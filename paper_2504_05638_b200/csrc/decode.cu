@@ -312,7 +312,7 @@ __device__ __forceinline__ void load_tile_raw(const DecItem& e, uint32_t wbase, 
 
 __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
   using Reduce = cub::BlockReduce<uint32_t, 256>;
-  __shared__ typename Reduce::TempStorage red_tmp;
+  __shared__ typename Reduce::TempStorage red_tmp[2];  // double-buffered: no barrier per tile
   span_begin(w.span);
   // two count CTAs per write CTA (k_list_write runs gridDim.x / 2 CTAs):
   // CTA c counts one half of write CTA c / 2's tile range
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
     t1 = sp == 1 ? b1 : ((blockIdx.x & 1) ? b1 : mid);
   }
   uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(w.tile_state);  // counter mode: tile_state is free
-  uint32_t cta_sum = 0;
+  uint32_t cta_sum = 0, item_sum = 0;  // item_sum: presence of item `it` so far (one stats atomic per item run)
   if (t0 >= t1) {
     if (threadIdx.x == 0) w.cta_cnt[blockIdx.x] = 0;
     return;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
     const DecItem& e = w.items[it];
     load_tile_raw(e, uint32_t(t0 - e.word_tile_begin) * kWordTile, raw);
   }
-  for (uint32_t wt = t0; wt < t1; ++wt) {
+  for (uint32_t wt = t0, buf = 0; wt < t1; ++wt, buf ^= 1u) {
     const DecItem& e = w.items[it];
     const bool w4 = (e.flags & kWidth4) != 0;
     const uint32_t wbase = uint32_t(wt - e.word_tile_begin) * kWordTile;
@@ -356,13 +356,16 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
       const DecItem& ne = w.items[nit];
       load_tile_raw(ne, uint32_t(wt + 1 - ne.word_tile_begin) * kWordTile, raw);
     }
-    const uint32_t total = Reduce(red_tmp).Sum(cnt);
+    const uint32_t total = Reduce(red_tmp[buf]).Sum(cnt);
     if (threadIdx.x == 0) {
       tile_cnt[wt] = total;
       cta_sum += total;
-      if (total) atomicAdd(&w.stats[it].presence, total);
+      item_sum += total;
+      if (nit != it || wt + 1 == t1) {
+        if (item_sum) atomicAdd(&w.stats[it].presence, item_sum);
+        item_sum = 0;
+      }
     }
-    __syncthreads();  // reduce storage reuse
     it = nit;
   }
   if (threadIdx.x == 0) w.cta_cnt[blockIdx.x] = cta_sum;
