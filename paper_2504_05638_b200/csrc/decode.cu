@@ -688,7 +688,7 @@ __device__ __forceinline__ void round0_phase1(const DecodeWork& w, const HashPar
                                             &w.qcount[14], lane);
   }
   won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
 }
 
 __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParams hp) {
@@ -716,10 +716,11 @@ __global__ void __launch_bounds__(256) k_r0_phase1(DecodeWork w, const HashParam
 template <int R, int PER>
 __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashParams hp) {
   __shared__ uint32_t s_q[kR0Stage], s_u[kR0Stage];
-  __shared__ uint32_t s_n[2], s_un[2], s_base;
+  __shared__ uint32_t s_n[2], s_un[2], s_base, s_won;
   const bool compact = w.r0_list != nullptr;
   const bool ulist = w.cnt8 != nullptr;
   if (threadIdx.x == 0) {
+    s_won = 0;
     s_n[0] = s_un[0] = 0;
     s_n[1] = s_un[1] = kR0Stage;
   }
@@ -830,9 +831,11 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
     }
   }
   won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&s_won, won);
   if (compact) stage_flush<uint32_t, kR0Stage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
   if (ulist) stage_flush<uint32_t, kR0Stage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_won) atomicAdd(&w.qcount[kPeeledWord], s_won);  // one RED per CTA
 }
 
 // Every entry peeled in round 0 leaves the buckets it shares with other
@@ -1155,8 +1158,9 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
   __shared__ uint2 s_lq[2][kLocalQ];
   __shared__ unsigned long long s_sbase[kPeelItemsSmem];
   __shared__ uint32_t s_ovf[kOvfStage];
-  __shared__ uint32_t s_ln[2], s_on[2], s_obase, s_base, s_total;
+  __shared__ uint32_t s_ln[2], s_on[2], s_obase, s_base, s_total, s_won;
   if (threadIdx.x == 0) {
+    s_won = 0;
     s_ln[0] = s_ln[1] = 0;
     s_on[0] = 0;
     s_on[1] = kOvfStage;
@@ -1261,8 +1265,12 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     if (threadIdx.x == 0) s_ln[k & 1] = 0;  // read by every thread before the barrier
     __syncthreads();
   }
+  // one RED per CTA (per-warp REDs queued ~2.4K operations on the counter's
+  // line ahead of CTA 0's tail reads: ~12 us of hand-over at W = 8)
   won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&s_won, won);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_won) atomicAdd(&w.qcount[kPeeledWord], s_won);
   if (!tail || blockIdx.x != 0) return;
   // ---- tail: one CTA finishes with block barriers; round k's global part
   // is qbuf(k) / cnt[k % 3] (the handed-over frontier), later rounds local
@@ -1285,7 +1293,7 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
     __syncthreads();
   }
   won = warp_sum32(won);
-  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[4], won);
+  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
 }
 
 // ------------------------------------------------------------------ ordered peel
@@ -1649,7 +1657,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
     ++ep;
   }
   won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
   if (blockIdx.x != 0) return;
   if (tail) {  // ---- one CTA finishes with block barriers
     won = 0;
@@ -1667,7 +1675,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
       ++ep;
     }
     won = warp_sum32(won);
-    if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+    if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
   }
   if (threadIdx.x == 0) *o.epoch = ep;
 }
@@ -1677,7 +1685,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
 // listed entry the peel left unresolved.
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
   const uint32_t total = w.qcount[5];
-  if (total == w.qcount[4]) return;  // every listed entry peeled: nothing to estimate
+  if (total == w.qcount[kPeeledWord]) return;  // every listed entry peeled: nothing to estimate
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < total; base += stride) {
@@ -2011,7 +2019,7 @@ __global__ void __launch_bounds__(256, 3) k_r0_emit(DecodeWork w, const HashPara
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&w.qcount[4], won);
+  if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
   stage_flush<uint32_t, kR0EStage>(s_q, s_n, &s_base, w.r0_list, &w.qcount[13]);
   stage_flush<uint32_t, kR0EStage>(s_u, s_un, &s_base, w.ulist, &w.qcount[14]);
 }

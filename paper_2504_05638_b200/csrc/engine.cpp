@@ -708,7 +708,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   w.pinfo = static_cast<uint2*>(ws_.get("pinfo", list * 8, false, stream_));
   w.queue[0] = static_cast<uint32_t*>(ws_.get("queue0", slots * 4, false, stream_));
   w.queue[1] = static_cast<uint32_t*>(ws_.get("queue1", slots * 4, false, stream_));
-  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", 64, false, stream_));
+  w.qcount = static_cast<uint32_t*>(ws_.get("qcount", kQcountBytes, false, stream_));
   w.bar = static_cast<unsigned long long*>(ws_.get("peel_bar", 32, false, stream_));
   w.handoff = static_cast<uint2*>(ws_.get("peel_handoff", kPeelHandoff * sizeof(uint2), false, stream_));
   w.stats = static_cast<DecStats*>(ws_.get("dec_stats", (stats_base + n) * sizeof(DecStats), false, stream_)) +
@@ -759,7 +759,7 @@ void Engine::run_decode(std::vector<DecItem>& items, const HashParams& hp, bool 
   const uint64_t wwords = mark_words + 1;
   w.wmask = ordered ? static_cast<uint32_t*>(ws_.get("ord_wmask", wwords * 4, false, stream_)) : nullptr;
   zero({{w.wmask, w.wmask ? wwords * 4 : 0},
-        {w.bitmap, bm * 4}, {w.qcount, 64}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
+        {w.bitmap, bm * 4}, {w.qcount, kQcountBytes}, {w.bar, 32}, {w.stats, n * sizeof(DecStats)},
         {w.slot_mark, w.slot_mark ? mark_words * 4 : 0},
         {counters ? static_cast<void*>(w.cnt8) : static_cast<void*>(w.slot_state), counters ? cnt_words * 4 : slots * 8},
         {zero_state ? static_cast<void*>(w.slot_state) : nullptr, zero_state ? slots * 8 : 0},

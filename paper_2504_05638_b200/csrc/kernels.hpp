@@ -149,6 +149,11 @@ int launch_audit(const AuditItem* items, uint32_t n_items, uint64_t max_n, const
                  const float* const* res, uint32_t world, cudaStream_t stream);
 
 // ---------------------------------------------------------------- decode
+// qcount word of the peeled-entry total: its own 128-byte line (qcount is
+// kQcountBytes long), away from the list / queue / hand-off counters that
+// the kernels read while many CTAs add into it
+constexpr uint32_t kPeeledWord = 32;
+constexpr uint64_t kQcountBytes = 256;
 constexpr uint32_t kPeelHandoff = 512;
 constexpr uint32_t kListMaxCtas = 1024;
 struct DecodeWork {
