@@ -1228,72 +1228,59 @@ __global__ void __launch_bounds__(256, 2) k_peel(DecodeWork w, const HashParams 
   } else {
     total = ldcg(&cnt[1]);  // k_r0_subtract's global pushes
   }
+  // Grid rounds, then (once a round's frontier is <= kTail) the tail: CTA 0
+  // alone with block barriers. ONE loop and one peel_round call site for
+  // both, so the tail runs the grid rounds' instructions (a separate inlined
+  // copy started with a cold instruction cache: its first round took 10 us
+  // against 3.4 for the next ones at W = 8).
   uint32_t won = 0, k = 1;
   bool tail = false;
   for (;; ++k) {
-    if (total == 0) break;
-    if (total <= kTail) {  // hand the local pairs to CTA 0 (w.handoff, count qcount[15])
-      const uint32_t n = min(s_ln[k & 1], kLocalQ);
-      if (threadIdx.x == 0) s_base = n ? atomicAdd(&w.qcount[15], n) : 0u;
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) w.handoff[s_base + j] = s_lq[k & 1][j];
-      if (threadIdx.x == 0) s_ln[k & 1] = 0;
-      grid_barrier_sum(w.bar, k, 0, &s_total);
-      if (blockIdx.x == 0) {
+    if (!tail) {
+      if (total == 0) break;
+      if (total <= kTail) {  // hand the local pairs to CTA 0 (w.handoff, count qcount[15])
+        const uint32_t n = min(s_ln[k & 1], kLocalQ);
+        if (threadIdx.x == 0) s_base = n ? atomicAdd(&w.qcount[15], n) : 0u;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) w.handoff[s_base + j] = s_lq[k & 1][j];
+        if (threadIdx.x == 0) s_ln[k & 1] = 0;
+        grid_barrier_sum(w.bar, k, 0, &s_total);
+        if (blockIdx.x != 0) break;
         const uint32_t nh = ldcg(&w.qcount[15]);  // <= total <= kTail <= kLocalQ
         for (uint32_t j = threadIdx.x; j < nh; j += blockDim.x) s_lq[k & 1][j] = __ldcg(w.handoff + j);
         if (threadIdx.x == 0) s_ln[k & 1] = nh;
         __syncthreads();
+        tail = true;  // round k's global part is qbuf(k) / cnt[k % 3], later rounds local
       }
-      tail = true;
-      break;
     }
-    if (gtid == 0) {
+    if (tail) {
+      if (threadIdx.x == 0) cnt[(k + 2) % 3] = 0;
+    } else if (gtid == 0) {
       cnt[(k + 2) % 3] = 0;
       w.qcount[2] += 1;
     }
     const uint32_t nl = min(s_ln[k & 1], kLocalQ);
     const uint32_t ng = ldcg(&cnt[k % 3]);
+    if (tail && nl == 0 && ng == 0) break;
     uint2* nxt = s_lq[(k + 1) & 1];
     uint32_t* nn = &s_ln[(k + 1) & 1];
     const PeelOvf ov{s_ovf, s_on, &s_obase, qbuf(k + 1), &cnt[(k + 1) % 3]};
-    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, uint64_t(blockIdx.x) * blockDim.x, gstride, nxt,
-                         nn, ov, lane);
+    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, tail ? 0ull : uint64_t(blockIdx.x) * blockDim.x,
+                         tail ? uint64_t(blockDim.x) : gstride, nxt, nn, ov, lane);
     __syncthreads();
-    total = grid_barrier_sum(w.bar, k, *nn, &s_total);
-    PEEL_MARK(mk++);
-    if (threadIdx.x == 0) s_ln[k & 1] = 0;  // read by every thread before the barrier
-    __syncthreads();
-  }
-  // one RED per CTA (per-warp REDs queued ~2.4K operations on the counter's
-  // line ahead of CTA 0's tail reads: ~12 us of hand-over at W = 8)
-  won = warp_sum32(won);
-  if (lane == 0 && won) atomicAdd(&s_won, won);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_won) atomicAdd(&w.qcount[kPeeledWord], s_won);
-  if (!tail || blockIdx.x != 0) return;
-  // ---- tail: one CTA finishes with block barriers; round k's global part
-  // is qbuf(k) / cnt[k % 3] (the handed-over frontier), later rounds local
-  won = 0;
-  for (;; ++k) {
-    if (threadIdx.x == 0) cnt[(k + 2) % 3] = 0;
-    const uint32_t nl = min(s_ln[k & 1], kLocalQ);
-    const uint32_t ng = ldcg(&cnt[k % 3]);
-    uint2* nxt = s_lq[(k + 1) & 1];
-    uint32_t* nn = &s_ln[(k + 1) & 1];
-    if (nl == 0 && ng == 0) break;
-    const PeelOvf ov{s_ovf, s_on, &s_obase, qbuf(k + 1), &cnt[(k + 1) % 3]};
-    won += peel_round<R>(w, hp, si, s_lq[k & 1], nl, qbuf(k), ng, 0, blockDim.x, nxt, nn, ov, lane);
-    __syncthreads();
+    if (!tail) total = grid_barrier_sum(w.bar, k, *nn, &s_total);
     if (threadIdx.x == 0) {
-      s_ln[k & 1] = 0;
-      w.qcount[3] += 1;
+      s_ln[k & 1] = 0;  // read by every thread before the barrier
+      if (tail) w.qcount[3] += 1;
     }
     PEEL_MARK(mk++);
     __syncthreads();
   }
+  // one RED per CTA (per-warp REDs shared a line with the queue counters)
   won = warp_sum32(won);
-  if ((threadIdx.x & 31) == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
+  if (lane == 0 && won) atomicAdd(&s_won, won);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_won) atomicAdd(&w.qcount[kPeeledWord], s_won);
 }
 
 // ------------------------------------------------------------------ ordered peel
