@@ -1624,46 +1624,40 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
   PEEL_MARK(mk++);
   // ---- generations >= 1
   uint64_t dom = uint64_t(n_win) * hp.rows;
+  // grid generations, then (at <= kOrdTail slots) CTA 0 alone with block
+  // barriers: one loop and one ord_generation instance for both, so the
+  // tail runs warm code (cf. k_peel)
   uint32_t won = 0, g = 0;
   bool tail = false;
   for (;; ++g) {
-    grid.sync();
+    if (tail) __syncthreads();
+    else grid.sync();
     const uint32_t n = ldcg(cnt + g % 3);
     if (n == 0) break;
-    if (n <= kOrdTail) {  // every CTA sees the same n
+    if (!tail && n <= kOrdTail) {  // every CTA sees the same n
+      if (blockIdx.x != 0) break;
       tail = true;
-      break;
     }
-    if (gtid == 0) {
+    if (tail) {
+      if (threadIdx.x == 0) {
+        cnt[(g + 2) % 3] = 0;
+        w.qcount[3] += 1;
+      }
+    } else if (gtid == 0) {
       cnt[(g + 2) % 3] = 0;
       w.qcount[2] += 1;
     }
-    won += ord_generation<R>(w, hp, o, g, n, dom, ep, blockIdx.x, gridDim.x, cnt, s_q, s_nq, &s_base, s_warp,
-                          [&] { grid.sync(); }, mk);
+    won += ord_generation<R>(w, hp, o, g, n, dom, ep, tail ? 0u : blockIdx.x, tail ? 1u : gridDim.x, cnt, s_q,
+                             s_nq, &s_base, s_warp, [&] {
+                               if (tail) __syncthreads();
+                               else grid.sync();
+                             }, mk);
     dom = uint64_t(n) * hp.rows;
     ++ep;
   }
   won = warp_sum32(won);
   if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
   if (blockIdx.x != 0) return;
-  if (tail) {  // ---- one CTA finishes with block barriers
-    won = 0;
-    for (;; ++g) {
-      __syncthreads();
-      const uint32_t n = ldcg(cnt + g % 3);
-      if (n == 0) break;
-      if (threadIdx.x == 0) {
-        cnt[(g + 2) % 3] = 0;
-        w.qcount[3] += 1;
-      }
-      won += ord_generation<R>(w, hp, o, g, n, dom, ep, 0, 1, cnt, s_q, s_nq, &s_base, s_warp,
-                            [] { __syncthreads(); }, mk);
-      dom = uint64_t(n) * hp.rows;
-      ++ep;
-    }
-    won = warp_sum32(won);
-    if (lane == 0 && won) atomicAdd(&w.qcount[kPeeledWord], won);
-  }
   if (threadIdx.x == 0) *o.epoch = ep;
 }
 
