@@ -2040,7 +2040,8 @@ int launch_deferred_scatter(const DevInfo& di, const EncItem* items, const SelSt
   const int smem_place = int(2 * kDsBatch * sizeof(uint2) + 3 * n_bins * sizeof(uint32_t));
   const uint32_t tight = std::getenv("TAGC_DS_TIGHT") && std::atoi(std::getenv("TAGC_DS_TIGHT")) != 0 ? 1u : 0u;
   cudaFuncSetAttribute((const void*)k_ds_place, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_place);
-  k_ds_place<<<di.sms * 2, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, group, shift,
+  static const int place_per_sm = std::getenv("TAGC_DS_PLACE_PER_SM") ? std::max(1, std::atoi(std::getenv("TAGC_DS_PLACE_PER_SM"))) : 2;
+  k_ds_place<<<di.sms * place_per_sm, kDsThreads, smem_place, stream>>>(items, state, n_items, hi_pool, hp, base, group, shift,
                                                          n_bins, tight, fill, ctl, records, ovf);
   int l = 1;
   if (smem) {
