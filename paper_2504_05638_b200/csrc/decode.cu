@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(256) k_list_count(DecodeWork w) {
 constexpr uint32_t kListStage = 2048;  // staged positions per word tile (beyond: read back)
 
 __global__ void __launch_bounds__(256, 4) k_list_write(DecodeWork w, const HashParams hp) {
+  PDL_WAIT();
   using Scan = cub::BlockScan<uint32_t, 256>;
   // double-buffered per tile (scan storage, staged positions), so a tile
   // needs no trailing barrier: tile i + 2 reuses tile i's buffers only after
@@ -851,6 +852,7 @@ __global__ void __launch_bounds__(256) k_r0_phase1_k(DecodeWork w, const HashPar
 // the peeled entries only take their values out of the marked buckets'
 // residuals. k_peel seeds round 1 from the unresolved entries' buckets.
 __global__ void __launch_bounds__(256) k_r0_subtract_cnt(DecodeWork w, const HashParams hp) {
+  PDL_WAIT();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint32_t total = ldcg(&w.qcount[13]);
@@ -1665,6 +1667,7 @@ __global__ void __launch_bounds__(256) k_ord_loop(DecodeWork w, const HashParams
 // Median-of-rows estimate (decode.cpp:130-138 / :43-47) into val[i] for every
 // listed entry the peel left unresolved.
 __global__ void __launch_bounds__(256) k_final(DecodeWork w, const HashParams hp) {
+  PDL_WAIT();
   const uint32_t total = w.qcount[5];
   if (total == w.qcount[kPeeledWord]) return;  // every listed entry peeled: nothing to estimate
   const uint32_t lane = threadIdx.x & 31;
@@ -2122,7 +2125,7 @@ int build_passes(const DevInfo& di, const DecodeWork& w, const HashParams& hp, c
     const uint64_t gc = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1),
                                            std::min<uint64_t>(list_ctas ? list_ctas : uint64_t(di.sms) * 4, kListMaxCtas));
     k_list_count<<<int(w.list_split * gc), 256, 0, stream>>>(w);
-    k_list_write<<<int(gc), 256, 0, stream>>>(w, hp);  // counters were zeroed by the caller
+    launch_pdl(k_list_write, dim3(unsigned(gc)), dim3(256), 0, stream, w, hp);  // counters were zeroed by the caller
     return int(gc);
   }
   const uint64_t g64 = std::min<uint64_t>(std::max<uint64_t>(w.total_word_tiles, 1), uint64_t(di.sms) * 4);
@@ -2156,7 +2159,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
   } else {
     k_r0_phase1<<<di.sms * 8, 256, 0, stream>>>(w, hp);
   }
-  if (w.cnt8) k_r0_subtract_cnt<<<di.sms * 8, 256, 0, stream>>>(w, hp);
+  if (w.cnt8) launch_pdl(k_r0_subtract_cnt, dim3(di.sms * 8), dim3(256), 0, stream, w, hp);
   else k_r0_subtract<<<di.sms * 8, 256, 0, stream>>>(w, hp);
 
   const void* peel = hp.rows == 3 ? (const void*)k_peel<3> : (const void*)k_peel<kMaxRows>;
@@ -2172,7 +2175,7 @@ int launch_decode(const DevInfo& di, const DecodeWork& w, const HashParams& hp,
     return list_launches + 4;  // list, round 0 + emit, subtraction, peel, final
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
-  k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
+  launch_pdl(k_final, dim3(std::max(per_sm, 1) * di.sms), dim3(256), 0, stream, w, hp);
   return list_launches + 4;  // list, round 0 (2), peel, final
 }
 
@@ -2203,7 +2206,7 @@ int launch_decode_ordered(const DevInfo& di, const DecodeWork& w, const HashPara
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loop, 256, 0);
   cudaLaunchCooperativeKernel(loop, dim3(std::max(per_sm, 1) * di.sms), dim3(256), args, 0, stream);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_final, 256, 0);
-  k_final<<<std::max(per_sm, 1) * di.sms, 256, 0, stream>>>(w, hp);
+  launch_pdl(k_final, dim3(std::max(per_sm, 1) * di.sms), dim3(256), 0, stream, w, hp);
   return (w.cnt8 ? 2 : 1) + 3;  // build, round 0, loop, estimate
 }
 

@@ -338,3 +338,43 @@ inline HashParams make_hash_params(uint64_t seed, uint32_t rows) {
 }
 
 }  // namespace tagc_b200
+
+// ---------------------------------------------------------- dependent launch
+// Programmatic dependent launch between consecutive kernels of a step: a
+// kernel launched with launch_pdl may be scheduled while its predecessor
+// drains, and waits (griddepcontrol.wait, its first statement) until the
+// predecessor has completed and its writes are visible. Only kernels that
+// open with PDL_WAIT() may be launched this way. TAGC_PDL=0 disables.
+#if defined(__CUDACC__)
+#include <cstdlib>
+#include <utility>
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+namespace tagc_b200 {
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TAGC_PDL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, block, smem, stream>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace tagc_b200
+#endif

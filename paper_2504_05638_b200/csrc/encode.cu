@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(256) k_window_coarse(const EncItem* __restrict
                                                        SelState* __restrict__ state,
                                                        const uint32_t* __restrict__ sample_hist,
                                                        unsigned long long* span) {
+  PDL_WAIT();
   (void)span;
   __shared__ RankBinSmem sm;
   const uint32_t item = blockIdx.x;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sample_fine(const EncItem* __r
                                                               const SelState* __restrict__ state,
                                                               uint32_t n_items, uint64_t total,
                                                               uint32_t* __restrict__ sample_hist) {
+  PDL_WAIT();
   uint64_t w0, w1;
   cta_range(total, w0, w1);
   uint32_t it = w0 < w1 ? find_sample_item(items, n_items, w0) : 0;
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sample_fine(const EncItem* __r
 __global__ void __launch_bounds__(256) k_window_fine(const EncItem* __restrict__ items,
                                                      SelState* __restrict__ state,
                                                      uint32_t* __restrict__ sample_hist) {
+  PDL_WAIT();
   __shared__ RankBinSmem sm;
   const uint32_t item = blockIdx.x;
   const EncItem e = items[item];
@@ -689,6 +692,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) k_fused_tma(const EncItem* _
                                                                 uint32_t* __restrict__ fine_hist,
                                                                 uint32_t* __restrict__ err,
                                                                 unsigned long long* span, uint32_t chunk) {
+  PDL_WAIT();
   extern __shared__ __align__(128) unsigned char fsm[];
   FusedStage* stg = reinterpret_cast<FusedStage*>(fsm);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(fsm + size_t(kFusedStages) * sizeof(FusedStage));
@@ -1883,12 +1887,12 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
     ++launches;
   }
   if (total_samples) {
-    k_window_coarse<<<n_items, 256, 0, stream>>>(items, state, sample_hist, span);
-    k_sample_fine<<<persistent_grid((const void*)k_sample_fine, kTileThreads, di, total_samples), kTileThreads,
-                    0, stream>>>(items, state, n_items, total_samples, sample_hist);
+    launch_pdl(k_window_coarse, dim3(n_items), dim3(256), 0, stream, items, state, sample_hist, span);
+    launch_pdl(k_sample_fine, dim3(persistent_grid((const void*)k_sample_fine, kTileThreads, di, total_samples)),
+               dim3(kTileThreads), 0, stream, items, state, n_items, total_samples, sample_hist);
     launches += 2;
   }
-  k_window_fine<<<n_items, 256, 0, stream>>>(items, state, sample_hist);
+  launch_pdl(k_window_fine, dim3(n_items), dim3(256), 0, stream, items, state, sample_hist);
   // every item of a batch shares the path: hook (accumulator) or per-stage outputs
   const bool hook = per_stage == 0;
   auto launch = [&](auto kern) {
@@ -1920,8 +1924,8 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       static const uint64_t chunk_tiles = std::getenv("TAGC_FUSED_CHUNK") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK"), nullptr, 10) : 2;
       static const uint64_t chunk_above = (std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB") ? std::strtoull(std::getenv("TAGC_FUSED_CHUNK_ABOVE_MB"), nullptr, 10) : 48ull) << 20;
       const uint32_t chunk = uint32_t(per_cta || sketch_bytes <= chunk_above ? 0 : std::min<uint64_t>(chunk_tiles, contiguous));
-      kern<<<int(g ? g : 1), kFusedThreads, kFusedSmem, stream>>>(items, state, n_items, total_tiles, hp, cand,
-                                                                 hi_pool, fine_hist, err, span, chunk);
+      launch_pdl(kern, dim3(unsigned(g ? g : 1)), dim3(kFusedThreads), kFusedSmem, stream, items, state, n_items,
+                 total_tiles, hp, cand, hi_pool, fine_hist, err, span, chunk);
     };
     if (w4) launch_tma(k_fused_tma<true>);
     else launch_tma(k_fused_tma<false>);
