@@ -1904,15 +1904,16 @@ int launch_select_fused(const DevInfo& di, const EncItem* items, SelState* state
       // opt-in to > 48 KB of dynamic shared memory (cheap; per launch keeps it per device)
       cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedSmem));
       // A batch that scatters into no sketch (every sketch deferred: C4) is a
-      // pure stream: non-persistent, ceil(tiles / 8) CTAs of 8 contiguous
+      // pure stream: non-persistent, ceil(tiles / 10) CTAs of 10 contiguous
       // tiles each, a retiring CTA's slot refilled, so no SM waits on the
-      // slowest share (C4: 0.580 -> 0.525 ms; the bare ring of
+      // slowest share (C4: 0.580 -> 0.522 ms; K = 4 / 6 / 8 / 12 / 16:
+      // 0.581 / 0.535 / 0.525 / 0.525 / 0.530; the bare ring of
       // tools/micro/tma_ring.cu: 6.2 -> 6.6 TB/s). Batches with direct
       // scatters stay persistent (GPT-2 0.25 -> 0.30 ms, Llama-3-8B 18.4 ->
       // 23.2 ms non-persistent). TAGC_FUSED_TILES_PER_CTA overrides (0:
       // persistent).
       static const char* per_env = std::getenv("TAGC_FUSED_TILES_PER_CTA");
-      const uint64_t per_cta = per_env ? std::strtoull(per_env, nullptr, 10) : (sketch_bytes == 0 ? 8 : 0);
+      const uint64_t per_cta = per_env ? std::strtoull(per_env, nullptr, 10) : (sketch_bytes == 0 ? 10 : 0);
       const uint64_t g = per_cta ? (total_tiles + per_cta - 1) / per_cta
                                  : std::min<uint64_t>(uint64_t(di.sms) * kFusedCtasPerSm, total_tiles);
       // one contiguous range per CTA while every sketch fits in L2 together;
